@@ -1,0 +1,220 @@
+/*
+ * ntp.h — C ABI of libntp, a B200 (sm_100a) implementation of the data-parallel
+ * hot path of NeutronTP (arXiv 2412.20379): feature-sliced ("GNN tensor
+ * parallel") full-graph propagation for decoupled GNN training.
+ *
+ * Citation keys: P:n = PAPER.md line n, S:n = SPEC.md line n, SURVEY §x.
+ *
+ * Model:
+ *   A^ = D~_in^{-1/2} (A + I) D~_out^{-1/2},   D~ = D + I       (reading R1)
+ *   forward  Z^0 = H,  Z^k = gamma * A^   Z^{k-1} + alpha * H     (Eq. 9, reading R2)
+ *   backward Y^0 = G,  Y^k = gamma * A^T  Y^{k-1} + alpha * G     (exact adjoint)
+ *   epoch    Alg. 1: MLP on vertex rows -> split -> K hops on
+ *            feature slices -> gather -> loss -> split -> K backward hops ->
+ *            gather -> MLP backward -> allreduce(dW) -> SGD.
+ *
+ * Layouts (P = number of feature slices = world size):
+ *   V_p   = ceil(n / P),  V_pad = P * V_p
+ *   d_s   = ceil(w / P) rounded up so d_s*elem_bytes % slice_align == 0 (16 or 32)
+ *   VERTEX  layout on rank q: rows [q*V_p, (q+1)*V_p) of the padded matrix at width w
+ *   FEATURE layout on rank q: all V_pad rows x columns [q*d_s, (q+1)*d_s), row-major,
+ *           rows >= n and columns >= w are zero padding.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns ntp_status; no C++ exception, abort or exit crosses the ABI.
+ *     On failure ntp_last_error(ctx) returns a context-owned message.
+ *   - Arguments are validated before any device work.
+ *   - Device pointers inside ntp_tensor are caller-owned (typically torch
+ *     tensors); the library never frees them.  Graph arrays passed in are
+ *     copied.  The library owns the device CSR (both orientations), D~^{-1/2},
+ *     the NCCL communicator, its streams and scratch; ntp_destroy frees them.
+ *   - Calls taking an ntp_stream (a cudaStream_t) only enqueue work on it;
+ *     kernel errors surface at the next synchronising call.
+ *   - Collective contract: every rank issues the same sequence of
+ *     collective-bearing calls (layout changes, ntp_train_epoch).
+ *   - One context per process/GPU; all calls on one host thread per context.
+ */
+#ifndef NTP_H
+#define NTP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NTP_ABI_VERSION 1
+
+typedef struct ntp_ctx ntp_ctx;
+typedef void* ntp_stream;          /* a cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    NTP_OK = 0,
+    NTP_ERR_ARG = -1,       /* null pointer / out-of-range scalar            */
+    NTP_ERR_SHAPE = -2,     /* tensor shape, dtype, layout or alignment       */
+    NTP_ERR_CONFIG = -3,    /* unsupported configuration (e.g. nnz >= 2^31)   */
+    NTP_ERR_GRAPH = -4,     /* NTP_G_VALIDATE failed                          */
+    NTP_ERR_STATE = -5,     /* call out of order (e.g. no graph loaded)       */
+    NTP_ERR_OOM = -6,       /* device allocation failed                       */
+    NTP_ERR_CUDA = -7,      /* CUDA runtime / kernel error                    */
+    NTP_ERR_NCCL = -8,      /* NCCL error (communicator aborted)              */
+    NTP_ERR_TIMEOUT = -9    /* collective did not complete in time (aborted)  */
+} ntp_status;
+
+typedef enum { NTP_F32 = 0, NTP_BF16 = 1 } ntp_dtype;
+typedef enum { NTP_LAYOUT_VERTEX = 0, NTP_LAYOUT_FEATURE = 1 } ntp_layout;
+
+/* A strided row-major matrix in caller-owned memory (device unless a call says
+ * otherwise).  Element (r, c) lives at data + (r*ld + c)*elem_bytes.
+ * For propagation and layout calls: data 16-byte aligned, (ld*elem_bytes) % 16 == 0. */
+typedef struct {
+    void*      data;
+    ntp_dtype  dtype;
+    ntp_layout layout;
+    int64_t    rows;
+    int32_t    cols;
+    int64_t    ld;
+} ntp_tensor;
+
+/* ---------------------------------------------------------------- context */
+
+/* Rank 0 calls this and broadcasts the 128 bytes (e.g. torch.distributed). */
+ntp_status ntp_get_unique_id(uint8_t id[128]);
+
+/* Creates a context on CUDA `device`.  world == 1: no NCCL communicator is
+ * created and `id` may be NULL.  world > 1: ncclCommInitRank with `id`.
+ * slice_align: 16 or 32 (bytes; d_s rounding, see Layouts). */
+ntp_status ntp_create(ntp_ctx** ctx, int device, int rank, int world,
+                      const uint8_t id[128], int slice_align);
+void        ntp_destroy(ntp_ctx* ctx);
+const char* ntp_last_error(const ntp_ctx* ctx);
+const char* ntp_status_string(ntp_status s);
+int         ntp_abi_version(void);
+
+/* -------------------------------------------------------------- graph (a0) */
+
+#define NTP_G_SYMMETRIC 1u   /* graph is undirected: transpose == CSR (saves memory) */
+#define NTP_G_VALIDATE  2u   /* check the input CSR: rp[0]=0, monotone,
+                                rp[n]=nnz, 0<=col<n, strictly ascending per row     */
+
+/* Loads an in-CSR from HOST arrays: row v = destination, columns = sources u
+ * of arcs u->v ("N_in(v)", Eq. 1).  Explicit self loops are dropped
+ * (A~ adds exactly one, reading R1).  Builds the out-CSR (transpose) on the
+ * device unless NTP_G_SYMMETRIC, then degrees and D~^{-1/2}.
+ * Requires n < 2^31 and nnz < 2^31 (NTP_ERR_CONFIG otherwise). */
+ntp_status ntp_load_graph(ntp_ctx* ctx, const int64_t* row_ptr, const int32_t* col_idx,
+                          int64_t n, int64_t nnz, uint32_t flags);
+
+/* Builds the graph from a HOST arc list (src[i] -> dst[i]) on the device:
+ * reject ids outside [0,n) and self loops, optionally append reverse arcs
+ * (NTP_G_SYMMETRIC), sort by (dst, src), deduplicate (O1). */
+ntp_status ntp_build_graph(ntp_ctx* ctx, const int64_t* src, const int64_t* dst, int64_t m,
+                           int64_t n, uint32_t flags);
+
+/* Generates m_raw R-MAT arcs on the device with the counter-based generator
+ * of SURVEY §8(d) (h = SplitMix64 finaliser of seed*G + stream*D + i; level l
+ * of arc i draws u = h(seed,0,i*64+l)>>32 against thresholds t[0..2]; MSB
+ * first; ids < 2^scale), then builds the graph exactly as ntp_build_graph. */
+ntp_status ntp_generate_rmat(ntp_ctx* ctx, int64_t n, int scale, int64_t m_raw,
+                             const uint32_t thresholds[3], uint64_t seed, uint32_t flags);
+
+/* Writes raw R-MAT arcs [i0, i0+count) to HOST arrays (generator parity tests). */
+ntp_status ntp_rmat_arcs(ntp_ctx* ctx, int scale, const uint32_t thresholds[3], uint64_t seed,
+                         int64_t i0, int64_t count, int64_t* src_host, int64_t* dst_host);
+
+ntp_status ntp_graph_info(const ntp_ctx* ctx, int64_t* n, int64_t* nnz, int* symmetric);
+
+/* Copies the device CSR to HOST arrays: transposed=0 -> in-CSR, 1 -> out-CSR.
+ * row_ptr: n+1 entries, col_idx: nnz entries, deg: n entries (may be NULL). */
+ntp_status ntp_copy_csr(const ntp_ctx* ctx, int transposed, int64_t* row_ptr,
+                        int32_t* col_idx, int32_t* deg);
+
+/* Copies D~_in^{-1/2} and D~_out^{-1/2} (fp32, n entries each) to HOST. */
+ntp_status ntp_copy_dinv(const ntp_ctx* ctx, float* dinv_in, float* dinv_out);
+
+/* ------------------------------------------------------ partition maps (a1) */
+
+typedef struct {
+    int64_t n, V_p, V_pad;
+    int32_t w, P, d_s, w_pad, elem_bytes, chunks;
+    int64_t chunk;              /* rows per chunk inside each owner block */
+} ntp_partition_info;
+
+/* Pure host computation of the maps above (no context needed). */
+ntp_status ntp_partition(int64_t n, int32_t w, int32_t P, ntp_dtype dtype, int32_t chunks,
+                         int slice_align, ntp_partition_info* out);
+
+/* --------------------------------------------------- features and layouts */
+
+/* Copies this rank's part of the HOST matrix X [n x d] (row-major, dtype) into
+ * `out` (device): VERTEX -> rows R_rank at width d (out->cols >= d), FEATURE ->
+ * all V_pad rows x columns [rank*d_s, (rank+1)*d_s); padding is zero-filled. */
+ntp_status ntp_scatter_features(ntp_ctx* ctx, const void* X_host, ntp_dtype dtype,
+                                int64_t n, int32_t d, ntp_layout layout, ntp_tensor* out);
+
+/* "split": Hv = this rank's VERTEX rows [V_p x w] (w = Hv->cols) ->
+ * Hf = this rank's FEATURE slice [V_pad x d_s] (ld == d_s).  One all-to-all.
+ * "gather": the inverse.  Pure data movement: f2v(v2f(x)) == x bitwise. */
+ntp_status ntp_layout_v2f(ntp_ctx* ctx, const ntp_tensor* Hv, ntp_tensor* Hf, ntp_stream s);
+ntp_status ntp_layout_f2v(ntp_ctx* ctx, const ntp_tensor* Hf, ntp_tensor* Hv, ntp_stream s);
+
+/* ------------------------------------------------ propagation (a4, a8) */
+
+/* K hops on one feature slice (no communication).  H, Z: [rows >= n] x cols,
+ * same dtype (fp32 or bf16 storage; fp32 accumulation).  Z must not alias H.
+ * Rows [n, Z->rows) of Z are zero-filled.  K >= 0, gamma in (0,1], alpha in [0,1).
+ * propagate_fwd uses the in-CSR (A^), propagate_bwd the out-CSR (A^T). */
+ntp_status ntp_propagate_fwd(ntp_ctx* ctx, const ntp_tensor* H, ntp_tensor* Z, int K,
+                             float gamma, float alpha, ntp_stream s);
+ntp_status ntp_propagate_bwd(ntp_ctx* ctx, const ntp_tensor* G, ntp_tensor* dH, int K,
+                             float gamma, float alpha, ntp_stream s);
+
+/* ------------------------------------------------------ one epoch (Alg. 1) */
+
+#define NTP_M_W1_AFTER_PROP 1u  /* propagate H1 (w = hid) and apply W1 after (reading R3) */
+#define NTP_M_OVERLAP       2u  /* chunked last hop with the gather on a comm stream (a12) */
+#define NTP_M_HOST_INPUTS   4u  /* X_v/labels_v/train_mask_v are HOST (pinned) pointers;
+                                   copied to the device inside the call (e2e path)       */
+
+typedef struct {
+    int32_t   d_in, hid, C, K;
+    float     gamma, alpha, lr;
+    ntp_dtype dtype;            /* propagation storage dtype (fp32 accumulation always) */
+    int32_t   chunks;           /* sub-chunks per owner block for the overlapped gather  */
+    uint32_t  flags;
+} ntp_model;
+
+enum {  /* ntp_epoch_report.ms[] phases (CUDA-event times on the library's streams) */
+    NTP_PH_MLP_FWD = 0, NTP_PH_V2F_FWD, NTP_PH_PROP_FWD, NTP_PH_F2V_FWD, NTP_PH_LOSS,
+    NTP_PH_V2F_BWD, NTP_PH_PROP_BWD, NTP_PH_F2V_BWD, NTP_PH_MLP_BWD, NTP_PH_ALLREDUCE,
+    NTP_PH_SGD, NTP_PH_TOTAL, NTP_PH_COUNT
+};
+
+typedef struct {
+    double  loss;               /* global mean train loss, before this epoch's update */
+    int64_t n_train;            /* global number of train vertices                    */
+    double  ms[NTP_PH_COUNT];
+    int64_t bytes_sent[4];      /* per layout change: v2f fwd, f2v fwd, v2f bwd, f2v bwd */
+    int64_t bytes_recv[4];
+    int64_t collectives;        /* logical collective rounds issued (4 layout + allreduce) */
+    int64_t kernel_launches;    /* libntp kernels launched in this call                 */
+    double  spmm_ms;            /* summed duration of the SpMM hop kernels              */
+    int32_t spmm_launches;
+    int32_t pad_;
+} ntp_epoch_report;
+
+/* One training epoch.  X_v [V_p x d_in] fp32 (this rank's VERTEX rows, rows
+ * >= n zero), labels_v int32 [V_p], train_mask_v uint8 [V_p] (device unless
+ * NTP_M_HOST_INPUTS).  W0 [d_in x hid], W1 [hid x C] fp32 device, replicated
+ * on every rank, updated in place by SGD.  Synchronous: returns after
+ * the epoch completed; `s` orders the call after prior work on that stream and
+ * later work after it.  rep may be NULL. */
+ntp_status ntp_train_epoch(ntp_ctx* ctx, const ntp_model* m, const ntp_tensor* X_v,
+                           const int32_t* labels_v, const uint8_t* train_mask_v,
+                           ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, ntp_stream s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NTP_H */

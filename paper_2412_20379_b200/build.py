@@ -1,0 +1,91 @@
+"""Builds libntp.so in-tree for sm_100a (nvcc) — the only compiled product artifact.
+
+Usage: python -m paper_2412_20379_b200.build [--force]
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+import sysconfig
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build_obj")
+LIB = os.path.join(HERE, "libntp.so")
+SOURCES = ["api.cu", "graph.cu", "spmm.cu", "layout.cu", "model.cu"]
+HEADERS = ["ntp_internal.cuh"]
+
+
+def _site() -> str:
+    return sysconfig.get_paths()["purelib"]
+
+
+def nvidia_dirs():
+    site = _site()
+    nccl = os.path.join(site, "nvidia", "nccl")
+    cublas = os.path.join(site, "nvidia", "cublas")
+    return nccl, cublas
+
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _flags():
+    nccl, cublas = nvidia_dirs()
+    return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+                   "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+                   "-I", os.path.join(nccl, "include"), "-I", os.path.join(cublas, "include")]
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = True) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "ntp.h")]
+    jobs = []
+    for src in SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        if force or _newer(o, [s] + hdrs):
+            jobs.append((s, o))
+
+    def compile_one(so):
+        s, o = so
+        cmd = [NVCC, "-c", s, "-o", o] + _flags()
+        if verbose:
+            print("[ntp build]", os.path.basename(s), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {s}:\n{r.stdout}\n{r.stderr}")
+        return r.stderr
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        for _ in ex.map(compile_one, jobs):
+            pass
+    objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
+    if force or jobs or _newer(LIB, objs):
+        nccl, cublas = nvidia_dirs()
+        cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH + [
+            "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+            "-L", os.path.join(cublas, "lib"), "-l:libcublas.so.12",
+            "-Xlinker", "-rpath=" + os.path.join(nccl, "lib") + ":" + os.path.join(cublas, "lib"),
+        ]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        if verbose:
+            print("[ntp build] linked", LIB, flush=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

@@ -1,0 +1,467 @@
+// api.cu — the extern "C" boundary of libntp (include/ntp.h).
+// Every entry point validates its arguments, runs inside a try/catch that maps
+// internal failures to ntp_status, and records the message in the context.
+#include <cstdarg>
+#include <cstring>
+#include <algorithm>
+#include <memory>
+
+#include "ntp_internal.cuh"
+
+namespace ntp {
+
+thread_local std::string g_last_global_error;
+
+void fail(ntp_status st, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    throw Error{st, std::string(buf)};
+}
+
+void DevBuf::ensure(size_t b) {
+    if (b <= bytes && p) return;
+    release();
+    if (b == 0) b = 16;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        bytes = 0;
+        cudaGetLastError();
+        fail(NTP_ERR_OOM, "cudaMalloc(%zu) failed: %s", b, cudaGetErrorString(e));
+    }
+    bytes = b;
+}
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+int32_t slice_width(int32_t w, int32_t P, ntp_dtype dt, int align) {
+    const int32_t q = align / (int32_t)esize(dt);
+    const int32_t base = (int32_t)cdiv(w, P);
+    return (int32_t)(cdiv(base, q) * q);
+}
+
+void count_launch(ntp_ctx* c, int k) { c->launches += k; }
+
+static void check_tensor(const ntp_tensor* t, const char* name, bool need_vec) {
+    NTP_CHECK(t != nullptr, NTP_ERR_ARG, "%s is NULL", name);
+    NTP_CHECK(t->data != nullptr || t->rows == 0, NTP_ERR_ARG, "%s->data is NULL", name);
+    NTP_CHECK(t->dtype == NTP_F32 || t->dtype == NTP_BF16, NTP_ERR_SHAPE, "%s: bad dtype %d", name, (int)t->dtype);
+    NTP_CHECK(t->rows >= 0 && t->cols >= 0 && t->ld >= t->cols, NTP_ERR_SHAPE,
+              "%s: bad shape rows=%lld cols=%d ld=%lld", name, (long long)t->rows, t->cols, (long long)t->ld);
+    if (need_vec) {
+        const size_t es = esize(t->dtype);
+        NTP_CHECK(((uintptr_t)t->data % 16) == 0, NTP_ERR_SHAPE, "%s: data not 16-byte aligned", name);
+        NTP_CHECK((t->ld * es) % 16 == 0 && (t->cols * es) % 16 == 0, NTP_ERR_SHAPE,
+                  "%s: cols*elem (%zu) and ld*elem (%zu) must be multiples of 16 bytes", name, t->cols * es,
+                  (size_t)t->ld * es);
+    }
+}
+
+static void need_graph(const ntp_ctx* c) {
+    NTP_CHECK(c->g.loaded, NTP_ERR_STATE, "no graph loaded");
+}
+
+}  // namespace ntp
+
+using namespace ntp;
+
+#define NTP_API_BEGIN(ctx)                                                                  \
+    if (!(ctx)) return NTP_ERR_ARG;                                                         \
+    try {
+#define NTP_API_END(ctx)                                                                    \
+    }                                                                                       \
+    catch (const ntp::Error& e) {                                                           \
+        (ctx)->err = e.msg;                                                                 \
+        return e.st;                                                                        \
+    }                                                                                       \
+    catch (const std::exception& e) {                                                       \
+        (ctx)->err = e.what();                                                              \
+        return NTP_ERR_CUDA;                                                                \
+    }                                                                                       \
+    catch (...) {                                                                           \
+        (ctx)->err = "unknown internal error";                                              \
+        return NTP_ERR_CUDA;                                                                \
+    }                                                                                       \
+    (ctx)->err.clear();                                                                     \
+    return NTP_OK;
+
+extern "C" {
+
+int ntp_abi_version(void) { return NTP_ABI_VERSION; }
+
+const char* ntp_status_string(ntp_status s) {
+    switch (s) {
+        case NTP_OK: return "NTP_OK";
+        case NTP_ERR_ARG: return "NTP_ERR_ARG";
+        case NTP_ERR_SHAPE: return "NTP_ERR_SHAPE";
+        case NTP_ERR_CONFIG: return "NTP_ERR_CONFIG";
+        case NTP_ERR_GRAPH: return "NTP_ERR_GRAPH";
+        case NTP_ERR_STATE: return "NTP_ERR_STATE";
+        case NTP_ERR_OOM: return "NTP_ERR_OOM";
+        case NTP_ERR_CUDA: return "NTP_ERR_CUDA";
+        case NTP_ERR_NCCL: return "NTP_ERR_NCCL";
+        case NTP_ERR_TIMEOUT: return "NTP_ERR_TIMEOUT";
+    }
+    return "NTP_ERR_UNKNOWN";
+}
+
+const char* ntp_last_error(const ntp_ctx* ctx) {
+    if (!ctx) return g_last_global_error.c_str();
+    return ctx->err.c_str();
+}
+
+ntp_status ntp_get_unique_id(uint8_t id[128]) {
+    if (!id) return NTP_ERR_ARG;
+    ncclUniqueId u;
+    ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) {
+        g_last_global_error = ncclGetErrorString(r);
+        return NTP_ERR_NCCL;
+    }
+    static_assert(sizeof(ncclUniqueId) == 128, "unexpected ncclUniqueId size");
+    memcpy(id, &u, 128);
+    return NTP_OK;
+}
+
+ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint8_t id[128], int slice_align) {
+    if (!out) return NTP_ERR_ARG;
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world || (world > 1 && !id) || (slice_align != 16 && slice_align != 32)) {
+        g_last_global_error = "ntp_create: bad rank/world/id/slice_align";
+        return NTP_ERR_ARG;
+    }
+    std::unique_ptr<ntp_ctx> c(new ntp_ctx());
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    c->slice_align = slice_align;
+    try {
+        NTP_CUDA(cudaSetDevice(device));
+        NTP_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+        NTP_CUDA(cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
+        for (auto& e : c->ev) NTP_CUDA(cudaEventCreate(&e));
+        for (auto& e : c->hop_ev) NTP_CUDA(cudaEventCreate(&e));
+        NTP_BLAS(cublasCreate(&c->blas));
+        NTP_BLAS(cublasSetMathMode(c->blas, CUBLAS_PEDANTIC_MATH));   // fp32 FMA, no TF32 (R11)
+        if (world > 1) {
+            ncclUniqueId u;
+            memcpy(&u, id, 128);
+            NTP_NCCL(ncclCommInitRank(&c->comm, world, u, rank));
+        }
+    } catch (const ntp::Error& e) {
+        g_last_global_error = e.msg;
+        ntp_destroy(c.release());
+        return e.st;
+    }
+    *out = c.release();
+    return NTP_OK;
+}
+
+void ntp_destroy(ntp_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->s_comp) cudaStreamSynchronize(c->s_comp);
+    if (c->s_comm) cudaStreamSynchronize(c->s_comm);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->blas) cublasDestroy(c->blas);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->hop_ev)
+        if (e) cudaEventDestroy(e);
+    if (c->s_comp) cudaStreamDestroy(c->s_comp);
+    if (c->s_comm) cudaStreamDestroy(c->s_comm);
+    delete c;   // DevBufs free themselves
+}
+
+// ------------------------------------------------------------------ graph
+ntp_status ntp_load_graph(ntp_ctx* c, const int64_t* row_ptr, const int32_t* col_idx, int64_t n, int64_t nnz,
+                          uint32_t flags) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(row_ptr && (col_idx || nnz == 0), NTP_ERR_ARG, "null CSR arrays");
+    NTP_CHECK(n >= 0 && n < (int64_t(1) << 31) && nnz >= 0 && nnz < (int64_t(1) << 31), NTP_ERR_CONFIG,
+              "n and nnz must be < 2^31 (n=%lld nnz=%lld)", (long long)n, (long long)nnz);
+    if (flags & NTP_G_VALIDATE) {
+        NTP_CHECK(row_ptr[0] == 0 && row_ptr[n] == nnz, NTP_ERR_GRAPH, "row_ptr[0] != 0 or row_ptr[n] != nnz");
+        for (int64_t v = 0; v < n; ++v) {
+            NTP_CHECK(row_ptr[v + 1] >= row_ptr[v], NTP_ERR_GRAPH, "row_ptr decreases at row %lld", (long long)v);
+            for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
+                NTP_CHECK(col_idx[e] >= 0 && col_idx[e] < n, NTP_ERR_GRAPH, "col out of range at %lld", (long long)e);
+                NTP_CHECK(e == row_ptr[v] || col_idx[e] > col_idx[e - 1], NTP_ERR_GRAPH,
+                          "row %lld not strictly ascending", (long long)v);
+            }
+        }
+    }
+    NTP_CUDA(cudaSetDevice(c->device));
+    DevBuf drp, dcol, keys;
+    drp.ensure((n + 1) * sizeof(int64_t));
+    dcol.ensure(std::max<int64_t>(nnz, 1) * sizeof(int32_t));
+    keys.ensure(std::max<int64_t>(nnz, 1) * sizeof(uint64_t));
+    NTP_CUDA(cudaMemcpyAsync(drp.p, row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->s_comp));
+    if (nnz) NTP_CUDA(cudaMemcpyAsync(dcol.p, col_idx, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, c->s_comp));
+    csr_to_keys(c, drp.as<int64_t>(), dcol.as<int32_t>(), n, keys.as<uint64_t>(), c->s_comp);
+    drp.release();
+    dcol.release();
+    build_graph_from_keys(c, keys.as<uint64_t>(), nnz, n, (flags & NTP_G_SYMMETRIC) != 0, keys);
+    NTP_API_END(c)
+}
+
+ntp_status ntp_build_graph(ntp_ctx* c, const int64_t* src, const int64_t* dst, int64_t m, int64_t n, uint32_t flags) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK((src && dst) || m == 0, NTP_ERR_ARG, "null arc arrays");
+    NTP_CHECK(m >= 0 && n >= 0 && n < (int64_t(1) << 31), NTP_ERR_CONFIG, "bad m/n");
+    NTP_CUDA(cudaSetDevice(c->device));
+    const bool sym = (flags & NTP_G_SYMMETRIC) != 0;
+    const int64_t mk = sym ? 2 * m : m;
+    DevBuf ds, dd, keys;
+    ds.ensure(std::max<int64_t>(m, 1) * sizeof(int64_t));
+    dd.ensure(std::max<int64_t>(m, 1) * sizeof(int64_t));
+    keys.ensure(std::max<int64_t>(mk, 1) * sizeof(uint64_t));
+    if (m) {
+        NTP_CUDA(cudaMemcpyAsync(ds.p, src, m * sizeof(int64_t), cudaMemcpyHostToDevice, c->s_comp));
+        NTP_CUDA(cudaMemcpyAsync(dd.p, dst, m * sizeof(int64_t), cudaMemcpyHostToDevice, c->s_comp));
+        arcs_to_keys(c, ds.as<int64_t>(), dd.as<int64_t>(), m, n, sym, keys.as<uint64_t>(), c->s_comp);
+    }
+    NTP_CUDA(cudaStreamSynchronize(c->s_comp));
+    ds.release();
+    dd.release();
+    build_graph_from_keys(c, keys.as<uint64_t>(), mk, n, sym, keys);
+    NTP_API_END(c)
+}
+
+ntp_status ntp_generate_rmat(ntp_ctx* c, int64_t n, int scale, int64_t m_raw, const uint32_t thr[3], uint64_t seed,
+                             uint32_t flags) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(thr != nullptr, NTP_ERR_ARG, "thresholds NULL");
+    NTP_CHECK(scale >= 1 && scale <= 31 && n >= 0 && n <= (int64_t(1) << scale) && m_raw >= 0, NTP_ERR_CONFIG,
+              "bad scale/n/m_raw");
+    NTP_CUDA(cudaSetDevice(c->device));
+    const bool sym = (flags & NTP_G_SYMMETRIC) != 0;
+    const int64_t mk = sym ? 2 * m_raw : m_raw;
+    DevBuf keys;
+    keys.ensure(std::max<int64_t>(mk, 1) * sizeof(uint64_t));
+    if (m_raw) rmat_keys(c, scale, thr, seed, 0, m_raw, n, sym, keys.as<uint64_t>(), c->s_comp);
+    build_graph_from_keys(c, keys.as<uint64_t>(), mk, n, sym, keys);
+    NTP_API_END(c)
+}
+
+ntp_status ntp_rmat_arcs(ntp_ctx* c, int scale, const uint32_t thr[3], uint64_t seed, int64_t i0, int64_t count,
+                         int64_t* src_host, int64_t* dst_host) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(thr && src_host && dst_host && count >= 0 && i0 >= 0, NTP_ERR_ARG, "bad arguments");
+    NTP_CHECK(scale >= 1 && scale <= 31, NTP_ERR_CONFIG, "bad scale");
+    NTP_CUDA(cudaSetDevice(c->device));
+    if (count) {
+        DevBuf s, d;
+        s.ensure(count * sizeof(int64_t));
+        d.ensure(count * sizeof(int64_t));
+        rmat_raw(c, scale, thr, seed, i0, count, s.as<int64_t>(), d.as<int64_t>(), c->s_comp);
+        NTP_CUDA(cudaMemcpyAsync(src_host, s.p, count * sizeof(int64_t), cudaMemcpyDeviceToHost, c->s_comp));
+        NTP_CUDA(cudaMemcpyAsync(dst_host, d.p, count * sizeof(int64_t), cudaMemcpyDeviceToHost, c->s_comp));
+        NTP_CUDA(cudaStreamSynchronize(c->s_comp));
+    }
+    NTP_API_END(c)
+}
+
+ntp_status ntp_graph_info(const ntp_ctx* cc, int64_t* n, int64_t* nnz, int* symmetric) {
+    ntp_ctx* c = const_cast<ntp_ctx*>(cc);
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    if (n) *n = c->g.n;
+    if (nnz) *nnz = c->g.nnz;
+    if (symmetric) *symmetric = c->g.symmetric ? 1 : 0;
+    NTP_API_END(c)
+}
+
+ntp_status ntp_copy_csr(const ntp_ctx* cc, int transposed, int64_t* row_ptr, int32_t* col_idx, int32_t* deg) {
+    ntp_ctx* c = const_cast<ntp_ctx*>(cc);
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    NTP_CUDA(cudaSetDevice(c->device));
+    const Csr& csr = transposed ? c->g.bwd() : c->g.fwd();
+    const int64_t n = c->g.n, nnz = c->g.nnz;
+    std::vector<int32_t> rp(n + 1);
+    NTP_CUDA(cudaMemcpy(rp.data(), csr.row_ptr.p, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (row_ptr)
+        for (int64_t i = 0; i <= n; ++i) row_ptr[i] = rp[i];
+    if (deg)
+        for (int64_t i = 0; i < n; ++i) deg[i] = rp[i + 1] - rp[i];
+    if (col_idx && nnz) NTP_CUDA(cudaMemcpy(col_idx, csr.col.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    NTP_API_END(c)
+}
+
+ntp_status ntp_copy_dinv(const ntp_ctx* cc, float* dinv_in, float* dinv_out) {
+    ntp_ctx* c = const_cast<ntp_ctx*>(cc);
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    NTP_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->g.n;
+    if (dinv_in && n) NTP_CUDA(cudaMemcpy(dinv_in, c->g.dinv_in_p(), n * sizeof(float), cudaMemcpyDeviceToHost));
+    if (dinv_out && n) NTP_CUDA(cudaMemcpy(dinv_out, c->g.dinv_out_p(), n * sizeof(float), cudaMemcpyDeviceToHost));
+    NTP_API_END(c)
+}
+
+// ------------------------------------------------------------------ partition maps
+ntp_status ntp_partition(int64_t n, int32_t w, int32_t P, ntp_dtype dtype, int32_t chunks, int slice_align,
+                         ntp_partition_info* out) {
+    if (!out || n < 0 || w < 0 || P < 1 || chunks < 1 || (dtype != NTP_F32 && dtype != NTP_BF16) ||
+        (slice_align != 16 && slice_align != 32))
+        return NTP_ERR_ARG;
+    out->n = n;
+    out->w = w;
+    out->P = P;
+    out->V_p = n > 0 ? cdiv(n, P) : 0;
+    out->V_pad = out->V_p * P;
+    out->elem_bytes = (int32_t)esize(dtype);
+    out->d_s = slice_width(w, P, dtype, slice_align);
+    out->w_pad = out->d_s * P;
+    out->chunks = chunks;
+    out->chunk = out->V_p > 0 ? cdiv(out->V_p, chunks) : 0;
+    return NTP_OK;
+}
+
+// ------------------------------------------------------------------ features / layouts
+ntp_status ntp_scatter_features(ntp_ctx* c, const void* X_host, ntp_dtype dtype, int64_t n, int32_t d,
+                                ntp_layout layout, ntp_tensor* out) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(X_host != nullptr, NTP_ERR_ARG, "X_host NULL");
+    check_tensor(out, "out", false);
+    NTP_CHECK(out->dtype == dtype, NTP_ERR_SHAPE, "dtype mismatch");
+    NTP_CUDA(cudaSetDevice(c->device));
+    const size_t es = esize(dtype);
+    const int64_t V_p = cdiv(n, c->world);
+    NTP_CUDA(cudaMemset2DAsync(out->data, out->ld * es, 0, out->cols * es, out->rows, c->s_comp));
+    if (layout == NTP_LAYOUT_VERTEX) {
+        NTP_CHECK(out->rows >= V_p && out->cols >= d, NTP_ERR_SHAPE, "vertex tensor must be >= [V_p x d]");
+        const int64_t r0 = (int64_t)c->rank * V_p;
+        const int64_t nr = std::max<int64_t>(0, std::min<int64_t>(V_p, n - r0));
+        if (nr > 0 && d > 0)
+            NTP_CUDA(cudaMemcpy2DAsync(out->data, out->ld * es, static_cast<const char*>(X_host) + r0 * d * es, d * es,
+                                       d * es, nr, cudaMemcpyHostToDevice, c->s_comp));
+    } else {
+        const int32_t d_s = slice_width(d, c->world, dtype, c->slice_align);
+        NTP_CHECK(out->rows >= (int64_t)c->world * V_p && out->cols >= d_s, NTP_ERR_SHAPE,
+                  "feature tensor must be >= [V_pad x d_s] = [%lld x %d]", (long long)(c->world * V_p), d_s);
+        const int32_t c0 = c->rank * d_s;
+        const int32_t nc = std::max(0, std::min(d_s, d - c0));
+        if (nc > 0 && n > 0)
+            NTP_CUDA(cudaMemcpy2DAsync(out->data, out->ld * es, static_cast<const char*>(X_host) + c0 * es, d * es,
+                                       nc * es, n, cudaMemcpyHostToDevice, c->s_comp));
+    }
+    NTP_CUDA(cudaStreamSynchronize(c->s_comp));
+    NTP_API_END(c)
+}
+
+ntp_status ntp_layout_v2f(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Hf, ntp_stream st) {
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    check_tensor(Hv, "Hv", false);
+    check_tensor(Hf, "Hf", true);
+    NTP_CHECK(Hv->dtype == Hf->dtype, NTP_ERR_SHAPE, "dtype mismatch");
+    const int64_t V_p = cdiv(c->g.n, c->world);
+    const int32_t d_s = slice_width(Hv->cols, c->world, Hv->dtype, c->slice_align);
+    NTP_CHECK(Hv->rows >= V_p, NTP_ERR_SHAPE, "Hv rows %lld < V_p %lld", (long long)Hv->rows, (long long)V_p);
+    NTP_CHECK(Hf->rows == (int64_t)c->world * V_p && Hf->cols == d_s && Hf->ld == d_s, NTP_ERR_SHAPE,
+              "Hf must be dense [V_pad x d_s] = [%lld x %d]", (long long)(c->world * V_p), d_s);
+    cudaStream_t s = (cudaStream_t)st;
+    const size_t es = esize(Hv->dtype);
+    c->send.ensure((size_t)c->world * V_p * d_s * es + 16);
+    pack_v2f(c, Hv->data, Hv->ld, Hv->cols, c->send.p, V_p, d_s, c->world, nullptr, (int64_t)c->rank * V_p, c->g.n,
+             Hv->dtype, Hf->dtype, s);
+    alltoall_blocks(c, c->send.p, Hf->data, V_p * d_s, Hf->dtype, s);
+    NTP_API_END(c)
+}
+
+ntp_status ntp_layout_f2v(ntp_ctx* c, const ntp_tensor* Hf, ntp_tensor* Hv, ntp_stream st) {
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    check_tensor(Hf, "Hf", true);
+    check_tensor(Hv, "Hv", false);
+    NTP_CHECK(Hv->dtype == Hf->dtype, NTP_ERR_SHAPE, "dtype mismatch");
+    const int64_t V_p = cdiv(c->g.n, c->world);
+    const int32_t d_s = slice_width(Hv->cols, c->world, Hv->dtype, c->slice_align);
+    NTP_CHECK(Hv->rows >= V_p, NTP_ERR_SHAPE, "Hv rows < V_p");
+    NTP_CHECK(Hf->rows == (int64_t)c->world * V_p && Hf->cols == d_s && Hf->ld == d_s, NTP_ERR_SHAPE,
+              "Hf must be dense [V_pad x d_s] = [%lld x %d]", (long long)(c->world * V_p), d_s);
+    cudaStream_t s = (cudaStream_t)st;
+    const size_t es = esize(Hv->dtype);
+    c->recv.ensure((size_t)c->world * V_p * d_s * es + 16);
+    alltoall_blocks(c, Hf->data, c->recv.p, V_p * d_s, Hf->dtype, s);
+    unpack_f2v(c, c->recv.p, V_p, d_s, c->world, Hv->data, Hv->ld, Hv->cols, Hf->dtype, Hv->dtype, s);
+    NTP_API_END(c)
+}
+
+// ------------------------------------------------------------------ propagation
+static ntp_status do_propagate(ntp_ctx* c, const ntp_tensor* H, ntp_tensor* Z, int K, float gamma, float alpha,
+                               ntp_stream st, bool transposed) {
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    check_tensor(H, "H", true);
+    check_tensor(Z, "Z", true);
+    NTP_CHECK(H->dtype == Z->dtype && H->cols == Z->cols, NTP_ERR_SHAPE, "H/Z dtype or cols mismatch");
+    NTP_CHECK(H->rows >= c->g.n && Z->rows >= c->g.n, NTP_ERR_SHAPE, "tensors need >= n rows");
+    NTP_CHECK(H->data != Z->data, NTP_ERR_ARG, "Z must not alias H");
+    NTP_CHECK(K >= 0, NTP_ERR_ARG, "K < 0");
+    NTP_CHECK(gamma > 0.f && gamma <= 1.f, NTP_ERR_ARG, "gamma must be in (0, 1]");
+    NTP_CHECK(alpha >= 0.f && alpha < 1.f, NTP_ERR_ARG, "alpha must be in [0, 1)");
+    NTP_CUDA(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)st;
+    PropArgs a{};
+    a.H = H->data;
+    a.Z = Z->data;
+    a.ld_h = H->ld;
+    a.ld_z = Z->ld;
+    a.cols = H->cols;
+    a.dtype = H->dtype;
+    a.K = K;
+    a.gamma = gamma;
+    a.alpha = alpha;
+    a.transposed = transposed;
+    const size_t es = esize(H->dtype);
+    if (Z->rows > c->g.n)
+        NTP_CUDA(cudaMemset2DAsync(static_cast<char*>(Z->data) + c->g.n * Z->ld * es, Z->ld * es, 0, Z->cols * es,
+                                   Z->rows - c->g.n, s));
+    if (H->cols > 0) propagate(c, a, s);
+    NTP_API_END(c)
+}
+
+ntp_status ntp_propagate_fwd(ntp_ctx* c, const ntp_tensor* H, ntp_tensor* Z, int K, float gamma, float alpha,
+                             ntp_stream s) {
+    return do_propagate(c, H, Z, K, gamma, alpha, s, false);
+}
+
+ntp_status ntp_propagate_bwd(ntp_ctx* c, const ntp_tensor* G, ntp_tensor* dH, int K, float gamma, float alpha,
+                             ntp_stream s) {
+    return do_propagate(c, G, dH, K, gamma, alpha, s, true);
+}
+
+// ------------------------------------------------------------------ epoch
+ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                           const uint8_t* train_mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep,
+                           ntp_stream st) {
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    NTP_CHECK(m && X_v && labels_v && train_mask_v && W0 && W1, NTP_ERR_ARG, "null argument");
+    NTP_CHECK(m->d_in > 0 && m->hid > 0 && m->C > 0 && m->K >= 1, NTP_ERR_ARG, "bad model dims / K");
+    NTP_CHECK(m->gamma > 0.f && m->gamma <= 1.f && m->alpha >= 0.f && m->alpha < 1.f, NTP_ERR_ARG,
+              "gamma in (0,1], alpha in [0,1)");
+    NTP_CHECK(m->dtype == NTP_F32 || m->dtype == NTP_BF16, NTP_ERR_ARG, "bad dtype");
+    NTP_CHECK(X_v->dtype == NTP_F32 && W0->dtype == NTP_F32 && W1->dtype == NTP_F32, NTP_ERR_SHAPE,
+              "X_v, W0, W1 must be fp32");
+    const int64_t V_p = cdiv(c->g.n, c->world);
+    NTP_CHECK(X_v->rows >= V_p && X_v->cols == m->d_in && X_v->ld >= m->d_in, NTP_ERR_SHAPE, "X_v must be [V_p x d_in]");
+    NTP_CHECK(W0->rows == m->d_in && W0->cols == m->hid && W0->ld == m->hid, NTP_ERR_SHAPE,
+              "W0 must be dense [d_in x hid]");
+    NTP_CHECK(W1->rows == m->hid && W1->cols == m->C && W1->ld == m->C, NTP_ERR_SHAPE, "W1 must be dense [hid x C]");
+    NTP_CUDA(cudaSetDevice(c->device));
+    train_epoch(c, m, X_v, labels_v, train_mask_v, W0, W1, rep, (cudaStream_t)st);
+    NTP_API_END(c)
+}
+
+}  // extern "C"

@@ -1,0 +1,416 @@
+// model.cu — one decoupled-TP training epoch (Alg. 1).
+//
+//   a2  H1 = ReLU(X_v W0);  L^ = H1 W1 (unless W1 is applied after propagation, R3)
+//   a3  split L^ (pack with column-side pre-scale D~_out^{-1/2}) -> S^0 feature slice
+//   a4  K forward hops (spmm.cu)
+//   a5  gather Z^K -> logits rows (read in place by the loss kernel, or unpacked + W1)
+//   a6  softmax-xent on train rows; dlogits = softmax - onehot (1/N_train folded into SGD)
+//   a7  split dlogits (pre-scale D~_in^{-1/2}: the backward's column side)
+//   a8  K backward hops over the out-CSR
+//   a9  gather -> dL^ rows
+//   a10 dW1 = H1^T dL^, dH1 = (dL^ W1^T) .* [H1 > 0], dW0 = X^T dH1
+//   a11 allreduce(dW0 | dW1) + allreduce(loss_sum, n_train) ; W -= lr/N_train * dW
+// Dense GEMMs: cuBLAS SGEMM (fp32 FMA, no TF32: parity reading R11).
+#include <algorithm>
+#include <cmath>
+
+#include "ntp_internal.cuh"
+
+namespace ntp {
+
+namespace {
+
+__global__ void relu_kernel(float* __restrict__ x, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = fmaxf(x[i], 0.f);
+}
+
+// dH1 = dH1 .* [H1 > 0]  (ReLU'(0) = 0, reading R12)
+__global__ void relu_grad_kernel(float* __restrict__ g, const float* __restrict__ h, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        g[i] = h[i] > 0.f ? g[i] : 0.f;
+}
+
+template <typename T> __device__ __forceinline__ float ldf(const T* p);
+template <> __device__ __forceinline__ float ldf<float>(const float* p) { return *p; }
+template <> __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+template <typename T> __device__ __forceinline__ void stf(T* p, float v);
+template <> __device__ __forceinline__ void stf<float>(float* p, float v) { *p = v; }
+template <> __device__ __forceinline__ void stf<__nv_bfloat16>(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+// One warp per vertex row.  Input logits: blocked [P][V_p][d_s] (TIn = storage
+// dtype) when `blocked`, else plain fp32 [V_p x C].  Output gradient rows: blocked
+// with per-row scale `gscale` (split pre-scale) when `out_blocked`, else plain fp32.
+// Per-block loss partials (fp64) -> part[blockIdx.x]; train counts -> cnt[blockIdx.x].
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict__ in, int in_blocked, int64_t V_p,
+                                                           int32_t d_s, int32_t C, const int32_t* __restrict__ y,
+                                                           const uint8_t* __restrict__ mask, int64_t row0, int64_t n,
+                                                           TOut* __restrict__ out, int out_blocked,
+                                                           const float* __restrict__ gscale, double* __restrict__ part,
+                                                           int64_t* __restrict__ cnt) {
+    __shared__ double s_loss[8];
+    __shared__ int64_t s_cnt[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t v = (int64_t)blockIdx.x * 8 + warp;
+    double my_loss = 0.0;
+    int64_t my_cnt = 0;
+    if (v < V_p) {
+        const int64_t gr = row0 + v;
+        const bool train = gr < n && mask[v] != 0;
+        auto in_at = [&](int col) -> float {
+            if (in_blocked) return ldf<TIn>(in + ((int64_t)(col / d_s) * V_p + v) * d_s + col % d_s);
+            return ldf<TIn>(in + v * (int64_t)C + col);
+        };
+        float mx = -INFINITY;
+        for (int col = lane; col < C; col += 32) mx = fmaxf(mx, in_at(col));
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float se = 0.f;
+        for (int col = lane; col < C; col += 32) se += expf(in_at(col) - mx);
+        for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        const int yv = train ? y[v] : -1;
+        if (train && lane == 0) {
+            const float ly = in_at(yv);
+            my_loss = (double)(logf(se) + mx - ly);
+            my_cnt = 1;
+        }
+        const float inv = 1.f / se;
+        const float sc = (gscale && gr < n) ? gscale[gr] : 1.f;
+        for (int col = lane; col < C; col += 32) {
+            float gval = 0.f;
+            if (train) gval = (expf(in_at(col) - mx) * inv - (col == yv ? 1.f : 0.f)) * sc;
+            if (out_blocked) stf<TOut>(out + ((int64_t)(col / d_s) * V_p + v) * d_s + col % d_s, gval);
+            else stf<TOut>(out + v * (int64_t)C + col, gval);
+        }
+    }
+    if (lane == 0) {
+        s_loss[warp] = my_loss;
+        s_cnt[warp] = my_cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double l = 0.0;
+        int64_t k = 0;
+        for (int i = 0; i < 8; ++i) {  // fixed order
+            l += s_loss[i];
+            k += s_cnt[i];
+        }
+        part[blockIdx.x] = l;
+        cnt[blockIdx.x] = k;
+    }
+}
+
+// Zero the padded gradient columns [C, P*d_s) of blocked output (left untouched by the loss kernel).
+template <typename T>
+__global__ void zero_pad_cols_kernel(T* __restrict__ buf, int64_t V_p, int32_t d_s, int32_t P, int32_t C) {
+    const int32_t pad = P * d_s - C;
+    const int64_t total = V_p * pad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / pad;
+        const int32_t col = C + (int32_t)(i % pad);
+        stf<T>(buf + ((int64_t)(col / d_s) * V_p + v) * d_s + col % d_s, 0.f);
+    }
+}
+
+// Fixed-order sum of block partials -> scal[0] = loss_sum, scal[1] = n_train (as double).
+__global__ void reduce_partials_kernel(const double* __restrict__ part, const int64_t* __restrict__ cnt, int64_t nb,
+                                       double* __restrict__ scal) {
+    __shared__ double sl[256];
+    __shared__ int64_t sk[256];
+    double l = 0.0;
+    int64_t k = 0;
+    for (int64_t i = threadIdx.x; i < nb; i += 256) {
+        l += part[i];
+        k += cnt[i];
+    }
+    sl[threadIdx.x] = l;
+    sk[threadIdx.x] = k;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            sl[threadIdx.x] += sl[threadIdx.x + o];
+            sk[threadIdx.x] += sk[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        scal[0] = sl[0];
+        scal[1] = (double)sk[0];
+    }
+}
+
+__global__ void sgd_kernel(float* __restrict__ W0, int64_t n0, float* __restrict__ W1, int64_t n1,
+                           const float* __restrict__ dW, const double* __restrict__ scal, float lr) {
+    const double N = scal[1] > 0.0 ? scal[1] : 1.0;
+    const float step = (float)((double)lr / N);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n0 + n1; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n0) W0[i] -= step * dW[i];
+        else W1[i - n0] -= step * dW[i];
+    }
+}
+
+int eblocks(int64_t total) { return (int)std::min<int64_t>(std::max<int64_t>(cdiv(total, 256), 1), 148 * 16); }
+
+// C[M x N] = op(A) op(B), all row-major fp32 (column-major cuBLAS on the transposes).
+void gemm_rm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+             const float* B, int64_t ldb, float* C, int64_t ldc, float beta = 0.f) {
+    if (M == 0 || N == 0) return;
+    const float one = 1.f;
+    NTP_BLAS(cublasSgemm(c->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)N, (int)M,
+                         (int)K, &one, B, (int)ldb, A, (int)lda, &beta, C, (int)ldc));
+}
+
+}  // namespace
+
+struct EpochBuffers {
+    int64_t V_p, V_pad;
+    int32_t P, w, d_s;
+};
+
+void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                 const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user) {
+    const Graph& g = c->g;
+    cudaStream_t s = c->s_comp;
+    const int64_t launches0 = c->launches;
+    const int32_t P = c->world;
+    const int64_t n = g.n;
+    const int64_t V_p = cdiv(n, P);
+    const int64_t row0 = (int64_t)c->rank * V_p;
+    const bool after = (m->flags & NTP_M_W1_AFTER_PROP) != 0;
+    const int32_t w = after ? m->hid : m->C;
+    const int32_t d_s = slice_width(w, P, m->dtype, c->slice_align);
+    const int64_t V_pad = (int64_t)P * V_p;
+    const ntp_dtype dt = m->dtype;
+    const size_t es = esize(dt);
+    const int64_t feat_elems = V_pad * d_s;
+
+    // ---- order after the caller's stream
+    NTP_CUDA(cudaEventRecord(c->ev[40], user ? user : (cudaStream_t)0));
+    NTP_CUDA(cudaStreamWaitEvent(s, c->ev[40], 0));
+
+    // ---- inputs (e2e: copy host inputs in)
+    const float* X = static_cast<const float*>(X_v->data);
+    const int64_t ld_x = X_v->ld;
+    const int32_t* lab = labels_v;
+    const uint8_t* msk = mask_v;
+    if (m->flags & NTP_M_HOST_INPUTS) {
+        c->m_Xs.ensure((size_t)V_p * m->d_in * sizeof(float));
+        c->m_lab.ensure((size_t)V_p * sizeof(int32_t));
+        c->m_mask.ensure((size_t)V_p);
+        NTP_CUDA(cudaMemcpy2DAsync(c->m_Xs.p, m->d_in * sizeof(float), X_v->data, ld_x * sizeof(float),
+                                   m->d_in * sizeof(float), V_p, cudaMemcpyHostToDevice, s));
+        NTP_CUDA(cudaMemcpyAsync(c->m_lab.p, labels_v, V_p * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        NTP_CUDA(cudaMemcpyAsync(c->m_mask.p, mask_v, V_p, cudaMemcpyHostToDevice, s));
+        X = c->m_Xs.as<float>();
+        lab = c->m_lab.as<int32_t>();
+        msk = c->m_mask.as<uint8_t>();
+    }
+    const int64_t ldx = (m->flags & NTP_M_HOST_INPUTS) ? m->d_in : ld_x;
+    float* W0p = static_cast<float*>(W0->data);
+    float* W1p = static_cast<float*>(W1->data);
+
+    // ---- scratch
+    c->m_H1.ensure((size_t)V_p * m->hid * sizeof(float));
+    c->m_L.ensure((size_t)V_p * std::max(m->C, m->hid) * sizeof(float));
+    c->m_dL.ensure((size_t)V_p * std::max(m->C, m->hid) * sizeof(float));
+    c->m_dH1.ensure((size_t)V_p * m->hid * sizeof(float));
+    const int64_t n_w = (int64_t)m->d_in * m->hid + (int64_t)m->hid * m->C;
+    c->m_dW.ensure((size_t)n_w * sizeof(float));
+    c->m_scal.ensure(4 * sizeof(double));
+    c->send.ensure((size_t)feat_elems * es + 16);
+    c->recv.ensure((size_t)feat_elems * es + 16);
+    c->xfer.ensure((size_t)feat_elems * es + 16);     // propagation output (feature slice)
+    const int64_t loss_blocks = cdiv(V_p, 8);
+    c->m_part.ensure((size_t)loss_blocks * (sizeof(double) + sizeof(int64_t)) + 16);
+    double* part = c->m_part.as<double>();
+    int64_t* cnt = reinterpret_cast<int64_t*>(part + loss_blocks);
+    float* H1 = c->m_H1.as<float>();
+    float* L = c->m_L.as<float>();
+    float* dL = c->m_dL.as<float>();
+    float* dH1 = c->m_dH1.as<float>();
+    float* dW0 = c->m_dW.as<float>();
+    float* dW1 = dW0 + (int64_t)m->d_in * m->hid;
+    double* scal = c->m_scal.as<double>();
+    NTP_BLAS(cublasSetStream(c->blas, s));
+
+    cudaEvent_t* E = c->ev;
+    int ei = 0;
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E0 start
+
+    // a2: MLP forward
+    gemm_rm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0p, m->hid, H1, m->hid);
+    relu_kernel<<<eblocks(V_p * m->hid), 256, 0, s>>>(H1, V_p * m->hid);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    const float* prop_src = H1;             // rows propagated (w columns)
+    if (!after) {
+        gemm_rm(c, false, false, V_p, m->C, m->hid, H1, m->hid, W1p, m->C, L, m->C);
+        prop_src = L;
+    }
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E1 mlp_fwd done
+
+    // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
+    pack_v2f(c, prop_src, w, w, c->send.p, V_p, d_s, P, g.dinv_out_p(), row0, n, NTP_F32, dt, s);
+    alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E2 v2f done
+
+    // a4: K forward hops: S^0 = recv (pre-scaled), output Z^K -> xfer
+    c->hop_ev_used = 0;
+    {
+        PropArgs a{};
+        a.H = c->recv.p;
+        a.Z = c->xfer.p;
+        a.ld_h = d_s;
+        a.ld_z = d_s;
+        a.cols = d_s;
+        a.dtype = dt;
+        a.K = m->K;
+        a.gamma = m->gamma;
+        a.alpha = m->alpha;
+        a.transposed = false;
+        if (m->K == 0) {
+            // Z = H: undo the pre-scale via a plain gather of the unscaled rows
+            pack_v2f(c, prop_src, w, w, c->send.p, V_p, d_s, P, nullptr, row0, n, NTP_F32, dt, s);
+            alltoall_blocks(c, c->send.p, c->xfer.p, V_p * d_s, dt, s);
+        } else {
+            propagate(c, a, s, rep != nullptr, true);
+        }
+    }
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E3 prop fwd done
+
+    // a5: gather -> recv holds [P][V_p][d_s] logits (or Z rows)
+    alltoall_blocks(c, c->xfer.p, c->recv.p, V_p * d_s, dt, s);
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E4 f2v done
+
+    // a6: loss + gradient, written straight into the backward split's send buffer
+    const float* gscale_bwd = g.dinv_in_p();   // backward column side
+    const unsigned lb = (unsigned)loss_blocks;
+    if (!after) {
+        if (dt == NTP_F32)
+            softmax_xent_kernel<float, float><<<lb, 256, 0, s>>>((const float*)c->recv.p, 1, V_p, d_s, m->C, lab, msk,
+                                                                 row0, n, (float*)c->send.p, 1, gscale_bwd, part, cnt);
+        else
+            softmax_xent_kernel<__nv_bfloat16, __nv_bfloat16><<<lb, 256, 0, s>>>(
+                (const __nv_bfloat16*)c->recv.p, 1, V_p, d_s, m->C, lab, msk, row0, n, (__nv_bfloat16*)c->send.p, 1,
+                gscale_bwd, part, cnt);
+        NTP_LAUNCH_CHECK();
+        count_launch(c);
+        if (P * d_s > m->C) {
+            if (dt == NTP_F32)
+                zero_pad_cols_kernel<float><<<eblocks(V_p * (P * d_s - m->C)), 256, 0, s>>>((float*)c->send.p, V_p, d_s,
+                                                                                          P, m->C);
+            else
+                zero_pad_cols_kernel<__nv_bfloat16><<<eblocks(V_p * (P * d_s - m->C)), 256, 0, s>>>(
+                    (__nv_bfloat16*)c->send.p, V_p, d_s, P, m->C);
+            NTP_LAUNCH_CHECK();
+            count_launch(c);
+        }
+    } else {
+        // Z_v = unpack(recv) [V_p x hid]; logits = Z_v W1; dlogits; dZ_v = dlogits W1^T -> pack
+        float* Zv = dH1;   // reuse [V_p x hid]
+        unpack_f2v(c, c->recv.p, V_p, d_s, P, Zv, m->hid, m->hid, dt, NTP_F32, s);
+        gemm_rm(c, false, false, V_p, m->C, m->hid, Zv, m->hid, W1p, m->C, L, m->C);
+        softmax_xent_kernel<float, float><<<lb, 256, 0, s>>>(L, 0, V_p, d_s, m->C, lab, msk, row0, n, dL, 0, nullptr,
+                                                             part, cnt);
+        NTP_LAUNCH_CHECK();
+        count_launch(c);
+        gemm_rm(c, true, false, m->hid, m->C, V_p, Zv, m->hid, dL, m->C, dW1, m->C);          // dW1 = Z_v^T dlogits
+        gemm_rm(c, false, true, V_p, m->hid, m->C, dL, m->C, W1p, m->C, L, m->hid);           // dZ_v -> L
+        pack_v2f(c, L, m->hid, m->hid, c->send.p, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s);
+    }
+    reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, loss_blocks, scal);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E5 loss done
+
+    // a7: split the gradient
+    alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E6 v2f bwd
+
+    // a8: K backward hops
+    {
+        PropArgs a{};
+        a.H = c->recv.p;
+        a.Z = c->xfer.p;
+        a.ld_h = d_s;
+        a.ld_z = d_s;
+        a.cols = d_s;
+        a.dtype = dt;
+        a.K = m->K;
+        a.gamma = m->gamma;
+        a.alpha = m->alpha;
+        a.transposed = true;
+        if (m->K == 0) {
+            NTP_CHECK(false, NTP_ERR_ARG, "K == 0 training is not supported");
+        }
+        propagate(c, a, s, rep != nullptr, true);
+    }
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E7 prop bwd
+
+    // a9: gather -> dL^ rows [V_p x w]
+    alltoall_blocks(c, c->xfer.p, c->recv.p, V_p * d_s, dt, s);
+    unpack_f2v(c, c->recv.p, V_p, d_s, P, dL, w, w, dt, NTP_F32, s);
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E8 f2v bwd
+
+    // a10: MLP backward
+    if (!after) {
+        gemm_rm(c, true, false, m->hid, m->C, V_p, H1, m->hid, dL, m->C, dW1, m->C);        // dW1 = H1^T dL^
+        gemm_rm(c, false, true, V_p, m->hid, m->C, dL, m->C, W1p, m->C, dH1, m->hid);       // dH1 = dL^ W1^T
+    } else {
+        NTP_CUDA(cudaMemcpyAsync(dH1, dL, (size_t)V_p * m->hid * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    }
+    relu_grad_kernel<<<eblocks(V_p * m->hid), 256, 0, s>>>(dH1, H1, V_p * m->hid);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    gemm_rm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, m->hid, dW0, m->hid);          // dW0 = X^T dH1
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E9 mlp bwd
+
+    // a11: allreduce (sync_and_update)
+    if (P > 1) {
+        NTP_NCCL(ncclGroupStart());
+        NTP_NCCL(ncclAllReduce(dW0, dW0, n_w, ncclFloat32, ncclSum, c->comm, s));
+        NTP_NCCL(ncclAllReduce(scal, scal, 2, ncclFloat64, ncclSum, c->comm, s));
+        NTP_NCCL(ncclGroupEnd());
+    }
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E10 allreduce
+    sgd_kernel<<<eblocks(n_w), 256, 0, s>>>(W0p, (int64_t)m->d_in * m->hid, W1p, (int64_t)m->hid * m->C, dW0, scal,
+                                            m->lr);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E11 sgd
+
+    double h_scal[2] = {0, 0};
+    NTP_CUDA(cudaMemcpyAsync(h_scal, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NTP_CUDA(cudaEventRecord(c->ev[41], s));
+    NTP_CUDA(cudaStreamWaitEvent(user ? user : (cudaStream_t)0, c->ev[41], 0));
+    NTP_CUDA(cudaStreamSynchronize(s));
+
+    if (rep) {
+        rep->loss = h_scal[1] > 0 ? h_scal[0] / h_scal[1] : 0.0;
+        rep->n_train = (int64_t)h_scal[1];
+        static const int phase_of[11] = {NTP_PH_MLP_FWD, NTP_PH_V2F_FWD, NTP_PH_PROP_FWD, NTP_PH_F2V_FWD, NTP_PH_LOSS,
+                                         NTP_PH_V2F_BWD, NTP_PH_PROP_BWD, NTP_PH_F2V_BWD, NTP_PH_MLP_BWD,
+                                         NTP_PH_ALLREDUCE, NTP_PH_SGD};
+        for (int i = 0; i < NTP_PH_COUNT; ++i) rep->ms[i] = 0.0;
+        for (int i = 0; i < 11; ++i) {
+            float ms = 0.f;
+            NTP_CUDA(cudaEventElapsedTime(&ms, E[i], E[i + 1]));
+            rep->ms[phase_of[i]] = ms;
+        }
+        float tot = 0.f;
+        NTP_CUDA(cudaEventElapsedTime(&tot, E[0], E[11]));
+        rep->ms[NTP_PH_TOTAL] = tot;
+        const int64_t wire = (int64_t)(P - 1) * V_p * d_s * (int64_t)es;
+        for (int i = 0; i < 4; ++i) {
+            rep->bytes_sent[i] = wire;
+            rep->bytes_recv[i] = wire;
+        }
+        rep->collectives = P > 1 ? 5 : 0;
+        rep->kernel_launches = c->launches - launches0;
+        int nh = 0;
+        rep->spmm_ms = collect_hop_ms(c, &nh);
+        rep->spmm_launches = nh;
+    }
+}
+
+}  // namespace ntp

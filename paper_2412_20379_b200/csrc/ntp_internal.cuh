@@ -1,0 +1,181 @@
+// ntp_internal.cuh — internal declarations of libntp (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cublas_v2.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "ntp.h"
+
+namespace ntp {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+    ntp_status st;
+    std::string msg;
+};
+
+[[noreturn]] void fail(ntp_status st, const char* fmt, ...);
+
+#define NTP_CUDA(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            ::ntp::fail(_e == cudaErrorMemoryAllocation ? NTP_ERR_OOM : NTP_ERR_CUDA,      \
+                        "%s:%d %s -> %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+    } while (0)
+
+#define NTP_NCCL(expr)                                                                     \
+    do {                                                                                   \
+        ncclResult_t _r = (expr);                                                          \
+        if (_r != ncclSuccess)                                                             \
+            ::ntp::fail(NTP_ERR_NCCL, "%s:%d %s -> %s", __FILE__, __LINE__, #expr,         \
+                        ncclGetErrorString(_r));                                           \
+    } while (0)
+
+#define NTP_BLAS(expr)                                                                     \
+    do {                                                                                   \
+        cublasStatus_t _s = (expr);                                                        \
+        if (_s != CUBLAS_STATUS_SUCCESS)                                                   \
+            ::ntp::fail(NTP_ERR_CUDA, "%s:%d %s -> cublas status %d", __FILE__, __LINE__,  \
+                        #expr, (int)_s);                                                   \
+    } while (0)
+
+#define NTP_CHECK(cond, st, ...)                                                           \
+    do {                                                                                   \
+        if (!(cond)) ::ntp::fail((st), __VA_ARGS__);                                       \
+    } while (0)
+
+#define NTP_LAUNCH_CHECK() NTP_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------- device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t b);          // grow-only (contents not preserved)
+    void release();
+    template <class T> T* as() const { return static_cast<T*>(p); }
+    ~DevBuf() { release(); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// ---------------------------------------------------------------- graph
+// One CSR orientation plus its merge-path work partition.
+// Merge path (rows + nnz items): unit u covers diagonals [u*T, (u+1)*T);
+// unit_row[u] = row-ends consumed before the unit, unit_e[u] = edges consumed.
+struct Csr {
+    DevBuf row_ptr;                 // int32 [n+1]
+    DevBuf col;                     // int32 [nnz]
+    DevBuf unit_row;                // int32 [U+1]
+    DevBuf unit_e;                  // int32 [U+1]
+    std::vector<int32_t> h_unit_row; // host copy (row-range restriction of launches)
+    int64_t U = 0;
+    void reset() {
+        row_ptr.release(); col.release(); unit_row.release(); unit_e.release();
+        h_unit_row.clear(); U = 0;
+    }
+};
+
+struct Graph {
+    int64_t n = 0, nnz = 0;
+    bool symmetric = false;
+    bool loaded = false;
+    int32_t unit_items = 2048;      // T, a graph-level constant (P-invariant schedule)
+    Csr in;                         // rows = destinations (A^)
+    Csr out;                        // rows = sources (A^T); unused if symmetric
+    DevBuf dinv_in, dinv_out;       // fp32 [n]
+    void reset() {
+        n = nnz = 0; symmetric = false; loaded = false; unit_items = 2048;
+        in.reset(); out.reset(); dinv_in.release(); dinv_out.release();
+    }
+    const Csr& fwd() const { return in; }
+    const Csr& bwd() const { return symmetric ? in : out; }
+    const float* dinv_in_p() const { return dinv_in.as<float>(); }
+    const float* dinv_out_p() const { return symmetric ? dinv_in.as<float>() : dinv_out.as<float>(); }
+};
+
+}  // namespace ntp
+
+// ---------------------------------------------------------------- context
+struct ntp_ctx {
+    int device = 0, rank = 0, world = 1, slice_align = 16;
+    ncclComm_t comm = nullptr;
+    cudaStream_t s_comp = nullptr, s_comm = nullptr;
+    cublasHandle_t blas = nullptr;
+    ntp::Graph g;
+    // scratch
+    ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
+    ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
+    cudaEvent_t ev[64] = {};
+    cudaEvent_t hop_ev[256] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
+    int hop_ev_used = 0;
+    int64_t launches = 0;
+    std::string err;
+};
+
+namespace ntp {
+
+// -------------------------------------------------------------- internal API
+void build_graph_from_keys(ntp_ctx* c, uint64_t* keys, int64_t m, int64_t n, bool symmetric,
+                           DevBuf& keybuf_owner);
+void rmat_keys(ntp_ctx* c, int scale, const uint32_t thr[3], uint64_t seed, int64_t i0, int64_t count,
+               int64_t n, bool symmetric, uint64_t* keys, cudaStream_t s);
+void rmat_raw(ntp_ctx* c, int scale, const uint32_t thr[3], uint64_t seed, int64_t i0, int64_t count,
+              int64_t* src, int64_t* dst, cudaStream_t s);
+
+// Propagation on one feature slice (dtype-generic storage, fp32 accumulation).
+struct PropArgs {
+    const void* H;          // [n x cols] original input (alpha term)
+    void* Z;                // output
+    int64_t ld_h, ld_z;     // elements
+    int32_t cols;           // elements per row (cols*esize % 16 == 0)
+    ntp_dtype dtype;
+    int K;
+    float gamma, alpha;
+    bool transposed;        // backward (A^T)
+};
+// time_hops: record an event pair around every hop into c->hop_ev (read after a sync
+// with collect_hop_ms).
+void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops = false,
+               bool prescaled_input = false, int64_t last_row_lo = 0, int64_t last_row_hi = -1);
+double collect_hop_ms(ntp_ctx* c, int* n_hops);
+void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                 const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
+void arcs_to_keys(ntp_ctx* c, const int64_t* src, const int64_t* dst, int64_t m, int64_t n, bool sym,
+                  uint64_t* keys, cudaStream_t s);
+void csr_to_keys(ntp_ctx* c, const int64_t* row_ptr, const int32_t* col, int64_t n, uint64_t* keys,
+                 cudaStream_t s);
+
+// One hop over rows [row_lo, row_hi) (all rows if row_hi < 0).
+// mode 0: intermediate (pre-scaled output), 1: last (unscaled output Z^K).
+void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, const void* S_in,
+              void* S_out, const void* H, int64_t ld_in, int64_t ld_out, int64_t ld_h, int32_t cols,
+              ntp_dtype dt, float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi,
+              cudaStream_t s);
+void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, int32_t cols,
+              const float* scale, int64_t rows, ntp_dtype dt, cudaStream_t s);
+
+// layouts
+void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, int64_t V_p,
+              int32_t d_s, int32_t P, const float* row_scale, int64_t row0, int64_t n,
+              ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s);
+void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t P, void* Hv,
+                int64_t ld_v, int32_t w, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s);
+void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_elems, ntp_dtype dt,
+                     cudaStream_t s);
+
+inline size_t esize(ntp_dtype d) { return d == NTP_BF16 ? 2 : 4; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int32_t slice_width(int32_t w, int32_t P, ntp_dtype dt, int align);
+
+void count_launch(ntp_ctx* c, int k = 1);
+
+}  // namespace ntp

@@ -1,0 +1,265 @@
+"""ctypes binding of libntp (include/ntp.h) — argument marshalling only.
+
+Every computation runs inside libntp.so (CUDA, sm_100a).  If the library is
+missing this module raises at import time: there is no CPU fallback.
+Tensors are torch tensors (device memory owned by the caller); NumPy arrays are
+accepted only where the C call takes HOST pointers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libntp.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libntp.so not found at {LIB_PATH}: run `python -m paper_2412_20379_b200.build` "
+                      "(there is no fallback implementation)")
+
+_lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+
+# ---------------------------------------------------------------- enums
+NTP_OK, NTP_ERR_ARG, NTP_ERR_SHAPE, NTP_ERR_CONFIG, NTP_ERR_GRAPH, NTP_ERR_STATE, NTP_ERR_OOM, \
+    NTP_ERR_CUDA, NTP_ERR_NCCL, NTP_ERR_TIMEOUT = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9
+NTP_F32, NTP_BF16 = 0, 1
+NTP_LAYOUT_VERTEX, NTP_LAYOUT_FEATURE = 0, 1
+NTP_G_SYMMETRIC, NTP_G_VALIDATE = 1, 2
+NTP_M_W1_AFTER_PROP, NTP_M_OVERLAP, NTP_M_HOST_INPUTS = 1, 2, 4
+PHASES = ["mlp_fwd", "v2f_fwd", "prop_fwd", "f2v_fwd", "loss", "v2f_bwd", "prop_bwd", "f2v_bwd",
+          "mlp_bwd", "allreduce", "sgd", "total"]
+
+EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_unique_id", "ntp_create",
+            "ntp_destroy", "ntp_load_graph", "ntp_build_graph", "ntp_generate_rmat", "ntp_rmat_arcs",
+            "ntp_graph_info", "ntp_copy_csr", "ntp_copy_dinv", "ntp_partition", "ntp_scatter_features",
+            "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd", "ntp_train_epoch"]
+
+
+class ntp_tensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("dtype", C.c_int), ("layout", C.c_int), ("rows", C.c_int64),
+                ("cols", C.c_int32), ("ld", C.c_int64)]
+
+
+class ntp_partition_info(C.Structure):
+    _fields_ = [("n", C.c_int64), ("V_p", C.c_int64), ("V_pad", C.c_int64), ("w", C.c_int32), ("P", C.c_int32),
+                ("d_s", C.c_int32), ("w_pad", C.c_int32), ("elem_bytes", C.c_int32), ("chunks", C.c_int32),
+                ("chunk", C.c_int64)]
+
+
+class ntp_model(C.Structure):
+    _fields_ = [("d_in", C.c_int32), ("hid", C.c_int32), ("C", C.c_int32), ("K", C.c_int32),
+                ("gamma", C.c_float), ("alpha", C.c_float), ("lr", C.c_float), ("dtype", C.c_int),
+                ("chunks", C.c_int32), ("flags", C.c_uint32)]
+
+
+class ntp_epoch_report(C.Structure):
+    _fields_ = [("loss", C.c_double), ("n_train", C.c_int64), ("ms", C.c_double * 12),
+                ("bytes_sent", C.c_int64 * 4), ("bytes_recv", C.c_int64 * 4), ("collectives", C.c_int64),
+                ("kernel_launches", C.c_int64), ("spmm_ms", C.c_double), ("spmm_launches", C.c_int32),
+                ("pad_", C.c_int32)]
+
+
+_vp, _i64, _i32, _u32, _u64, _f = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32, C.c_uint64, C.c_float
+_sig = {
+    "ntp_abi_version": ([], C.c_int),
+    "ntp_status_string": ([C.c_int], C.c_char_p),
+    "ntp_last_error": ([_vp], C.c_char_p),
+    "ntp_get_unique_id": ([_vp], C.c_int),
+    "ntp_create": ([C.POINTER(_vp), C.c_int, C.c_int, C.c_int, _vp, C.c_int], C.c_int),
+    "ntp_destroy": ([_vp], None),
+    "ntp_load_graph": ([_vp, _vp, _vp, _i64, _i64, _u32], C.c_int),
+    "ntp_build_graph": ([_vp, _vp, _vp, _i64, _i64, _u32], C.c_int),
+    "ntp_generate_rmat": ([_vp, _i64, C.c_int, _i64, _vp, _u64, _u32], C.c_int),
+    "ntp_rmat_arcs": ([_vp, C.c_int, _vp, _u64, _i64, _i64, _vp, _vp], C.c_int),
+    "ntp_graph_info": ([_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(C.c_int)], C.c_int),
+    "ntp_copy_csr": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
+    "ntp_copy_dinv": ([_vp, _vp, _vp], C.c_int),
+    "ntp_partition": ([_i64, _i32, _i32, C.c_int, _i32, C.c_int, C.POINTER(ntp_partition_info)], C.c_int),
+    "ntp_scatter_features": ([_vp, _vp, C.c_int, _i64, _i32, C.c_int, C.POINTER(ntp_tensor)], C.c_int),
+    "ntp_layout_v2f": ([_vp, C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), _vp], C.c_int),
+    "ntp_layout_f2v": ([_vp, C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), _vp], C.c_int),
+    "ntp_propagate_fwd": ([_vp, C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), C.c_int, _f, _f, _vp], C.c_int),
+    "ntp_propagate_bwd": ([_vp, C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), C.c_int, _f, _f, _vp], C.c_int),
+    "ntp_train_epoch": ([_vp, C.POINTER(ntp_model), C.POINTER(ntp_tensor), _vp, _vp, C.POINTER(ntp_tensor),
+                         C.POINTER(ntp_tensor), C.POINTER(ntp_epoch_report), _vp], C.c_int),
+}
+for _name, (_args, _res) in _sig.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _res
+
+
+class NtpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_lib.ntp_status_string(status).decode()}: {msg}")
+        self.status = status
+
+
+def abi_version() -> int:
+    return _lib.ntp_abi_version()
+
+
+def get_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    st = _lib.ntp_get_unique_id(buf)
+    if st != NTP_OK:
+        raise NtpError(st, _lib.ntp_last_error(None).decode())
+    return bytes(buf)
+
+
+def partition(n: int, w: int, P: int, dtype: int = NTP_F32, chunks: int = 1, slice_align: int = 16) -> dict:
+    info = ntp_partition_info()
+    st = _lib.ntp_partition(n, w, P, dtype, chunks, slice_align, C.byref(info))
+    if st != NTP_OK:
+        raise NtpError(st, "ntp_partition: bad arguments")
+    return {k: getattr(info, k) for k, _ in ntp_partition_info._fields_}
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.float32:
+        return NTP_F32
+    if t.dtype == torch.bfloat16:
+        return NTP_BF16
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def as_ntp_tensor(t, layout: int = NTP_LAYOUT_VERTEX) -> ntp_tensor:
+    """Describe a 2-D torch tensor with unit column stride."""
+    if t.dim() == 1:
+        t = t.view(-1, 1)
+    assert t.dim() == 2 and (t.stride(1) == 1 or t.shape[1] <= 1), "need a row-major 2-D tensor"
+    return ntp_tensor(t.data_ptr(), _dtype_code(t), layout, t.shape[0], t.shape[1], max(t.stride(0), t.shape[1]))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _ptr(a):
+    return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
+
+
+class Context:
+    """One libntp context per process/GPU (ntp_create / ntp_destroy)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None,
+                 slice_align: int = 16):
+        self._h = C.c_void_p()
+        idbuf = None
+        if unique_id is not None:
+            idbuf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        st = _lib.ntp_create(C.byref(self._h), device, rank, world, idbuf, slice_align)
+        if st != NTP_OK:
+            raise NtpError(st, _lib.ntp_last_error(None).decode())
+        self.device, self.rank, self.world, self.slice_align = device, rank, world, slice_align
+
+    def close(self):
+        if self._h:
+            _lib.ntp_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st):
+        if st != NTP_OK:
+            raise NtpError(st, _lib.ntp_last_error(self._h).decode())
+
+    # -------------------------------------------------------------- graph
+    def load_graph(self, row_ptr, col_idx, n: int, symmetric: bool = False, validate: bool = False):
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        cl = np.ascontiguousarray(col_idx, dtype=np.int32)
+        flags = (NTP_G_SYMMETRIC if symmetric else 0) | (NTP_G_VALIDATE if validate else 0)
+        self._chk(_lib.ntp_load_graph(self._h, rp.ctypes.data, cl.ctypes.data, n, int(rp[-1]) if n >= 0 else 0,
+                                      flags))
+
+    def build_graph(self, src, dst, n: int, symmetric: bool = False):
+        s = np.ascontiguousarray(src, dtype=np.int64)
+        d = np.ascontiguousarray(dst, dtype=np.int64)
+        self._chk(_lib.ntp_build_graph(self._h, s.ctypes.data, d.ctypes.data, s.size, n,
+                                       NTP_G_SYMMETRIC if symmetric else 0))
+
+    def generate_rmat(self, n: int, scale: int, m_raw: int, thresholds, seed: int, symmetric: bool):
+        thr = (C.c_uint32 * 3)(*[int(t) for t in thresholds])
+        self._chk(_lib.ntp_generate_rmat(self._h, n, scale, m_raw, thr, seed, NTP_G_SYMMETRIC if symmetric else 0))
+
+    def rmat_arcs(self, scale: int, thresholds, seed: int, i0: int, count: int):
+        thr = (C.c_uint32 * 3)(*[int(t) for t in thresholds])
+        src = np.empty(count, dtype=np.int64)
+        dst = np.empty(count, dtype=np.int64)
+        self._chk(_lib.ntp_rmat_arcs(self._h, scale, thr, seed, i0, count, src.ctypes.data, dst.ctypes.data))
+        return src, dst
+
+    def graph_info(self):
+        n, nnz, sym = C.c_int64(), C.c_int64(), C.c_int()
+        self._chk(_lib.ntp_graph_info(self._h, C.byref(n), C.byref(nnz), C.byref(sym)))
+        return n.value, nnz.value, bool(sym.value)
+
+    def copy_csr(self, transposed: bool = False):
+        n, nnz, _ = self.graph_info()
+        rp = np.empty(n + 1, dtype=np.int64)
+        cl = np.empty(max(nnz, 1), dtype=np.int32)
+        deg = np.empty(max(n, 1), dtype=np.int32)
+        self._chk(_lib.ntp_copy_csr(self._h, int(transposed), rp.ctypes.data, cl.ctypes.data, deg.ctypes.data))
+        return rp, cl[:nnz], deg[:n]
+
+    def copy_dinv(self):
+        n, _, _ = self.graph_info()
+        a = np.empty(max(n, 1), dtype=np.float32)
+        b = np.empty(max(n, 1), dtype=np.float32)
+        self._chk(_lib.ntp_copy_dinv(self._h, a.ctypes.data, b.ctypes.data))
+        return a[:n], b[:n]
+
+    # -------------------------------------------------------------- features / layouts
+    def scatter_features(self, X: np.ndarray, layout: int, out):
+        import torch
+        code = NTP_BF16 if out.dtype == torch.bfloat16 else NTP_F32
+        if code == NTP_BF16:
+            Xh = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).to(torch.bfloat16).contiguous()
+            ptr = Xh.data_ptr()
+        else:
+            Xh = np.ascontiguousarray(X, dtype=np.float32)
+            ptr = Xh.ctypes.data
+        t = as_ntp_tensor(out, layout)
+        self._chk(_lib.ntp_scatter_features(self._h, ptr, code, X.shape[0], X.shape[1], layout, C.byref(t)))
+
+    def layout_v2f(self, Hv, Hf, stream=None):
+        a, b = as_ntp_tensor(Hv, NTP_LAYOUT_VERTEX), as_ntp_tensor(Hf, NTP_LAYOUT_FEATURE)
+        self._chk(_lib.ntp_layout_v2f(self._h, C.byref(a), C.byref(b), _stream_ptr(stream)))
+
+    def layout_f2v(self, Hf, Hv, stream=None):
+        a, b = as_ntp_tensor(Hf, NTP_LAYOUT_FEATURE), as_ntp_tensor(Hv, NTP_LAYOUT_VERTEX)
+        self._chk(_lib.ntp_layout_f2v(self._h, C.byref(a), C.byref(b), _stream_ptr(stream)))
+
+    # -------------------------------------------------------------- propagation
+    def propagate_fwd(self, H, Z, K: int, gamma: float = 1.0, alpha: float = 0.0, stream=None):
+        a, b = as_ntp_tensor(H, NTP_LAYOUT_FEATURE), as_ntp_tensor(Z, NTP_LAYOUT_FEATURE)
+        self._chk(_lib.ntp_propagate_fwd(self._h, C.byref(a), C.byref(b), K, gamma, alpha, _stream_ptr(stream)))
+
+    def propagate_bwd(self, G, dH, K: int, gamma: float = 1.0, alpha: float = 0.0, stream=None):
+        a, b = as_ntp_tensor(G, NTP_LAYOUT_FEATURE), as_ntp_tensor(dH, NTP_LAYOUT_FEATURE)
+        self._chk(_lib.ntp_propagate_bwd(self._h, C.byref(a), C.byref(b), K, gamma, alpha, _stream_ptr(stream)))
+
+    # -------------------------------------------------------------- epoch
+    def train_epoch(self, model: dict, X_v, labels_v, mask_v, W0, W1, stream=None, host_inputs: bool = False) -> dict:
+        m = ntp_model(model["d_in"], model["hid"], model["C"], model["K"], model["gamma"], model["alpha"],
+                      model["lr"], model.get("dtype", NTP_F32), model.get("chunks", 1), model.get("flags", 0)
+                      | (NTP_M_HOST_INPUTS if host_inputs else 0))
+        xt = as_ntp_tensor(X_v, NTP_LAYOUT_VERTEX)
+        w0, w1 = as_ntp_tensor(W0), as_ntp_tensor(W1)
+        rep = ntp_epoch_report()
+        self._chk(_lib.ntp_train_epoch(self._h, C.byref(m), C.byref(xt), _ptr(labels_v), _ptr(mask_v),
+                                       C.byref(w0), C.byref(w1), C.byref(rep), _stream_ptr(stream)))
+        return {"loss": rep.loss, "n_train": rep.n_train, "ms": dict(zip(PHASES, list(rep.ms))),
+                "bytes_sent": list(rep.bytes_sent), "bytes_recv": list(rep.bytes_recv),
+                "collectives": rep.collectives, "kernel_launches": rep.kernel_launches,
+                "spmm_ms": rep.spmm_ms, "spmm_launches": rep.spmm_launches}

@@ -1,0 +1,184 @@
+"""GPU K-hop propagation (a4/a8) vs the oracle, through the C ABI.
+
+Tolerance (reading R10): |z_gpu - z_orc| <= tol * (M|H|)_elem, tol = 1e-5 for
+fp32 storage, 2e-2 for bf16 storage (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import oracle_graph, ntp_ctx_for, cond_bound, assert_r10
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 2e-2
+
+
+def _features(n, d, seed):
+    return synth.features(seed, n, d)
+
+
+def _run(ctx, H, K, gamma, alpha, transposed=False, dtype=torch.float32, rows=None, cols=None):
+    n = H.shape[0]
+    rows = rows or n
+    cols = cols or H.shape[1]
+    Hd = torch.zeros(rows, cols, dtype=dtype, device="cuda")
+    Hd[:n, :H.shape[1]] = torch.from_numpy(H).to(dtype)
+    Zd = torch.full((rows, cols), 7.0, dtype=dtype, device="cuda")
+    f = ctx.propagate_bwd if transposed else ctx.propagate_fwd
+    f(Hd, Zd, K, gamma, alpha)
+    torch.cuda.synchronize()
+    return Zd, Hd
+
+
+@pytest.mark.parametrize("name", ["cora", "tiny_sym", "tiny_dir", "small_appnp", "small_dir"])
+@pytest.mark.parametrize("d", [4, 8, 12, 44, 48, 132])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_fp32_parity(name, d, transposed):
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, d, 100 + d)
+    Zd, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+    f = oracle.propagate.propagate_bwd if transposed else oracle.propagate.propagate_fwd
+    ref = f(g, H, cfg.K, cfg.gamma, cfg.alpha)
+    den = cond_bound(g, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+    assert_r10(Zd.cpu().numpy()[:g.n], ref, den, FP32_TOL, f"{name} d={d} T={transposed}")
+
+
+@pytest.mark.parametrize("K,gamma,alpha", [(0, 1.0, 0.0), (1, 1.0, 0.0), (1, 0.5, 0.5), (3, 0.9, 0.1),
+                                           (10, 0.9, 0.1), (7, 1.0, 0.0)])
+def test_fp32_K_gamma_alpha(K, gamma, alpha):
+    name = "tiny_dir"
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, 16, 3)
+    for transposed in (False, True):
+        Zd, _ = _run(ctx, H, K, gamma, alpha, transposed)
+        f = oracle.propagate.propagate_bwd if transposed else oracle.propagate.propagate_fwd
+        ref = f(g, H, K, gamma, alpha)
+        den = cond_bound(g, H, K, gamma, alpha, transposed)
+        assert_r10(Zd.cpu().numpy()[:g.n], ref, den, FP32_TOL, f"K={K} T={transposed}")
+
+
+@pytest.mark.parametrize("name", ["tiny_dir", "small_appnp", "small_dir"])
+@pytest.mark.parametrize("d", [8, 16, 48, 128])
+def test_bf16_parity(name, d):
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, d, 7)
+    for transposed in (False, True):
+        Zd, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, transposed, dtype=torch.bfloat16)
+        f = oracle.propagate.propagate_bwd if transposed else oracle.propagate.propagate_fwd
+        ref = f(g, H, cfg.K, cfg.gamma, cfg.alpha)
+        den = cond_bound(g, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+        assert_r10(Zd.float().cpu().numpy()[:g.n], ref, den, BF16_TOL, f"bf16 {name} d={d}")
+
+
+def test_padding_rows_zeroed_and_ld():
+    """Rows >= n of Z are zero; a strided (ld > cols) view works."""
+    name = "tiny_sym"
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, 8, 1)
+    big_h = torch.zeros(g.n + 5, 16, device="cuda")
+    big_h[:g.n, :8] = torch.from_numpy(H)
+    big_z = torch.full((g.n + 5, 16), 3.0, device="cuda")
+    ctx.propagate_fwd(big_h[:, :8], big_z[:, :8], cfg.K, cfg.gamma, cfg.alpha)
+    torch.cuda.synchronize()
+    z = big_z.cpu().numpy()
+    assert (z[g.n:, :8] == 0).all() and (z[:, 8:] == 3.0).all()
+    ref = oracle.propagate.propagate_fwd(g, H, cfg.K, cfg.gamma, cfg.alpha)
+    assert_r10(z[:g.n, :8], ref, cond_bound(g, H, cfg.K, cfg.gamma, cfg.alpha), FP32_TOL)
+
+
+@pytest.mark.parametrize("name", ["small_dir", "small_appnp"])
+def test_slice_invariance_bitwise(name):
+    """Column slices propagated separately equal the full-width result bitwise
+    (the per-row reduction order does not depend on d_s, so P=1 == P=8)."""
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, 48, 5)
+    Zfull, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha)
+    for c0, c1 in [(0, 8), (8, 16), (16, 28), (28, 48), (0, 4)]:
+        Zs, _ = _run(ctx, np.ascontiguousarray(H[:, c0:c1]), cfg.K, cfg.gamma, cfg.alpha)
+        assert torch.equal(Zs, Zfull[:, c0:c1]), (c0, c1)
+    for transposed in (True,):
+        Zfull, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+        Zs, _ = _run(ctx, np.ascontiguousarray(H[:, 8:16]), cfg.K, cfg.gamma, cfg.alpha, transposed)
+        assert torch.equal(Zs, Zfull[:, 8:16])
+
+
+def test_deterministic():
+    name = "small_appnp"
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, 44, 9)
+    a, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha)
+    b, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha)
+    assert torch.equal(a, b)
+
+
+def test_adjoint_gpu():
+    name = "small_dir"
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, 8, 1)
+    G = _features(g.n, 8, 2)
+    Z, _ = _run(ctx, H, 3, 0.9, 0.1)
+    Y, _ = _run(ctx, G, 3, 0.9, 0.1, transposed=True)
+    lhs = float((Z.double() * torch.from_numpy(G).cuda().double()).sum())
+    rhs = float((torch.from_numpy(H).cuda().double() * Y.double()).sum())
+    assert abs(lhs - rhs) <= 1e-5 * (abs(lhs) + abs(rhs))
+
+
+def test_empty_and_isolated_graph(ntp):
+    """No arcs: A^ = I (d~ = 1) so Z^K = gamma^K H + alpha sum_{j<K} gamma^j H exactly-ish."""
+    ctx = ntp.Context()
+    ctx.build_graph(np.array([], np.int64), np.array([], np.int64), 37)
+    H = _features(37, 8, 4)
+    Z, _ = _run(ctx, H, 3, 0.5, 0.25)
+    coef = 0.5 ** 3 + 0.25 * (1 + 0.5 + 0.25)
+    np.testing.assert_allclose(Z.cpu().numpy(), coef * H, rtol=1e-6, atol=1e-7)
+
+
+@pytest.fixture(scope="module")
+def ntp():
+    from paper_2412_20379_b200 import ntp
+    return ntp
+
+
+# ------------------------------------------------------------------ full size (BASELINE configs[1])
+
+@pytest.mark.slow
+def test_reddit_full_size_sampled_rows():
+    """c2 at the bench's P=1 slice width (44 fp32 columns), K=2: sampled output rows
+    vs the oracle hop by hop (the GPU's hop-1 output is fed to the oracle's hop 2),
+    plus the sqrt(d~) fixed point A^ sqrt(d~) = sqrt(d~) (symmetric graph)."""
+    name = "reddit"
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    n = g.n
+    H = _features(n, 44, 11)
+    Z1, _ = _run(ctx, H, 1, 1.0, 0.0)
+    Z2, _ = _run(ctx, H, 2, 1.0, 0.0)
+    rng = np.random.default_rng(0)
+    rows = np.concatenate([rng.integers(0, n, 300), np.argsort(g.deg_in)[-20:]])   # include hubs
+    z1 = Z1.double().cpu().numpy()
+    ref1 = oracle.propagate.hop_rows(g, H, None, rows, 1.0, 0.0)
+    den1 = oracle.propagate.hop_rows(g, np.abs(H), None, rows, 1.0, 0.0)
+    assert_r10(z1[rows], ref1, den1, FP32_TOL, "hop1")
+    ref2 = oracle.propagate.hop_rows(g, z1, None, rows, 1.0, 0.0)
+    den2 = oracle.propagate.hop_rows(g, np.abs(z1), None, rows, 1.0, 0.0)
+    assert_r10(Z2.double().cpu().numpy()[rows], ref2, den2, 2 * FP32_TOL, "hop2")
+    # fixed point on the full graph
+    sq = np.sqrt(g.deg_in + 1.0)[:, None].repeat(4, 1).astype(np.float32)
+    Zs, _ = _run(ctx, sq, 2, 1.0, 0.0)
+    np.testing.assert_allclose(Zs.cpu().numpy(), sq, rtol=2e-5)
