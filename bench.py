@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: one decoupled-TP training epoch (all SURVEY §8(a) rows) per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config reddit] [--impl ntp|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1: one rank per GPU, NCCL)
+
+Metric (BASELINE.json): epoch time and aggregation GE/s; value = epoch GE/s =
+2*K*nnz*w / t_epoch summed over the whole job (strong scaling: the graph is
+fixed, its feature columns are split over the N GPUs).  The dominant kernel's
+roofline uses the algorithmic bytes of DESIGN.md §6 and CUDA-event durations
+recorded by the library on the stream the SpMM kernel runs on.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "epoch time (s) and aggregation GE/s at 1/2/4/8 B200; % of HBM roofline"
+WORKLOADS = {
+    "reddit": "Reddit-shaped R-MAT graph (232,965 vertices, ~114M arcs, 602 features, 41 classes), "
+              "decoupled 2-hop GCN training epoch",
+    "products": "ogbn-products-shaped R-MAT graph (2.45M vertices, ~62M arcs, 100 features, 47 classes), "
+                "APPNP K=10 training epoch",
+    "cora": "Cora-shaped R-MAT graph (2,708 vertices, ~10.6K arcs, 1,433 binary features, 7 classes), "
+            "decoupled 2-hop GCN training epoch",
+    "orkut": "Orkut-shaped R-MAT graph (3.07M vertices, ~116M arcs), 512-feature decoupled training epoch",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ algorithmic bytes
+def hop_bytes(n, nnz, d_s, elem, symmetric, alpha):
+    """Compulsory HBM bytes of one SpMM hop on one GPU (every array touched once):
+    col_idx 4*nnz + row_ptr 4*(n+1) + D~^{-1/2} (4n, or 8n directed) + row slices:
+    gathered rows read once (n*r), self/S^0 rows (already counted in the gathered set),
+    output written once (n*r), S^0 read once more if alpha > 0 (n*r).  r = row-slice bytes."""
+    r = d_s * elem
+    return 4 * nnz + 4 * (n + 1) + (4 if symmetric else 8) * n + n * r * (2 + (1 if alpha > 0 else 0))
+
+
+def l2_gather_bytes(nnz, n, d_s, elem):
+    """Bytes the gather pulls through L2 (no-reuse model): every arc and self row, sector-rounded."""
+    r = -(-(d_s * elem) // 32) * 32
+    return (nnz + n) * r
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+def load_traffic(config, P, dtype):
+    """ncu dram bytes per launch of the SpMM hop kernel, from the committed profile summary."""
+    path = os.path.join(ROOT, "profiles", "spmm_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(f"{config}/P{P}/{dtype}")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
+def oracle_epoch_time(cfg, epochs=1):
+    """Times the fp64 oracle (as it stands) for `epochs` full epochs on this host."""
+    import oracle
+    t0 = time.time()
+    g = oracle.graph.graph_from_config(cfg)
+    t_graph = time.time() - t0
+    X, y, m = synth.config_inputs(cfg)
+    W0, W1 = synth.model_weights(cfg)
+    t0 = time.time()
+    for _ in range(epochs):
+        loss, W0, W1 = oracle.model.train_epoch(g, X, y, m, W0, W1, cfg.K, cfg.gamma, cfg.alpha, cfg.lr)
+    dt = (time.time() - t0) / epochs
+    return dt, g.nnz, oracle.lib.oracle_num_threads(), t_graph
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    w = cfg.w
+    times = []
+    import oracle
+    g = oracle.graph.graph_from_config(cfg)
+    X, y, m = synth.config_inputs(cfg)
+    W0, W1 = synth.model_weights(cfg)
+    for i in range(args.warmup + args.steps):
+        t0 = time.time()
+        loss, W0, W1 = oracle.model.train_epoch(g, X, y, m, W0, W1, cfg.K, cfg.gamma, cfg.alpha, cfg.lr)
+        if i >= args.warmup:
+            times.append(time.time() - t0)
+    t = sum(times) / len(times)
+    ge = 2 * cfg.K * g.nnz * w / t / 1e9
+    cores = oracle.lib.oracle_num_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": ge, "unit": "GE/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS.get(args.config, args.config), "n": cfg.n, "nnz": g.nnz, "w": w,
+                       "K": cfg.K},
+            "cpu_baseline": {"value": ge, "unit": "GE/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} full fp64 oracle epochs of the same workload (after "
+                                       f"{args.warmup} warm-up), OpenMP rows + numpy BLAS"},
+            "e2e": {"value": ge, "unit": "GE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="reddit")
+    ap.add_argument("--impl", default="ntp", choices=["ntp", "reference"])
+    ap.add_argument("--dtype", default=None, choices=[None, "f32", "bf16"])
+    ap.add_argument("--chunks", type=int, default=1)
+    ap.add_argument("--overlap", action="store_true",
+                    help="chunked last hop with the gather on the comm stream (a12); off by default: on "
+                         "reddit the gather moves ~1-10 MB and chunking costs more than it hides")
+    ap.add_argument("--slice-align", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-epochs", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = synth.get_config(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+    from paper_2412_20379_b200 import ntp
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # NCCL bootstrap id for the library's own communicator
+    uid = None
+    if world > 1:
+        obj = [ntp.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = ntp.Context(device=local, rank=rank, world=world, unique_id=uid, slice_align=args.slice_align)
+
+    t0 = time.time()
+    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric)
+    n, nnz, sym = ctx.graph_info()
+    t_graph = time.time() - t0
+
+    dtype_name = args.dtype or ("bf16" if cfg.name == "papers" else "f32")
+    dt = ntp.NTP_BF16 if dtype_name == "bf16" else ntp.NTP_F32
+    part = ntp.partition(n, cfg.w, world, dt, args.chunks, args.slice_align)
+    V_p, d_s = part["V_p"], part["d_s"]
+    row0 = rank * V_p
+    rows = max(0, min(V_p, n - row0))
+    Xh = np.zeros((V_p, cfg.d_in), np.float32)
+    yh = np.zeros(V_p, np.int32)
+    mh = np.zeros(V_p, np.uint8)
+    if rows:
+        Xh[:rows], yh[:rows], mh[:rows] = synth.config_inputs(cfg, row0, rows)
+    W0h, W1h = synth.model_weights(cfg)
+    X = torch.from_numpy(Xh).cuda()
+    y = torch.from_numpy(yh).cuda()
+    msk = torch.from_numpy(mh).cuda()
+    W0 = torch.from_numpy(W0h).cuda()
+    W1 = torch.from_numpy(W1h).cuda()
+    flags = (ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if args.overlap else 0)
+    model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=cfg.lr,
+                 dtype=dt, chunks=args.chunks, flags=flags)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream)
+    # ---- timed (device events on the caller's stream; the library orders its streams after it)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        reps.append(ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream))
+    ev1.record(stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    clk = clocks.stop()
+    spmm_ms = sum(r["spmm_ms"] for r in reps)
+    spmm_n = sum(r["spmm_launches"] for r in reps)
+    launches = sum(r["kernel_launches"] for r in reps)
+    phase = {k: sum(r["ms"][k] for r in reps) / len(reps) for k in reps[0]["ms"]}
+
+    # ---- e2e: same call with HOST (pinned) inputs copied in every step, loss read back
+    e2e_ms = None
+    h2d = Xh.nbytes + yh.nbytes + mh.nbytes
+    if not args.no_e2e:
+        Xp = torch.from_numpy(Xh).pin_memory()
+        yp = torch.from_numpy(yh).pin_memory()
+        mp = torch.from_numpy(mh).pin_memory()
+        for _ in range(2):
+            ctx.train_epoch(model, Xp, yp, mp, W0, W1, stream=stream, host_inputs=True)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ctx.train_epoch(model, Xp, yp, mp, W0, W1, stream=stream, host_inputs=True)
+        ev1.record(stream)
+        barrier()
+        e2e_ms = ev0.elapsed_time(ev1) / args.steps
+
+    def allmax(v):
+        if dist is None or v is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = allmax(ms)
+    e2e_ms = allmax(e2e_ms)
+    spmm_avg = allmax(spmm_ms / max(spmm_n, 1))
+
+    if rank == 0:
+        w = cfg.w
+        esz = 2 if dt == ntp.NTP_BF16 else 4
+        ge = 2 * cfg.K * nnz * w / (ms * 1e-3) / 1e9
+        peaks = load_peaks()
+        if peaks and peaks.get("hbm_gbs"):
+            peak, peak_src = peaks["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)"
+        else:
+            peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+        bh = hop_bytes(n, nnz, d_s, esz, sym, cfg.alpha)
+        achieved = bh / (spmm_avg * 1e-3) / 1e9
+        traffic = load_traffic(args.config, world, dtype_name)
+        l2b = l2_gather_bytes(nnz, n, d_s, esz)
+        line = {
+            "metric": METRIC, "value": ge, "unit": "GE/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if dt == ntp.NTP_F32 else "bf16", "data": "synthetic",
+            "epoch_s": ms / 1e3,
+            "config": {"workload": WORKLOADS.get(args.config, args.config), "n": n, "nnz": nnz, "w": w, "K": cfg.K,
+                       "gamma": cfg.gamma, "alpha": cfg.alpha, "P": world, "d_s": d_s, "V_p": V_p,
+                       "chunks": args.chunks, "overlap": bool(args.overlap),
+                       "l2": f"inputs larger than L2 (col_idx {4 * nnz / 1e6:.0f} MB streamed per hop; "
+                             f"X_v {Xh.nbytes / 1e6:.0f} MB per rank)",
+                       "graph_setup_s": round(t_graph, 3)},
+            "roofline": {"kernel": "spmm_hop_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": bh, "avg_launch_ms": spmm_avg,
+                         "launches_timed": spmm_n, "peak_source": peak_src,
+                         "l2_gather_bytes_per_launch": l2b,
+                         "l2_gather_GBps": l2b / (spmm_avg * 1e-3) / 1e9,
+                         "note": "algorithmic bytes = compulsory HBM bytes (DESIGN.md §6); the gathered "
+                                 "slice rows are re-read through L2 (l2_gather_*)"},
+            "prop_GE_per_s": 2 * cfg.K * nnz * w / (spmm_ms / len(reps) * 1e-3) / 1e9 * 1.0,
+            "phase_ms": {k: round(v, 4) for k, v in phase.items()},
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "e2e": None if e2e_ms is None else {
+                "value": 2 * cfg.K * nnz * w / (e2e_ms * 1e-3) / 1e9, "unit": "GE/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                t_cpu, nnz_o, cores, _ = oracle_epoch_time(cfg, args.cpu_epochs)
+                line["cpu_baseline"] = {"value": 2 * cfg.K * nnz_o * w / t_cpu / 1e9, "unit": "GE/s",
+                                        "cores": cores, "kind": "oracle", "epoch_s": t_cpu,
+                                        "sample": f"{args.cpu_epochs} full fp64 oracle epochs of the same workload "
+                                                  f"(graph build excluded), OpenMP over rows + numpy BLAS"}
+            except Exception as e:  # pragma: no cover
+                line["cpu_baseline"] = {"value": None, "unit": "GE/s", "cores": os.cpu_count(), "kind": "oracle",
+                                        "sample": f"failed: {e}"}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

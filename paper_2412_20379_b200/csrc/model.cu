@@ -162,10 +162,60 @@ void gemm_rm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, cons
 
 }  // namespace
 
-struct EpochBuffers {
-    int64_t V_p, V_pad;
-    int32_t P, w, d_s;
-};
+// Propagate K hops on this rank's feature slice (a.Z = output slice [V_pad x d_s])
+// and gather the result into `recv` ([P][V_p][d_s], block p = rank p's columns of
+// my rows).  overlap == false: all hops, then one block exchange on `s`.
+// overlap == true (a12, Fig. 7(c)): hops 1..K-1, then the last hop chunk by
+// chunk -- peer blocks in the rotated order rank+1, rank+2, ..., rank (own block
+// last), each split into `chunks` row ranges -- and every finished chunk is sent to
+// its owner on the comm stream while the next chunk computes.  At step s rank r
+// sends block (r+s)%P and receives from (r-s)%P, so each step is a permutation and
+// all ranks issue the same NCCL sequence.  Arithmetic is unchanged.
+static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool overlap, int chunks, int64_t V_p,
+                                 int32_t d_s, bool timed, cudaStream_t s) {
+    const int P = c->world;
+    const size_t es = esize(a.dtype);
+    const int64_t n = c->g.n;
+    const int64_t V_pad = (int64_t)P * V_p;
+    if (V_pad > n)   // padding rows of the slice travel to the last owner: keep them zero
+        NTP_CUDA(cudaMemsetAsync(static_cast<char*>(a.Z) + n * a.ld_z * es, 0, (V_pad - n) * a.ld_z * es, s));
+    if (!overlap || P == 1) {
+        propagate(c, a, s, timed, true);
+        alltoall_blocks(c, a.Z, recv, V_p * d_s, a.dtype, s);
+        return;
+    }
+    LastHop lh;
+    propagate(c, a, s, timed, true, &lh);
+    const int64_t csz = cdiv(V_p, std::max(chunks, 1));
+    const ncclDataType_t t = a.dtype == NTP_BF16 ? ncclBfloat16 : ncclFloat32;
+    char* zf = static_cast<char*>(a.Z);
+    char* rv = static_cast<char*>(recv);
+    cudaEvent_t ev = c->ev[50];
+    for (int st = 1; st <= P; ++st) {
+        const int sidx = st % P;
+        const int q = (c->rank + sidx) % P;          // block computed and sent
+        const int pr = (c->rank - sidx + P) % P;     // block received from
+        for (int64_t r = 0; r < V_p; r += csz) {
+            const int64_t lo = (int64_t)q * V_p + r;
+            const int64_t hi = (int64_t)q * V_p + std::min(r + csz, V_p);
+            if (lo < n) run_last_hop(c, lh, lo, std::min(hi, n), s, timed);
+            NTP_CUDA(cudaEventRecord(ev, s));
+            NTP_CUDA(cudaStreamWaitEvent(c->s_comm, ev, 0));
+            const int64_t cnt = (hi - lo) * d_s;
+            char* dst = rv + ((int64_t)pr * V_p + r) * d_s * es;
+            if (sidx == 0) {
+                NTP_CUDA(cudaMemcpyAsync(dst, zf + lo * d_s * es, cnt * es, cudaMemcpyDeviceToDevice, c->s_comm));
+            } else {
+                NTP_NCCL(ncclGroupStart());
+                NTP_NCCL(ncclSend(zf + lo * d_s * es, cnt, t, q, c->comm, c->s_comm));
+                NTP_NCCL(ncclRecv(dst, cnt, t, pr, c->comm, c->s_comm));
+                NTP_NCCL(ncclGroupEnd());
+            }
+        }
+    }
+    NTP_CUDA(cudaEventRecord(c->ev[51], c->s_comm));
+    NTP_CUDA(cudaStreamWaitEvent(s, c->ev[51], 0));
+}
 
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user) {
@@ -254,7 +304,8 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(cudaEventRecord(E[ei++], s));   // E2 v2f done
 
-    // a4: K forward hops: S^0 = recv (pre-scaled), output Z^K -> xfer
+    // a4 + a5: K forward hops on S^0 = recv (pre-scaled) -> Z^K in xfer, gathered into recv
+    const bool overlap = (m->flags & NTP_M_OVERLAP) != 0;
     c->hop_ev_used = 0;
     {
         PropArgs a{};
@@ -268,19 +319,9 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = false;
-        if (m->K == 0) {
-            // Z = H: undo the pre-scale via a plain gather of the unscaled rows
-            pack_v2f(c, prop_src, w, w, c->send.p, V_p, d_s, P, nullptr, row0, n, NTP_F32, dt, s);
-            alltoall_blocks(c, c->send.p, c->xfer.p, V_p * d_s, dt, s);
-        } else {
-            propagate(c, a, s, rep != nullptr, true);
-        }
+        propagate_and_gather(c, a, c->recv.p, overlap, m->chunks, V_p, d_s, rep != nullptr, s);
     }
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E3 prop fwd done
-
-    // a5: gather -> recv holds [P][V_p][d_s] logits (or Z rows)
-    alltoall_blocks(c, c->xfer.p, c->recv.p, V_p * d_s, dt, s);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E4 f2v done
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E3 prop fwd + f2v done
 
     // a6: loss + gradient, written straight into the backward split's send buffer
     const float* gscale_bwd = g.dinv_in_p();   // backward column side
@@ -321,13 +362,13 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, loss_blocks, scal);
     NTP_LAUNCH_CHECK();
     count_launch(c);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E5 loss done
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E4 loss done
 
     // a7: split the gradient
     alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E6 v2f bwd
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E5 v2f bwd
 
-    // a8: K backward hops
+    // a8 + a9: K backward hops on the split gradient, gathered -> dL^ rows [V_p x w]
     {
         PropArgs a{};
         a.H = c->recv.p;
@@ -340,17 +381,10 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = true;
-        if (m->K == 0) {
-            NTP_CHECK(false, NTP_ERR_ARG, "K == 0 training is not supported");
-        }
-        propagate(c, a, s, rep != nullptr, true);
+        propagate_and_gather(c, a, c->send.p, overlap, m->chunks, V_p, d_s, rep != nullptr, s);
     }
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E7 prop bwd
-
-    // a9: gather -> dL^ rows [V_p x w]
-    alltoall_blocks(c, c->xfer.p, c->recv.p, V_p * d_s, dt, s);
-    unpack_f2v(c, c->recv.p, V_p, d_s, P, dL, w, w, dt, NTP_F32, s);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E8 f2v bwd
+    unpack_f2v(c, c->send.p, V_p, d_s, P, dL, w, w, dt, NTP_F32, s);
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E6 prop bwd + f2v bwd
 
     // a10: MLP backward
     if (!after) {
@@ -363,7 +397,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     NTP_LAUNCH_CHECK();
     count_launch(c);
     gemm_rm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, m->hid, dW0, m->hid);          // dW0 = X^T dH1
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E9 mlp bwd
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E7 mlp bwd
 
     // a11: allreduce (sync_and_update)
     if (P > 1) {
@@ -372,12 +406,12 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         NTP_NCCL(ncclAllReduce(scal, scal, 2, ncclFloat64, ncclSum, c->comm, s));
         NTP_NCCL(ncclGroupEnd());
     }
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E10 allreduce
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E8 allreduce
     sgd_kernel<<<eblocks(n_w), 256, 0, s>>>(W0p, (int64_t)m->d_in * m->hid, W1p, (int64_t)m->hid * m->C, dW0, scal,
                                             m->lr);
     NTP_LAUNCH_CHECK();
     count_launch(c);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E11 sgd
+    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E9 sgd
 
     double h_scal[2] = {0, 0};
     NTP_CUDA(cudaMemcpyAsync(h_scal, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -388,17 +422,18 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     if (rep) {
         rep->loss = h_scal[1] > 0 ? h_scal[0] / h_scal[1] : 0.0;
         rep->n_train = (int64_t)h_scal[1];
-        static const int phase_of[11] = {NTP_PH_MLP_FWD, NTP_PH_V2F_FWD, NTP_PH_PROP_FWD, NTP_PH_F2V_FWD, NTP_PH_LOSS,
-                                         NTP_PH_V2F_BWD, NTP_PH_PROP_BWD, NTP_PH_F2V_BWD, NTP_PH_MLP_BWD,
-                                         NTP_PH_ALLREDUCE, NTP_PH_SGD};
+        // E0 start, E1 mlp fwd, E2 v2f, E3 prop fwd (+gather), E4 loss, E5 v2f bwd,
+        // E6 prop bwd (+gather, unpack), E7 mlp bwd, E8 allreduce, E9 sgd.
+        static const int phase_of[9] = {NTP_PH_MLP_FWD, NTP_PH_V2F_FWD, NTP_PH_PROP_FWD, NTP_PH_LOSS, NTP_PH_V2F_BWD,
+                                        NTP_PH_PROP_BWD, NTP_PH_MLP_BWD, NTP_PH_ALLREDUCE, NTP_PH_SGD};
         for (int i = 0; i < NTP_PH_COUNT; ++i) rep->ms[i] = 0.0;
-        for (int i = 0; i < 11; ++i) {
+        for (int i = 0; i < 9; ++i) {
             float ms = 0.f;
             NTP_CUDA(cudaEventElapsedTime(&ms, E[i], E[i + 1]));
             rep->ms[phase_of[i]] = ms;
         }
         float tot = 0.f;
-        NTP_CUDA(cudaEventElapsedTime(&tot, E[0], E[11]));
+        NTP_CUDA(cudaEventElapsedTime(&tot, E[0], E[9]));
         rep->ms[NTP_PH_TOTAL] = tot;
         const int64_t wire = (int64_t)(P - 1) * V_p * d_s * (int64_t)es;
         for (int i = 0; i < 4; ++i) {

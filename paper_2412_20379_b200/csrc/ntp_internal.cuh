@@ -142,10 +142,26 @@ struct PropArgs {
     float gamma, alpha;
     bool transposed;        // backward (A^T)
 };
-// time_hops: record an event pair around every hop into c->hop_ev (read after a sync
-// with collect_hop_ms).
+// State needed to run the last hop later, chunk by chunk (overlap scheduler, a12).
+struct LastHop {
+    const Csr* csr;
+    const float* rs;
+    const float* cs;
+    const void* sin;
+    int64_t ld_sin;
+    const void* S0;
+    int64_t ld_s0;
+    void* out;
+    int64_t ld_out;
+    int32_t cols;
+    ntp_dtype dt;
+    float gamma, alpha;
+};
+// time_hops: record an event pair around every hop launch into c->hop_ev (read after a
+// sync with collect_hop_ms).  defer_last: run hops 1..K-1 only and describe hop K.
 void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops = false,
-               bool prescaled_input = false, int64_t last_row_lo = 0, int64_t last_row_hi = -1);
+               bool prescaled_input = false, LastHop* defer_last = nullptr);
+void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi, cudaStream_t s, bool time_hops);
 double collect_hop_ms(ntp_ctx* c, int* n_hops);
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);

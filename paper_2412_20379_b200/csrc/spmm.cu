@@ -21,6 +21,7 @@
 // The per-row order depends only on (G, T, graph), not on the slice width or
 // P, so every column's result is bitwise independent of the slicing.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ntp_internal.cuh"
 
@@ -32,8 +33,31 @@ constexpr int kG = 8;           // edge lanes per group (fixed: part of the redu
 constexpr int kBlock = 256;
 
 template <typename T> struct V16;
+__device__ __forceinline__ uint4 ld_raw(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+
+// Gather load with a cache policy: 0 = ld.global.nc (L1 allocate), 1 = ld.global.nc.L1::no_allocate,
+// 2 = ld.global.cg (L2 only).
+template <int POL>
+__device__ __forceinline__ uint4 ld_gather(const void* p) {
+    uint4 r;
+    if constexpr (POL == 0) {
+        r = __ldg(reinterpret_cast<const uint4*>(p));
+    } else if constexpr (POL == 1) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    } else {
+        asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    }
+    return r;
+}
+
 template <> struct V16<float> {
     static constexpr int N = 4;
+    __device__ __forceinline__ static void add_raw(float (&a)[4], const uint4 x) {
+        a[0] += __uint_as_float(x.x); a[1] += __uint_as_float(x.y);
+        a[2] += __uint_as_float(x.z); a[3] += __uint_as_float(x.w);
+    }
     __device__ __forceinline__ static void load(const void* p, float (&v)[4]) {
         const float4 x = __ldg(reinterpret_cast<const float4*>(p));
         v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
@@ -58,6 +82,12 @@ template <> struct V16<__nv_bfloat16> {
     }
     __device__ __forceinline__ static void load(const void* p, float (&v)[8]) {
         unpack(__ldg(reinterpret_cast<const uint4*>(p)), v);
+    }
+    __device__ __forceinline__ static void add_raw(float (&a)[8], const uint4 x) {
+        float v[8];
+        unpack(x, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] += v[i];
     }
     __device__ __forceinline__ static void add(const void* p, float (&a)[8]) {
         float v[8];
@@ -96,25 +126,47 @@ struct HopParams {
     int mode;                          // 0 intermediate, 1 last
 };
 
-template <typename T, int CW>
-__global__ void __launch_bounds__(kBlock) spmm_hop_kernel(const HopParams p) {
-    constexpr int L = kG * CW;
+// Lane layout ("full row per edge"): a group of L lanes works on one unit.  Lane
+// gl = e*VP + c holds edge slot e in [0, E) and 16-byte column vector c in [0, VP):
+// one load instruction fetches the complete row slices of E edges with
+// consecutive lanes, so it touches the fewest distinct 128-byte lines (the L1TEX
+// wavefront count is what bounds a gather).  Edge j of a unit piece
+// starting at eb belongs to reduction group g = (j - eb) mod 8, g = e + E*k: lane
+// slot e keeps 8/E accumulators acc[k].  The 8 groups are combined by the fixed
+// butterfly ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) -- cross-lane for the bits of e,
+// in-lane for the bits of k -- so the per-column order is the same for every
+// (E, VP), i.e. for every slice width.  Column indices are loaded coalesced (one
+// per lane) and distributed with shuffles.
+template <typename T, int E, int L, int POL>
+__global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p) {
+    constexpr int NACC = kG / E;
+    constexpr int LOG_E = (E == 1) ? 0 : (E == 2) ? 1 : (E == 4) ? 2 : 3;
     constexpr int VALS = V16<T>::N;
+    // edges per pipeline batch: 16-byte loads per lane per batch = BATCH / E (4 or 8)
+    constexpr int BATCH = (E == 8) ? 64 : (E == 4) ? 32 : 8 * E;
+    constexpr int LPB = BATCH / E;                        // loads per lane per batch
+    constexpr int ISL = (BATCH + L - 1) / L;              // column indices held per lane
     const int lane = threadIdx.x & 31;
     const int gl = lane % L;
-    const int g = gl % kG;
-    const int c = gl / kG;
+    const int gbase = lane - gl;
     const int64_t group = ((int64_t)blockIdx.x * kBlock + threadIdx.x) / L;
     const int64_t u = p.u_begin + group;
     if (u >= p.u_end) return;                           // group-uniform exit
-    const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << ((lane / L) * L));
+    const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << gbase);
+    const int VP = (E == 1) ? min(p.nvec, 32) : p.nvec;  // vectors per pass
+    const int e_raw = gl / VP;
+    const int c = gl - e_raw * VP;
+    const bool active = e_raw < E;
+    const int e = active ? e_raw : E - 1;                // idle lanes mirror a real lane's addresses
+    const int32_t* __restrict__ colp = p.col;
+    const uint32_t ld_in = (uint32_t)p.ld_in;
 
     const int r0 = p.unit_row[u], r1 = p.unit_row[u + 1];
     const int e0 = p.unit_e[u], e1 = p.unit_e[u + 1];
     const bool has_tail = (r1 < p.n) && (e1 > max(p.rp[r1], e0));
     const int r_end = has_tail ? r1 + 1 : r1;
     const int row_vals = p.nvec * VALS;
-    const int npass = (p.nvec + CW - 1) / CW;
+    const int npass = (p.nvec + VP - 1) / VP;
 
     for (int r = max((int64_t)r0, p.row_lo); r < min((int64_t)r_end, p.row_hi); ++r) {
         const int rs_e = p.rp[r], re_e = p.rp[r + 1];
@@ -122,58 +174,103 @@ __global__ void __launch_bounds__(kBlock) spmm_hop_kernel(const HopParams p) {
         const bool head = (r == r0) && (rs_e < e0);
         const bool tail = (r == r1);
         for (int pass = 0; pass < npass; ++pass) {
-            const int vcol = pass * CW + c;
-            const bool col_ok = vcol < p.nvec;
-            const int64_t voff = (int64_t)vcol * 16;
-            float acc[VALS];
+            const int vcol = pass * VP + c;
+            const bool col_ok = active && vcol < p.nvec;
+            const char* __restrict__ vbase = p.S_in + (int64_t)min(vcol, p.nvec - 1) * 16;
+            float acc[NACC][VALS];
 #pragma unroll
-            for (int i = 0; i < VALS; ++i) acc[i] = 0.f;
-            if (col_ok) {
-                int j = eb + g;
-                for (; j + 3 * kG < ee; j += 4 * kG) {
-                    const int s0 = __ldg(p.col + j), s1 = __ldg(p.col + j + kG);
-                    const int s2 = __ldg(p.col + j + 2 * kG), s3 = __ldg(p.col + j + 3 * kG);
-                    float v0[VALS], v1[VALS], v2[VALS], v3[VALS];
-                    V16<T>::load(p.S_in + (int64_t)s0 * p.ld_in + voff, v0);
-                    V16<T>::load(p.S_in + (int64_t)s1 * p.ld_in + voff, v1);
-                    V16<T>::load(p.S_in + (int64_t)s2 * p.ld_in + voff, v2);
-                    V16<T>::load(p.S_in + (int64_t)s3 * p.ld_in + voff, v3);
+            for (int k = 0; k < NACC; ++k)
 #pragma unroll
-                    for (int i = 0; i < VALS; ++i) acc[i] = (((acc[i] + v0[i]) + v1[i]) + v2[i]) + v3[i];
+                for (int i = 0; i < VALS; ++i) acc[k][i] = 0.f;
+            // column indices of a batch: lane gl holds edges base + sl*L + gl (0 past the end)
+            auto load_idx = [&](int base, int (&dst)[ISL]) {
+#pragma unroll
+                for (int sl = 0; sl < ISL; ++sl) {
+                    const int j = base + sl * L + gl;
+                    dst[sl] = (sl * L + gl < BATCH && j < ee) ? __ldg(colp + j) : 0;
                 }
-                for (; j < ee; j += kG) {
-                    const int s0 = __ldg(p.col + j);
-                    V16<T>::add(p.S_in + (int64_t)s0 * p.ld_in + voff, acc);
+            };
+            // 16-byte loads of a batch; slots past the end read row 0 (never accumulated)
+            auto load_data = [&](const int (&ix)[ISL], uint4 (&dst)[LPB]) {
+#pragma unroll
+                for (int t = 0; t < LPB; ++t) {
+                    // edge t*E + e of the batch: held by lane (t*E % L) + e in slot (t*E)/L (E divides L)
+                    const int src = __shfl_sync(gmask, ix[(t * E) / L], gbase + ((t * E) % L) + e);
+                    dst[t] = ld_gather<POL>(vbase + (size_t)(uint32_t)src * ld_in);
+                }
+            };
+            // edge base + t*E + e belongs to group (t*E + e) mod 8, i.e. acc[t % NACC]
+            auto consume = [&](const uint4 (&v)[LPB], int base) {
+                const int rem = ee - base;
+                if (rem >= BATCH) {
+#pragma unroll
+                    for (int t = 0; t < LPB; ++t) V16<T>::add_raw(acc[t % NACC], v[t]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < LPB; ++t)
+                        if (t * E + e < rem) V16<T>::add_raw(acc[t % NACC], v[t]);
+                }
+            };
+            // two-deep software pipeline, unrolled by 2 so the buffers ping-pong without copies:
+            // while batch b is accumulated, batch b+1's rows and batch b+2's indices are in flight
+            int ia[ISL], ib[ISL];
+            uint4 va[LPB], vb[LPB];
+            load_idx(eb, ia);
+            if (eb < ee) load_data(ia, va);
+            load_idx(eb + BATCH, ib);
+            for (int base = eb; base < ee;) {
+                load_idx(base + 2 * BATCH, ia);
+                if (base + BATCH < ee) load_data(ib, vb);
+                consume(va, base);
+                base += BATCH;
+                if (base >= ee) break;
+                load_idx(base + 2 * BATCH, ib);
+                if (base + BATCH < ee) load_data(ia, va);
+                consume(vb, base);
+                base += BATCH;
+            }
+            // fixed butterfly over the 8 reduction groups
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                if (b < LOG_E) {
+                    const int partner = gbase + ((e ^ (1 << b)) * VP + c);
+#pragma unroll
+                    for (int k = 0; k < NACC; ++k)
+#pragma unroll
+                        for (int i = 0; i < VALS; ++i) acc[k][i] += __shfl_sync(gmask, acc[k][i], partner);
+                } else {
+                    const int kb = 1 << (b - LOG_E);
+#pragma unroll
+                    for (int k = 0; k < NACC; ++k)
+                        if ((k & kb) == 0 && (k | kb) < NACC) {
+#pragma unroll
+                            for (int i = 0; i < VALS; ++i) acc[k][i] += acc[k | kb][i];
+                        }
                 }
             }
-            // fixed xor-tree over the 8 edge lanes (lane g == 0 holds the canonical order)
-#pragma unroll
-            for (int o = 1; o < kG; o <<= 1) {
-#pragma unroll
-                for (int i = 0; i < VALS; ++i) acc[i] += __shfl_xor_sync(gmask, acc[i], o);
-            }
-            if (g != 0 || !col_ok) continue;
+            if (e_raw != 0 || !col_ok) continue;
             if (head || tail) {
                 float* dst = p.carry + ((u * 2 + (head ? 0 : 1)) * (int64_t)row_vals) + vcol * VALS;
 #pragma unroll
-                for (int i = 0; i < VALS; ++i) dst[i] = acc[i];
+                for (int i = 0; i < VALS; ++i) dst[i] = acc[0][i];
                 continue;
             }
+            const int64_t voff = (int64_t)vcol * 16;
             float self[VALS];
             V16<T>::load(p.S_in + (int64_t)r * p.ld_in + voff, self);
             const float a = p.rs[r];
-            float out[VALS];
             const float b = p.cs[r];
             const float sig = (p.mode == 0) ? p.gamma * a * b : p.gamma * a;
+            float out[VALS];
             if (p.alpha != 0.f) {
                 float h[VALS];
                 V16<T>::load(p.S0 + (int64_t)r * p.ld_s0 + voff, h);
                 const float beta = (p.mode == 0) ? p.alpha : p.alpha / b;
 #pragma unroll
-                for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[i] + self[i]) + beta * h[i];
+                for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + self[i]) + beta * h[i];
             } else {
 #pragma unroll
-                for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[i] + self[i]);
+                for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + self[i]);
             }
             V16<T>::store(p.S_out + (int64_t)r * p.ld_out + voff, out);
         }
@@ -237,13 +334,26 @@ __global__ void prescale_kernel(const char* __restrict__ H, int64_t ld_h, char* 
     }
 }
 
-template <typename T, int CW>
+template <typename T, int E, int L>
 void launch_hop(const HopParams& p, cudaStream_t s) {
-    constexpr int L = kG * CW;
+    static const int pol = [] { const char* v = getenv("NTP_GATHER_POLICY"); return v ? atoi(v) : 0; }();
     const int64_t groups = p.u_end - p.u_begin;
     const int64_t blocks = cdiv(groups * L, kBlock);
-    spmm_hop_kernel<T, CW><<<(unsigned)blocks, kBlock, 0, s>>>(p);
+    if (pol == 1) spmm_hop_kernel<T, E, L, 1><<<(unsigned)blocks, kBlock, 0, s>>>(p);
+    else if (pol == 2) spmm_hop_kernel<T, E, L, 2><<<(unsigned)blocks, kBlock, 0, s>>>(p);
+    else spmm_hop_kernel<T, E, L, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p);
     NTP_LAUNCH_CHECK();
+}
+
+// (E, L) from the row width: E edge slots of nvec lanes each, E*nvec <= L.
+template <typename T>
+void dispatch_hop(const HopParams& p, int nvec, cudaStream_t s) {
+    if (nvec == 1) launch_hop<T, 8, 8>(p, s);
+    else if (nvec == 2) launch_hop<T, 8, 16>(p, s);
+    else if (nvec <= 4) launch_hop<T, 8, 32>(p, s);
+    else if (nvec <= 8) launch_hop<T, 4, 32>(p, s);
+    else if (nvec <= 16) launch_hop<T, 2, 32>(p, s);
+    else launch_hop<T, 1, 32>(p, s);
 }
 
 }  // namespace
@@ -293,16 +403,8 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     c->carry.ensure((size_t)(csr.U * 2) * nvec * vals * sizeof(float) + 16);
     p.carry = c->carry.as<float>();
     if (p.u_end <= p.u_begin) return;
-    const int CW = nvec >= 3 ? 4 : (nvec == 2 ? 2 : 1);
-    if (dt == NTP_F32) {
-        if (CW == 4) launch_hop<float, 4>(p, s);
-        else if (CW == 2) launch_hop<float, 2>(p, s);
-        else launch_hop<float, 1>(p, s);
-    } else {
-        if (CW == 4) launch_hop<__nv_bfloat16, 4>(p, s);
-        else if (CW == 2) launch_hop<__nv_bfloat16, 2>(p, s);
-        else launch_hop<__nv_bfloat16, 1>(p, s);
-    }
+    if (dt == NTP_F32) dispatch_hop<float>(p, nvec, s);
+    else dispatch_hop<__nv_bfloat16>(p, nvec, s);
     const int64_t fblocks = cdiv((p.u_end - p.u_begin) * 32, kBlock);
     if (dt == NTP_F32) spmm_fixup_kernel<float><<<(unsigned)fblocks, kBlock, 0, s>>>(p);
     else spmm_fixup_kernel<__nv_bfloat16><<<(unsigned)fblocks, kBlock, 0, s>>>(p);
@@ -331,7 +433,7 @@ void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, in
 // (prescaled_input: a.H points at S^0, e.g. the pack epilogue of the split).
 // With alpha != 0, S^0 must outlive hop 1, so it gets its own buffer.
 void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bool prescaled_input,
-               int64_t last_row_lo, int64_t last_row_hi) {
+               LastHop* defer_last) {
     const Graph& g = c->g;
     const Csr& csr = a.transposed ? g.bwd() : g.fwd();
     const float* rs = a.transposed ? g.dinv_out_p() : g.dinv_in_p();
@@ -370,18 +472,32 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
     for (int k = 1; k <= a.K; ++k) {
         const int nxt = (a.K - k) % 2;
         const bool last = (k == a.K);
+        if (last && defer_last) {
+            *defer_last = LastHop{&csr, rs, cs, sin, ld_sin, S0, ld_s0, bufs[nxt], lds[nxt], a.cols, a.dtype,
+                                  a.gamma, a.alpha};
+            return;
+        }
         const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
         if (timed) NTP_CUDA(cudaEventRecord(c->hop_ev[c->hop_ev_used], s));
-        const int64_t lo = last ? last_row_lo : 0;
-        const int64_t hi = last ? last_row_hi : -1;
         spmm_hop(c, csr, rs, cs, sin, bufs[nxt], S0, ld_sin, lds[nxt], ld_s0, a.cols, a.dtype, a.gamma, a.alpha,
-                 last ? 1 : 0, lo, hi, s);
+                 last ? 1 : 0, 0, -1, s);
         if (timed) {
             NTP_CUDA(cudaEventRecord(c->hop_ev[c->hop_ev_used + 1], s));
             c->hop_ev_used += 2;
         }
         sin = bufs[nxt];
         ld_sin = lds[nxt];
+    }
+}
+
+void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi, cudaStream_t s, bool time_hops) {
+    const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
+    if (timed) NTP_CUDA(cudaEventRecord(c->hop_ev[c->hop_ev_used], s));
+    spmm_hop(c, *lh.csr, lh.rs, lh.cs, lh.sin, lh.out, lh.S0, lh.ld_sin, lh.ld_out, lh.ld_s0, lh.cols, lh.dt, lh.gamma,
+             lh.alpha, 1, row_lo, row_hi, s);
+    if (timed) {
+        NTP_CUDA(cudaEventRecord(c->hop_ev[c->hop_ev_used + 1], s));
+        c->hop_ev_used += 2;
     }
 }
 

@@ -1,0 +1,117 @@
+"""Multi-GPU parity check, one rank per GPU (run by tests/test_gpu_multi.py):
+
+    python -m torch.distributed.run --nproc-per-node P --master-addr 127.0.0.1 tests/mp_check.py [config]
+
+Per rank, through the C ABI with the library's own NCCL communicator:
+  1. split/gather (v2f/f2v) against the oracle's layout definitions, bitwise (fp32, bf16);
+  2. K-hop propagation of this rank's FEATURE slice vs the oracle (R10, 1e-5) and
+     bitwise vs the same columns of a single-GPU (P = 1) propagation;
+  3. 3 training epochs with the overlap scheduler on and off: losses vs the oracle
+     (1e-4), and on == off bitwise (scheduling neutrality).
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2412_20379_b200 import ntp  # noqa: E402
+from paper_2412_20379_b200 import dist as pd  # noqa: E402
+
+
+def main(name):
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = pd.broadcast_unique_id(dist, rank)
+    cfg = synth.get_config(name)
+    ctx = ntp.Context(device=local, rank=rank, world=world, unique_id=uid)
+    thr = synth.rmat_thresholds(*cfg.abc)
+    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric)
+    g = oracle.graph.graph_from_config(cfg)
+    n = g.n
+
+    # ---- 1. layouts
+    for dt, tdt, eb in ((ntp.NTP_F32, torch.float32, 4), (ntp.NTP_BF16, torch.bfloat16, 2)):
+        w = 37
+        Xfull = synth.features(99, n, w)
+        part = oracle.layout.partition(n, w, world, eb)
+        Xv = torch.from_numpy(oracle.layout.vertex_part(Xfull, n, w, world, rank, eb)[:, :w].copy()).to(tdt).cuda()
+        Hf = torch.empty(part["V_pad"], part["d_s"], dtype=tdt, device="cuda")
+        ctx.layout_v2f(Xv, Hf)
+        ref_f = oracle.layout.feature_part(torch.from_numpy(Xfull).to(tdt).float().numpy(), n, w, world, rank, eb)
+        torch.cuda.synchronize()
+        assert np.array_equal(Hf.float().cpu().numpy(), ref_f), f"v2f mismatch rank {rank}"
+        back = torch.zeros_like(Xv)
+        ctx.layout_f2v(Hf, back)
+        torch.cuda.synchronize()
+        assert torch.equal(back, Xv), f"f2v(v2f(x)) != x rank {rank}"
+
+    # ---- 2. propagation of this rank's slice
+    w = 41
+    part = oracle.layout.partition(n, w, world, 4)
+    d_s = part["d_s"]
+    H = synth.features(5, n, w)
+    Hs = oracle.layout.feature_part(H, n, w, world, rank, 4)       # [V_pad x d_s]
+    ctx1 = ntp.Context(device=local)                                 # P = 1 reference on the same GPU
+    ctx1.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric)
+    full_w = oracle.layout.slice_width(w, 1, 4)
+    Hp = np.zeros((n, full_w), np.float32)
+    Hp[:, :w] = H
+    Hp1 = np.zeros((n, world * d_s), np.float32)
+    Hp1[:, :w] = H
+    for transposed in (False, True):
+        f = ctx.propagate_bwd if transposed else ctx.propagate_fwd
+        Ht = torch.from_numpy(Hs).cuda()
+        Zt = torch.empty_like(Ht)
+        f(Ht, Zt, cfg.K, cfg.gamma, cfg.alpha)
+        torch.cuda.synchronize()
+        of = oracle.propagate.propagate_bwd if transposed else oracle.propagate.propagate_fwd
+        ref = of(g, Hs[:n], cfg.K, cfg.gamma, cfg.alpha)
+        den = of(g, np.abs(Hs[:n]), cfg.K, cfg.gamma, cfg.alpha)
+        err = np.abs(Zt.double().cpu().numpy()[:n] - ref)
+        assert (err <= 1e-5 * den + 1e-30).all(), f"propagation parity rank {rank} T={transposed}"
+        # slice invariance across GPUs: same columns of the P=1 run, bitwise
+        H1 = torch.from_numpy(Hp1).cuda()
+        Z1 = torch.empty_like(H1)
+        (ctx1.propagate_bwd if transposed else ctx1.propagate_fwd)(H1, Z1, cfg.K, cfg.gamma, cfg.alpha)
+        torch.cuda.synchronize()
+        assert torch.equal(Z1[:, rank * d_s:(rank + 1) * d_s], Zt[:n]), f"P-invariance rank {rank}"
+
+    # ---- 3. epochs, overlap off / on
+    X, y, m = pd.rank_inputs(cfg, world, rank)
+    W0h, W1h = synth.model_weights(cfg)
+    lr = cfg.lr * 50
+    ref_losses, _, _ = oracle.model.train(g, *synth.config_inputs(cfg), W0h, W1h, cfg.K, cfg.gamma, cfg.alpha, lr, 3)
+    results = []
+    for overlap in (False, True):
+        W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+        flags = (ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if overlap else 0)
+        model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
+                     dtype=ntp.NTP_F32, chunks=3, flags=flags)
+        losses = []
+        for _ in range(3):
+            rep = ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
+            losses.append(rep["loss"])
+        for a, b in zip(losses, ref_losses):
+            assert abs(a - b) <= 1e-4, f"loss {a} vs oracle {b} (overlap={overlap})"
+        results.append((losses, W0.cpu(), W1.cpu()))
+    assert results[0][0] == results[1][0], "overlap changed the loss"
+    assert torch.equal(results[0][1], results[1][1]) and torch.equal(results[0][2], results[1][2])
+    dist.barrier()
+    if rank == 0:
+        print(f"MP OK world={world} config={name} losses={results[1][0]}", flush=True)
+    ctx.close()
+    ctx1.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "small_dir")
