@@ -170,6 +170,18 @@ ntp_status ntp_propagate_fwd(ntp_ctx* ctx, const ntp_tensor* H, ntp_tensor* Z, i
 ntp_status ntp_propagate_bwd(ntp_ctx* ctx, const ntp_tensor* G, ntp_tensor* dH, int K,
                              float gamma, float alpha, ntp_stream s);
 
+/* ------------------------------------------------------ MLP contraction (a2, a10) */
+
+/* C[M x N] = op(A) op(B) on the tensor cores (tcgen05 kind::tf32, 3xTF32 split: fp32-level
+ * accuracy, reading R11).  All matrices fp32, row-major, DEVICE memory, caller-owned.
+ * op(A) = A (stored [M x K], lda) or A^T (trans_a: stored [K x M]); op(B) = B (stored [K x N])
+ * or B^T (trans_b: stored [N x K]).  lda, ldb: multiples of 4, 16-byte aligned bases
+ * (NTP_ERR_SHAPE otherwise).  epilogue: 0 plain, 1 ReLU (Eq. 4 sigma).  These are the
+ * GEMMs of the MLP forward and backward inside ntp_train_epoch. */
+ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int trans_a,
+                        const float* B, int64_t ldb, int trans_b, float* C, int64_t ldc, int epilogue,
+                        ntp_stream s);
+
 /* ------------------------------------------------------ one epoch (Alg. 1) */
 
 #define NTP_M_W1_AFTER_PROP 1u  /* propagate H1 (w = hid) and apply W1 after (reading R3) */

@@ -441,6 +441,21 @@ ntp_status ntp_propagate_bwd(ntp_ctx* c, const ntp_tensor* G, ntp_tensor* dH, in
     return do_propagate(c, G, dH, K, gamma, alpha, s, true);
 }
 
+// ------------------------------------------------------------------ MLP GEMM
+ntp_status ntp_gemm_f32(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int trans_a,
+                        const float* B, int64_t ldb, int trans_b, float* C, int64_t ldc, int epilogue,
+                        ntp_stream st) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(A && B && C, NTP_ERR_ARG, "null operand");
+    NTP_CHECK(M >= 0 && N >= 0 && K > 0 && M < (int64_t(1) << 31) && N <= 65535 * 256, NTP_ERR_ARG, "bad sizes");
+    NTP_CHECK(epilogue == 0 || epilogue == 1, NTP_ERR_ARG, "epilogue must be 0 or 1");
+    NTP_CHECK(ldc >= N, NTP_ERR_SHAPE, "ldc < N");
+    NTP_CUDA(cudaSetDevice(c->device));
+    gemm_tf32x3(c, M, N, K, A, lda, trans_a != 0, B, ldb, trans_b == 0, C, ldc, epilogue, nullptr, 0,
+                (cudaStream_t)st);
+    NTP_API_END(c)
+}
+
 // ------------------------------------------------------------------ epoch
 ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                            const uint8_t* train_mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep,

@@ -1,0 +1,418 @@
+// gemm.cu — tensor-core MLP GEMMs ("Tensor cores are used only for the
+// small dense MLP GEMMs", BASELINE north_star) on 5th-generation tensor cores (tcgen05).
+//
+// C[M x N] = op(A)[M x K] . op(B)[K x N] in fp32 with fp32-level accuracy (reading R11):
+// 3xTF32 split.  Every fp32 operand x is split into hi = rn_tf32(x) and lo = x - hi (exact in
+// fp32); the product is accumulated in fp32 TMEM as hi_a*hi_b + hi_a*lo_b + lo_a*hi_b (the
+// dropped lo*lo term is ~2^-22 relative), i.e. three kind::tf32 MMAs per K step.
+//
+// Structure (one 128 x BN output tile per CTA, optional split-K over grid.z):
+//   warp 0   : TMEM allocation + TMA producer (one elected lane; 128-byte swizzled tiles)
+//   warp 1   : MMA issuer (one lane: tcgen05.mma.cta_group::1.kind::tf32, tcgen05.commit)
+//   warps 2-5: split workers (rn_tf32 in place + lo tile, fence.proxy.async) during the main
+//              loop, then the epilogue (tcgen05.ld 32x32b -> registers -> global)
+// Operands may be K-major (K contiguous) or MN-major (M/N contiguous); both are loaded by TMA
+// with SWIZZLE_128B and described to the tensor core with the matching smem descriptor.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "ntp_internal.cuh"
+
+namespace ntp {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;                 // fp32 elements per 128-byte swizzle row
+constexpr int kGemmThreads = 192;
+constexpr int kTileA = BM * BK * 4;    // 16 KB
+
+struct GemmParams {
+    int M, N, K;
+    int k_tiles_total, k_tiles_per_split;
+    int BN, bn_alloc, stages;
+    uint32_t idesc;
+    uint32_t tmem_cols;
+    float* C;
+    int64_t ldc;
+    int64_t split_stride;               // elements between split-K partial outputs
+    const float* aux;
+    int64_t ldaux;
+    int epi;                            // 0 store, 1 relu, 2 keep where aux > 0
+    uint32_t mn_lbo, mn_sbo;            // MN-major descriptor byte offsets (16-byte units)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// 128B-swizzled UMMA smem descriptors (sm_100 format: version 1, layout type 2 = SWIZZLE_128B).
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t addr) {
+    // rows of 128 B, 8-row atoms 1024 B apart (SBO); LBO unused for swizzled K-major
+    return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    // MN-major tf32 needs layout type 1 = SWIZZLE_128B_BASE32B (32-byte swizzle atoms, 4 K-rows
+    // of 128 B per atom): 32-element MN atoms `lbo` apart, 4-row K groups `sbo` apart (16-B units)
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)lbo << 16) | ((uint64_t)sbo << 32) | (1ull << 46) |
+           (1ull << 61);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ float tf32_rn(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// split a tile in place: t <- rn_tf32(t), lo <- t - rn_tf32(t)   (16 bytes per step)
+__device__ __forceinline__ void split_tile(uint8_t* t, uint8_t* lo, int bytes, int tid, int nthreads) {
+    for (int off = tid * 16; off < bytes; off += nthreads * 16) {
+        float4 x = *reinterpret_cast<float4*>(t + off);
+        float4 h = make_float4(tf32_rn(x.x), tf32_rn(x.y), tf32_rn(x.z), tf32_rn(x.w));
+        float4 l = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        *reinterpret_cast<float4*>(t + off) = h;
+        *reinterpret_cast<float4*>(lo + off) = l;
+    }
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages;
+    const int tileB = p.bn_alloc * BK * 4;
+    const int stage_bytes = 2 * kTileA + 2 * tileB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+    uint64_t* full = bars;
+    uint64_t* split = bars + S;
+    uint64_t* empty = bars + 2 * S;
+    uint64_t* accum = bars + 3 * S;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM;
+    const int n0 = blockIdx.y * p.BN;
+    const int kt0 = blockIdx.z * p.k_tiles_per_split;
+    const int nk = min(p.k_tiles_per_split, p.k_tiles_total - kt0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&split[s], 128);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(p.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0 && nk > 0) {
+            // ---------------- TMA producer
+            for (int i = 0; i < nk; ++i) {
+                const int s = i % S;
+                if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+                uint8_t* sa = smem + s * stage_bytes;
+                uint8_t* sb = sa + 2 * kTileA;
+                const int k0 = (kt0 + i) * BK;
+                mbar_expect_tx(&full[s], kTileA + tileB);
+                if (A_MN) {
+                    for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 4096, &tmA, &full[s], m0 + 32 * j, k0);
+                } else {
+                    tma_load_2d(sa, &tmA, &full[s], k0, m0);
+                }
+                if (B_MN) {
+                    for (int j = 0; j < p.bn_alloc / 32; ++j) tma_load_2d(sb + j * 4096, &tmB, &full[s], n0 + 32 * j, k0);
+                } else {
+                    tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && nk > 0) {
+            // ---------------- MMA issuer
+            for (int i = 0; i < nk; ++i) {
+                const int s = i % S;
+                mbar_wait(&split[s], (i / S) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a = smem_u32(smem + s * stage_bytes);
+                const uint32_t alo = a + kTileA;
+                const uint32_t b = a + 2 * kTileA;
+                const uint32_t blo = b + tileB;
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {
+                    const uint32_t ao = A_MN ? k * 1024 : k * 32;   // K step of 8 tf32
+                    const uint32_t bo = B_MN ? k * 1024 : k * 32;
+                    const uint64_t dA = A_MN ? desc_mnmajor(a + ao, p.mn_lbo, p.mn_sbo) : desc_kmajor(a + ao);
+                    const uint64_t dAlo = A_MN ? desc_mnmajor(alo + ao, p.mn_lbo, p.mn_sbo) : desc_kmajor(alo + ao);
+                    const uint64_t dB = B_MN ? desc_mnmajor(b + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(b + bo);
+                    const uint64_t dBlo = B_MN ? desc_mnmajor(blo + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(blo + bo);
+                    mma_tf32(tmem, dA, dB, p.idesc, (i > 0 || k > 0) ? 1u : 0u);
+                    mma_tf32(tmem, dA, dBlo, p.idesc, 1u);
+                    mma_tf32(tmem, dAlo, dB, p.idesc, 1u);
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(accum);
+        }
+    } else {
+        // ---------------- split workers, then epilogue
+        const int tid = threadIdx.x - 64;
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % S;
+            mbar_wait(&full[s], (i / S) & 1);
+            uint8_t* sa = smem + s * stage_bytes;
+            split_tile(sa, sa + kTileA, kTileA, tid, 128);
+            uint8_t* sb = sa + 2 * kTileA;
+            split_tile(sb, sb + tileB, tileB, tid, 128);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&split[s]);
+        }
+        const int q = warp & 3;                       // TMEM lane quarter of this warp
+        const int row = m0 + 32 * q + lane;
+        if (nk > 0) {
+            mbar_wait(accum, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        float* Cb = p.C + (int64_t)blockIdx.z * p.split_stride;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+            uint32_t r[32];
+            if (nk > 0) {
+                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) r[j] = 0u;
+            }
+            if (row < p.M) {
+                float* dst = Cb + (int64_t)row * p.ldc + n0 + c0;
+                const int ncol = min(32, p.N - (n0 + c0));
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    v[j] = __uint_as_float(r[j]);
+                    if (p.epi == 1) v[j] = fmaxf(v[j], 0.f);
+                }
+                if (p.epi == 2) {
+                    const float* ax = p.aux + (int64_t)row * p.ldaux + n0 + c0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < ncol && !(ax[j] > 0.f)) v[j] = 0.f;
+                }
+                if (ncol == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < ncol) dst[j] = v[j];
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
+    }
+}
+
+// out[m][n] = sum_z part[z][m][n] in split order (deterministic), then the epilogue.
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int M, int N,
+                                     int64_t ldp, float* __restrict__ C, int64_t ldc, int epi,
+                                     const float* __restrict__ aux, int64_t ldaux) {
+    const int64_t total = (int64_t)M * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = i / N, n = i % N;
+        float acc = 0.f;
+        for (int z = 0; z < splits; ++z) acc += part[z * split_stride + m * ldp + n];
+        if (epi == 1) acc = fmaxf(acc, 0.f);
+        else if (epi == 2) acc = aux[m * ldaux + n] > 0.f ? acc : 0.f;
+        C[m * ldc + n] = acc;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    NTP_CHECK(fn != nullptr, NTP_ERR_CUDA, "cuTensorMapEncodeTiled not available");
+    return fn;
+}
+
+// 2-D fp32 tensor map over a row-major matrix with `rows` rows of `cols` elements (stride ld).
+CUtensorMap make_map(const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    NTP_CHECK(((uintptr_t)base % 16) == 0 && (ld * 4) % 16 == 0, NTP_ERR_SHAPE,
+              "GEMM operand must be 16-byte aligned with ld %% 4 == 0 (ld=%lld)", (long long)ld);
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    NTP_CHECK(r == CUDA_SUCCESS, NTP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return m;
+}
+
+template <bool A_MN, bool B_MN>
+void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, dim3 grid, size_t smem,
+                 cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        NTP_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      227 * 1024));
+        configured = true;
+    }
+    gemm_tf32x3_kernel<A_MN, B_MN><<<grid, kGemmThreads, smem, s>>>(ta, tb, p);
+    NTP_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+// C[M x N] = op(A) op(B).  A: a_mn ? stored [K][M] (ld lda) : stored [M][K];
+// B: b_mn ? stored [K][N] : stored [N][K].  epi: 0 store, 1 ReLU, 2 keep where aux > 0.
+void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool a_mn, const float* B,
+                 int64_t ldb, bool b_mn, float* C, int64_t ldc, int epi, const float* aux, int64_t ldaux,
+                 cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    NTP_CHECK(K > 0, NTP_ERR_ARG, "GEMM with K == 0");
+    GemmParams p{};
+    p.M = (int)M;
+    p.N = (int)N;
+    p.K = (int)K;
+    p.BN = (int)std::min<int64_t>(256, ((N + 15) / 16) * 16);
+    p.bn_alloc = ((p.BN + 31) / 32) * 32;
+    const int stage_bytes = 2 * kTileA + 2 * p.bn_alloc * BK * 4;
+    p.stages = std::max(2, std::min(4, (225 * 1024 - 1024 - 256) / stage_bytes));
+    p.tmem_cols = 32;
+    while ((int)p.tmem_cols < p.BN) p.tmem_cols <<= 1;
+    p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+              ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    p.k_tiles_total = (int)cdiv(K, BK);
+    const int m_tiles = (int)cdiv(M, BM);
+    const int n_tiles = (int)cdiv(N, p.BN);
+    int splits = 1;
+    if ((int64_t)m_tiles * n_tiles < 2 * 148) {
+        splits = (int)std::min<int64_t>(cdiv(2 * 148, (int64_t)m_tiles * n_tiles), std::max(1, p.k_tiles_total / 4));
+        splits = std::max(splits, 1);
+    }
+    p.k_tiles_per_split = (int)cdiv(p.k_tiles_total, splits);
+    splits = (int)cdiv(p.k_tiles_total, p.k_tiles_per_split);
+    p.aux = aux;
+    p.ldaux = ldaux;
+    p.mn_lbo = 4096 >> 4;
+    p.mn_sbo = 512 >> 4;
+    if (const char* v = getenv("NTP_MN_LBO")) p.mn_lbo = (uint32_t)atoi(v) >> 4;
+    if (const char* v = getenv("NTP_MN_SBO")) p.mn_sbo = (uint32_t)atoi(v) >> 4;
+    const CUtensorMapSwizzle mnswz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    CUtensorMap ta = a_mn ? make_map(A, M, K, lda, 32, 32, mnswz) : make_map(A, K, M, lda, 32, BM);
+    CUtensorMap tb = b_mn ? make_map(B, N, K, ldb, 32, 32, mnswz) : make_map(B, K, N, ldb, 32, p.bn_alloc);
+    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (3 * p.stages + 2) * 8;
+    dim3 grid(m_tiles, n_tiles, splits);
+    if (splits == 1) {
+        p.C = C;
+        p.ldc = ldc;
+        p.epi = epi;
+        p.split_stride = 0;
+    } else {
+        const int64_t ldp = N;
+        c->m_gemm_part.ensure((size_t)splits * M * ldp * sizeof(float) + 16);
+        p.C = c->m_gemm_part.as<float>();
+        p.ldc = ldp;
+        p.epi = 0;
+        p.split_stride = M * ldp;
+    }
+    if (a_mn && b_mn) launch_gemm<true, true>(ta, tb, p, grid, smem, s);
+    else if (a_mn) launch_gemm<true, false>(ta, tb, p, grid, smem, s);
+    else if (b_mn) launch_gemm<false, true>(ta, tb, p, grid, smem, s);
+    else launch_gemm<false, false>(ta, tb, p, grid, smem, s);
+    count_launch(c);
+    if (splits > 1) {
+        const int64_t total = M * N;
+        splitk_reduce_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 8), 256, 0, s>>>(
+            c->m_gemm_part.as<float>(), splits, M * N, (int)M, (int)N, N, C, ldc, epi, aux, ldaux);
+        NTP_LAUNCH_CHECK();
+        count_launch(c);
+    }
+}
+
+}  // namespace ntp

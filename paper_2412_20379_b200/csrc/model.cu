@@ -13,6 +13,8 @@
 // Dense GEMMs: cuBLAS SGEMM (fp32 FMA, no TF32: parity reading R11).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "ntp_internal.cuh"
 
@@ -20,15 +22,22 @@ namespace ntp {
 
 namespace {
 
-__global__ void relu_kernel(float* __restrict__ x, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        x[i] = fmaxf(x[i], 0.f);
+// dH1 = dH1 .* [H1 > 0]  (ReLU'(0) = 0, reading R12), strided rows
+__global__ void relu_grad_kernel(float* __restrict__ g, const float* __restrict__ h, int64_t rows, int32_t cols,
+                                 int64_t ldg, int64_t ldh) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * cols;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / cols, k = i % cols;
+        g[r * ldg + k] = h[r * ldh + k] > 0.f ? g[r * ldg + k] : 0.f;
+    }
 }
 
-// dH1 = dH1 .* [H1 > 0]  (ReLU'(0) = 0, reading R12)
-__global__ void relu_grad_kernel(float* __restrict__ g, const float* __restrict__ h, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        g[i] = h[i] > 0.f ? g[i] : 0.f;
+__global__ void relu_rows_kernel(float* __restrict__ x, int64_t rows, int32_t cols, int64_t ld) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * cols;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / cols, k = i % cols;
+        x[r * ld + k] = fmaxf(x[r * ld + k], 0.f);
+    }
 }
 
 template <typename T> __device__ __forceinline__ float ldf(const T* p);
@@ -48,7 +57,7 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
                                                            const uint8_t* __restrict__ mask, int64_t row0, int64_t n,
                                                            TOut* __restrict__ out, int out_blocked,
                                                            const float* __restrict__ gscale, double* __restrict__ part,
-                                                           int64_t* __restrict__ cnt) {
+                                                           int64_t* __restrict__ cnt, int64_t ld_plain) {
     __shared__ double s_loss[8];
     __shared__ int64_t s_cnt[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -60,7 +69,7 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
         const bool train = gr < n && mask[v] != 0;
         auto in_at = [&](int col) -> float {
             if (in_blocked) return ldf<TIn>(in + ((int64_t)(col / d_s) * V_p + v) * d_s + col % d_s);
-            return ldf<TIn>(in + v * (int64_t)C + col);
+            return ldf<TIn>(in + v * ld_plain + col);
         };
         float mx = -INFINITY;
         for (int col = lane; col < C; col += 32) mx = fmaxf(mx, in_at(col));
@@ -80,7 +89,7 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
             float gval = 0.f;
             if (train) gval = (expf(in_at(col) - mx) * inv - (col == yv ? 1.f : 0.f)) * sc;
             if (out_blocked) stf<TOut>(out + ((int64_t)(col / d_s) * V_p + v) * d_s + col % d_s, gval);
-            else stf<TOut>(out + v * (int64_t)C + col, gval);
+            else stf<TOut>(out + v * ld_plain + col, gval);
         }
     }
     if (lane == 0) {
@@ -160,6 +169,30 @@ void gemm_rm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, cons
                          (int)K, &one, B, (int)ldb, A, (int)lda, &beta, C, (int)ldc));
 }
 
+// MLP GEMM C = op(A) op(B) (+ epilogue: 1 ReLU, 2 keep where aux > 0) on the tensor cores
+// (gemm.cu, tcgen05 3xTF32); NTP_GEMM=cublas selects cuBLAS SGEMM instead (A/B comparison).
+void mlp_gemm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+              const float* B, int64_t ldb, float* C, int64_t ldc, cudaStream_t s, int epi = 0,
+              const float* aux = nullptr, int64_t ldaux = 0) {
+    static const bool use_cublas = [] {
+        const char* v = getenv("NTP_GEMM");
+        return v && std::string(v) == "cublas";
+    }();
+    if (!use_cublas) {
+        gemm_tf32x3(c, M, N, K, A, lda, ta, B, ldb, !tb, C, ldc, epi, aux, ldaux, s);
+        return;
+    }
+    gemm_rm(c, ta, tb, M, N, K, A, lda, B, ldb, C, ldc);
+    if (epi == 1) relu_rows_kernel<<<eblocks(M * N), 256, 0, s>>>(C, M, (int32_t)N, ldc);
+    if (epi == 2) relu_grad_kernel<<<eblocks(M * N), 256, 0, s>>>(C, aux, M, (int32_t)N, ldc, ldaux);
+    if (epi) {
+        NTP_LAUNCH_CHECK();
+        count_launch(c);
+    }
+}
+
+inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
+
 }  // namespace
 
 // Propagate K hops on this rank's feature slice (a.Z = output slice [V_pad x d_s])
@@ -238,32 +271,58 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     NTP_CUDA(cudaEventRecord(c->ev[40], user ? user : (cudaStream_t)0));
     NTP_CUDA(cudaStreamWaitEvent(s, c->ev[40], 0));
 
-    // ---- inputs (e2e: copy host inputs in)
+    // ---- inputs (e2e: copy host inputs in).  GEMM operands need 16-byte row pitch (TMA).
+    const int64_t ldXp = round4(m->d_in), ldH = round4(m->hid), ldL = round4(std::max(m->C, m->hid));
+    const int64_t ldC1 = round4(m->C);
     const float* X = static_cast<const float*>(X_v->data);
-    const int64_t ld_x = X_v->ld;
+    int64_t ldx = X_v->ld;
     const int32_t* lab = labels_v;
     const uint8_t* msk = mask_v;
     if (m->flags & NTP_M_HOST_INPUTS) {
-        c->m_Xs.ensure((size_t)V_p * m->d_in * sizeof(float));
+        c->m_Xs.ensure((size_t)V_p * ldXp * sizeof(float));
         c->m_lab.ensure((size_t)V_p * sizeof(int32_t));
         c->m_mask.ensure((size_t)V_p);
-        NTP_CUDA(cudaMemcpy2DAsync(c->m_Xs.p, m->d_in * sizeof(float), X_v->data, ld_x * sizeof(float),
+        NTP_CUDA(cudaMemcpy2DAsync(c->m_Xs.p, ldXp * sizeof(float), X_v->data, ldx * sizeof(float),
                                    m->d_in * sizeof(float), V_p, cudaMemcpyHostToDevice, s));
         NTP_CUDA(cudaMemcpyAsync(c->m_lab.p, labels_v, V_p * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         NTP_CUDA(cudaMemcpyAsync(c->m_mask.p, mask_v, V_p, cudaMemcpyHostToDevice, s));
         X = c->m_Xs.as<float>();
+        ldx = ldXp;
         lab = c->m_lab.as<int32_t>();
         msk = c->m_mask.as<uint8_t>();
+    } else if ((ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(X) % 16) != 0) {
+        c->m_Xs.ensure((size_t)V_p * ldXp * sizeof(float));
+        NTP_CUDA(cudaMemcpy2DAsync(c->m_Xs.p, ldXp * sizeof(float), X, ldx * sizeof(float), m->d_in * sizeof(float),
+                                   V_p, cudaMemcpyDeviceToDevice, s));
+        X = c->m_Xs.as<float>();
+        ldx = ldXp;
     }
-    const int64_t ldx = (m->flags & NTP_M_HOST_INPUTS) ? m->d_in : ld_x;
-    float* W0p = static_cast<float*>(W0->data);
-    float* W1p = static_cast<float*>(W1->data);
+    float* W0u = static_cast<float*>(W0->data);   // updated in place by SGD
+    float* W1u = static_cast<float*>(W1->data);
+    const float* W0g = W0u;                       // GEMM views (16-byte pitch)
+    int64_t ldw0 = m->hid;
+    if ((m->hid % 4) != 0 || (reinterpret_cast<uintptr_t>(W0u) % 16) != 0) {
+        c->m_W0p.ensure((size_t)m->d_in * ldH * sizeof(float));
+        NTP_CUDA(cudaMemcpy2DAsync(c->m_W0p.p, ldH * sizeof(float), W0u, m->hid * sizeof(float),
+                                   m->hid * sizeof(float), m->d_in, cudaMemcpyDeviceToDevice, s));
+        W0g = c->m_W0p.as<float>();
+        ldw0 = ldH;
+    }
+    const float* W1g = W1u;
+    int64_t ldw1 = m->C;
+    if ((m->C % 4) != 0 || (reinterpret_cast<uintptr_t>(W1u) % 16) != 0) {
+        c->m_W1p.ensure((size_t)m->hid * ldC1 * sizeof(float));
+        NTP_CUDA(cudaMemcpy2DAsync(c->m_W1p.p, ldC1 * sizeof(float), W1u, m->C * sizeof(float), m->C * sizeof(float),
+                                   m->hid, cudaMemcpyDeviceToDevice, s));
+        W1g = c->m_W1p.as<float>();
+        ldw1 = ldC1;
+    }
 
     // ---- scratch
-    c->m_H1.ensure((size_t)V_p * m->hid * sizeof(float));
-    c->m_L.ensure((size_t)V_p * std::max(m->C, m->hid) * sizeof(float));
-    c->m_dL.ensure((size_t)V_p * std::max(m->C, m->hid) * sizeof(float));
-    c->m_dH1.ensure((size_t)V_p * m->hid * sizeof(float));
+    c->m_H1.ensure((size_t)V_p * ldH * sizeof(float));
+    c->m_L.ensure((size_t)V_p * ldL * sizeof(float));
+    c->m_dL.ensure((size_t)V_p * ldL * sizeof(float));
+    c->m_dH1.ensure((size_t)V_p * ldH * sizeof(float));
     const int64_t n_w = (int64_t)m->d_in * m->hid + (int64_t)m->hid * m->C;
     c->m_dW.ensure((size_t)n_w * sizeof(float));
     c->m_scal.ensure(4 * sizeof(double));
@@ -287,20 +346,19 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     int ei = 0;
     NTP_CUDA(cudaEventRecord(E[ei++], s));   // E0 start
 
-    // a2: MLP forward
-    gemm_rm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0p, m->hid, H1, m->hid);
-    relu_kernel<<<eblocks(V_p * m->hid), 256, 0, s>>>(H1, V_p * m->hid);
-    NTP_LAUNCH_CHECK();
-    count_launch(c);
+    // a2: MLP forward (ReLU fused into the GEMM epilogue)
+    mlp_gemm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0g, ldw0, H1, ldH, s, /*relu*/ 1);
     const float* prop_src = H1;             // rows propagated (w columns)
+    int64_t ld_src = ldH;
     if (!after) {
-        gemm_rm(c, false, false, V_p, m->C, m->hid, H1, m->hid, W1p, m->C, L, m->C);
+        mlp_gemm(c, false, false, V_p, m->C, m->hid, H1, ldH, W1g, ldw1, L, ldL, s);
         prop_src = L;
+        ld_src = ldL;
     }
     NTP_CUDA(cudaEventRecord(E[ei++], s));   // E1 mlp_fwd done
 
     // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
-    pack_v2f(c, prop_src, w, w, c->send.p, V_p, d_s, P, g.dinv_out_p(), row0, n, NTP_F32, dt, s);
+    pack_v2f(c, prop_src, ld_src, w, c->send.p, V_p, d_s, P, g.dinv_out_p(), row0, n, NTP_F32, dt, s);
     alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(cudaEventRecord(E[ei++], s));   // E2 v2f done
 
@@ -329,11 +387,12 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     if (!after) {
         if (dt == NTP_F32)
             softmax_xent_kernel<float, float><<<lb, 256, 0, s>>>((const float*)c->recv.p, 1, V_p, d_s, m->C, lab, msk,
-                                                                 row0, n, (float*)c->send.p, 1, gscale_bwd, part, cnt);
+                                                                 row0, n, (float*)c->send.p, 1, gscale_bwd, part, cnt,
+                                                                 0);
         else
             softmax_xent_kernel<__nv_bfloat16, __nv_bfloat16><<<lb, 256, 0, s>>>(
                 (const __nv_bfloat16*)c->recv.p, 1, V_p, d_s, m->C, lab, msk, row0, n, (__nv_bfloat16*)c->send.p, 1,
-                gscale_bwd, part, cnt);
+                gscale_bwd, part, cnt, 0);
         NTP_LAUNCH_CHECK();
         count_launch(c);
         if (P * d_s > m->C) {
@@ -348,16 +407,16 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         }
     } else {
         // Z_v = unpack(recv) [V_p x hid]; logits = Z_v W1; dlogits; dZ_v = dlogits W1^T -> pack
-        float* Zv = dH1;   // reuse [V_p x hid]
-        unpack_f2v(c, c->recv.p, V_p, d_s, P, Zv, m->hid, m->hid, dt, NTP_F32, s);
-        gemm_rm(c, false, false, V_p, m->C, m->hid, Zv, m->hid, W1p, m->C, L, m->C);
+        float* Zv = dH1;   // reuse [V_p x ldH]
+        unpack_f2v(c, c->recv.p, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s);
+        mlp_gemm(c, false, false, V_p, m->C, m->hid, Zv, ldH, W1g, ldw1, L, ldL, s);
         softmax_xent_kernel<float, float><<<lb, 256, 0, s>>>(L, 0, V_p, d_s, m->C, lab, msk, row0, n, dL, 0, nullptr,
-                                                             part, cnt);
+                                                             part, cnt, ldL);
         NTP_LAUNCH_CHECK();
         count_launch(c);
-        gemm_rm(c, true, false, m->hid, m->C, V_p, Zv, m->hid, dL, m->C, dW1, m->C);          // dW1 = Z_v^T dlogits
-        gemm_rm(c, false, true, V_p, m->hid, m->C, dL, m->C, W1p, m->C, L, m->hid);           // dZ_v -> L
-        pack_v2f(c, L, m->hid, m->hid, c->send.p, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s);
+        mlp_gemm(c, true, false, m->hid, m->C, V_p, Zv, ldH, dL, ldL, dW1, m->C, s);          // dW1 = Z_v^T dlogits
+        mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s);           // dZ_v -> L
+        pack_v2f(c, L, ldL, m->hid, c->send.p, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s);
     }
     reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, loss_blocks, scal);
     NTP_LAUNCH_CHECK();
@@ -383,20 +442,21 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         a.transposed = true;
         propagate_and_gather(c, a, c->send.p, overlap, m->chunks, V_p, d_s, rep != nullptr, s);
     }
-    unpack_f2v(c, c->send.p, V_p, d_s, P, dL, w, w, dt, NTP_F32, s);
+    float* dLw = after ? dH1 : dL;            // gathered dL^ rows (dH1 before the mask when W1 is applied after)
+    const int64_t ld_dLw = after ? ldH : ldL;
+    unpack_f2v(c, c->send.p, V_p, d_s, P, dLw, ld_dLw, w, dt, NTP_F32, s);
     NTP_CUDA(cudaEventRecord(E[ei++], s));   // E6 prop bwd + f2v bwd
 
-    // a10: MLP backward
+    // a10: MLP backward (ReLU' mask fused into the dH1 GEMM epilogue)
     if (!after) {
-        gemm_rm(c, true, false, m->hid, m->C, V_p, H1, m->hid, dL, m->C, dW1, m->C);        // dW1 = H1^T dL^
-        gemm_rm(c, false, true, V_p, m->hid, m->C, dL, m->C, W1p, m->C, dH1, m->hid);       // dH1 = dL^ W1^T
+        mlp_gemm(c, true, false, m->hid, m->C, V_p, H1, ldH, dL, ldL, dW1, m->C, s);              // dW1 = H1^T dL^
+        mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, dH1, ldH, s, 2, H1, ldH); // dH1
     } else {
-        NTP_CUDA(cudaMemcpyAsync(dH1, dL, (size_t)V_p * m->hid * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        relu_grad_kernel<<<eblocks(V_p * m->hid), 256, 0, s>>>(dH1, H1, V_p, m->hid, ldH, ldH);
+        NTP_LAUNCH_CHECK();
+        count_launch(c);
     }
-    relu_grad_kernel<<<eblocks(V_p * m->hid), 256, 0, s>>>(dH1, H1, V_p * m->hid);
-    NTP_LAUNCH_CHECK();
-    count_launch(c);
-    gemm_rm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, m->hid, dW0, m->hid);          // dW0 = X^T dH1
+    mlp_gemm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, ldH, dW0, m->hid, s);            // dW0 = X^T dH1
     NTP_CUDA(cudaEventRecord(E[ei++], s));   // E7 mlp bwd
 
     // a11: allreduce (sync_and_update)
@@ -407,7 +467,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         NTP_NCCL(ncclGroupEnd());
     }
     NTP_CUDA(cudaEventRecord(E[ei++], s));   // E8 allreduce
-    sgd_kernel<<<eblocks(n_w), 256, 0, s>>>(W0p, (int64_t)m->d_in * m->hid, W1p, (int64_t)m->hid * m->C, dW0, scal,
+    sgd_kernel<<<eblocks(n_w), 256, 0, s>>>(W0u, (int64_t)m->d_in * m->hid, W1u, (int64_t)m->hid * m->C, dW0, scal,
                                             m->lr);
     NTP_LAUNCH_CHECK();
     count_launch(c);

@@ -114,6 +114,7 @@ struct ntp_ctx {
     // scratch
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
+    ntp::DevBuf m_gemm_part, m_W0p, m_W1p;
     cudaEvent_t ev[64] = {};
     cudaEvent_t hop_ev[256] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
     int hop_ev_used = 0;
@@ -187,6 +188,12 @@ void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t 
                 int64_t ld_v, int32_t w, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s);
 void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_elems, ntp_dtype dt,
                      cudaStream_t s);
+
+// Tensor-core (tcgen05 kind::tf32, 3xTF32) GEMM, gemm.cu.  A stored [K][M] if a_mn else [M][K];
+// B stored [K][N] if b_mn else [N][K]; lda/ldb multiples of 4.  epi: 0 store, 1 ReLU, 2 keep where aux > 0.
+void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool a_mn,
+                 const float* B, int64_t ldb, bool b_mn, float* C, int64_t ldc, int epi, const float* aux,
+                 int64_t ldaux, cudaStream_t s);
 
 inline size_t esize(ntp_dtype d) { return d == NTP_BF16 ? 2 : 4; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

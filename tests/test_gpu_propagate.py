@@ -182,3 +182,34 @@ def test_reddit_full_size_sampled_rows():
     sq = np.sqrt(g.deg_in + 1.0)[:, None].repeat(4, 1).astype(np.float32)
     Zs, _ = _run(ctx, sq, 2, 1.0, 0.0)
     np.testing.assert_allclose(Zs.cpu().numpy(), sq, rtol=2e-5)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,d", [("products", 48), ("products", 12), ("orkut", 64)])
+def test_full_size_sampled_rows(name, d):
+    """c3 (APPNP K=10, gamma=0.9, alpha=0.1) and c4 at full size, slice width d: every hop's
+    output on sampled rows (random + the 20 largest in-degrees + isolated vertices) vs the
+    oracle applied to the GPU's previous-hop state, and the whole K-hop result on the
+    sqrt(d~) fixed point (symmetric graphs: A^ sqrt(d~) = sqrt(d~), kept by gamma = 1 - alpha)."""
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    n = g.n
+    H = _features(n, d, 21)
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([rng.integers(0, n, 300), np.argsort(g.deg_in)[-20:],
+                                     np.flatnonzero(g.deg_in == 0)[:10]]))
+    prev = H.astype(np.float64)
+    for k in range(1, min(cfg.K, 3) + 1):
+        Zk, _ = _run(ctx, H, k, cfg.gamma, cfg.alpha)
+        zk = Zk.double().cpu().numpy()
+        ref = oracle.propagate.hop_rows(g, prev, H, rows, cfg.gamma, cfg.alpha)
+        den = oracle.propagate.hop_rows(g, np.abs(prev), np.abs(H), rows, cfg.gamma, cfg.alpha)
+        assert_r10(zk[rows], ref, den, 2 * FP32_TOL, f"{name} hop {k}")
+        prev = zk
+    sq = np.sqrt(g.deg_in + 1.0)[:, None].repeat(4, 1).astype(np.float32)
+    gam = 1.0 - cfg.alpha
+    Zs, _ = _run(ctx, sq, cfg.K, gam, cfg.alpha)
+    np.testing.assert_allclose(Zs.cpu().numpy(), sq, rtol=5e-5)
+    Ys, _ = _run(ctx, sq, cfg.K, gam, cfg.alpha, transposed=True)
+    np.testing.assert_allclose(Ys.cpu().numpy(), sq, rtol=5e-5)
