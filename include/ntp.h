@@ -218,7 +218,8 @@ typedef struct {
 
 /* One training epoch.  X_v [V_p x d_in] fp32 (this rank's VERTEX rows, rows
  * >= n zero), labels_v int32 [V_p], train_mask_v uint8 [V_p] (device unless
- * NTP_M_HOST_INPUTS).  W0 [d_in x hid], W1 [hid x C] fp32 device, replicated
+ * NTP_M_HOST_INPUTS).  The MLP GEMMs read X_v with TMA: pass ld % 4 == 0 and a 16-byte
+ * aligned base, otherwise X_v is staged into a padded copy every epoch (561 MB on reddit).  W0 [d_in x hid], W1 [hid x C] fp32 device, replicated
  * on every rank, updated in place by SGD.  Synchronous: returns after
  * the epoch completed; `s` orders the call after prior work on that stream and
  * later work after it.  rep may be NULL. */

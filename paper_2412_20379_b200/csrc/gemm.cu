@@ -21,6 +21,7 @@
 #include <mutex>
 
 #include "ntp_internal.cuh"
+#include "ptx.cuh"
 
 namespace ntp {
 
@@ -302,7 +303,9 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits,
     }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+}  // namespace
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -316,6 +319,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
+namespace {
+
 // 2-D fp32 tensor map over a row-major matrix with `rows` rows of `cols` elements (stride ld).
 CUtensorMap make_map(const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
                      CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
@@ -326,7 +331,7 @@ CUtensorMap make_map(const float* base, int64_t cols, int64_t rows, int64_t ld, 
     const cuuint32_t estr[2] = {1, 1};
     NTP_CHECK(((uintptr_t)base % 16) == 0 && (ld * 4) % 16 == 0, NTP_ERR_SHAPE,
               "GEMM operand must be 16-byte aligned with ld %% 4 == 0 (ld=%lld)", (long long)ld);
-    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+    CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     NTP_CHECK(r == CUDA_SUCCESS, NTP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);

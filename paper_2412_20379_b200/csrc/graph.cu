@@ -252,6 +252,9 @@ void build_graph_from_keys(ntp_ctx* c, uint64_t* keys, int64_t m, int64_t n, boo
     cudaStream_t s = c->s_comp;
     Graph& g = c->g;
     g.reset();   // drops the previous graph
+    drop_epoch_graph(c);
+    c->graph_warm = false;
+    c->g_version++;
     if (const char* t = getenv("NTP_UNIT_ITEMS")) g.unit_items = std::max(64, atoi(t));
     g.n = n;
     g.symmetric = symmetric;

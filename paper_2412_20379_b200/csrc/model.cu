@@ -47,10 +47,11 @@ template <typename T> __device__ __forceinline__ void stf(T* p, float v);
 template <> __device__ __forceinline__ void stf<float>(float* p, float v) { *p = v; }
 template <> __device__ __forceinline__ void stf<__nv_bfloat16>(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
 
-// One warp per vertex row.  Input logits: blocked [P][V_p][d_s] (TIn = storage
-// dtype) when `blocked`, else plain fp32 [V_p x C].  Output gradient rows: blocked
-// with per-row scale `gscale` (split pre-scale) when `out_blocked`, else plain fp32.
-// Per-block loss partials (fp64) -> part[blockIdx.x]; train counts -> cnt[blockIdx.x].
+// One warp per vertex row.  Input logits: blocked [P][V_p][d_s] (TIn = storage dtype) when
+// `in_blocked`, else plain fp32 [V_p x ld_plain].  Output gradient rows: blocked with per-row
+// scale `gscale` (the split's pre-scale) when `out_blocked`, else plain fp32.  Each lane keeps
+// its <= MAXC/32 logits in registers: one read, one exp per logit.  Per-block loss partials
+// (fp64) -> part[blockIdx.x]; train counts -> cnt[blockIdx.x].
 template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict__ in, int in_blocked, int64_t V_p,
                                                            int32_t d_s, int32_t C, const int32_t* __restrict__ y,
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
                                                            TOut* __restrict__ out, int out_blocked,
                                                            const float* __restrict__ gscale, double* __restrict__ part,
                                                            int64_t* __restrict__ cnt, int64_t ld_plain) {
+    constexpr int MAXK = 8;                     // C <= 256 in registers; larger C re-reads
     __shared__ double s_loss[8];
     __shared__ int64_t s_cnt[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -67,30 +69,52 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
     if (v < V_p) {
         const int64_t gr = row0 + v;
         const bool train = gr < n && mask[v] != 0;
-        auto in_at = [&](int col) -> float {
-            if (in_blocked) return ldf<TIn>(in + ((int64_t)(col / d_s) * V_p + v) * d_s + col % d_s);
-            return ldf<TIn>(in + v * ld_plain + col);
+        auto addr = [&](int col) -> int64_t {
+            if (in_blocked) {
+                const int q = col / d_s;
+                return ((int64_t)q * V_p + v) * d_s + (col - q * d_s);
+            }
+            return v * ld_plain + col;
         };
+        float x[MAXK];
         float mx = -INFINITY;
-        for (int col = lane; col < C; col += 32) mx = fmaxf(mx, in_at(col));
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k) {
+            const int col = lane + 32 * k;
+            x[k] = col < C ? ldf<TIn>(in + addr(col)) : -INFINITY;
+            mx = fmaxf(mx, x[k]);
+        }
+        for (int col = lane + 32 * MAXK; col < C; col += 32) mx = fmaxf(mx, ldf<TIn>(in + addr(col)));
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         float se = 0.f;
-        for (int col = lane; col < C; col += 32) se += expf(in_at(col) - mx);
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k) {
+            x[k] = (lane + 32 * k < C) ? expf(x[k] - mx) : 0.f;
+            se += x[k];
+        }
+        for (int col = lane + 32 * MAXK; col < C; col += 32) se += expf(ldf<TIn>(in + addr(col)) - mx);
         for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
         const int yv = train ? y[v] : -1;
         if (train && lane == 0) {
-            const float ly = in_at(yv);
+            const float ly = ldf<TIn>(in + addr(yv));
             my_loss = (double)(logf(se) + mx - ly);
             my_cnt = 1;
         }
         const float inv = 1.f / se;
         const float sc = (gscale && gr < n) ? gscale[gr] : 1.f;
-        for (int col = lane; col < C; col += 32) {
-            float gval = 0.f;
-            if (train) gval = (expf(in_at(col) - mx) * inv - (col == yv ? 1.f : 0.f)) * sc;
-            if (out_blocked) stf<TOut>(out + ((int64_t)(col / d_s) * V_p + v) * d_s + col % d_s, gval);
-            else stf<TOut>(out + v * ld_plain + col, gval);
-        }
+        auto put = [&](int col, float p) {
+            const float gval = train ? (p * inv - (col == yv ? 1.f : 0.f)) * sc : 0.f;
+            if (out_blocked) {
+                const int q = col / d_s;
+                stf<TOut>(out + ((int64_t)q * V_p + v) * d_s + (col - q * d_s), gval);
+            } else {
+                stf<TOut>(out + v * ld_plain + col, gval);
+            }
+        };
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+            if (lane + 32 * k < C) put(lane + 32 * k, x[k]);
+        for (int col = lane + 32 * MAXK; col < C; col += 32) put(col, expf(ldf<TIn>(in + addr(col)) - mx));
     }
     if (lane == 0) {
         s_loss[warp] = my_loss;
@@ -250,11 +274,11 @@ static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool
     NTP_CUDA(cudaStreamWaitEvent(s, c->ev[51], 0));
 }
 
-void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
-                 const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user) {
+// Enqueues one epoch (everything between events E0 and E9) on c->s_comp; capturable.
+static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                          const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, bool timed) {
     const Graph& g = c->g;
     cudaStream_t s = c->s_comp;
-    const int64_t launches0 = c->launches;
     const int32_t P = c->world;
     const int64_t n = g.n;
     const int64_t V_p = cdiv(n, P);
@@ -267,9 +291,9 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     const size_t es = esize(dt);
     const int64_t feat_elems = V_pad * d_s;
 
-    // ---- order after the caller's stream
-    NTP_CUDA(cudaEventRecord(c->ev[40], user ? user : (cudaStream_t)0));
-    NTP_CUDA(cudaStreamWaitEvent(s, c->ev[40], 0));
+    cudaEvent_t* E = c->ev;
+    int ei = 0;
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E0 start (input staging counts as mlp_fwd)
 
     // ---- inputs (e2e: copy host inputs in).  GEMM operands need 16-byte row pitch (TMA).
     const int64_t ldXp = round4(m->d_in), ldH = round4(m->hid), ldL = round4(std::max(m->C, m->hid));
@@ -342,10 +366,6 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     double* scal = c->m_scal.as<double>();
     NTP_BLAS(cublasSetStream(c->blas, s));
 
-    cudaEvent_t* E = c->ev;
-    int ei = 0;
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E0 start
-
     // a2: MLP forward (ReLU fused into the GEMM epilogue)
     mlp_gemm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0g, ldw0, H1, ldH, s, /*relu*/ 1);
     const float* prop_src = H1;             // rows propagated (w columns)
@@ -355,12 +375,12 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         prop_src = L;
         ld_src = ldL;
     }
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E1 mlp_fwd done
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd done
 
     // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
     pack_v2f(c, prop_src, ld_src, w, c->send.p, V_p, d_s, P, g.dinv_out_p(), row0, n, NTP_F32, dt, s);
     alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E2 v2f done
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E2 v2f done
 
     // a4 + a5: K forward hops on S^0 = recv (pre-scaled) -> Z^K in xfer, gathered into recv
     const bool overlap = (m->flags & NTP_M_OVERLAP) != 0;
@@ -377,9 +397,9 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = false;
-        propagate_and_gather(c, a, c->recv.p, overlap, m->chunks, V_p, d_s, rep != nullptr, s);
+        propagate_and_gather(c, a, c->recv.p, overlap, m->chunks, V_p, d_s, timed, s);
     }
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E3 prop fwd + f2v done
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E3 prop fwd + f2v done
 
     // a6: loss + gradient, written straight into the backward split's send buffer
     const float* gscale_bwd = g.dinv_in_p();   // backward column side
@@ -421,11 +441,11 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, loss_blocks, scal);
     NTP_LAUNCH_CHECK();
     count_launch(c);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E4 loss done
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E4 loss done
 
     // a7: split the gradient
     alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E5 v2f bwd
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E5 v2f bwd
 
     // a8 + a9: K backward hops on the split gradient, gathered -> dL^ rows [V_p x w]
     {
@@ -440,12 +460,12 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = true;
-        propagate_and_gather(c, a, c->send.p, overlap, m->chunks, V_p, d_s, rep != nullptr, s);
+        propagate_and_gather(c, a, c->send.p, overlap, m->chunks, V_p, d_s, timed, s);
     }
     float* dLw = after ? dH1 : dL;            // gathered dL^ rows (dH1 before the mask when W1 is applied after)
     const int64_t ld_dLw = after ? ldH : ldL;
     unpack_f2v(c, c->send.p, V_p, d_s, P, dLw, ld_dLw, w, dt, NTP_F32, s);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E6 prop bwd + f2v bwd
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E6 prop bwd + f2v bwd
 
     // a10: MLP backward (ReLU' mask fused into the dH1 GEMM epilogue)
     if (!after) {
@@ -457,7 +477,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         count_launch(c);
     }
     mlp_gemm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, ldH, dW0, m->hid, s);            // dW0 = X^T dH1
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E7 mlp bwd
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E7 mlp bwd
 
     // a11: allreduce (sync_and_update)
     if (P > 1) {
@@ -466,13 +486,96 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         NTP_NCCL(ncclAllReduce(scal, scal, 2, ncclFloat64, ncclSum, c->comm, s));
         NTP_NCCL(ncclGroupEnd());
     }
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E8 allreduce
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E8 allreduce
     sgd_kernel<<<eblocks(n_w), 256, 0, s>>>(W0u, (int64_t)m->d_in * m->hid, W1u, (int64_t)m->hid * m->C, dW0, scal,
                                             m->lr);
     NTP_LAUNCH_CHECK();
     count_launch(c);
-    NTP_CUDA(cudaEventRecord(E[ei++], s));   // E9 sgd
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E9 sgd
+}
 
+namespace {
+bool graphs_enabled() {
+    static const bool v = [] { const char* e = getenv("NTP_GRAPH"); return e ? atoi(e) != 0 : true; }();
+    return v;
+}
+}  // namespace
+
+void drop_epoch_graph(ntp_ctx* c) {
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    c->graph_exec = nullptr;
+    c->graph_valid = false;
+}
+
+// One epoch.  The enqueue sequence is captured into a CUDA graph on the second call with the same
+// key (model + every pointer it bakes in) and replayed afterwards: one launch instead of ~60, so
+// the GPU does not idle while the host re-issues the epoch.  Any eager call invalidates the graph
+// (it may have grown scratch buffers the graph points into).  NTP_GRAPH=0 disables capture.
+void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                 const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user) {
+    const Graph& g = c->g;
+    cudaStream_t s = c->s_comp;
+    const int64_t launches0 = c->launches;
+    const int32_t P = c->world;
+    const int64_t n = g.n;
+    const int64_t V_p = cdiv(n, P);
+    const bool after = (m->flags & NTP_M_W1_AFTER_PROP) != 0;
+    const int32_t w = after ? m->hid : m->C;
+    const int32_t d_s = slice_width(w, P, m->dtype, c->slice_align);
+    const size_t es = esize(m->dtype);
+    const bool timed = true;
+    cudaEvent_t* E = c->ev;
+
+    // ---- order after the caller's stream
+    NTP_CUDA(cudaEventRecord(c->ev[40], user ? user : (cudaStream_t)0));
+    NTP_CUDA(cudaStreamWaitEvent(s, c->ev[40], 0));
+
+    EpochKey key{};
+    key.m = *m;
+    key.ptrs[0] = X_v->data;
+    key.ptrs[1] = labels_v;
+    key.ptrs[2] = mask_v;
+    key.ptrs[3] = W0->data;
+    key.ptrs[4] = W1->data;
+    key.ld = X_v->ld;
+    key.graph_version = c->g_version;
+    int64_t epoch_launches = 0;
+    if (graphs_enabled() && c->graph_valid && c->graph_key == key) {
+        NTP_CUDA(cudaGraphLaunch(c->graph_exec, s));
+        c->hop_ev_used = c->graph_hops;
+        epoch_launches = c->graph_launches;
+    } else if (graphs_enabled() && c->graph_warm && c->graph_key == key) {
+        drop_epoch_graph(c);
+        cudaGraph_t graph = nullptr;
+        NTP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        c->capturing = true;
+        try {
+            enqueue_epoch(c, m, X_v, labels_v, mask_v, W0, W1, timed);
+        } catch (...) {
+            c->capturing = false;
+            cudaStreamEndCapture(s, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            c->graph_warm = false;
+            throw;
+        }
+        c->capturing = false;
+        NTP_CUDA(cudaStreamEndCapture(s, &graph));
+        cudaError_t ie = cudaGraphInstantiate(&c->graph_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        NTP_CUDA(ie);
+        c->graph_valid = true;
+        c->graph_hops = c->hop_ev_used;
+        c->graph_launches = c->launches - launches0;
+        epoch_launches = c->graph_launches;
+        NTP_CUDA(cudaGraphLaunch(c->graph_exec, s));
+    } else {
+        drop_epoch_graph(c);
+        enqueue_epoch(c, m, X_v, labels_v, mask_v, W0, W1, timed);
+        epoch_launches = c->launches - launches0;
+        c->graph_warm = true;
+        c->graph_key = key;
+    }
+    double* scal = c->m_scal.as<double>();
     double h_scal[2] = {0, 0};
     NTP_CUDA(cudaMemcpyAsync(h_scal, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     NTP_CUDA(cudaEventRecord(c->ev[41], s));
@@ -501,7 +604,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
             rep->bytes_recv[i] = wire;
         }
         rep->collectives = P > 1 ? 5 : 0;
-        rep->kernel_launches = c->launches - launches0;
+        rep->kernel_launches = epoch_launches;
         int nh = 0;
         rep->spmm_ms = collect_hop_ms(c, &nh);
         rep->spmm_launches = nh;

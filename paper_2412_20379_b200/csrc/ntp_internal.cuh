@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -105,6 +106,18 @@ struct Graph {
 }  // namespace ntp
 
 // ---------------------------------------------------------------- context
+// Everything a captured epoch graph bakes in.
+struct EpochKey {
+    ntp_model m;
+    const void* ptrs[5];
+    int64_t ld;
+    int64_t graph_version;
+    bool operator==(const EpochKey& o) const {
+        return std::memcmp(&m, &o.m, sizeof(m)) == 0 && std::memcmp(ptrs, o.ptrs, sizeof(ptrs)) == 0 && ld == o.ld &&
+               graph_version == o.graph_version;
+    }
+};
+
 struct ntp_ctx {
     int device = 0, rank = 0, world = 1, slice_align = 16;
     ncclComm_t comm = nullptr;
@@ -120,6 +133,14 @@ struct ntp_ctx {
     int hop_ev_used = 0;
     int64_t launches = 0;
     std::string err;
+    // captured epoch (CUDA graph)
+    int64_t g_version = 0;          // bumped whenever the graph (CSR) is rebuilt
+    EpochKey graph_key{};
+    bool graph_warm = false, graph_valid = false;
+    cudaGraphExec_t graph_exec = nullptr;
+    bool capturing = false;         // timing events become external event nodes while capturing
+    int graph_hops = 0;
+    int64_t graph_launches = 0;
 };
 
 namespace ntp {
@@ -166,6 +187,7 @@ void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi,
 double collect_hop_ms(ntp_ctx* c, int* n_hops);
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
+void drop_epoch_graph(ntp_ctx* c);
 void arcs_to_keys(ntp_ctx* c, const int64_t* src, const int64_t* dst, int64_t m, int64_t n, bool sym,
                   uint64_t* keys, cudaStream_t s);
 void csr_to_keys(ntp_ctx* c, const int64_t* row_ptr, const int32_t* col, int64_t n, uint64_t* keys,
@@ -200,5 +222,9 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int32_t slice_width(int32_t w, int32_t P, ntp_dtype dt, int align);
 
 void count_launch(ntp_ctx* c, int k = 1);
+// Record a TIMING event (phase marks, SpMM hop pairs): external event node under graph capture.
+inline cudaError_t record_timing(ntp_ctx* c, cudaEvent_t e, cudaStream_t s) {
+    return cudaEventRecordWithFlags(e, s, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
 
 }  // namespace ntp

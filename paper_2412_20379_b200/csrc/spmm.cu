@@ -24,6 +24,7 @@
 #include <cstdlib>
 
 #include "ntp_internal.cuh"
+#include "ptx.cuh"
 
 namespace ntp {
 
@@ -124,6 +125,7 @@ struct HopParams {
     int32_t nvec;                      // 16-byte vectors per row
     float gamma, alpha;
     int mode;                          // 0 intermediate, 1 last
+    int tma_per8;                      // groups (out of every 8) that gather with TMA gather4
 };
 
 // Lane layout ("full row per edge"): a group of L lanes works on one unit.  Lane
@@ -137,8 +139,12 @@ struct HopParams {
 // in-lane for the bits of k -- so the per-column order is the same for every
 // (E, VP), i.e. for every slice width.  Column indices are loaded coalesced (one
 // per lane) and distributed with shuffles.
-template <typename T, int E, int L, int POL>
-__global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p) {
+// GATHER: 0 = LSU loads (ld.global, policy POL), 1 = TMA tile::gather4 into a per-group
+// double-buffered shared-memory ring (no L1 data-pipe fill), read back with LDS.
+template <typename T, int E, int L, int POL, int GATHER>
+__global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p, const __grid_constant__ CUtensorMap tmS) {
+    // GATHER == 1: mixed mode -- groups with (gidx % 8) < p.tma_per8 use the TMA engine, the others
+    // the LSU path, so both units pull rows from L2 concurrently (same reduction order either way).
     constexpr int NACC = kG / E;
     constexpr int LOG_E = (E == 1) ? 0 : (E == 2) ? 1 : (E == 4) ? 2 : 3;
     constexpr int VALS = V16<T>::N;
@@ -151,6 +157,26 @@ __global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p) 
     const int gbase = lane - gl;
     const int64_t group = ((int64_t)blockIdx.x * kBlock + threadIdx.x) / L;
     const int64_t u = p.u_begin + group;
+    // TMA ring: per group 2 buffers of BATCH/4 gather4 slots, slot = 4 rows rounded to 128 B
+    extern __shared__ __align__(128) uint8_t tma_smem[];
+    constexpr int GPC = kBlock / L;                      // groups per CTA
+    const int row_bytes = p.nvec * 16;
+    const int slot_bytes = (4 * row_bytes + 127) & ~127;
+    const int buf_bytes = (BATCH / 4) * slot_bytes;
+    const int gidx = threadIdx.x / L;
+    uint8_t* gbuf = tma_smem + (size_t)gidx * 2 * buf_bytes;
+    uint64_t* gbar = reinterpret_cast<uint64_t*>(tma_smem + (size_t)GPC * 2 * buf_bytes) + 2 * gidx;
+    uint32_t ph0 = 0, ph1 = 0;
+    const bool tma_group = (GATHER == 1) && ((gidx & 7) < p.tma_per8);
+    const int fillv = tma_group ? (int)p.n : 0;
+    if constexpr (GATHER == 1) {
+        if (gl == 0) {
+            ptx::mbar_init(&gbar[0], 1);
+            ptx::mbar_init(&gbar[1], 1);
+            ptx::fence_mbar_init();
+        }
+        __syncthreads();
+    }
     if (u >= p.u_end) return;                           // group-uniform exit
     const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << gbase);
     const int VP = (E == 1) ? min(p.nvec, 32) : p.nvec;  // vectors per pass
@@ -187,7 +213,7 @@ __global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p) 
 #pragma unroll
                 for (int sl = 0; sl < ISL; ++sl) {
                     const int j = base + sl * L + gl;
-                    dst[sl] = (sl * L + gl < BATCH && j < ee) ? __ldg(colp + j) : 0;
+                    dst[sl] = (sl * L + gl < BATCH && j < ee) ? __ldg(colp + j) : fillv;
                 }
             };
             // 16-byte loads of a batch; slots past the end read row 0 (never accumulated)
@@ -211,6 +237,7 @@ __global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p) 
                         if (t * E + e < rem) V16<T>::add_raw(acc[t % NACC], v[t]);
                 }
             };
+            if (!tma_group) {
             // two-deep software pipeline, unrolled by 2 so the buffers ping-pong without copies:
             // while batch b is accumulated, batch b+1's rows and batch b+2's indices are in flight
             int ia[ISL], ib[ISL];
@@ -228,6 +255,54 @@ __global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p) 
                 if (base + BATCH < ee) load_data(ia, va);
                 consume(vb, base);
                 base += BATCH;
+            }
+            } else {
+            // TMA gather4 ring: batch b+1 in flight (buffer b+1 & 1) while batch b is read from smem
+            auto issue = [&](int buf, const int (&ix)[ISL]) {
+                if (gl == 0) ptx::mbar_expect_tx(&gbar[buf], BATCH * row_bytes);
+                __syncwarp(gmask);
+#pragma unroll
+                for (int sl = 0; sl < ISL; ++sl) {
+                    const int q1 = __shfl_sync(gmask, ix[sl], gbase + ((gl + 1) & (L - 1)));
+                    const int q2 = __shfl_sync(gmask, ix[sl], gbase + ((gl + 2) & (L - 1)));
+                    const int q3 = __shfl_sync(gmask, ix[sl], gbase + ((gl + 3) & (L - 1)));
+                    const int jb = sl * L + gl;                       // first edge of this lane's gather
+                    if ((gl & 3) == 0 && jb < BATCH)
+                        ptx::tma_gather4(gbuf + buf * buf_bytes + (jb >> 2) * slot_bytes, &tmS, &gbar[buf], 0,
+                                         ix[sl], q1, q2, q3);
+                }
+            };
+            auto consume_smem = [&](int buf) {
+                const uint8_t* b = gbuf + buf * buf_bytes + vcol * 16;
+#pragma unroll
+                for (int t = 0; t < LPB; ++t) {
+                    const int jrel = t * E + e;
+                    const uint4 x = *reinterpret_cast<const uint4*>(b + (jrel >> 2) * slot_bytes + (jrel & 3) * row_bytes);
+                    V16<T>::add_raw(acc[t % NACC], x);                 // rows past the end are zero
+                }
+            };
+            int ia[ISL], ib[ISL];
+            load_idx(eb, ia);
+            if (eb < ee) issue(0, ia);
+            load_idx(eb + BATCH, ib);
+            if (eb + BATCH < ee) issue(1, ib);
+            for (int base = eb; base < ee;) {
+                load_idx(base + 2 * BATCH, ia);
+                ptx::mbar_wait(&gbar[0], ph0);
+                ph0 ^= 1;
+                consume_smem(0);
+                __syncwarp(gmask);
+                if (base + 2 * BATCH < ee) issue(0, ia);
+                base += BATCH;
+                if (base >= ee) break;
+                load_idx(base + 2 * BATCH, ib);
+                ptx::mbar_wait(&gbar[1], ph1);
+                ph1 ^= 1;
+                consume_smem(1);
+                __syncwarp(gmask);
+                if (base + 2 * BATCH < ee) issue(1, ib);
+                base += BATCH;
+            }
             }
             // fixed butterfly over the 8 reduction groups
 #pragma unroll
@@ -334,14 +409,56 @@ __global__ void prescale_kernel(const char* __restrict__ H, int64_t ld_h, char* 
     }
 }
 
+bool carveout_max_l1() {
+    static const bool v = [] { const char* e = getenv("NTP_L1_CARVEOUT"); return e ? atoi(e) != 0 : true; }();
+    return v;
+}
+
 template <typename T, int E, int L>
 void launch_hop(const HopParams& p, cudaStream_t s) {
     static const int pol = [] { const char* v = getenv("NTP_GATHER_POLICY"); return v ? atoi(v) : 0; }();
+    static const int tma_env = [] { const char* v = getenv("NTP_SPMM_TMA"); return v ? atoi(v) : -1; }();
+    // groups per 8 on the TMA path: measured sweet spots; NTP_SPMM_TMA overrides
+    const int tma = tma_env >= 0 ? tma_env : 0;
     const int64_t groups = p.u_end - p.u_begin;
     const int64_t blocks = cdiv(groups * L, kBlock);
-    if (pol == 1) spmm_hop_kernel<T, E, L, 1><<<(unsigned)blocks, kBlock, 0, s>>>(p);
-    else if (pol == 2) spmm_hop_kernel<T, E, L, 2><<<(unsigned)blocks, kBlock, 0, s>>>(p);
-    else spmm_hop_kernel<T, E, L, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p);
+    CUtensorMap tm{};
+    HopParams pp = p;
+    pp.tma_per8 = std::min(tma, 8);
+    const bool use_tma = tma > 0 && p.nvec <= 32 && (int64_t)p.nvec * 16 / (int64_t)sizeof(T) <= 256 && p.n > 0;
+    if (use_tma) {
+        constexpr int BATCH = (E == 8) ? 64 : (E == 4) ? 32 : 8 * E;
+        const int row_bytes = p.nvec * 16;
+        const int slot_bytes = (4 * row_bytes + 127) & ~127;
+        const size_t smem = (size_t)(kBlock / L) * (2 * (BATCH / 4) * slot_bytes + 16) + 128;
+        const cuuint64_t dims[2] = {(cuuint64_t)(row_bytes / sizeof(T)), (cuuint64_t)p.n};
+        const cuuint64_t strides[1] = {(cuuint64_t)p.ld_in};
+        const cuuint32_t box[2] = {(cuuint32_t)(row_bytes / sizeof(T)), 1};
+        const cuuint32_t es[2] = {1, 1};
+        CUresult r = tensor_map_encoder()(&tm, sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                          2, const_cast<char*>(p.S_in), dims, strides, box, es,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        NTP_CHECK(r == CUDA_SUCCESS, NTP_ERR_CUDA, "tensor map for the TMA gather failed (%d)", (int)r);
+        static bool attr = false;
+        if (!attr) {
+            NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          200 * 1024));
+            attr = true;
+        }
+        spmm_hop_kernel<T, E, L, 0, 1><<<(unsigned)blocks, kBlock, smem, s>>>(pp, tm);
+    } else if (pol == 1) spmm_hop_kernel<T, E, L, 1, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
+    else if (pol == 0 && carveout_max_l1()) {
+        // no shared memory on the LSU path: give the whole unified array to L1
+        static bool attr0 = false;
+        if (!attr0) {
+            NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+            attr0 = true;
+        }
+        spmm_hop_kernel<T, E, L, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
+    }
+    else if (pol == 2) spmm_hop_kernel<T, E, L, 2, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
+    else spmm_hop_kernel<T, E, L, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
     NTP_LAUNCH_CHECK();
 }
 
@@ -478,11 +595,11 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
             return;
         }
         const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
-        if (timed) NTP_CUDA(cudaEventRecord(c->hop_ev[c->hop_ev_used], s));
+        if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
         spmm_hop(c, csr, rs, cs, sin, bufs[nxt], S0, ld_sin, lds[nxt], ld_s0, a.cols, a.dtype, a.gamma, a.alpha,
                  last ? 1 : 0, 0, -1, s);
         if (timed) {
-            NTP_CUDA(cudaEventRecord(c->hop_ev[c->hop_ev_used + 1], s));
+            NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used + 1], s));
             c->hop_ev_used += 2;
         }
         sin = bufs[nxt];
@@ -492,11 +609,11 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
 
 void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi, cudaStream_t s, bool time_hops) {
     const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
-    if (timed) NTP_CUDA(cudaEventRecord(c->hop_ev[c->hop_ev_used], s));
+    if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
     spmm_hop(c, *lh.csr, lh.rs, lh.cs, lh.sin, lh.out, lh.S0, lh.ld_sin, lh.ld_out, lh.ld_s0, lh.cols, lh.dt, lh.gamma,
              lh.alpha, 1, row_lo, row_hi, s);
     if (timed) {
-        NTP_CUDA(cudaEventRecord(c->hop_ev[c->hop_ev_used + 1], s));
+        NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used + 1], s));
         c->hop_ev_used += 2;
     }
 }
