@@ -32,6 +32,8 @@ def _load():
     L.oracle_propagate.restype = None
     L.oracle_hop_rows.argtypes = [vp, vp, vp, vp, i64, vp, vp, dbl, dbl, vp, i64, vp]
     L.oracle_hop_rows.restype = None
+    L.oracle_rmat_filter.argtypes = [i32, u32, u32, u32, u64, i64, i64, i32, vp, i32, vp, vp, i64]
+    L.oracle_rmat_filter.restype = i64
     L.oracle_num_threads.argtypes = []
     L.oracle_num_threads.restype = i32
     return L

@@ -55,6 +55,42 @@ void oracle_rmat_arcs(int scale, uint32_t t0, uint32_t t1, uint32_t t2, uint64_t
     }
 }
 
+/* Full-scale sampled pin: regenerate ALL raw arcs [0, m_raw) and keep the valid ones (ids < n,
+ * no self loop) whose destination (by_dst = 1) or source (by_dst = 0) is flagged in `bitmap`
+ * (bit v of bitmap[v >> 6]); reverse arcs are included when `symmetric`.  Writes up to `cap`
+ * (src, dst) pairs in unspecified order and returns how many matched (may exceed cap). */
+int64_t oracle_rmat_filter(int scale, uint32_t t0, uint32_t t1, uint32_t t2, uint64_t seed, int64_t m_raw,
+                           int64_t n, int symmetric, const uint64_t* bitmap, int by_dst,
+                           int64_t* out_src, int64_t* out_dst, int64_t cap) {
+    int64_t count = 0;
+    #pragma omp parallel for schedule(static, 65536)
+    for (int64_t k = 0; k < m_raw; ++k) {
+        int64_t s = 0, d = 0;
+        for (int l = 0; l < scale; ++l) {
+            uint32_t u = (uint32_t)(oracle_hash(seed, 0, (uint64_t)k * 64u + (uint64_t)l) >> 32);
+            int sb, db;
+            if (u < t0)      { sb = 0; db = 0; }
+            else if (u < t1) { sb = 0; db = 1; }
+            else if (u < t2) { sb = 1; db = 0; }
+            else             { sb = 1; db = 1; }
+            s = (s << 1) | sb;
+            d = (d << 1) | db;
+        }
+        if (s >= n || d >= n || s == d) continue;
+        for (int rev = 0; rev <= (symmetric ? 1 : 0); ++rev) {
+            const int64_t a = rev ? d : s, b = rev ? s : d;     /* arc a -> b */
+            const int64_t key = by_dst ? b : a;
+            if ((bitmap[key >> 6] >> (key & 63)) & 1ull) {
+                int64_t slot;
+                #pragma omp atomic capture
+                slot = count++;
+                if (slot < cap) { out_src[slot] = a; out_dst[slot] = b; }
+            }
+        }
+    }
+    return count;
+}
+
 /* ------------------------------------------------------------------------ *
  * K-hop propagation, O3 (fwd) / O4 (bwd), SURVEY §8(c):
  *   Z^0 = H

@@ -110,6 +110,37 @@ def graph_from_config(cfg) -> Graph:
     return build_graph(src, dst, cfg.n, cfg.symmetric)
 
 
+def sampled_rows(cfg, rows, transposed: bool = False):
+    """O1 restricted to sampled rows, for configs too large to build whole on the CPU:
+    {v: sorted unique in-neighbours} (or out-neighbours if `transposed`) for v in `rows`,
+    from a full regeneration of the raw arc stream filtered by a row bitmap."""
+    from synth import rmat_thresholds
+    rows = np.unique(np.asarray(rows, dtype=np.int64))
+    bitmap = np.zeros((cfg.n + 63) // 64, dtype=np.uint64)
+    np.bitwise_or.at(bitmap, rows >> 6, np.left_shift(np.uint64(1), (rows & 63).astype(np.uint64)))
+    t0, t1, t2 = rmat_thresholds(*cfg.abc)
+    cap = 1 << 20
+    while True:
+        src = np.empty(cap, dtype=np.int64)
+        dst = np.empty(cap, dtype=np.int64)
+        cnt = lib.oracle_rmat_filter(cfg.scale, t0, t1, t2, cfg.seed, cfg.m_raw, cfg.n, int(cfg.symmetric),
+                                     bitmap.ctypes.data, 0 if transposed else 1, src.ctypes.data, dst.ctypes.data, cap)
+        if cnt <= cap:
+            break
+        cap = int(cnt) + 1
+    src, dst = src[:cnt], dst[:cnt]
+    key_row, key_col = (src, dst) if transposed else (dst, src)
+    keys = _sort_dedup((key_row << np.int64(32)) | key_col)
+    kr = keys >> np.int64(32)
+    kc = (keys & np.int64(0xFFFFFFFF)).astype(np.int32)
+    out = {}
+    bounds = np.searchsorted(kr, rows)
+    ends = np.searchsorted(kr, rows, side="right")
+    for v, a, b in zip(rows.tolist(), bounds.tolist(), ends.tolist()):
+        out[v] = kc[a:b]
+    return out
+
+
 def dinv(deg) -> np.ndarray:
     """(deg + 1)^{-1/2} in fp64 (O2)."""
     return 1.0 / np.sqrt(np.asarray(deg, dtype=np.float64) + 1.0)

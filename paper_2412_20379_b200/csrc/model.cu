@@ -47,23 +47,28 @@ template <typename T> __device__ __forceinline__ void stf(T* p, float v);
 template <> __device__ __forceinline__ void stf<float>(float* p, float v) { *p = v; }
 template <> __device__ __forceinline__ void stf<__nv_bfloat16>(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
 
-// One warp per vertex row.  Input logits: blocked [P][V_p][d_s] (TIn = storage dtype) when
-// `in_blocked`, else plain fp32 [V_p x ld_plain].  Output gradient rows: blocked with per-row
-// scale `gscale` (the split's pre-scale) when `out_blocked`, else plain fp32.  Each lane keeps
-// its <= MAXC/32 logits in registers: one read, one exp per logit.  Per-block loss partials
-// (fp64) -> part[blockIdx.x]; train counts -> cnt[blockIdx.x].
-template <typename TIn, typename TOut>
+// LPR lanes per vertex row (32/LPR rows per warp, so short rows do not leave a warp's
+// dependent load -> max -> exp -> sum chain idle).  Input logits: blocked [P][V_p][d_s]
+// (TIn = storage dtype) when `in_blocked`, else plain fp32 [V_p x ld_plain].  Output gradient
+// rows: blocked with per-row scale `gscale` (the split's pre-scale) when `out_blocked`, else
+// plain fp32.  Each lane keeps its <= MAXK logits in registers (one read, one exp per logit;
+// LPR*MAXK >= C is guaranteed by the launcher).  Per-block loss partials (fp64, fixed order)
+// -> part[blockIdx.x]; train counts -> cnt[blockIdx.x].
+template <typename TIn, typename TOut, int LPR>
 __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict__ in, int in_blocked, int64_t V_p,
                                                            int32_t d_s, int32_t C, const int32_t* __restrict__ y,
                                                            const uint8_t* __restrict__ mask, int64_t row0, int64_t n,
                                                            TOut* __restrict__ out, int out_blocked,
                                                            const float* __restrict__ gscale, double* __restrict__ part,
                                                            int64_t* __restrict__ cnt, int64_t ld_plain) {
-    constexpr int MAXK = 8;                     // C <= 256 in registers; larger C re-reads
-    __shared__ double s_loss[8];
-    __shared__ int64_t s_cnt[8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t v = (int64_t)blockIdx.x * 8 + warp;
+    constexpr int MAXK = 8;
+    constexpr int RPB = 256 / LPR;                     // rows per block
+    __shared__ double s_loss[RPB];
+    __shared__ int64_t s_cnt[RPB];
+    const int sub = threadIdx.x % LPR;
+    const int rloc = threadIdx.x / LPR;
+    const unsigned smask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << ((threadIdx.x & 31) / LPR * LPR));
+    const int64_t v = (int64_t)blockIdx.x * RPB + rloc;
     double my_loss = 0.0;
     int64_t my_cnt = 0;
     if (v < V_p) {
@@ -80,57 +85,77 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
         float mx = -INFINITY;
 #pragma unroll
         for (int k = 0; k < MAXK; ++k) {
-            const int col = lane + 32 * k;
+            const int col = sub + LPR * k;
             x[k] = col < C ? ldf<TIn>(in + addr(col)) : -INFINITY;
             mx = fmaxf(mx, x[k]);
         }
-        for (int col = lane + 32 * MAXK; col < C; col += 32) mx = fmaxf(mx, ldf<TIn>(in + addr(col)));
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int o = LPR / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(smask, mx, o));
         float se = 0.f;
 #pragma unroll
         for (int k = 0; k < MAXK; ++k) {
-            x[k] = (lane + 32 * k < C) ? expf(x[k] - mx) : 0.f;
+            x[k] = (sub + LPR * k < C) ? expf(x[k] - mx) : 0.f;
             se += x[k];
         }
-        for (int col = lane + 32 * MAXK; col < C; col += 32) se += expf(ldf<TIn>(in + addr(col)) - mx);
-        for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        for (int o = LPR / 2; o > 0; o >>= 1) se += __shfl_xor_sync(smask, se, o);
         const int yv = train ? y[v] : -1;
-        if (train && lane == 0) {
+        if (train && sub == 0) {
             const float ly = ldf<TIn>(in + addr(yv));
             my_loss = (double)(logf(se) + mx - ly);
             my_cnt = 1;
         }
         const float inv = 1.f / se;
         const float sc = (gscale && gr < n) ? gscale[gr] : 1.f;
-        auto put = [&](int col, float p) {
-            const float gval = train ? (p * inv - (col == yv ? 1.f : 0.f)) * sc : 0.f;
-            if (out_blocked) {
-                const int q = col / d_s;
-                stf<TOut>(out + ((int64_t)q * V_p + v) * d_s + (col - q * d_s), gval);
-            } else {
-                stf<TOut>(out + v * ld_plain + col, gval);
-            }
-        };
 #pragma unroll
-        for (int k = 0; k < MAXK; ++k)
-            if (lane + 32 * k < C) put(lane + 32 * k, x[k]);
-        for (int col = lane + 32 * MAXK; col < C; col += 32) put(col, expf(ldf<TIn>(in + addr(col)) - mx));
+        for (int k = 0; k < MAXK; ++k) {
+            const int col = sub + LPR * k;
+            if (col < C) {
+                const float gval = train ? (x[k] * inv - (col == yv ? 1.f : 0.f)) * sc : 0.f;
+                if (out_blocked) {
+                    const int q = col / d_s;
+                    stf<TOut>(out + ((int64_t)q * V_p + v) * d_s + (col - q * d_s), gval);
+                } else {
+                    stf<TOut>(out + v * ld_plain + col, gval);
+                }
+            }
+        }
     }
-    if (lane == 0) {
-        s_loss[warp] = my_loss;
-        s_cnt[warp] = my_cnt;
+    if (sub == 0) {
+        s_loss[rloc] = my_loss;
+        s_cnt[rloc] = my_cnt;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double l = 0.0;
         int64_t k = 0;
-        for (int i = 0; i < 8; ++i) {  // fixed order
+        for (int i = 0; i < RPB; ++i) {  // fixed order
             l += s_loss[i];
             k += s_cnt[i];
         }
         part[blockIdx.x] = l;
         cnt[blockIdx.x] = k;
     }
+}
+
+// Launches the loss kernel with the narrowest row group that holds C logits in registers.
+template <typename TIn, typename TOut>
+int64_t launch_softmax_xent(ntp_ctx* c, const TIn* in, int in_blocked, int64_t V_p, int32_t d_s, int32_t C,
+                            const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n, TOut* out,
+                            int out_blocked, const float* gscale, double* part, int64_t* cnt, int64_t ld_plain,
+                            cudaStream_t s) {
+    NTP_CHECK(C <= 256, NTP_ERR_CONFIG, "C = %d > 256 classes is not supported", C);
+    int64_t nb;
+#define NTP_LOSS_LAUNCH(LPR)                                                                                    \
+    nb = cdiv(V_p, 256 / LPR);                                                                                  \
+    softmax_xent_kernel<TIn, TOut, LPR><<<(unsigned)nb, 256, 0, s>>>(in, in_blocked, V_p, d_s, C, y, mask, row0, n, \
+                                                                     out, out_blocked, gscale, part, cnt, ld_plain)
+    if (C <= 32) { NTP_LOSS_LAUNCH(4); }
+    else if (C <= 64) { NTP_LOSS_LAUNCH(8); }
+    else if (C <= 128) { NTP_LOSS_LAUNCH(16); }
+    else { NTP_LOSS_LAUNCH(32); }
+#undef NTP_LOSS_LAUNCH
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    return nb;
 }
 
 // Zero the padded gradient columns [C, P*d_s) of blocked output (left untouched by the loss kernel).
@@ -353,7 +378,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     c->send.ensure((size_t)feat_elems * es + 16);
     c->recv.ensure((size_t)feat_elems * es + 16);
     c->xfer.ensure((size_t)feat_elems * es + 16);     // propagation output (feature slice)
-    const int64_t loss_blocks = cdiv(V_p, 8);
+    const int64_t loss_blocks = cdiv(V_p, 8);        // upper bound on loss-kernel blocks (>= 8 rows per block)
     c->m_part.ensure((size_t)loss_blocks * (sizeof(double) + sizeof(int64_t)) + 16);
     double* part = c->m_part.as<double>();
     int64_t* cnt = reinterpret_cast<int64_t*>(part + loss_blocks);
@@ -403,18 +428,14 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
 
     // a6: loss + gradient, written straight into the backward split's send buffer
     const float* gscale_bwd = g.dinv_in_p();   // backward column side
-    const unsigned lb = (unsigned)loss_blocks;
+    int64_t nb_loss = 0;
     if (!after) {
         if (dt == NTP_F32)
-            softmax_xent_kernel<float, float><<<lb, 256, 0, s>>>((const float*)c->recv.p, 1, V_p, d_s, m->C, lab, msk,
-                                                                 row0, n, (float*)c->send.p, 1, gscale_bwd, part, cnt,
-                                                                 0);
+            nb_loss = launch_softmax_xent(c, (const float*)c->recv.p, 1, V_p, d_s, m->C, lab, msk, row0, n,
+                                          (float*)c->send.p, 1, gscale_bwd, part, cnt, 0, s);
         else
-            softmax_xent_kernel<__nv_bfloat16, __nv_bfloat16><<<lb, 256, 0, s>>>(
-                (const __nv_bfloat16*)c->recv.p, 1, V_p, d_s, m->C, lab, msk, row0, n, (__nv_bfloat16*)c->send.p, 1,
-                gscale_bwd, part, cnt, 0);
-        NTP_LAUNCH_CHECK();
-        count_launch(c);
+            nb_loss = launch_softmax_xent(c, (const __nv_bfloat16*)c->recv.p, 1, V_p, d_s, m->C, lab, msk, row0, n,
+                                          (__nv_bfloat16*)c->send.p, 1, gscale_bwd, part, cnt, 0, s);
         if (P * d_s > m->C) {
             if (dt == NTP_F32)
                 zero_pad_cols_kernel<float><<<eblocks(V_p * (P * d_s - m->C)), 256, 0, s>>>((float*)c->send.p, V_p, d_s,
@@ -430,15 +451,13 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         float* Zv = dH1;   // reuse [V_p x ldH]
         unpack_f2v(c, c->recv.p, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s);
         mlp_gemm(c, false, false, V_p, m->C, m->hid, Zv, ldH, W1g, ldw1, L, ldL, s);
-        softmax_xent_kernel<float, float><<<lb, 256, 0, s>>>(L, 0, V_p, d_s, m->C, lab, msk, row0, n, dL, 0, nullptr,
-                                                             part, cnt, ldL);
-        NTP_LAUNCH_CHECK();
-        count_launch(c);
+        nb_loss = launch_softmax_xent(c, (const float*)L, 0, V_p, d_s, m->C, lab, msk, row0, n, dL, 0, nullptr, part,
+                                      cnt, ldL, s);
         mlp_gemm(c, true, false, m->hid, m->C, V_p, Zv, ldH, dL, ldL, dW1, m->C, s);          // dW1 = Z_v^T dlogits
         mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s);           // dZ_v -> L
         pack_v2f(c, L, ldL, m->hid, c->send.p, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s);
     }
-    reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, loss_blocks, scal);
+    reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb_loss, scal);
     NTP_LAUNCH_CHECK();
     count_launch(c);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E4 loss done

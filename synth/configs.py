@@ -62,7 +62,7 @@ _add(Config("products", 3, 2_449_029, 22, 40_600_000, GRAPH500, True, 100, 64, 4
 _add(Config("orkut", 4, 3_072_441, 22, 69_000_000, GRAPH500, True, 512, 128, 64, 2, 1.0, 0.0,
             note="BASELINE configs[3]; d=512 propagation pipeline"))
 # c5: ogbn-papers100M-shaped (111M vertices, ~1.6B arcs, directed, 128 features, 172 classes)
-_add(Config("papers", 5, 111_059_956, 27, 1_900_000_000, GRAPH500, False, 128, 128, 172, 2, 1.0, 0.0,
+_add(Config("papers", 5, 111_059_956, 27, 1_693_000_000, GRAPH500, False, 128, 128, 172, 2, 1.0, 0.0,
             w_after_prop=True, note="BASELINE configs[4]; bf16 storage"))
 
 # Small parity cases (several tiles, ragged tails, directed + symmetric, hubs)

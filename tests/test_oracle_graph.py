@@ -161,3 +161,16 @@ def test_norm_spectral_bound(seed, symmetric):
     sig = np.sqrt(np.linalg.norm(A.T @ (A @ x)))
     assert sig <= 1 + 1e-9
     assert np.linalg.norm(A, 2) <= 1 + 1e-9
+
+
+@pytest.mark.parametrize("name", ["small_dir", "tiny_sym", "small_appnp"])
+def test_sampled_rows_matches_full_build(name):
+    """oracle.graph.sampled_rows (arc-stream filter, used at papers100M scale) == rows of the full O1 build."""
+    cfg = synth.get_config(name)
+    g = oracle.graph.graph_from_config(cfg)
+    rows = np.unique(np.concatenate([np.arange(5), np.random.default_rng(0).integers(0, cfg.n, 40), [cfg.n - 1]]))
+    for tr in (False, True):
+        d = oracle.graph.sampled_rows(cfg, rows, tr)
+        rp, cl = (g.row_ptr_t, g.col_t) if tr else (g.row_ptr, g.col)
+        for v in rows:
+            assert np.array_equal(d[int(v)], cl[rp[v]:rp[v + 1]])
