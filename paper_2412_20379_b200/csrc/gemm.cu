@@ -29,7 +29,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;                 // fp32 elements per 128-byte swizzle row
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;
 constexpr int kTileA = BM * BK * 4;    // 16 KB
 
 struct GemmParams {
@@ -124,6 +124,12 @@ __device__ __forceinline__ void split_tile(uint8_t* t, uint8_t* lo, int bytes, i
     }
 }
 
+// Persistent: grid = min(#tiles, #SMs); CTA b walks tiles b, b + grid, ... (tile = (m, n, split),
+// m fastest so concurrent CTAs share the B operand in L2).  Pipeline stages and phases run on across
+// tiles; the accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue of tile i
+// overlaps the MMAs of tile i+1.
+//   warp 0   : TMEM alloc + TMA producer        warp 1   : MMA issuer
+//   warps 2-5: split workers                    warps 6-9: epilogue (TMEM lane quarter = warp % 4)
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -137,23 +143,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint64_t* full = bars;
     uint64_t* split = bars + S;
     uint64_t* empty = bars + 2 * S;
-    uint64_t* accum = bars + 3 * S;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 1);
+    uint64_t* tfull = bars + 3 * S;          // [2] accumulator ready
+    uint64_t* tempty = bars + 3 * S + 2;     // [2] accumulator drained
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM;
-    const int n0 = blockIdx.y * p.BN;
-    const int kt0 = blockIdx.z * p.k_tiles_per_split;
-    const int nk = min(p.k_tiles_per_split, p.k_tiles_total - kt0);
+    const int m_tiles = (p.M + BM - 1) / BM;
+    const int n_tiles = (p.N + p.BN - 1) / p.BN;
+    const int splits = (p.k_tiles_total + p.k_tiles_per_split - 1) / p.k_tiles_per_split;
+    const int num_tiles = m_tiles * n_tiles * splits;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&split[s], 128);
-            mbar_init(&empty[s], 1);
+        for (int st = 0; st < S; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&split[st], 128);
+            mbar_init(&empty[st], 1);
         }
-        mbar_init(accum, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -166,79 +176,114 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_holder;
 
+    auto decode = [&](int t, int& m0, int& n0, int& kt0, int& nk, int& z) {
+        const int mt = t % m_tiles;
+        const int rest = t / m_tiles;
+        const int nt = rest % n_tiles;
+        z = rest / n_tiles;
+        m0 = mt * BM;
+        n0 = nt * p.BN;
+        kt0 = z * p.k_tiles_per_split;
+        nk = min(p.k_tiles_per_split, p.k_tiles_total - kt0);
+    };
+
     if (warp == 0) {
-        if (lane == 0 && nk > 0) {
+        if (lane == 0) {
             // ---------------- TMA producer
-            for (int i = 0; i < nk; ++i) {
-                const int s = i % S;
-                if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-                uint8_t* sa = smem + s * stage_bytes;
-                uint8_t* sb = sa + 2 * kTileA;
-                const int k0 = (kt0 + i) * BK;
-                mbar_expect_tx(&full[s], kTileA + tileB);
-                if (A_MN) {
-                    for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 4096, &tmA, &full[s], m0 + 32 * j, k0);
-                } else {
-                    tma_load_2d(sa, &tmA, &full[s], k0, m0);
-                }
-                if (B_MN) {
-                    for (int j = 0; j < p.bn_alloc / 32; ++j) tma_load_2d(sb + j * 4096, &tmB, &full[s], n0 + 32 * j, k0);
-                } else {
-                    tma_load_2d(sb, &tmB, &full[s], k0, n0);
+            int it = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                int m0, n0, kt0, nk, z;
+                decode(t, m0, n0, kt0, nk, z);
+                for (int i = 0; i < nk; ++i, ++it) {
+                    const int s = it % S;
+                    if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+                    uint8_t* sa = smem + s * stage_bytes;
+                    uint8_t* sb = sa + 2 * kTileA;
+                    const int k0 = (kt0 + i) * BK;
+                    mbar_expect_tx(&full[s], kTileA + tileB);
+                    if (A_MN) {
+                        for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 4096, &tmA, &full[s], m0 + 32 * j, k0);
+                    } else {
+                        tma_load_2d(sa, &tmA, &full[s], k0, m0);
+                    }
+                    if (B_MN) {
+                        for (int j = 0; j < p.bn_alloc / 32; ++j)
+                            tma_load_2d(sb + j * 4096, &tmB, &full[s], n0 + 32 * j, k0);
+                    } else {
+                        tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && nk > 0) {
+        if (lane == 0) {
             // ---------------- MMA issuer
-            for (int i = 0; i < nk; ++i) {
-                const int s = i % S;
-                mbar_wait(&split[s], (i / S) & 1);
+            int it = 0, tc = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tc) {
+                int m0, n0, kt0, nk, z;
+                decode(t, m0, n0, kt0, nk, z);
+                const int a = tc & 1;
+                if (tc >= 2) mbar_wait(&tempty[a], ((tc >> 1) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a = smem_u32(smem + s * stage_bytes);
-                const uint32_t alo = a + kTileA;
-                const uint32_t b = a + 2 * kTileA;
-                const uint32_t blo = b + tileB;
+                const uint32_t acc = tmem + (uint32_t)(a * p.BN);
+                for (int i = 0; i < nk; ++i, ++it) {
+                    const int s = it % S;
+                    mbar_wait(&split[s], (it / S) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t sa = smem_u32(smem + s * stage_bytes);
+                    const uint32_t salo = sa + kTileA;
+                    const uint32_t sb = sa + 2 * kTileA;
+                    const uint32_t sblo = sb + tileB;
 #pragma unroll
-                for (int k = 0; k < BK / 8; ++k) {
-                    const uint32_t ao = A_MN ? k * 1024 : k * 32;   // K step of 8 tf32
-                    const uint32_t bo = B_MN ? k * 1024 : k * 32;
-                    const uint64_t dA = A_MN ? desc_mnmajor(a + ao, p.mn_lbo, p.mn_sbo) : desc_kmajor(a + ao);
-                    const uint64_t dAlo = A_MN ? desc_mnmajor(alo + ao, p.mn_lbo, p.mn_sbo) : desc_kmajor(alo + ao);
-                    const uint64_t dB = B_MN ? desc_mnmajor(b + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(b + bo);
-                    const uint64_t dBlo = B_MN ? desc_mnmajor(blo + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(blo + bo);
-                    mma_tf32(tmem, dA, dB, p.idesc, (i > 0 || k > 0) ? 1u : 0u);
-                    mma_tf32(tmem, dA, dBlo, p.idesc, 1u);
-                    mma_tf32(tmem, dAlo, dB, p.idesc, 1u);
+                    for (int k = 0; k < BK / 8; ++k) {
+                        const uint32_t ao = A_MN ? k * 1024 : k * 32;   // K step of 8 tf32
+                        const uint32_t bo = B_MN ? k * 1024 : k * 32;
+                        const uint64_t dA = A_MN ? desc_mnmajor(sa + ao, p.mn_lbo, p.mn_sbo) : desc_kmajor(sa + ao);
+                        const uint64_t dAlo = A_MN ? desc_mnmajor(salo + ao, p.mn_lbo, p.mn_sbo) : desc_kmajor(salo + ao);
+                        const uint64_t dB = B_MN ? desc_mnmajor(sb + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(sb + bo);
+                        const uint64_t dBlo = B_MN ? desc_mnmajor(sblo + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(sblo + bo);
+                        mma_tf32(acc, dA, dB, p.idesc, (i > 0 || k > 0) ? 1u : 0u);
+                        mma_tf32(acc, dA, dBlo, p.idesc, 1u);
+                        mma_tf32(acc, dAlo, dB, p.idesc, 1u);
+                    }
+                    mma_commit(&empty[s]);
                 }
-                mma_commit(&empty[s]);
+                mma_commit(&tfull[a]);
             }
-            mma_commit(accum);
+        }
+    } else if (warp < 6) {
+        // ---------------- split workers
+        const int tid = threadIdx.x - 64;
+        int it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            int m0, n0, kt0, nk, z;
+            decode(t, m0, n0, kt0, nk, z);
+            for (int i = 0; i < nk; ++i, ++it) {
+                const int s = it % S;
+                mbar_wait(&full[s], (it / S) & 1);
+                uint8_t* sa = smem + s * stage_bytes;
+                split_tile(sa, sa + kTileA, kTileA, tid, 128);
+                uint8_t* sb = sa + 2 * kTileA;
+                split_tile(sb, sb + tileB, tileB, tid, 128);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&split[s]);
+            }
         }
     } else {
-        // ---------------- split workers, then epilogue
-        const int tid = threadIdx.x - 64;
-        for (int i = 0; i < nk; ++i) {
-            const int s = i % S;
-            mbar_wait(&full[s], (i / S) & 1);
-            uint8_t* sa = smem + s * stage_bytes;
-            split_tile(sa, sa + kTileA, kTileA, tid, 128);
-            uint8_t* sb = sa + 2 * kTileA;
-            split_tile(sb, sb + tileB, tileB, tid, 128);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&split[s]);
-        }
+        // ---------------- epilogue
         const int q = warp & 3;                       // TMEM lane quarter of this warp
-        const int row = m0 + 32 * q + lane;
-        if (nk > 0) {
-            mbar_wait(accum, 0);
+        int tc = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tc) {
+            int m0, n0, kt0, nk, z;
+            decode(t, m0, n0, kt0, nk, z);
+            const int a = tc & 1;
+            mbar_wait(&tfull[a], (tc >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        }
-        float* Cb = p.C + (int64_t)blockIdx.z * p.split_stride;
-        for (int c0 = 0; c0 < p.BN; c0 += 32) {
-            uint32_t r[32];
-            if (nk > 0) {
-                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+            const int row = m0 + 32 * q + lane;
+            float* Cb = p.C + (int64_t)z * p.split_stride;
+            for (int c0 = 0; c0 < p.BN; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * p.BN + c0);
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -249,35 +294,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                       "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            } else {
+                if (row < p.M && n0 + c0 < p.N) {
+                    float* dst = Cb + (int64_t)row * p.ldc + n0 + c0;
+                    const int ncol = min(32, p.N - (n0 + c0));
+                    float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) r[j] = 0u;
-            }
-            if (row < p.M) {
-                float* dst = Cb + (int64_t)row * p.ldc + n0 + c0;
-                const int ncol = min(32, p.N - (n0 + c0));
-                float v[32];
+                    for (int j = 0; j < 32; ++j) {
+                        v[j] = __uint_as_float(r[j]);
+                        if (p.epi == 1) v[j] = fmaxf(v[j], 0.f);
+                    }
+                    if (p.epi == 2) {
+                        const float* ax = p.aux + (int64_t)row * p.ldaux + n0 + c0;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    v[j] = __uint_as_float(r[j]);
-                    if (p.epi == 1) v[j] = fmaxf(v[j], 0.f);
-                }
-                if (p.epi == 2) {
-                    const float* ax = p.aux + (int64_t)row * p.ldaux + n0 + c0;
+                        for (int j = 0; j < 32; ++j)
+                            if (j < ncol && !(ax[j] > 0.f)) v[j] = 0.f;
+                    }
+                    if (ncol == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (j < ncol && !(ax[j] > 0.f)) v[j] = 0.f;
-                }
-                if (ncol == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (j < ncol) dst[j] = v[j];
+                        for (int j = 0; j < 32; ++j)
+                            if (j < ncol) dst[j] = v[j];
+                    }
                 }
             }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&tempty[a]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -369,7 +413,7 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     const int stage_bytes = 2 * kTileA + 2 * p.bn_alloc * BK * 4;
     p.stages = std::max(2, std::min(4, (225 * 1024 - 1024 - 256) / stage_bytes));
     p.tmem_cols = 32;
-    while ((int)p.tmem_cols < p.BN) p.tmem_cols <<= 1;
+    while ((int)p.tmem_cols < 2 * p.BN) p.tmem_cols <<= 1;   // double-buffered accumulator
     p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
               ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     p.k_tiles_total = (int)cdiv(K, BK);
@@ -391,8 +435,9 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     const CUtensorMapSwizzle mnswz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
     CUtensorMap ta = a_mn ? make_map(A, M, K, lda, 32, 32, mnswz) : make_map(A, K, M, lda, 32, BM);
     CUtensorMap tb = b_mn ? make_map(B, N, K, ldb, 32, 32, mnswz) : make_map(B, K, N, ldb, 32, p.bn_alloc);
-    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (3 * p.stages + 2) * 8;
-    dim3 grid(m_tiles, n_tiles, splits);
+    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (3 * p.stages + 6) * 8;
+    const int64_t num_tiles = (int64_t)m_tiles * n_tiles * splits;
+    dim3 grid((unsigned)std::min<int64_t>(num_tiles, 148));
     if (splits == 1) {
         p.C = C;
         p.ldc = ldc;

@@ -70,6 +70,9 @@ template <> struct V16<float> {
     __device__ __forceinline__ static void store(void* p, const float (&v)[4]) {
         *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
     }
+    __device__ __forceinline__ static uint4 pack(const float (&v)[4]) {
+        return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+    }
 };
 template <> struct V16<__nv_bfloat16> {
     static constexpr int N = 8;
@@ -95,6 +98,15 @@ template <> struct V16<__nv_bfloat16> {
         unpack(__ldg(reinterpret_cast<const uint4*>(p)), v);
 #pragma unroll
         for (int i = 0; i < 8; ++i) a[i] += v[i];
+    }
+    __device__ __forceinline__ static uint4 pack(const float (&v)[8]) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            w[i] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        return make_uint4(w[0], w[1], w[2], w[3]);
     }
     __device__ __forceinline__ static void store(void* p, const float (&v)[8]) {
         uint32_t w[4];
@@ -126,6 +138,7 @@ struct HopParams {
     float gamma, alpha;
     int mode;                          // 0 intermediate, 1 last
     int tma_per8;                      // groups (out of every 8) that gather with TMA gather4
+    int64_t nnz;
 };
 
 // Lane layout ("full row per edge"): a group of L lanes works on one unit.  Lane
@@ -141,15 +154,18 @@ struct HopParams {
 // per lane) and distributed with shuffles.
 // GATHER: 0 = LSU loads (ld.global, policy POL), 1 = TMA tile::gather4 into a per-group
 // double-buffered shared-memory ring (no L1 data-pipe fill), read back with LDS.
-template <typename T, int E, int L, int POL, int GATHER>
-__global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p, const __grid_constant__ CUtensorMap tmS) {
+// SHORT: short-row variant (graphs with average degree < 32): 8-16-edge batches so a ~15-arc row
+// does not pay for a 64-slot batch, and fewer registers for 3 CTAs per SM.  The batch size does
+// not enter the reduction order (groups are (j - eb) mod 8 for any batch that is a multiple of 8).
+template <typename T, int E, int L, int POL, int GATHER, int SHORT = 0>
+__global__ void __launch_bounds__(kBlock, (SHORT && E == 8) ? 3 : 2) spmm_hop_kernel(const HopParams p, const __grid_constant__ CUtensorMap tmS) {
     // GATHER == 1: mixed mode -- groups with (gidx % 8) < p.tma_per8 use the TMA engine, the others
     // the LSU path, so both units pull rows from L2 concurrently (same reduction order either way).
     constexpr int NACC = kG / E;
     constexpr int LOG_E = (E == 1) ? 0 : (E == 2) ? 1 : (E == 4) ? 2 : 3;
     constexpr int VALS = V16<T>::N;
     // edges per pipeline batch: 16-byte loads per lane per batch = BATCH / E (4 or 8)
-    constexpr int BATCH = (E == 8) ? 64 : (E == 4) ? 32 : 8 * E;
+    constexpr int BATCH = SHORT ? ((E >= 4) ? 16 : 8) : ((E == 8) ? 64 : (E == 4) ? 32 : 8 * E);
     constexpr int LPB = BATCH / E;                        // loads per lane per batch
     constexpr int ISL = (BATCH + L - 1) / L;              // column indices held per lane
     const int lane = threadIdx.x & 31;
@@ -203,6 +219,16 @@ __global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p, 
             const int vcol = pass * VP + c;
             const bool col_ok = active && vcol < p.nvec;
             const char* __restrict__ vbase = p.S_in + (int64_t)min(vcol, p.nvec - 1) * 16;
+            // epilogue operands issued now so their latency hides behind the gather (short rows)
+            const bool fin = !(head || tail) && e_raw == 0 && col_ok;
+            uint4 self_raw = make_uint4(0u, 0u, 0u, 0u), s0_raw = make_uint4(0u, 0u, 0u, 0u);
+            float ra = 0.f, rb = 0.f;
+            if (fin) {
+                self_raw = ld_raw(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * 16);
+                if (p.alpha != 0.f) s0_raw = ld_raw(p.S0 + (int64_t)r * p.ld_s0 + (int64_t)vcol * 16);
+                ra = __ldg(p.rs + r);
+                rb = __ldg(p.cs + r);
+            }
             float acc[NACC][VALS];
 #pragma unroll
             for (int k = 0; k < NACC; ++k)
@@ -332,14 +358,18 @@ __global__ void __launch_bounds__(kBlock, 2) spmm_hop_kernel(const HopParams p, 
             }
             const int64_t voff = (int64_t)vcol * 16;
             float self[VALS];
-            V16<T>::load(p.S_in + (int64_t)r * p.ld_in + voff, self);
-            const float a = p.rs[r];
-            const float b = p.cs[r];
+#pragma unroll
+            for (int i = 0; i < VALS; ++i) self[i] = 0.f;
+            V16<T>::add_raw(self, self_raw);
+            const float a = ra;
+            const float b = rb;
             const float sig = (p.mode == 0) ? p.gamma * a * b : p.gamma * a;
             float out[VALS];
             if (p.alpha != 0.f) {
                 float h[VALS];
-                V16<T>::load(p.S0 + (int64_t)r * p.ld_s0 + voff, h);
+#pragma unroll
+                for (int i = 0; i < VALS; ++i) h[i] = 0.f;
+                V16<T>::add_raw(h, s0_raw);
                 const float beta = (p.mode == 0) ? p.alpha : p.alpha / b;
 #pragma unroll
                 for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + self[i]) + beta * h[i];
@@ -418,6 +448,9 @@ template <typename T, int E, int L>
 void launch_hop(const HopParams& p, cudaStream_t s) {
     static const int pol = [] { const char* v = getenv("NTP_GATHER_POLICY"); return v ? atoi(v) : 0; }();
     static const int tma_env = [] { const char* v = getenv("NTP_SPMM_TMA"); return v ? atoi(v) : -1; }();
+    static const int short_env = [] { const char* v = getenv("NTP_SPMM_SHORT"); return v ? atoi(v) : -1; }();
+    // short-row variant when the average degree is below 32 (products, papers shapes)
+    const bool short_rows = E >= 4 && (short_env >= 0 ? short_env != 0 : (p.nnz < 32 * std::max<int64_t>(p.n, 1)));
     // groups per 8 on the TMA path: measured sweet spots; NTP_SPMM_TMA overrides
     const int tma = tma_env >= 0 ? tma_env : 0;
     const int64_t groups = p.u_end - p.u_begin;
@@ -455,7 +488,8 @@ void launch_hop(const HopParams& p, cudaStream_t s) {
             NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
             attr0 = true;
         }
-        spmm_hop_kernel<T, E, L, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
+        if (short_rows) spmm_hop_kernel<T, E, L, 0, 0, 1><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
+        else spmm_hop_kernel<T, E, L, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
     }
     else if (pol == 2) spmm_hop_kernel<T, E, L, 2, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
     else spmm_hop_kernel<T, E, L, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
@@ -510,6 +544,8 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     p.ld_out = ld_out * es;
     p.ld_s0 = ld_s0 * es;
     p.n = g.n;
+    p.nnz = g.nnz;
+
     unit_range(csr, row_lo, row_hi, p.u_begin, p.u_end);
     p.row_lo = row_lo;
     p.row_hi = row_hi;
