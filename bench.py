@@ -220,7 +220,7 @@ def main():
     n, nnz, sym = ctx.graph_info()
     t_graph = time.time() - t0
 
-    dtype_name = args.dtype or ("bf16" if cfg.name == "papers" else "f32")
+    dtype_name = args.dtype or ("bf16" if cfg.name.startswith("papers") else "f32")
     dt = ntp.NTP_BF16 if dtype_name == "bf16" else ntp.NTP_F32
     part = ntp.partition(n, cfg.w, world, dt, args.chunks, args.slice_align)
     V_p, d_s = part["V_p"], part["d_s"]

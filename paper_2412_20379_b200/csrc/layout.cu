@@ -24,77 +24,137 @@ template <> __device__ __forceinline__ __nv_bfloat16 cvt<float, __nv_bfloat16>(f
 template <> __device__ __forceinline__ float cvt<__nv_bfloat16, float>(__nv_bfloat16 x) { return __bfloat162float(x); }
 template <> __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16, __nv_bfloat16>(__nv_bfloat16 x) { return x; }
 
+template <typename T> struct Q4;   // 4 consecutive elements
+template <> struct Q4<float> {
+    __device__ __forceinline__ static void ld(const float* p, float (&v)[4]) {
+        const float4 x = *reinterpret_cast<const float4*>(p);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+    __device__ __forceinline__ static void st(float* p, const float (&v)[4]) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <> struct Q4<__nv_bfloat16> {
+    __device__ __forceinline__ static void ld(const __nv_bfloat16* p, float (&v)[4]) {
+        const uint2 x = *reinterpret_cast<const uint2*>(p);
+        v[0] = __uint_as_float(x.x << 16); v[1] = __uint_as_float(x.x & 0xFFFF0000u);
+        v[2] = __uint_as_float(x.y << 16); v[3] = __uint_as_float(x.y & 0xFFFF0000u);
+    }
+    __device__ __forceinline__ static void st(__nv_bfloat16* p, const float (&v)[4]) {
+        const __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+        *reinterpret_cast<uint2*>(p) = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+    }
+};
+
+// One warp per vertex row (grid-stride), each lane 4 consecutive columns: block q of `send`
+// gets columns [q*d_s, (q+1)*d_s) of the row (d_s is a multiple of 4, so a quad never straddles
+// two blocks), pre-scaled by row_scale[row0 + v] and cast; columns >= w and rows >= n are zero.
+// `vec`: Hv rows are 16-byte aligned with ld % 4 == 0 (quad loads), else element loads.
 template <typename Tin, typename Tout>
-__global__ void pack_v2f_kernel(const Tin* __restrict__ Hv, int64_t ld_v, int32_t w, Tout* __restrict__ send,
-                                int64_t V_p, int32_t d_s, int32_t P, const float* __restrict__ row_scale,
-                                int64_t row0, int64_t n) {
-    const int64_t total = (int64_t)P * V_p * d_s;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t c = (int32_t)(i % d_s);
-        const int64_t v = (i / d_s) % V_p;
-        const int32_t q = (int32_t)(i / ((int64_t)d_s * V_p));
-        const int32_t col = q * d_s + c;
+__global__ void __launch_bounds__(256) pack_v2f_kernel(const Tin* __restrict__ Hv, int64_t ld_v, int32_t w,
+                                                       Tout* __restrict__ send, int64_t V_p, int32_t d_s, int32_t P,
+                                                       const float* __restrict__ row_scale, int64_t row0, int64_t n,
+                                                       int vec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int wpad = P * d_s;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < V_p; v += warps) {
         const int64_t gr = row0 + v;
-        float x = 0.f;
-        if (col < w && gr < n) {
-            x = cvt<Tin, float>(Hv[v * ld_v + col]);
-            if (row_scale) x *= row_scale[gr];
+        const bool real = gr < n;
+        const float sc = (real && row_scale) ? row_scale[gr] : 1.f;
+        const Tin* src = Hv + v * ld_v;
+        for (int k = lane * 4; k < wpad; k += 128) {
+            float x[4] = {0.f, 0.f, 0.f, 0.f};
+            if (real) {
+                if (vec && k + 3 < w) {
+                    Q4<Tin>::ld(src + k, x);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) x[i] = (k + i < w) ? cvt<Tin, float>(src[k + i]) : 0.f;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) x[i] *= sc;
+            }
+            const int q = k / d_s;
+            Q4<Tout>::st(send + ((int64_t)q * V_p + v) * d_s + (k - q * d_s), x);
         }
-        send[i] = cvt<float, Tout>(x);
     }
 }
 
+// One warp per vertex row: columns [4k, 4k+4) of the row come from block q = 4k / d_s of `recv`.
+// `keep` (optional, same row/column indexing as Hv, ld_keep): zero where keep <= 0 (the fused
+// ReLU' mask of the MLP backward, reading R12).
 template <typename Tin, typename Tout>
-__global__ void unpack_f2v_kernel(const Tin* __restrict__ recv, int64_t V_p, int32_t d_s, Tout* __restrict__ Hv,
-                                  int64_t ld_v, int32_t w) {
-    const int64_t total = V_p * (int64_t)w;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = i / w;
-        const int32_t col = (int32_t)(i % w);
-        const int32_t q = col / d_s, c = col % d_s;
-        Hv[v * ld_v + col] = cvt<Tin, Tout>(recv[((int64_t)q * V_p + v) * d_s + c]);
+__global__ void __launch_bounds__(256) unpack_f2v_kernel(const Tin* __restrict__ recv, int64_t V_p, int32_t d_s,
+                                                         Tout* __restrict__ Hv, int64_t ld_v, int32_t w, int vec,
+                                                         const float* __restrict__ keep, int64_t ld_keep) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < V_p; v += warps) {
+        Tout* dst = Hv + v * ld_v;
+        for (int k = lane * 4; k < w; k += 128) {
+            const int q = k / d_s;
+            float x[4];
+            Q4<Tin>::ld(recv + ((int64_t)q * V_p + v) * d_s + (k - q * d_s), x);
+            if (keep) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (k + i < w && !(keep[v * ld_keep + k + i] > 0.f)) x[i] = 0.f;
+            }
+            if (vec && k + 3 < w) {
+                Q4<Tout>::st(dst + k, x);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (k + i < w) dst[k + i] = cvt<float, Tout>(x[i]);
+            }
+        }
     }
 }
 
 int blocks_for(int64_t total) { return (int)std::min<int64_t>(std::max<int64_t>(cdiv(total, 256), 1), 148 * 16); }
+int row_blocks(int64_t rows) { return (int)std::min<int64_t>(std::max<int64_t>(cdiv(rows, 8), 1), 148 * 16); }
+template <typename T> bool quad_ok(const void* p, int64_t ld) {
+    return (reinterpret_cast<uintptr_t>(p) % (4 * sizeof(T))) == 0 && (ld % 4) == 0;
+}
 
 }  // namespace
 
 void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, int64_t V_p, int32_t d_s, int32_t P,
               const float* row_scale, int64_t row0, int64_t n, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s) {
-    const int64_t total = (int64_t)P * V_p * d_s;
-    if (total == 0) return;
-    const int b = blocks_for(total);
+    if (V_p == 0 || d_s == 0) return;
+    const int b = row_blocks(V_p);
+    const int vec = (dt_in == NTP_F32) ? quad_ok<float>(Hv, ld_v) : quad_ok<__nv_bfloat16>(Hv, ld_v);
     if (dt_in == NTP_F32 && dt_out == NTP_F32)
-        pack_v2f_kernel<float, float><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (float*)send, V_p, d_s, P, row_scale, row0, n);
+        pack_v2f_kernel<float, float><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (float*)send, V_p, d_s, P, row_scale, row0, n, vec);
     else if (dt_in == NTP_F32 && dt_out == NTP_BF16)
         pack_v2f_kernel<float, __nv_bfloat16><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (__nv_bfloat16*)send, V_p, d_s, P,
-                                                                row_scale, row0, n);
+                                                                row_scale, row0, n, vec);
     else if (dt_in == NTP_BF16 && dt_out == NTP_BF16)
         pack_v2f_kernel<__nv_bfloat16, __nv_bfloat16><<<b, 256, 0, s>>>((const __nv_bfloat16*)Hv, ld_v, w,
-                                                                        (__nv_bfloat16*)send, V_p, d_s, P, row_scale, row0, n);
+                                                                        (__nv_bfloat16*)send, V_p, d_s, P, row_scale, row0, n, vec);
     else
         pack_v2f_kernel<__nv_bfloat16, float><<<b, 256, 0, s>>>((const __nv_bfloat16*)Hv, ld_v, w, (float*)send, V_p, d_s,
-                                                                P, row_scale, row0, n);
+                                                                P, row_scale, row0, n, vec);
     NTP_LAUNCH_CHECK();
     count_launch(c);
 }
 
 void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t P, void* Hv, int64_t ld_v, int32_t w,
-                ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s) {
+                ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s, const float* keep, int64_t ld_keep) {
     (void)P;
-    const int64_t total = V_p * (int64_t)w;
-    if (total == 0) return;
-    const int b = blocks_for(total);
+    if (V_p == 0 || w == 0) return;
+    const int b = row_blocks(V_p);
+    const int vec = (dt_out == NTP_F32) ? quad_ok<float>(Hv, ld_v) : quad_ok<__nv_bfloat16>(Hv, ld_v);
     if (dt_in == NTP_F32 && dt_out == NTP_F32)
-        unpack_f2v_kernel<float, float><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (float*)Hv, ld_v, w);
+        unpack_f2v_kernel<float, float><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (float*)Hv, ld_v, w, vec, keep, ld_keep);
     else if (dt_in == NTP_BF16 && dt_out == NTP_F32)
-        unpack_f2v_kernel<__nv_bfloat16, float><<<b, 256, 0, s>>>((const __nv_bfloat16*)recv, V_p, d_s, (float*)Hv, ld_v, w);
+        unpack_f2v_kernel<__nv_bfloat16, float><<<b, 256, 0, s>>>((const __nv_bfloat16*)recv, V_p, d_s, (float*)Hv, ld_v, w, vec, keep, ld_keep);
     else if (dt_in == NTP_BF16 && dt_out == NTP_BF16)
         unpack_f2v_kernel<__nv_bfloat16, __nv_bfloat16><<<b, 256, 0, s>>>((const __nv_bfloat16*)recv, V_p, d_s,
-                                                                          (__nv_bfloat16*)Hv, ld_v, w);
+                                                                          (__nv_bfloat16*)Hv, ld_v, w, vec, keep, ld_keep);
     else
-        unpack_f2v_kernel<float, __nv_bfloat16><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (__nv_bfloat16*)Hv, ld_v, w);
+        unpack_f2v_kernel<float, __nv_bfloat16><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (__nv_bfloat16*)Hv, ld_v, w, vec, keep, ld_keep);
     NTP_LAUNCH_CHECK();
     count_launch(c);
 }

@@ -68,10 +68,11 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
     const int sub = threadIdx.x % LPR;
     const int rloc = threadIdx.x / LPR;
     const unsigned smask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << ((threadIdx.x & 31) / LPR * LPR));
-    const int64_t v = (int64_t)blockIdx.x * RPB + rloc;
     double my_loss = 0.0;
     int64_t my_cnt = 0;
-    if (v < V_p) {
+    // grid-stride over row groups: a fixed grid keeps the partials few (the fixed-order
+    // reduce stays one small pass) and the per-thread accumulation order fixed.
+    for (int64_t v = (int64_t)blockIdx.x * RPB + rloc; v < V_p; v += (int64_t)gridDim.x * RPB) {
         const int64_t gr = row0 + v;
         const bool train = gr < n && mask[v] != 0;
         auto addr = [&](int col) -> int64_t {
@@ -100,8 +101,8 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
         const int yv = train ? y[v] : -1;
         if (train && sub == 0) {
             const float ly = ldf<TIn>(in + addr(yv));
-            my_loss = (double)(logf(se) + mx - ly);
-            my_cnt = 1;
+            my_loss += (double)(logf(se) + mx - ly);
+            my_cnt += 1;
         }
         const float inv = 1.f / se;
         const float sc = (gscale && gr < n) ? gscale[gr] : 1.f;
@@ -145,7 +146,7 @@ int64_t launch_softmax_xent(ntp_ctx* c, const TIn* in, int in_blocked, int64_t V
     NTP_CHECK(C <= 256, NTP_ERR_CONFIG, "C = %d > 256 classes is not supported", C);
     int64_t nb;
 #define NTP_LOSS_LAUNCH(LPR)                                                                                    \
-    nb = cdiv(V_p, 256 / LPR);                                                                                  \
+    nb = std::min<int64_t>(std::max<int64_t>(cdiv(V_p, 256 / LPR), 1), 148 * 8);                              \
     softmax_xent_kernel<TIn, TOut, LPR><<<(unsigned)nb, 256, 0, s>>>(in, in_blocked, V_p, d_s, C, y, mask, row0, n, \
                                                                      out, out_blocked, gscale, part, cnt, ld_plain)
     if (C <= 32) { NTP_LOSS_LAUNCH(4); }
@@ -483,7 +484,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     }
     float* dLw = after ? dH1 : dL;            // gathered dL^ rows (dH1 before the mask when W1 is applied after)
     const int64_t ld_dLw = after ? ldH : ldL;
-    unpack_f2v(c, c->send.p, V_p, d_s, P, dLw, ld_dLw, w, dt, NTP_F32, s);
+    unpack_f2v(c, c->send.p, V_p, d_s, P, dLw, ld_dLw, w, dt, NTP_F32, s, after ? H1 : nullptr, ldH);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E6 prop bwd + f2v bwd
 
     // a10: MLP backward (ReLU' mask fused into the dH1 GEMM epilogue)
@@ -491,9 +492,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         mlp_gemm(c, true, false, m->hid, m->C, V_p, H1, ldH, dL, ldL, dW1, m->C, s);              // dW1 = H1^T dL^
         mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, dH1, ldH, s, 2, H1, ldH); // dH1
     } else {
-        relu_grad_kernel<<<eblocks(V_p * m->hid), 256, 0, s>>>(dH1, H1, V_p, m->hid, ldH, ldH);
-        NTP_LAUNCH_CHECK();
-        count_launch(c);
+        // ReLU' mask fused into the gather's unpack above
     }
     mlp_gemm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, ldH, dW0, m->hid, s);            // dW0 = X^T dH1
     NTP_CUDA(record_timing(c, E[ei++], s));   // E7 mlp bwd

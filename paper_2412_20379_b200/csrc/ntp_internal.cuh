@@ -207,7 +207,8 @@ void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, i
               int32_t d_s, int32_t P, const float* row_scale, int64_t row0, int64_t n,
               ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s);
 void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t P, void* Hv,
-                int64_t ld_v, int32_t w, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s);
+                int64_t ld_v, int32_t w, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s,
+                const float* keep = nullptr, int64_t ld_keep = 0);
 void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_elems, ntp_dtype dt,
                      cudaStream_t s);
 

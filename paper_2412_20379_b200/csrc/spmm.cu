@@ -55,6 +55,9 @@ __device__ __forceinline__ uint4 ld_gather(const void* p) {
 
 template <> struct V16<float> {
     static constexpr int N = 4;
+    __device__ __forceinline__ static float elem(const uint4 x, int i) {
+        return __uint_as_float(i == 0 ? x.x : i == 1 ? x.y : i == 2 ? x.z : x.w);
+    }
     __device__ __forceinline__ static void add_raw(float (&a)[4], const uint4 x) {
         a[0] += __uint_as_float(x.x); a[1] += __uint_as_float(x.y);
         a[2] += __uint_as_float(x.z); a[3] += __uint_as_float(x.w);
@@ -76,6 +79,10 @@ template <> struct V16<float> {
 };
 template <> struct V16<__nv_bfloat16> {
     static constexpr int N = 8;
+    __device__ __forceinline__ static float elem(const uint4 x, int i) {
+        const uint32_t w = (i >> 1) == 0 ? x.x : (i >> 1) == 1 ? x.y : (i >> 1) == 2 ? x.z : x.w;
+        return __uint_as_float((i & 1) ? (w & 0xFFFF0000u) : (w << 16));
+    }
     __device__ __forceinline__ static void unpack(const uint4 x, float (&v)[8]) {
         const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -210,7 +217,51 @@ __global__ void __launch_bounds__(kBlock, (SHORT && E == 8) ? 3 : 2) spmm_hop_ke
     const int row_vals = p.nvec * VALS;
     const int npass = (p.nvec + VP - 1) / VP;
 
-    for (int r = max((int64_t)r0, p.row_lo); r < min((int64_t)r_end, p.row_hi); ++r) {
+    const int r_stop = (int)min((int64_t)r_end, p.row_hi);
+    for (int r = max((int64_t)r0, p.row_lo); r < r_stop; ++r) {
+        // ---- tiny-row fast path: E consecutive rows with <= 8 arcs each, wholly inside this unit,
+        // one row per edge slot.  With <= 8 arcs every reduction group holds at most one arc, so
+        // acc_g = 0 + v_g and the in-lane tree ((v0+v1)+(v2+v3))+((v4+v5)+(v6+v7)) is exactly the
+        // canonical butterfly: results are bitwise those of the general path.
+        if (E >= 2 && npass == 1 && r + E <= r1 && r + E <= r_stop) {
+            const int my_r = r + e;
+            const int trs = __ldg(p.rp + my_r), tre = __ldg(p.rp + my_r + 1);
+            const int deg = tre - trs;
+            const bool ok = deg <= 8 && !(my_r == r0 && trs < e0);
+            if (__all_sync(gmask, ok)) {
+                const bool cok = active && c < p.nvec;
+                const int64_t voff = (int64_t)min(c, p.nvec - 1) * 16;
+                const uint4 self_raw = ld_raw(p.S_in + (int64_t)my_r * p.ld_in + voff);
+                const uint4 s0_raw = (p.alpha != 0.f) ? ld_raw(p.S0 + (int64_t)my_r * p.ld_s0 + voff)
+                                                      : make_uint4(0u, 0u, 0u, 0u);
+                const float ra = __ldg(p.rs + my_r), rb = __ldg(p.cs + my_r);
+                int src[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) src[k] = (k < deg) ? __ldg(colp + trs + k) : 0;
+                uint4 x8[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    x8[k] = (k < deg) ? ld_raw(p.S_in + (int64_t)src[k] * p.ld_in + voff) : make_uint4(0u, 0u, 0u, 0u);
+                float self[VALS], h[VALS], out[VALS];
+#pragma unroll
+                for (int i = 0; i < VALS; ++i) self[i] = h[i] = 0.f;
+                V16<T>::add_raw(self, self_raw);
+                V16<T>::add_raw(h, s0_raw);
+                const float sig = (p.mode == 0) ? p.gamma * ra * rb : p.gamma * ra;
+                const float beta = (p.mode == 0) ? p.alpha : p.alpha / rb;
+#pragma unroll
+                for (int i = 0; i < VALS; ++i) {
+                    float g[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) g[k] = 0.f + V16<T>::elem(x8[k], i);   // acc_g = 0 + v_g
+                    const float tot = ((g[0] + g[1]) + (g[2] + g[3])) + ((g[4] + g[5]) + (g[6] + g[7]));
+                    out[i] = (p.alpha != 0.f) ? sig * (tot + self[i]) + beta * h[i] : sig * (tot + self[i]);
+                }
+                if (cok && e_raw < E) V16<T>::store(p.S_out + (int64_t)my_r * p.ld_out + voff, out);
+                r += E - 1;
+                continue;
+            }
+        }
         const int rs_e = p.rp[r], re_e = p.rp[r + 1];
         const int eb = max(rs_e, e0), ee = min(re_e, e1);
         const bool head = (r == r0) && (rs_e < e0);

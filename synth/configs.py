@@ -78,3 +78,9 @@ def get_config(name: str) -> Config:
         return CONFIGS[name]
     except KeyError as e:
         raise KeyError(f"unknown config {name!r}; known: {sorted(CONFIGS)}") from e
+
+# Single-GPU proxy for one rank of the papers100M shape at P = 8 (same dims, 1/8 of the vertices and
+# arcs, directed): used to profile the W1-after-propagation MLP/loss path, which the full graph only
+# runs at P >= 4 (ncu cannot wrap a multi-rank command).
+_add(Config("papers_slice8", 15, 13_882_495, 24, 211_625_000, GRAPH500, False, 128, 128, 172, 2, 1.0, 0.0,
+            w_after_prop=True, note="profiling proxy; bf16 storage"))
