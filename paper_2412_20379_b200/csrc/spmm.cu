@@ -161,11 +161,15 @@ struct HopParams {
 // per lane) and distributed with shuffles.
 // GATHER: 0 = LSU loads (ld.global, policy POL), 1 = TMA tile::gather4 into a per-group
 // double-buffered shared-memory ring (no L1 data-pipe fill), read back with LDS.
-// SHORT: short-row variant (graphs with average degree < 32): 8-16-edge batches so a ~15-arc row
-// does not pay for a 64-slot batch, and fewer registers for 3 CTAs per SM.  The batch size does
-// not enter the reduction order (groups are (j - eb) mod 8 for any batch that is a multiple of 8).
-template <typename T, int E, int L, int POL, int GATHER, int SHORT = 0>
-__global__ void __launch_bounds__(kBlock, (SHORT && E == 8) ? 3 : 2) spmm_hop_kernel(const HopParams p, const __grid_constant__ CUtensorMap tmS) {
+// MODE (low-degree graphs, average degree < 32): bit 0 = short batches (E >= 4): 8-16-edge
+// batches so a ~15-arc row does not pay for a 64-slot batch, and fewer registers for 3 CTAs per
+// SM; bit 1 = tiny-row path (E >= 2, below).  Neither enters the reduction order (groups are
+// (j - eb) mod 8 for any batch that is a multiple of 8), and the tiny path's registers are only
+// paid where it is used.
+template <typename T, int E, int L, int POL, int GATHER, int MODE = 0>
+__global__ void __launch_bounds__(kBlock, ((MODE & 1) && E == 8) ? 3 : 2) spmm_hop_kernel(const HopParams p, const __grid_constant__ CUtensorMap tmS) {
+    constexpr bool SHORT = (MODE & 1) != 0;
+    constexpr bool TINY = (MODE & 2) != 0 && E >= 2;
     // GATHER == 1: mixed mode -- groups with (gidx % 8) < p.tma_per8 use the TMA engine, the others
     // the LSU path, so both units pull rows from L2 concurrently (same reduction order either way).
     constexpr int NACC = kG / E;
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(kBlock, (SHORT && E == 8) ? 3 : 2) spmm_hop_ke
         // one row per edge slot.  With <= 8 arcs every reduction group holds at most one arc, so
         // acc_g = 0 + v_g and the in-lane tree ((v0+v1)+(v2+v3))+((v4+v5)+(v6+v7)) is exactly the
         // canonical butterfly: results are bitwise those of the general path.
-        if (E >= 2 && npass == 1 && r + E <= r1 && r + E <= r_stop) {
+        if (TINY && npass == 1 && r + E <= r1 && r + E <= r_stop) {
             const int my_r = r + e;
             const int trs = __ldg(p.rp + my_r), tre = __ldg(p.rp + my_r + 1);
             const int deg = tre - trs;
@@ -497,11 +501,10 @@ bool carveout_max_l1() {
 
 template <typename T, int E, int L>
 void launch_hop(const HopParams& p, cudaStream_t s) {
-    static const int pol = [] { const char* v = getenv("NTP_GATHER_POLICY"); return v ? atoi(v) : 0; }();
     static const int tma_env = [] { const char* v = getenv("NTP_SPMM_TMA"); return v ? atoi(v) : -1; }();
     static const int short_env = [] { const char* v = getenv("NTP_SPMM_SHORT"); return v ? atoi(v) : -1; }();
-    // short-row variant when the average degree is below 32 (products, papers shapes)
-    const bool short_rows = E >= 4 && (short_env >= 0 ? short_env != 0 : (p.nnz < 32 * std::max<int64_t>(p.n, 1)));
+    // low-degree variants when the average degree is below 32 (products, papers shapes)
+    const bool low_deg = short_env >= 0 ? short_env != 0 : (p.nnz < 32 * std::max<int64_t>(p.n, 1));
     // groups per 8 on the TMA path: measured sweet spots; NTP_SPMM_TMA overrides
     const int tma = tma_env >= 0 ? tma_env : 0;
     const int64_t groups = p.u_end - p.u_begin;
@@ -531,19 +534,19 @@ void launch_hop(const HopParams& p, cudaStream_t s) {
             attr = true;
         }
         spmm_hop_kernel<T, E, L, 0, 1><<<(unsigned)blocks, kBlock, smem, s>>>(pp, tm);
-    } else if (pol == 1) spmm_hop_kernel<T, E, L, 1, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
-    else if (pol == 0 && carveout_max_l1()) {
+    } else {
         // no shared memory on the LSU path: give the whole unified array to L1
+        // low-degree mode: short batches where E >= 4, the tiny-row path where E >= 2
+        constexpr int LOW = (E >= 4) ? 3 : (E >= 2) ? 2 : 0;
         static bool attr0 = false;
-        if (!attr0) {
-            NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+        if (!attr0 && carveout_max_l1()) {
+            NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+            NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 0, LOW>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
             attr0 = true;
         }
-        if (short_rows) spmm_hop_kernel<T, E, L, 0, 0, 1><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
-        else spmm_hop_kernel<T, E, L, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
+        if (low_deg) spmm_hop_kernel<T, E, L, 0, 0, LOW><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
+        else spmm_hop_kernel<T, E, L, 0, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
     }
-    else if (pol == 2) spmm_hop_kernel<T, E, L, 2, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
-    else spmm_hop_kernel<T, E, L, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
     NTP_LAUNCH_CHECK();
 }
 
