@@ -31,6 +31,7 @@ constexpr int BM = 128;
 constexpr int BK = 32;                 // fp32 elements per 128-byte swizzle row
 constexpr int kGemmThreads = 320;
 constexpr int kTileA = BM * BK * 4;    // 16 KB
+constexpr int kEpiStage = 4 * 32 * 32 * 4;   // epilogue transpose buffers: 4 warps x 32 x 32 fp32
 
 struct GemmParams {
     int M, N, K;
@@ -44,6 +45,7 @@ struct GemmParams {
     const float* aux;
     int64_t ldaux;
     int epi;                            // 0 store, 1 relu, 2 keep where aux > 0
+    int vec;                            // C (and aux) rows 16-byte aligned: float4 epilogue
     uint32_t mn_lbo, mn_sbo;            // MN-major descriptor byte offsets (16-byte units)
 };
 
@@ -270,8 +272,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
     } else {
-        // ---------------- epilogue
+        // ---------------- epilogue: TMEM -> registers (thread = tile row) -> XOR-swizzled smem
+        // transpose -> coalesced rows (a warp stores 4 rows x 128 B per instruction; the aux
+        // mask is read the same way)
         const int q = warp & 3;                       // TMEM lane quarter of this warp
+        float* stg = reinterpret_cast<float*>(smem + S * stage_bytes + 1024) + (warp - 6) * 1024;
         int tc = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tc) {
             int m0, n0, kt0, nk, z;
@@ -279,7 +284,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int a = tc & 1;
             mbar_wait(&tfull[a], (tc >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int row = m0 + 32 * q + lane;
             float* Cb = p.C + (int64_t)z * p.split_stride;
             for (int c0 = 0; c0 < p.BN; c0 += 32) {
                 uint32_t r[32];
@@ -294,31 +298,45 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                       "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < p.M && n0 + c0 < p.N) {
-                    float* dst = Cb + (int64_t)row * p.ldc + n0 + c0;
-                    const int ncol = min(32, p.N - (n0 + c0));
-                    float v[32];
+                if (n0 + c0 >= p.N) continue;         // warp-uniform
+                // row `lane` of the 32 x 32 chunk: 16-byte piece j lands in slot j ^ (lane & 7)
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        v[j] = __uint_as_float(r[j]);
-                        if (p.epi == 1) v[j] = fmaxf(v[j], 0.f);
+                for (int j = 0; j < 8; ++j)
+                    *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+                        make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                __syncwarp();
+                const int cj = lane & 7;
+                const int col = n0 + c0 + 4 * cj;
+#pragma unroll
+                for (int it = 0; it < 8; ++it) {
+                    const int rr = it * 4 + (lane >> 3);
+                    const int row = m0 + 32 * q + rr;
+                    float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cj ^ (rr & 7)) << 2));
+                    if (row >= p.M || col >= p.N) continue;
+                    float e[4] = {v.x, v.y, v.z, v.w};
+                    if (p.epi == 1) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) e[i] = fmaxf(e[i], 0.f);
                     }
-                    if (p.epi == 2) {
-                        const float* ax = p.aux + (int64_t)row * p.ldaux + n0 + c0;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (j < ncol && !(ax[j] > 0.f)) v[j] = 0.f;
-                    }
-                    if (ncol == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    const float* ax = p.aux + (int64_t)row * p.ldaux + col;
+                    float* dst = Cb + (int64_t)row * p.ldc + col;
+                    if (p.vec && col + 3 < p.N) {
+                        if (p.epi == 2) {
+                            const float4 m = *reinterpret_cast<const float4*>(ax);
+                            if (!(m.x > 0.f)) e[0] = 0.f;
+                            if (!(m.y > 0.f)) e[1] = 0.f;
+                            if (!(m.z > 0.f)) e[2] = 0.f;
+                            if (!(m.w > 0.f)) e[3] = 0.f;
+                        }
+                        *reinterpret_cast<float4*>(dst) = make_float4(e[0], e[1], e[2], e[3]);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (j < ncol) dst[j] = v[j];
+                        for (int i = 0; i < 4; ++i)
+                            if (col + i < p.N) dst[i] = (p.epi == 2 && !(ax[i] > 0.f)) ? 0.f : e[i];
                     }
                 }
+                __syncwarp();
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(&tempty[a]);
@@ -411,7 +429,7 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     p.BN = (int)std::min<int64_t>(256, ((N + 15) / 16) * 16);
     p.bn_alloc = ((p.BN + 31) / 32) * 32;
     const int stage_bytes = 2 * kTileA + 2 * p.bn_alloc * BK * 4;
-    p.stages = std::max(2, std::min(4, (225 * 1024 - 1024 - 256) / stage_bytes));
+    p.stages = std::max(2, std::min(4, (225 * 1024 - 2048 - kEpiStage) / stage_bytes));
     p.tmem_cols = 32;
     while ((int)p.tmem_cols < 2 * p.BN) p.tmem_cols <<= 1;   // double-buffered accumulator
     p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
@@ -420,8 +438,9 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     const int m_tiles = (int)cdiv(M, BM);
     const int n_tiles = (int)cdiv(N, p.BN);
     int splits = 1;
-    if ((int64_t)m_tiles * n_tiles < 2 * 148) {
-        splits = (int)std::min<int64_t>(cdiv(2 * 148, (int64_t)m_tiles * n_tiles), std::max(1, p.k_tiles_total / 4));
+    if ((int64_t)m_tiles * n_tiles < 148) {
+        // split-K to (at most) one full wave: floor, so no CTA runs a second round of long tiles
+        splits = (int)std::min<int64_t>(148 / ((int64_t)m_tiles * n_tiles), std::max(1, p.k_tiles_total / 4));
         splits = std::max(splits, 1);
     }
     p.k_tiles_per_split = (int)cdiv(p.k_tiles_total, splits);
@@ -435,21 +454,24 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     const CUtensorMapSwizzle mnswz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
     CUtensorMap ta = a_mn ? make_map(A, M, K, lda, 32, 32, mnswz) : make_map(A, K, M, lda, 32, BM);
     CUtensorMap tb = b_mn ? make_map(B, N, K, ldb, 32, 32, mnswz) : make_map(B, K, N, ldb, 32, p.bn_alloc);
-    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (3 * p.stages + 6) * 8;
+    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 1024 + kEpiStage;   // align pad, barriers, staging
     const int64_t num_tiles = (int64_t)m_tiles * n_tiles * splits;
     dim3 grid((unsigned)std::min<int64_t>(num_tiles, 148));
+    const int64_t ldp = (N + 3) / 4 * 4;      // split-K partials row pitch
     if (splits == 1) {
         p.C = C;
         p.ldc = ldc;
         p.epi = epi;
         p.split_stride = 0;
+        p.vec = ((uintptr_t)C % 16) == 0 && ldc % 4 == 0 &&
+                (epi != 2 || (((uintptr_t)aux % 16) == 0 && ldaux % 4 == 0));
     } else {
-        const int64_t ldp = N;
         c->m_gemm_part.ensure((size_t)splits * M * ldp * sizeof(float) + 16);
         p.C = c->m_gemm_part.as<float>();
         p.ldc = ldp;
         p.epi = 0;
         p.split_stride = M * ldp;
+        p.vec = 1;
     }
     if (a_mn && b_mn) launch_gemm<true, true>(ta, tb, p, grid, smem, s);
     else if (a_mn) launch_gemm<true, false>(ta, tb, p, grid, smem, s);
@@ -459,7 +481,7 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     if (splits > 1) {
         const int64_t total = M * N;
         splitk_reduce_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 8), 256, 0, s>>>(
-            c->m_gemm_part.as<float>(), splits, M * N, (int)M, (int)N, N, C, ldc, epi, aux, ldaux);
+            c->m_gemm_part.as<float>(), splits, M * ldp, (int)M, (int)N, ldp, C, ldc, epi, aux, ldaux);
         NTP_LAUNCH_CHECK();
         count_launch(c);
     }

@@ -33,98 +33,86 @@ namespace {
 constexpr int kG = 8;           // edge lanes per group (fixed: part of the reduction order)
 constexpr int kBlock = 256;
 
-template <typename T> struct V16;
-__device__ __forceinline__ uint4 ld_raw(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+// Vector of VB bytes (16: LDG.128, 32: LDG.E.ENL2.256, sm_100) held as raw 32-bit words.
+template <int VB> struct Raw { uint32_t w[VB / 4]; };
 
-// Gather load with a cache policy: 0 = ld.global.nc (L1 allocate), 1 = ld.global.nc.L1::no_allocate,
-// 2 = ld.global.cg (L2 only).
-template <int POL>
-__device__ __forceinline__ uint4 ld_gather(const void* p) {
-    uint4 r;
-    if constexpr (POL == 0) {
-        r = __ldg(reinterpret_cast<const uint4*>(p));
-    } else if constexpr (POL == 1) {
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    } else {
-        asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    }
+template <int VB> __device__ __forceinline__ Raw<VB> ldv(const void* p);
+template <> __device__ __forceinline__ Raw<16> ldv<16>(const void* p) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+    return Raw<16>{{x.x, x.y, x.z, x.w}};
+}
+template <> __device__ __forceinline__ Raw<32> ldv<32>(const void* p) {
+    Raw<32> r;
+    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+                   "=r"(r.w[7])
+                 : "l"(p));
+    return r;
+}
+template <int VB> __device__ __forceinline__ void stv(void* p, const Raw<VB>& r);
+template <> __device__ __forceinline__ void stv<16>(void* p, const Raw<16>& r) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(r.w[0], r.w[1], r.w[2], r.w[3]);
+}
+template <> __device__ __forceinline__ void stv<32>(void* p, const Raw<32>& r) {
+    asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(r.w[0]), "r"(r.w[1]),
+                 "r"(r.w[2]), "r"(r.w[3]), "r"(r.w[4]), "r"(r.w[5]), "r"(r.w[6]), "r"(r.w[7])
+                 : "memory");
+}
+template <int VB> __device__ __forceinline__ Raw<VB> zero_raw() {
+    Raw<VB> r;
+#pragma unroll
+    for (int i = 0; i < VB / 4; ++i) r.w[i] = 0u;
     return r;
 }
 
-template <> struct V16<float> {
-    static constexpr int N = 4;
-    __device__ __forceinline__ static float elem(const uint4 x, int i) {
-        return __uint_as_float(i == 0 ? x.x : i == 1 ? x.y : i == 2 ? x.z : x.w);
-    }
-    __device__ __forceinline__ static void add_raw(float (&a)[4], const uint4 x) {
-        a[0] += __uint_as_float(x.x); a[1] += __uint_as_float(x.y);
-        a[2] += __uint_as_float(x.z); a[3] += __uint_as_float(x.w);
-    }
-    __device__ __forceinline__ static void load(const void* p, float (&v)[4]) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(p));
-        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    }
-    __device__ __forceinline__ static void add(const void* p, float (&a)[4]) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(p));
-        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
-    }
-    __device__ __forceinline__ static void store(void* p, const float (&v)[4]) {
-        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-    }
-    __device__ __forceinline__ static uint4 pack(const float (&v)[4]) {
-        return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+// Element view of a vector: fp32 (VB/4 values) or bf16 (VB/2 values, widened exactly to fp32).
+template <typename T, int VB> struct Vec;
+template <int VB> struct Vec<float, VB> {
+    static constexpr int N = VB / 4;
+    __device__ __forceinline__ static float elem(const Raw<VB>& x, int i) { return __uint_as_float(x.w[i]); }
+    __device__ __forceinline__ static Raw<VB> pack(const float (&v)[N]) {
+        Raw<VB> r;
+#pragma unroll
+        for (int i = 0; i < N; ++i) r.w[i] = __float_as_uint(v[i]);
+        return r;
     }
 };
-template <> struct V16<__nv_bfloat16> {
-    static constexpr int N = 8;
-    __device__ __forceinline__ static float elem(const uint4 x, int i) {
-        const uint32_t w = (i >> 1) == 0 ? x.x : (i >> 1) == 1 ? x.y : (i >> 1) == 2 ? x.z : x.w;
+template <int VB> struct Vec<__nv_bfloat16, VB> {
+    static constexpr int N = VB / 2;
+    __device__ __forceinline__ static float elem(const Raw<VB>& x, int i) {
+        const uint32_t w = x.w[i >> 1];
         return __uint_as_float((i & 1) ? (w & 0xFFFF0000u) : (w << 16));
     }
-    __device__ __forceinline__ static void unpack(const uint4 x, float (&v)[8]) {
-        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    __device__ __forceinline__ static Raw<VB> pack(const float (&v)[N]) {
+        Raw<VB> r;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            v[2 * i] = __uint_as_float(w[i] << 16);
-            v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-        }
-    }
-    __device__ __forceinline__ static void load(const void* p, float (&v)[8]) {
-        unpack(__ldg(reinterpret_cast<const uint4*>(p)), v);
-    }
-    __device__ __forceinline__ static void add_raw(float (&a)[8], const uint4 x) {
-        float v[8];
-        unpack(x, v);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] += v[i];
-    }
-    __device__ __forceinline__ static void add(const void* p, float (&a)[8]) {
-        float v[8];
-        unpack(__ldg(reinterpret_cast<const uint4*>(p)), v);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] += v[i];
-    }
-    __device__ __forceinline__ static uint4 pack(const float (&v)[8]) {
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < N / 2; ++i) {
             const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-            w[i] = *reinterpret_cast<const uint32_t*>(&h);
+            r.w[i] = *reinterpret_cast<const uint32_t*>(&h);
         }
-        return make_uint4(w[0], w[1], w[2], w[3]);
-    }
-    __device__ __forceinline__ static void store(void* p, const float (&v)[8]) {
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-            w[i] = *reinterpret_cast<const uint32_t*>(&h);
-        }
-        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+        return r;
     }
 };
+template <typename T, int VB>
+__device__ __forceinline__ void vadd(float (&a)[Vec<T, VB>::N], const Raw<VB>& x) {
+#pragma unroll
+    for (int i = 0; i < Vec<T, VB>::N; ++i) a[i] += Vec<T, VB>::elem(x, i);
+}
+
+// 16-byte element loads for the fix-up / prescale kernels
+template <typename T> __device__ __forceinline__ void load16(const void* p, float (&v)[16 / sizeof(T)]) {
+    const Raw<16> x = ldv<16>(p);
+#pragma unroll
+    for (int i = 0; i < (int)(16 / sizeof(T)); ++i) v[i] = Vec<T, 16>::elem(x, i);
+}
+template <typename T> __device__ __forceinline__ void store16(void* p, const float (&v)[16 / sizeof(T)]) {
+    stv<16>(p, Vec<T, 16>::pack(v));
+}
+
+
+// resident 256-thread CTAs per SM (register budget)
+template <int E, int VB, int MODE>
+__host__ __device__ constexpr int hop_ctas() { return ((MODE & 1) && E == 8 && VB == 16) ? 3 : 2; }
 
 struct HopParams {
     const int32_t* __restrict__ rp;
@@ -136,7 +124,7 @@ struct HopParams {
     const char* __restrict__ S_in;     // pre-scaled state, row stride ld_in bytes
     char* __restrict__ S_out;
     const char* __restrict__ S0;       // alpha term input S^0 = cs .* H (may be null if alpha == 0)
-    float* __restrict__ carry;         // [U][2][nvec*VALS] fp32
+    float* __restrict__ carry;         // [U][2][row_vals] fp32
     int64_t ld_in, ld_out, ld_s0;      // bytes
     int64_t n;
     int64_t u_begin, u_end;
@@ -144,82 +132,64 @@ struct HopParams {
     int32_t nvec;                      // 16-byte vectors per row
     float gamma, alpha;
     int mode;                          // 0 intermediate, 1 last
-    int tma_per8;                      // groups (out of every 8) that gather with TMA gather4
     int64_t nnz;
 };
 
 // Lane layout ("full row per edge"): a group of L lanes works on one unit.  Lane
-// gl = e*VP + c holds edge slot e in [0, E) and 16-byte column vector c in [0, VP):
+// gl = e*VP + c holds edge slot e in [0, E) and VB-byte column vector c in [0, VP):
 // one load instruction fetches the complete row slices of E edges with
-// consecutive lanes, so it touches the fewest distinct 128-byte lines (the L1TEX
-// wavefront count is what bounds a gather).  Edge j of a unit piece
-// starting at eb belongs to reduction group g = (j - eb) mod 8, g = e + E*k: lane
-// slot e keeps 8/E accumulators acc[k].  The 8 groups are combined by the fixed
-// butterfly ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) -- cross-lane for the bits of e,
-// in-lane for the bits of k -- so the per-column order is the same for every
-// (E, VP), i.e. for every slice width.  Column indices are loaded coalesced (one
+// consecutive lanes.  The per-instruction cost of a gather (not its bytes) is what
+// bounds the hop, so rows whose width is a multiple of 32 bytes use
+// 32-byte loads (VB = 32, LDG.E.ENL2.256): twice the edges per instruction.
+// Edge j of a unit piece starting at eb belongs to reduction group g = (j - eb) mod 8,
+// g = e + E*k: lane slot e keeps 8/E accumulators acc[k].  The 8 groups are combined by
+// the fixed butterfly ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) -- cross-lane for the bits
+// of e, in-lane for the bits of k -- so the per-column order is the same for every
+// (E, VP, VB), i.e. for every slice width.  Column indices are loaded coalesced (one
 // per lane) and distributed with shuffles.
-// GATHER: 0 = LSU loads (ld.global, policy POL), 1 = TMA tile::gather4 into a per-group
-// double-buffered shared-memory ring (no L1 data-pipe fill), read back with LDS.
 // MODE (low-degree graphs, average degree < 32): bit 0 = short batches (E >= 4): 8-16-edge
 // batches so a ~15-arc row does not pay for a 64-slot batch, and fewer registers for 3 CTAs per
 // SM; bit 1 = tiny-row path (E >= 2, below).  Neither enters the reduction order (groups are
 // (j - eb) mod 8 for any batch that is a multiple of 8), and the tiny path's registers are only
 // paid where it is used.
-template <typename T, int E, int L, int POL, int GATHER, int MODE = 0>
-__global__ void __launch_bounds__(kBlock, ((MODE & 1) && E == 8) ? 3 : 2) spmm_hop_kernel(const HopParams p, const __grid_constant__ CUtensorMap tmS) {
+template <typename T, int VB, int E, int L, int MODE>
+__global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kernel(const HopParams p) {
     constexpr bool SHORT = (MODE & 1) != 0;
     constexpr bool TINY = (MODE & 2) != 0 && E >= 2;
-    // GATHER == 1: mixed mode -- groups with (gidx % 8) < p.tma_per8 use the TMA engine, the others
-    // the LSU path, so both units pull rows from L2 concurrently (same reduction order either way).
     constexpr int NACC = kG / E;
     constexpr int LOG_E = (E == 1) ? 0 : (E == 2) ? 1 : (E == 4) ? 2 : 3;
-    constexpr int VALS = V16<T>::N;
-    // edges per pipeline batch: 16-byte loads per lane per batch = BATCH / E (4 or 8)
-    constexpr int BATCH = SHORT ? ((E >= 4) ? 16 : 8) : ((E == 8) ? 64 : (E == 4) ? 32 : 8 * E);
+    constexpr int VALS = Vec<T, VB>::N;
+    // edges per pipeline batch (a multiple of 8); loads per lane per batch LPB = BATCH / E:
+    // 8 x 16 B (2-4 x 16 B short), or 4 x 32 B (2 x 32 B short) -- the same bytes in flight
+    constexpr int BATCH = (VB == 16) ? (SHORT ? ((E >= 4) ? 16 : 8) : ((E == 8) ? 64 : (E == 4) ? 32 : 8 * E))
+                                     : (SHORT ? ((E >= 4) ? 2 * E : 8) : ((E >= 2) ? 4 * E : 8));
     constexpr int LPB = BATCH / E;                        // loads per lane per batch
     constexpr int ISL = (BATCH + L - 1) / L;              // column indices held per lane
+    static_assert(BATCH % 8 == 0, "batch must preserve the (j - eb) mod 8 grouping");
     const int lane = threadIdx.x & 31;
     const int gl = lane % L;
     const int gbase = lane - gl;
-    const int64_t group = ((int64_t)blockIdx.x * kBlock + threadIdx.x) / L;
-    const int64_t u = p.u_begin + group;
-    // TMA ring: per group 2 buffers of BATCH/4 gather4 slots, slot = 4 rows rounded to 128 B
-    extern __shared__ __align__(128) uint8_t tma_smem[];
-    constexpr int GPC = kBlock / L;                      // groups per CTA
-    const int row_bytes = p.nvec * 16;
-    const int slot_bytes = (4 * row_bytes + 127) & ~127;
-    const int buf_bytes = (BATCH / 4) * slot_bytes;
-    const int gidx = threadIdx.x / L;
-    uint8_t* gbuf = tma_smem + (size_t)gidx * 2 * buf_bytes;
-    uint64_t* gbar = reinterpret_cast<uint64_t*>(tma_smem + (size_t)GPC * 2 * buf_bytes) + 2 * gidx;
-    uint32_t ph0 = 0, ph1 = 0;
-    const bool tma_group = (GATHER == 1) && ((gidx & 7) < p.tma_per8);
-    const int fillv = tma_group ? (int)p.n : 0;
-    if constexpr (GATHER == 1) {
-        if (gl == 0) {
-            ptx::mbar_init(&gbar[0], 1);
-            ptx::mbar_init(&gbar[1], 1);
-            ptx::fence_mbar_init();
-        }
-        __syncthreads();
-    }
+    const int64_t u = p.u_begin + ((int64_t)blockIdx.x * kBlock + threadIdx.x) / L;
     if (u >= p.u_end) return;                           // group-uniform exit
     const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << gbase);
-    const int VP = (E == 1) ? min(p.nvec, 32) : p.nvec;  // vectors per pass
-    const int e_raw = gl / VP;
-    const int c = gl - e_raw * VP;
-    const bool active = e_raw < E;
-    const int e = active ? e_raw : E - 1;                // idle lanes mirror a real lane's addresses
+    const int nv = p.nvec / (VB / 16);                   // VB-byte vectors per row
+    const int VP = (E == 1) ? min(nv, 32) : nv;          // vectors per pass
+    // lane stride of an edge slot: VP rounded up to 8 lanes when that still fits, so no 8-lane
+    // phase of a load straddles two rows (idle lanes mirror the row's last vector: same line)
+    const int VPP = (E > 1 && E * ((VP + 7) & ~7) <= L) ? ((VP + 7) & ~7) : VP;
+    const int e_raw = gl / VPP;
+    const int c_raw = gl - e_raw * VPP;
+    const bool active = e_raw < E && c_raw < VP;
+    const int e = min(e_raw, E - 1);
+    const int c = min(c_raw, VP - 1);
     const int32_t* __restrict__ colp = p.col;
     const uint32_t ld_in = (uint32_t)p.ld_in;
-
     const int r0 = p.unit_row[u], r1 = p.unit_row[u + 1];
     const int e0 = p.unit_e[u], e1 = p.unit_e[u + 1];
     const bool has_tail = (r1 < p.n) && (e1 > max(p.rp[r1], e0));
     const int r_end = has_tail ? r1 + 1 : r1;
-    const int row_vals = p.nvec * VALS;
-    const int npass = (p.nvec + VP - 1) / VP;
+    const int row_vals = p.nvec * (16 / (int)sizeof(T));
+    const int npass = (nv + VP - 1) / VP;
 
     const int r_stop = (int)min((int64_t)r_end, p.row_hi);
     for (int r = max((int64_t)r0, p.row_lo); r < r_stop; ++r) {
@@ -227,43 +197,43 @@ __global__ void __launch_bounds__(kBlock, ((MODE & 1) && E == 8) ? 3 : 2) spmm_h
         // one row per edge slot.  With <= 8 arcs every reduction group holds at most one arc, so
         // acc_g = 0 + v_g and the in-lane tree ((v0+v1)+(v2+v3))+((v4+v5)+(v6+v7)) is exactly the
         // canonical butterfly: results are bitwise those of the general path.
-        if (TINY && npass == 1 && r + E <= r1 && r + E <= r_stop) {
-            const int my_r = r + e;
-            const int trs = __ldg(p.rp + my_r), tre = __ldg(p.rp + my_r + 1);
-            const int deg = tre - trs;
-            const bool ok = deg <= 8 && !(my_r == r0 && trs < e0);
-            if (__all_sync(gmask, ok)) {
-                const bool cok = active && c < p.nvec;
-                const int64_t voff = (int64_t)min(c, p.nvec - 1) * 16;
-                const uint4 self_raw = ld_raw(p.S_in + (int64_t)my_r * p.ld_in + voff);
-                const uint4 s0_raw = (p.alpha != 0.f) ? ld_raw(p.S0 + (int64_t)my_r * p.ld_s0 + voff)
-                                                      : make_uint4(0u, 0u, 0u, 0u);
-                const float ra = __ldg(p.rs + my_r), rb = __ldg(p.cs + my_r);
-                int src[8];
+        if constexpr (TINY) {
+            if (npass == 1 && r + E <= r1 && r + E <= r_stop) {
+                const int my_r = r + e;
+                const int trs = __ldg(p.rp + my_r), tre = __ldg(p.rp + my_r + 1);
+                const int deg = tre - trs;
+                const bool ok = deg <= 8 && !(my_r == r0 && trs < e0);
+                if (__all_sync(gmask, ok)) {
+                    const bool cok = active && c < nv;
+                    const int64_t voff = (int64_t)min(c, nv - 1) * VB;
+                    const Raw<VB> self_raw = ldv<VB>(p.S_in + (int64_t)my_r * p.ld_in + voff);
+                    const Raw<VB> s0_raw =
+                        (p.alpha != 0.f) ? ldv<VB>(p.S0 + (int64_t)my_r * p.ld_s0 + voff) : zero_raw<VB>();
+                    const float ra = __ldg(p.rs + my_r), rb = __ldg(p.cs + my_r);
+                    int src[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) src[k] = (k < deg) ? __ldg(colp + trs + k) : 0;
-                uint4 x8[8];
+                    for (int k = 0; k < 8; ++k) src[k] = (k < deg) ? __ldg(colp + trs + k) : 0;
+                    Raw<VB> x8[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    x8[k] = (k < deg) ? ld_raw(p.S_in + (int64_t)src[k] * p.ld_in + voff) : make_uint4(0u, 0u, 0u, 0u);
-                float self[VALS], h[VALS], out[VALS];
+                    for (int k = 0; k < 8; ++k)
+                        x8[k] = (k < deg) ? ldv<VB>(p.S_in + (int64_t)src[k] * p.ld_in + voff) : zero_raw<VB>();
+                    const float sig = (p.mode == 0) ? p.gamma * ra * rb : p.gamma * ra;
+                    const float beta = (p.mode == 0) ? p.alpha : p.alpha / rb;
+                    float out[VALS];
 #pragma unroll
-                for (int i = 0; i < VALS; ++i) self[i] = h[i] = 0.f;
-                V16<T>::add_raw(self, self_raw);
-                V16<T>::add_raw(h, s0_raw);
-                const float sig = (p.mode == 0) ? p.gamma * ra * rb : p.gamma * ra;
-                const float beta = (p.mode == 0) ? p.alpha : p.alpha / rb;
+                    for (int i = 0; i < VALS; ++i) {
+                        float g[8];
 #pragma unroll
-                for (int i = 0; i < VALS; ++i) {
-                    float g[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) g[k] = 0.f + V16<T>::elem(x8[k], i);   // acc_g = 0 + v_g
-                    const float tot = ((g[0] + g[1]) + (g[2] + g[3])) + ((g[4] + g[5]) + (g[6] + g[7]));
-                    out[i] = (p.alpha != 0.f) ? sig * (tot + self[i]) + beta * h[i] : sig * (tot + self[i]);
+                        for (int k = 0; k < 8; ++k) g[k] = 0.f + Vec<T, VB>::elem(x8[k], i);   // acc_g = 0 + v_g
+                        const float tot = ((g[0] + g[1]) + (g[2] + g[3])) + ((g[4] + g[5]) + (g[6] + g[7]));
+                        const float self = 0.f + Vec<T, VB>::elem(self_raw, i);
+                        out[i] = (p.alpha != 0.f) ? sig * (tot + self) + beta * (0.f + Vec<T, VB>::elem(s0_raw, i))
+                                                  : sig * (tot + self);
+                    }
+                    if (cok) stv<VB>(p.S_out + (int64_t)my_r * p.ld_out + voff, Vec<T, VB>::pack(out));
+                    r += E - 1;
+                    continue;
                 }
-                if (cok && e_raw < E) V16<T>::store(p.S_out + (int64_t)my_r * p.ld_out + voff, out);
-                r += E - 1;
-                continue;
             }
         }
         const int rs_e = p.rp[r], re_e = p.rp[r + 1];
@@ -272,15 +242,14 @@ __global__ void __launch_bounds__(kBlock, ((MODE & 1) && E == 8) ? 3 : 2) spmm_h
         const bool tail = (r == r1);
         for (int pass = 0; pass < npass; ++pass) {
             const int vcol = pass * VP + c;
-            const bool col_ok = active && vcol < p.nvec;
-            const char* __restrict__ vbase = p.S_in + (int64_t)min(vcol, p.nvec - 1) * 16;
+            const bool col_ok = active && vcol < nv;
+            const char* __restrict__ vbase = p.S_in + (int64_t)min(vcol, nv - 1) * VB;
             // epilogue operands issued now so their latency hides behind the gather (short rows)
             const bool fin = !(head || tail) && e_raw == 0 && col_ok;
-            uint4 self_raw = make_uint4(0u, 0u, 0u, 0u), s0_raw = make_uint4(0u, 0u, 0u, 0u);
+            Raw<VB> self_raw = zero_raw<VB>();
             float ra = 0.f, rb = 0.f;
             if (fin) {
-                self_raw = ld_raw(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * 16);
-                if (p.alpha != 0.f) s0_raw = ld_raw(p.S0 + (int64_t)r * p.ld_s0 + (int64_t)vcol * 16);
+                self_raw = ldv<VB>(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * VB);
                 ra = __ldg(p.rs + r);
                 rb = __ldg(p.cs + r);
             }
@@ -294,35 +263,34 @@ __global__ void __launch_bounds__(kBlock, ((MODE & 1) && E == 8) ? 3 : 2) spmm_h
 #pragma unroll
                 for (int sl = 0; sl < ISL; ++sl) {
                     const int j = base + sl * L + gl;
-                    dst[sl] = (sl * L + gl < BATCH && j < ee) ? __ldg(colp + j) : fillv;
+                    dst[sl] = (sl * L + gl < BATCH && j < ee) ? __ldg(colp + j) : 0;
                 }
             };
-            // 16-byte loads of a batch; slots past the end read row 0 (never accumulated)
-            auto load_data = [&](const int (&ix)[ISL], uint4 (&dst)[LPB]) {
+            // row loads of a batch; slots past the end read row 0 (never accumulated)
+            auto load_data = [&](const int (&ix)[ISL], Raw<VB> (&dst)[LPB]) {
 #pragma unroll
                 for (int t = 0; t < LPB; ++t) {
                     // edge t*E + e of the batch: held by lane (t*E % L) + e in slot (t*E)/L (E divides L)
                     const int src = __shfl_sync(gmask, ix[(t * E) / L], gbase + ((t * E) % L) + e);
-                    dst[t] = ld_gather<POL>(vbase + (size_t)(uint32_t)src * ld_in);
+                    dst[t] = ldv<VB>(vbase + (size_t)(uint32_t)src * ld_in);
                 }
             };
             // edge base + t*E + e belongs to group (t*E + e) mod 8, i.e. acc[t % NACC]
-            auto consume = [&](const uint4 (&v)[LPB], int base) {
+            auto consume = [&](const Raw<VB> (&v)[LPB], int base) {
                 const int rem = ee - base;
                 if (rem >= BATCH) {
 #pragma unroll
-                    for (int t = 0; t < LPB; ++t) V16<T>::add_raw(acc[t % NACC], v[t]);
+                    for (int t = 0; t < LPB; ++t) vadd<T, VB>(acc[t % NACC], v[t]);
                 } else {
 #pragma unroll
                     for (int t = 0; t < LPB; ++t)
-                        if (t * E + e < rem) V16<T>::add_raw(acc[t % NACC], v[t]);
+                        if (t * E + e < rem) vadd<T, VB>(acc[t % NACC], v[t]);
                 }
             };
-            if (!tma_group) {
             // two-deep software pipeline, unrolled by 2 so the buffers ping-pong without copies:
             // while batch b is accumulated, batch b+1's rows and batch b+2's indices are in flight
             int ia[ISL], ib[ISL];
-            uint4 va[LPB], vb[LPB];
+            Raw<VB> va[LPB], vb[LPB];
             load_idx(eb, ia);
             if (eb < ee) load_data(ia, va);
             load_idx(eb + BATCH, ib);
@@ -337,59 +305,11 @@ __global__ void __launch_bounds__(kBlock, ((MODE & 1) && E == 8) ? 3 : 2) spmm_h
                 consume(vb, base);
                 base += BATCH;
             }
-            } else {
-            // TMA gather4 ring: batch b+1 in flight (buffer b+1 & 1) while batch b is read from smem
-            auto issue = [&](int buf, const int (&ix)[ISL]) {
-                if (gl == 0) ptx::mbar_expect_tx(&gbar[buf], BATCH * row_bytes);
-                __syncwarp(gmask);
-#pragma unroll
-                for (int sl = 0; sl < ISL; ++sl) {
-                    const int q1 = __shfl_sync(gmask, ix[sl], gbase + ((gl + 1) & (L - 1)));
-                    const int q2 = __shfl_sync(gmask, ix[sl], gbase + ((gl + 2) & (L - 1)));
-                    const int q3 = __shfl_sync(gmask, ix[sl], gbase + ((gl + 3) & (L - 1)));
-                    const int jb = sl * L + gl;                       // first edge of this lane's gather
-                    if ((gl & 3) == 0 && jb < BATCH)
-                        ptx::tma_gather4(gbuf + buf * buf_bytes + (jb >> 2) * slot_bytes, &tmS, &gbar[buf], 0,
-                                         ix[sl], q1, q2, q3);
-                }
-            };
-            auto consume_smem = [&](int buf) {
-                const uint8_t* b = gbuf + buf * buf_bytes + vcol * 16;
-#pragma unroll
-                for (int t = 0; t < LPB; ++t) {
-                    const int jrel = t * E + e;
-                    const uint4 x = *reinterpret_cast<const uint4*>(b + (jrel >> 2) * slot_bytes + (jrel & 3) * row_bytes);
-                    V16<T>::add_raw(acc[t % NACC], x);                 // rows past the end are zero
-                }
-            };
-            int ia[ISL], ib[ISL];
-            load_idx(eb, ia);
-            if (eb < ee) issue(0, ia);
-            load_idx(eb + BATCH, ib);
-            if (eb + BATCH < ee) issue(1, ib);
-            for (int base = eb; base < ee;) {
-                load_idx(base + 2 * BATCH, ia);
-                ptx::mbar_wait(&gbar[0], ph0);
-                ph0 ^= 1;
-                consume_smem(0);
-                __syncwarp(gmask);
-                if (base + 2 * BATCH < ee) issue(0, ia);
-                base += BATCH;
-                if (base >= ee) break;
-                load_idx(base + 2 * BATCH, ib);
-                ptx::mbar_wait(&gbar[1], ph1);
-                ph1 ^= 1;
-                consume_smem(1);
-                __syncwarp(gmask);
-                if (base + 2 * BATCH < ee) issue(1, ib);
-                base += BATCH;
-            }
-            }
             // fixed butterfly over the 8 reduction groups
 #pragma unroll
             for (int b = 0; b < 3; ++b) {
                 if (b < LOG_E) {
-                    const int partner = gbase + ((e ^ (1 << b)) * VP + c);
+                    const int partner = gbase + ((e ^ (1 << b)) * VPP + c);
 #pragma unroll
                     for (int k = 0; k < NACC; ++k)
 #pragma unroll
@@ -411,28 +331,20 @@ __global__ void __launch_bounds__(kBlock, ((MODE & 1) && E == 8) ? 3 : 2) spmm_h
                 for (int i = 0; i < VALS; ++i) dst[i] = acc[0][i];
                 continue;
             }
-            const int64_t voff = (int64_t)vcol * 16;
-            float self[VALS];
-#pragma unroll
-            for (int i = 0; i < VALS; ++i) self[i] = 0.f;
-            V16<T>::add_raw(self, self_raw);
-            const float a = ra;
-            const float b = rb;
-            const float sig = (p.mode == 0) ? p.gamma * a * b : p.gamma * a;
+            const float sig = (p.mode == 0) ? p.gamma * ra * rb : p.gamma * ra;
             float out[VALS];
             if (p.alpha != 0.f) {
-                float h[VALS];
+                const Raw<VB> s0_raw = ldv<VB>(p.S0 + (int64_t)r * p.ld_s0 + (int64_t)vcol * VB);
+                const float beta = (p.mode == 0) ? p.alpha : p.alpha / rb;
 #pragma unroll
-                for (int i = 0; i < VALS; ++i) h[i] = 0.f;
-                V16<T>::add_raw(h, s0_raw);
-                const float beta = (p.mode == 0) ? p.alpha : p.alpha / b;
-#pragma unroll
-                for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + self[i]) + beta * h[i];
+                for (int i = 0; i < VALS; ++i)
+                    out[i] = sig * (acc[0][i] + (0.f + Vec<T, VB>::elem(self_raw, i))) +
+                             beta * (0.f + Vec<T, VB>::elem(s0_raw, i));
             } else {
 #pragma unroll
-                for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + self[i]);
+                for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + (0.f + Vec<T, VB>::elem(self_raw, i)));
             }
-            V16<T>::store(p.S_out + (int64_t)r * p.ld_out + voff, out);
+            stv<VB>(p.S_out + (int64_t)r * p.ld_out + (int64_t)vcol * VB, Vec<T, VB>::pack(out));
         }
     }
 }
@@ -449,7 +361,7 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
     if (r >= p.n || r < p.row_lo || r >= p.row_hi) return;
     const int rs_e = p.rp[r];
     if (!(rs_e >= e0 && rs_e < e1)) return;            // row r does not start (with edges) in unit u
-    constexpr int VALS = V16<T>::N;
+    constexpr int VALS = 16 / sizeof(T);
     const int row_vals = p.nvec * VALS;
     const float a = p.rs[r];
     const float b = p.cs[r];
@@ -461,12 +373,12 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
         }
         const int vcol = k / VALS, comp = k % VALS;
         float self[VALS];
-        V16<T>::load(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * 16, self);
+        load16<T>(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * 16, self);
         const float sig = (p.mode == 0) ? p.gamma * a * b : p.gamma * a;
         float out = sig * (acc + self[comp]);
         if (p.alpha != 0.f) {
             float h[VALS];
-            V16<T>::load(p.S0 + (int64_t)r * p.ld_s0 + (int64_t)vcol * 16, h);
+            load16<T>(p.S0 + (int64_t)r * p.ld_s0 + (int64_t)vcol * 16, h);
             out += ((p.mode == 0) ? p.alpha : p.alpha / b) * h[comp];
         }
         if (sizeof(T) == 4) {
@@ -480,17 +392,17 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
 template <typename T>
 __global__ void prescale_kernel(const char* __restrict__ H, int64_t ld_h, char* __restrict__ S, int64_t ld_s,
                                 int32_t nvec, const float* __restrict__ scale, int64_t rows) {
-    constexpr int VALS = V16<T>::N;
+    constexpr int VALS = 16 / sizeof(T);
     const int64_t total = rows * nvec;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = i / nvec;
         const int64_t vc = i % nvec;
         float v[VALS];
-        V16<T>::load(H + r * ld_h + vc * 16, v);
+        load16<T>(H + r * ld_h + vc * 16, v);
         const float s = scale[r];
 #pragma unroll
         for (int k = 0; k < VALS; ++k) v[k] *= s;
-        V16<T>::store(S + r * ld_s + vc * 16, v);
+        store16<T>(S + r * ld_s + vc * 16, v);
     }
 }
 
@@ -499,66 +411,39 @@ bool carveout_max_l1() {
     return v;
 }
 
-template <typename T, int E, int L>
-void launch_hop(const HopParams& p, cudaStream_t s) {
-    static const int tma_env = [] { const char* v = getenv("NTP_SPMM_TMA"); return v ? atoi(v) : -1; }();
-    static const int short_env = [] { const char* v = getenv("NTP_SPMM_SHORT"); return v ? atoi(v) : -1; }();
-    // low-degree variants when the average degree is below 32 (products, papers shapes)
-    const bool low_deg = short_env >= 0 ? short_env != 0 : (p.nnz < 32 * std::max<int64_t>(p.n, 1));
-    // groups per 8 on the TMA path: measured sweet spots; NTP_SPMM_TMA overrides
-    const int tma = tma_env >= 0 ? tma_env : 0;
-    const int64_t groups = p.u_end - p.u_begin;
-    const int64_t blocks = cdiv(groups * L, kBlock);
-    CUtensorMap tm{};
-    HopParams pp = p;
-    pp.tma_per8 = std::min(tma, 8);
-    const bool use_tma = tma > 0 && p.nvec <= 32 && (int64_t)p.nvec * 16 / (int64_t)sizeof(T) <= 256 && p.n > 0;
-    if (use_tma) {
-        constexpr int BATCH = (E == 8) ? 64 : (E == 4) ? 32 : 8 * E;
-        const int row_bytes = p.nvec * 16;
-        const int slot_bytes = (4 * row_bytes + 127) & ~127;
-        const size_t smem = (size_t)(kBlock / L) * (2 * (BATCH / 4) * slot_bytes + 16) + 128;
-        const cuuint64_t dims[2] = {(cuuint64_t)(row_bytes / sizeof(T)), (cuuint64_t)p.n};
-        const cuuint64_t strides[1] = {(cuuint64_t)p.ld_in};
-        const cuuint32_t box[2] = {(cuuint32_t)(row_bytes / sizeof(T)), 1};
-        const cuuint32_t es[2] = {1, 1};
-        CUresult r = tensor_map_encoder()(&tm, sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                          2, const_cast<char*>(p.S_in), dims, strides, box, es,
-                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        NTP_CHECK(r == CUDA_SUCCESS, NTP_ERR_CUDA, "tensor map for the TMA gather failed (%d)", (int)r);
-        static bool attr = false;
-        if (!attr) {
-            NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          200 * 1024));
-            attr = true;
-        }
-        spmm_hop_kernel<T, E, L, 0, 1><<<(unsigned)blocks, kBlock, smem, s>>>(pp, tm);
-    } else {
-        // no shared memory on the LSU path: give the whole unified array to L1
-        // low-degree mode: short batches where E >= 4, the tiny-row path where E >= 2
-        constexpr int LOW = (E >= 4) ? 3 : (E >= 2) ? 2 : 0;
-        static bool attr0 = false;
-        if (!attr0 && carveout_max_l1()) {
-            NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 0, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-            NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, E, L, 0, 0, LOW>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-            attr0 = true;
-        }
-        if (low_deg) spmm_hop_kernel<T, E, L, 0, 0, LOW><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
-        else spmm_hop_kernel<T, E, L, 0, 0, 0><<<(unsigned)blocks, kBlock, 0, s>>>(p, tm);
+// 256-thread CTAs, one unit per lane group, the whole unified array as L1 (no shared memory).
+template <typename T, int VB, int E, int L, int MODE>
+void launch_variant(const HopParams& p, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr && carveout_max_l1()) {
+        NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, VB, E, L, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+        attr = true;
     }
+    spmm_hop_kernel<T, VB, E, L, MODE><<<(unsigned)cdiv((p.u_end - p.u_begin) * L, kBlock), kBlock, 0, s>>>(p);
     NTP_LAUNCH_CHECK();
 }
 
-// (E, L) from the row width: E edge slots of nvec lanes each, E*nvec <= L.
-template <typename T>
-void dispatch_hop(const HopParams& p, int nvec, cudaStream_t s) {
-    if (nvec == 1) launch_hop<T, 8, 8>(p, s);
-    else if (nvec == 2) launch_hop<T, 8, 16>(p, s);
-    else if (nvec <= 4) launch_hop<T, 8, 32>(p, s);
-    else if (nvec <= 8) launch_hop<T, 4, 32>(p, s);
-    else if (nvec <= 16) launch_hop<T, 2, 32>(p, s);
-    else launch_hop<T, 1, 32>(p, s);
+template <typename T, int VB, int E, int L>
+void launch_hop(const HopParams& p, cudaStream_t s) {
+    static const int short_env = [] { const char* v = getenv("NTP_SPMM_SHORT"); return v ? atoi(v) : -1; }();
+    // low-degree variants when the average degree is below 32 (products, papers shapes)
+    const bool low_deg = short_env >= 0 ? short_env != 0 : (p.nnz < 32 * std::max<int64_t>(p.n, 1));
+    constexpr int LOW = (E >= 4) ? 3 : (E >= 2) ? 2 : 0;   // short batches where E >= 4, tiny rows where E >= 2
+    if (low_deg) launch_variant<T, VB, E, L, LOW>(p, s);
+    else launch_variant<T, VB, E, L, 0>(p, s);
+}
+
+// (E, L) from the row width in VB-byte vectors: E edge slots of nv lanes each, E*nv <= L.
+template <typename T, int VB>
+void dispatch_hop(const HopParams& p, int nv, cudaStream_t s) {
+    if (nv == 1) launch_hop<T, VB, 8, 8>(p, s);
+    else if (nv == 2) launch_hop<T, VB, 8, 16>(p, s);
+    else if (nv <= 4) launch_hop<T, VB, 8, 32>(p, s);
+    else if (nv <= 8) launch_hop<T, VB, 4, 32>(p, s);
+    else if constexpr (VB == 16) {
+        if (nv <= 16) launch_hop<T, VB, 2, 32>(p, s);
+        else launch_hop<T, VB, 1, 32>(p, s);
+    }
 }
 
 }  // namespace
@@ -610,8 +495,19 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     c->carry.ensure((size_t)(csr.U * 2) * nvec * vals * sizeof(float) + 16);
     p.carry = c->carry.as<float>();
     if (p.u_end <= p.u_begin) return;
-    if (dt == NTP_F32) dispatch_hop<float>(p, nvec, s);
-    else dispatch_hop<__nv_bfloat16>(p, nvec, s);
+    // 32-byte vectors when every row the hop touches is 32-byte aligned and at most 8 of them wide
+    // (E >= 4 edge slots: wider rows would need more accumulator registers than the kernel has)
+    static const int vb_env = [] { const char* v = getenv("NTP_SPMM_VB"); return v ? atoi(v) : 16; }();
+    const bool al32 = (nvec % 2) == 0 && nvec <= 16 && p.ld_in % 32 == 0 && p.ld_out % 32 == 0 &&
+                      ((uintptr_t)S_in % 32) == 0 && ((uintptr_t)S_out % 32) == 0 &&
+                      (S0 == nullptr || (p.ld_s0 % 32 == 0 && ((uintptr_t)S0 % 32) == 0));
+    if (vb_env == 32 && al32) {
+        if (dt == NTP_F32) dispatch_hop<float, 32>(p, nvec / 2, s);
+        else dispatch_hop<__nv_bfloat16, 32>(p, nvec / 2, s);
+    } else {
+        if (dt == NTP_F32) dispatch_hop<float, 16>(p, nvec, s);
+        else dispatch_hop<__nv_bfloat16, 16>(p, nvec, s);
+    }
     const int64_t fblocks = cdiv((p.u_end - p.u_begin) * 32, kBlock);
     if (dt == NTP_F32) spmm_fixup_kernel<float><<<(unsigned)fblocks, kBlock, 0, s>>>(p);
     else spmm_fixup_kernel<__nv_bfloat16><<<(unsigned)fblocks, kBlock, 0, s>>>(p);
