@@ -46,6 +46,8 @@ struct GemmParams {
     int64_t ldaux;
     int epi;                            // 0 store, 1 relu, 2 keep where aux > 0
     int vec;                            // C (and aux) rows 16-byte aligned: float4 epilogue
+    int exp;                            // development timing knob (NTP_GEMM_EXP), 0 in production
+    int b_presplit;                     // B arrives as (hi, lo) pair: tmB = hi, tmBlo = lo (weights)
     uint32_t mn_lbo, mn_sbo;            // MN-major descriptor byte offsets (16-byte units)
 };
 
@@ -115,13 +117,17 @@ __device__ __forceinline__ float tf32_rn(float x) {
     return __uint_as_float(r);
 }
 
-// split a tile in place: t <- rn_tf32(t), lo <- t - rn_tf32(t)   (16 bytes per step)
-__device__ __forceinline__ void split_tile(uint8_t* t, uint8_t* lo, int bytes, int tid, int nthreads) {
+// Split of a staged fp32 tile.  The tensor core reads a kind::tf32 operand's 32-bit container and
+// ignores the low 13 mantissa bits, so the raw tile IS the hi part, hi = trunc_tf32(x), and only
+// lo = rn_tf32(x - trunc_tf32(x)) is written (x - trunc is exact in fp32): one smem write stream
+// instead of two.  |x - hi| < 2^-10 |x|, so the dropped lo*lo term and the rounding of lo are
+// ~2^-20 relative (reading R11).
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ void split_tile(const uint8_t* t, uint8_t* lo, int bytes, int tid, int nthreads) {
     for (int off = tid * 16; off < bytes; off += nthreads * 16) {
-        float4 x = *reinterpret_cast<float4*>(t + off);
-        float4 h = make_float4(tf32_rn(x.x), tf32_rn(x.y), tf32_rn(x.z), tf32_rn(x.w));
-        float4 l = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
-        *reinterpret_cast<float4*>(t + off) = h;
+        const float4 x = *reinterpret_cast<const float4*>(t + off);
+        const float4 l = make_float4(tf32_rn(x.x - tf32_trunc(x.x)), tf32_rn(x.y - tf32_trunc(x.y)),
+                                     tf32_rn(x.z - tf32_trunc(x.z)), tf32_rn(x.w - tf32_trunc(x.w)));
         *reinterpret_cast<float4*>(lo + off) = l;
     }
 }
@@ -135,7 +141,7 @@ __device__ __forceinline__ void split_tile(uint8_t* t, uint8_t* lo, int bytes, i
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                       const GemmParams p) {
+                       const __grid_constant__ CUtensorMap tmBlo, const GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = p.stages;
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     uint8_t* sa = smem + s * stage_bytes;
                     uint8_t* sb = sa + 2 * kTileA;
                     const int k0 = (kt0 + i) * BK;
-                    mbar_expect_tx(&full[s], kTileA + tileB);
+                    mbar_expect_tx(&full[s], kTileA + (p.b_presplit ? 2 : 1) * tileB);
                     if (A_MN) {
                         for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 4096, &tmA, &full[s], m0 + 32 * j, k0);
                     } else {
@@ -211,8 +217,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     if (B_MN) {
                         for (int j = 0; j < p.bn_alloc / 32; ++j)
                             tma_load_2d(sb + j * 4096, &tmB, &full[s], n0 + 32 * j, k0);
+                        if (p.b_presplit)
+                            for (int j = 0; j < p.bn_alloc / 32; ++j)
+                                tma_load_2d(sb + tileB + j * 4096, &tmBlo, &full[s], n0 + 32 * j, k0);
                     } else {
                         tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                        if (p.b_presplit) tma_load_2d(sb + tileB, &tmBlo, &full[s], k0, n0);
                     }
                 }
             }
@@ -245,8 +255,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         const uint64_t dB = B_MN ? desc_mnmajor(sb + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(sb + bo);
                         const uint64_t dBlo = B_MN ? desc_mnmajor(sblo + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(sblo + bo);
                         mma_tf32(acc, dA, dB, p.idesc, (i > 0 || k > 0) ? 1u : 0u);
-                        mma_tf32(acc, dA, dBlo, p.idesc, 1u);
-                        mma_tf32(acc, dAlo, dB, p.idesc, 1u);
+                        if (p.exp != 2) {   // dev timing knob: exp 2 = one MMA per step (wrong results)
+                            mma_tf32(acc, dA, dBlo, p.idesc, 1u);
+                            mma_tf32(acc, dAlo, dB, p.idesc, 1u);
+                        }
                     }
                     mma_commit(&empty[s]);
                 }
@@ -264,9 +276,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int s = it % S;
                 mbar_wait(&full[s], (it / S) & 1);
                 uint8_t* sa = smem + s * stage_bytes;
-                split_tile(sa, sa + kTileA, kTileA, tid, 128);
-                uint8_t* sb = sa + 2 * kTileA;
-                split_tile(sb, sb + tileB, tileB, tid, 128);
+                if (p.exp != 1) {   // dev timing knob: exp 1 = no split (wrong results)
+                    split_tile(sa, sa + kTileA, kTileA, tid, 128);
+                    uint8_t* sb = sa + 2 * kTileA;
+                    if (!p.b_presplit) split_tile(sb, sb + tileB, tileB, tid, 128);
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&split[s]);
             }
@@ -401,15 +415,15 @@ CUtensorMap make_map(const float* base, int64_t cols, int64_t rows, int64_t ld, 
 }
 
 template <bool A_MN, bool B_MN>
-void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, dim3 grid, size_t smem,
-                 cudaStream_t s) {
+void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tblo, const GemmParams& p, dim3 grid,
+                 size_t smem, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
         NTP_CUDA(cudaFuncSetAttribute(gemm_tf32x3_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       227 * 1024));
         configured = true;
     }
-    gemm_tf32x3_kernel<A_MN, B_MN><<<grid, kGemmThreads, smem, s>>>(ta, tb, p);
+    gemm_tf32x3_kernel<A_MN, B_MN><<<grid, kGemmThreads, smem, s>>>(ta, tb, tblo, p);
     NTP_LAUNCH_CHECK();
 }
 
@@ -419,7 +433,7 @@ void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams&
 // B: b_mn ? stored [K][N] : stored [N][K].  epi: 0 store, 1 ReLU, 2 keep where aux > 0.
 void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool a_mn, const float* B,
                  int64_t ldb, bool b_mn, float* C, int64_t ldc, int epi, const float* aux, int64_t ldaux,
-                 cudaStream_t s) {
+                 cudaStream_t s, const float* B_lo) {
     if (M <= 0 || N <= 0) return;
     NTP_CHECK(K > 0, NTP_ERR_ARG, "GEMM with K == 0");
     GemmParams p{};
@@ -447,6 +461,8 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     splits = (int)cdiv(p.k_tiles_total, p.k_tiles_per_split);
     p.aux = aux;
     p.ldaux = ldaux;
+    static const int gemm_exp = [] { const char* v = getenv("NTP_GEMM_EXP"); return v ? atoi(v) : 0; }();
+    p.exp = gemm_exp;
     p.mn_lbo = 4096 >> 4;
     p.mn_sbo = 512 >> 4;
     if (const char* v = getenv("NTP_MN_LBO")) p.mn_lbo = (uint32_t)atoi(v) >> 4;
@@ -454,6 +470,9 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     const CUtensorMapSwizzle mnswz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
     CUtensorMap ta = a_mn ? make_map(A, M, K, lda, 32, 32, mnswz) : make_map(A, K, M, lda, 32, BM);
     CUtensorMap tb = b_mn ? make_map(B, N, K, ldb, 32, 32, mnswz) : make_map(B, K, N, ldb, 32, p.bn_alloc);
+    CUtensorMap tblo = tb;
+    p.b_presplit = B_lo != nullptr;
+    if (B_lo) tblo = b_mn ? make_map(B_lo, N, K, ldb, 32, 32, mnswz) : make_map(B_lo, K, N, ldb, 32, p.bn_alloc);
     const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 1024 + kEpiStage;   // align pad, barriers, staging
     const int64_t num_tiles = (int64_t)m_tiles * n_tiles * splits;
     dim3 grid((unsigned)std::min<int64_t>(num_tiles, 148));
@@ -473,10 +492,10 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
         p.split_stride = M * ldp;
         p.vec = 1;
     }
-    if (a_mn && b_mn) launch_gemm<true, true>(ta, tb, p, grid, smem, s);
-    else if (a_mn) launch_gemm<true, false>(ta, tb, p, grid, smem, s);
-    else if (b_mn) launch_gemm<false, true>(ta, tb, p, grid, smem, s);
-    else launch_gemm<false, false>(ta, tb, p, grid, smem, s);
+    if (a_mn && b_mn) launch_gemm<true, true>(ta, tb, tblo, p, grid, smem, s);
+    else if (a_mn) launch_gemm<true, false>(ta, tb, tblo, p, grid, smem, s);
+    else if (b_mn) launch_gemm<false, true>(ta, tb, tblo, p, grid, smem, s);
+    else launch_gemm<false, false>(ta, tb, tblo, p, grid, smem, s);
     count_launch(c);
     if (splits > 1) {
         const int64_t total = M * N;
@@ -485,6 +504,29 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
         NTP_LAUNCH_CHECK();
         count_launch(c);
     }
+}
+
+namespace {
+__global__ void tf32_split_kernel(const float* __restrict__ src, int64_t rows, int32_t cols, int64_t ld,
+                                  float* __restrict__ hi, float* __restrict__ lo) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * cols; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / cols, k = i - r * cols;
+        const float x = src[r * ld + k];
+        const float h = tf32_rn(x);
+        hi[r * ld + k] = h;
+        lo[r * ld + k] = tf32_rn(x - h);
+    }
+}
+}  // namespace
+
+// hi = rn_tf32(W), lo = rn_tf32(W - hi), same [rows x cols] / ld layout (pre-split GEMM operand).
+void tf32_split(ntp_ctx* c, const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
+                cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return;
+    tf32_split_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 148 * 8), 256, 0, s>>>(src, rows, (int32_t)cols,
+                                                                                                  ld, hi, lo);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
 }
 
 }  // namespace ntp

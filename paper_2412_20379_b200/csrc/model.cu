@@ -221,15 +221,18 @@ void gemm_rm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, cons
 
 // MLP GEMM C = op(A) op(B) (+ epilogue: 1 ReLU, 2 keep where aux > 0) on the tensor cores
 // (gemm.cu, tcgen05 3xTF32); NTP_GEMM=cublas selects cuBLAS SGEMM instead (A/B comparison).
+// (Bs: optional pre-split {hi, lo} copy of B for the tensor-core path, same layout and ldb.)
+struct Split { const float* hi = nullptr; const float* lo = nullptr; };
 void mlp_gemm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
               const float* B, int64_t ldb, float* C, int64_t ldc, cudaStream_t s, int epi = 0,
-              const float* aux = nullptr, int64_t ldaux = 0) {
+              const float* aux = nullptr, int64_t ldaux = 0, Split Bs = Split{}) {
     static const bool use_cublas = [] {
         const char* v = getenv("NTP_GEMM");
         return v && std::string(v) == "cublas";
     }();
     if (!use_cublas) {
-        gemm_tf32x3(c, M, N, K, A, lda, ta, B, ldb, !tb, C, ldc, epi, aux, ldaux, s);
+        if (Bs.hi) gemm_tf32x3(c, M, N, K, A, lda, ta, Bs.hi, ldb, !tb, C, ldc, epi, aux, ldaux, s, Bs.lo);
+        else gemm_tf32x3(c, M, N, K, A, lda, ta, B, ldb, !tb, C, ldc, epi, aux, ldaux, s);
         return;
     }
     gemm_rm(c, ta, tb, M, N, K, A, lda, B, ldb, C, ldc);
@@ -332,8 +335,16 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         c->m_Xs.ensure((size_t)V_p * ldXp * sizeof(float));
         c->m_lab.ensure((size_t)V_p * sizeof(int32_t));
         c->m_mask.ensure((size_t)V_p);
-        NTP_CUDA(cudaMemcpy2DAsync(c->m_Xs.p, ldXp * sizeof(float), X_v->data, ldx * sizeof(float),
-                                   m->d_in * sizeof(float), V_p, cudaMemcpyHostToDevice, s));
+        if (ldx == ldXp) {
+            NTP_CUDA(cudaMemcpyAsync(c->m_Xs.p, X_v->data, (size_t)V_p * ldx * sizeof(float), cudaMemcpyHostToDevice, s));
+        } else {
+            // one contiguous DMA in the host pitch (a 2-D host copy with ~2 KB rows runs at a third of
+            // the link rate), then the 16-byte GEMM pitch on the device
+            c->m_Xh.ensure((size_t)V_p * ldx * sizeof(float));
+            NTP_CUDA(cudaMemcpyAsync(c->m_Xh.p, X_v->data, (size_t)V_p * ldx * sizeof(float), cudaMemcpyHostToDevice, s));
+            NTP_CUDA(cudaMemcpy2DAsync(c->m_Xs.p, ldXp * sizeof(float), c->m_Xh.p, ldx * sizeof(float),
+                                       m->d_in * sizeof(float), V_p, cudaMemcpyDeviceToDevice, s));
+        }
         NTP_CUDA(cudaMemcpyAsync(c->m_lab.p, labels_v, V_p * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         NTP_CUDA(cudaMemcpyAsync(c->m_mask.p, mask_v, V_p, cudaMemcpyHostToDevice, s));
         X = c->m_Xs.as<float>();
@@ -368,6 +379,21 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         ldw1 = ldC1;
     }
 
+    // weights split once per epoch into {rn_tf32(W), rn_tf32(W - hi)} for the tensor-core GEMMs
+    c->m_Wsplit.ensure((size_t)2 * ((int64_t)m->d_in * ldw0 + (int64_t)m->hid * ldw1) * sizeof(float));
+    Split W0s, W1s;
+    {
+        float* w = c->m_Wsplit.as<float>();
+        float* w0h = w;
+        float* w0l = w0h + (int64_t)m->d_in * ldw0;
+        float* w1h = w0l + (int64_t)m->d_in * ldw0;
+        float* w1l = w1h + (int64_t)m->hid * ldw1;
+        tf32_split(c, W0g, m->d_in, m->hid, ldw0, w0h, w0l, s);
+        tf32_split(c, W1g, m->hid, m->C, ldw1, w1h, w1l, s);
+        W0s = Split{w0h, w0l};
+        W1s = Split{w1h, w1l};
+    }
+
     // ---- scratch
     c->m_H1.ensure((size_t)V_p * ldH * sizeof(float));
     c->m_L.ensure((size_t)V_p * ldL * sizeof(float));
@@ -393,11 +419,11 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     NTP_BLAS(cublasSetStream(c->blas, s));
 
     // a2: MLP forward (ReLU fused into the GEMM epilogue)
-    mlp_gemm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0g, ldw0, H1, ldH, s, /*relu*/ 1);
+    mlp_gemm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0g, ldw0, H1, ldH, s, /*relu*/ 1, nullptr, 0, W0s);
     const float* prop_src = H1;             // rows propagated (w columns)
     int64_t ld_src = ldH;
     if (!after) {
-        mlp_gemm(c, false, false, V_p, m->C, m->hid, H1, ldH, W1g, ldw1, L, ldL, s);
+        mlp_gemm(c, false, false, V_p, m->C, m->hid, H1, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
         prop_src = L;
         ld_src = ldL;
     }
@@ -451,11 +477,11 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         // Z_v = unpack(recv) [V_p x hid]; logits = Z_v W1; dlogits; dZ_v = dlogits W1^T -> pack
         float* Zv = dH1;   // reuse [V_p x ldH]
         unpack_f2v(c, c->recv.p, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s);
-        mlp_gemm(c, false, false, V_p, m->C, m->hid, Zv, ldH, W1g, ldw1, L, ldL, s);
+        mlp_gemm(c, false, false, V_p, m->C, m->hid, Zv, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
         nb_loss = launch_softmax_xent(c, (const float*)L, 0, V_p, d_s, m->C, lab, msk, row0, n, dL, 0, nullptr, part,
                                       cnt, ldL, s);
         mlp_gemm(c, true, false, m->hid, m->C, V_p, Zv, ldH, dL, ldL, dW1, m->C, s);          // dW1 = Z_v^T dlogits
-        mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s);           // dZ_v -> L
+        mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);  // dZ_v -> L
         pack_v2f(c, L, ldL, m->hid, c->send.p, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s);
     }
     reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb_loss, scal);
@@ -490,7 +516,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     // a10: MLP backward (ReLU' mask fused into the dH1 GEMM epilogue)
     if (!after) {
         mlp_gemm(c, true, false, m->hid, m->C, V_p, H1, ldH, dL, ldL, dW1, m->C, s);              // dW1 = H1^T dL^
-        mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, dH1, ldH, s, 2, H1, ldH); // dH1
+        mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, dH1, ldH, s, 2, H1, ldH, W1s);  // dH1
     } else {
         // ReLU' mask fused into the gather's unpack above
     }

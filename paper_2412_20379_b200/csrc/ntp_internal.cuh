@@ -127,7 +127,7 @@ struct ntp_ctx {
     // scratch
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
-    ntp::DevBuf m_gemm_part, m_W0p, m_W1p;
+    ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit;
     cudaEvent_t ev[64] = {};
     cudaEvent_t hop_ev[256] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
     int hop_ev_used = 0;
@@ -216,7 +216,10 @@ void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_ele
 // B stored [K][N] if b_mn else [N][K]; lda/ldb multiples of 4.  epi: 0 store, 1 ReLU, 2 keep where aux > 0.
 void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool a_mn,
                  const float* B, int64_t ldb, bool b_mn, float* C, int64_t ldc, int epi, const float* aux,
-                 int64_t ldaux, cudaStream_t s);
+                 int64_t ldaux, cudaStream_t s, const float* B_lo = nullptr);
+// B_lo != nullptr: B is already rn_tf32-rounded and B_lo holds the residual (tf32_split), e.g. weights.
+void tf32_split(ntp_ctx* c, const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
+                cudaStream_t s);
 
 inline size_t esize(ntp_dtype d) { return d == NTP_BF16 ? 2 : 4; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
