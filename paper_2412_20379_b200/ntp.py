@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libntp.so")
+LIB_PATH = os.environ.get("NTP_LIB") or os.path.join(_HERE, "libntp.so")   # NTP_LIB: dev A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libntp.so not found at {LIB_PATH}: run `python -m paper_2412_20379_b200.build` "
