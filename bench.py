@@ -184,6 +184,10 @@ def main():
                     help="chunked last hop with the gather on the comm stream (a12); off by default: on "
                          "reddit the gather moves ~1-10 MB and chunking costs more than it hides")
     ap.add_argument("--slice-align", type=int, default=16)
+    ap.add_argument("--reorder", default="auto", choices=["auto", "on", "off"],
+                    help="NTP_G_REORDER (internal degree-class numbering). auto: on when the vertex table is "
+                         "far larger than L2 (n >= 1M: products, orkut, papers), off for the L2-resident Reddit "
+                         "shape where it measured slower (DESIGN.md §5); never with --overlap")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=3)
@@ -216,7 +220,9 @@ def main():
     ctx = ntp.Context(device=local, rank=rank, world=world, unique_id=uid, slice_align=args.slice_align)
 
     t0 = time.time()
-    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric)
+    reorder = (args.reorder == "on" or (args.reorder == "auto" and cfg.n >= 1_000_000)) and not args.overlap
+    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric,
+                      reorder=reorder)
     n, nnz, sym = ctx.graph_info()
     t_graph = time.time() - t0
 
@@ -320,6 +326,7 @@ def main():
             "config": {"workload": WORKLOADS.get(args.config, args.config), "n": n, "nnz": nnz, "w": w, "K": cfg.K,
                        "gamma": cfg.gamma, "alpha": cfg.alpha, "P": world, "d_s": d_s, "V_p": V_p,
                        "chunks": args.chunks, "overlap": bool(args.overlap),
+                       "vertex_order": "degree-ordered internally (NTP_G_REORDER)" if reorder else "R-MAT ids",
                        "l2": f"inputs larger than L2 (col_idx {4 * nnz / 1e6:.0f} MB streamed per hop; "
                              f"X_v {Xh.nbytes / 1e6:.0f} MB per rank)",
                        "graph_setup_s": round(t_graph, 3)},

@@ -97,6 +97,11 @@ int         ntp_abi_version(void);
 #define NTP_G_SYMMETRIC 1u   /* graph is undirected: transpose == CSR (saves memory) */
 #define NTP_G_VALIDATE  2u   /* check the input CSR: rp[0]=0, monotone,
                                 rp[n]=nnz, 0<=col<n, strictly ascending per row     */
+#define NTP_G_REORDER   4u   /* store the graph under an internal vertex numbering by
+                                descending total degree (the hot rows of the gather
+                                become contiguous).  Invisible at the ABI: slices,
+                                ntp_copy_csr and ntp_copy_dinv stay in original ids.
+                                Not combinable with NTP_M_OVERLAP (NTP_ERR_CONFIG). */
 
 /* Loads an in-CSR from HOST arrays: row v = destination, columns = sources u
  * of arcs u->v ("N_in(v)", Eq. 1).  Explicit self loops are dropped

@@ -209,7 +209,8 @@ ntp_status ntp_load_graph(ntp_ctx* c, const int64_t* row_ptr, const int32_t* col
     csr_to_keys(c, drp.as<int64_t>(), dcol.as<int32_t>(), n, keys.as<uint64_t>(), c->s_comp);
     drp.release();
     dcol.release();
-    build_graph_from_keys(c, keys.as<uint64_t>(), nnz, n, (flags & NTP_G_SYMMETRIC) != 0, keys);
+    build_graph_from_keys(c, keys.as<uint64_t>(), nnz, n, (flags & NTP_G_SYMMETRIC) != 0, keys,
+                          (flags & NTP_G_REORDER) != 0);
     NTP_API_END(c)
 }
 
@@ -232,7 +233,7 @@ ntp_status ntp_build_graph(ntp_ctx* c, const int64_t* src, const int64_t* dst, i
     NTP_CUDA(cudaStreamSynchronize(c->s_comp));
     ds.release();
     dd.release();
-    build_graph_from_keys(c, keys.as<uint64_t>(), mk, n, sym, keys);
+    build_graph_from_keys(c, keys.as<uint64_t>(), mk, n, sym, keys, (flags & NTP_G_REORDER) != 0);
     NTP_API_END(c)
 }
 
@@ -248,7 +249,7 @@ ntp_status ntp_generate_rmat(ntp_ctx* c, int64_t n, int scale, int64_t m_raw, co
     DevBuf keys;
     keys.ensure(std::max<int64_t>(mk, 1) * sizeof(uint64_t));
     if (m_raw) rmat_keys(c, scale, thr, seed, 0, m_raw, n, sym, keys.as<uint64_t>(), c->s_comp);
-    build_graph_from_keys(c, keys.as<uint64_t>(), mk, n, sym, keys);
+    build_graph_from_keys(c, keys.as<uint64_t>(), mk, n, sym, keys, (flags & NTP_G_REORDER) != 0);
     NTP_API_END(c)
 }
 
@@ -285,7 +286,13 @@ ntp_status ntp_copy_csr(const ntp_ctx* cc, int transposed, int64_t* row_ptr, int
     NTP_API_BEGIN(c)
     need_graph(c);
     NTP_CUDA(cudaSetDevice(c->device));
-    const Csr& csr = transposed ? c->g.bwd() : c->g.fwd();
+    const Csr* csrp = transposed ? &c->g.bwd() : &c->g.fwd();
+    Csr orig;
+    if (c->g.reordered) {   // internal ids -> original ids, columns re-sorted
+        export_original_csr(c, *csrp, orig);
+        csrp = &orig;
+    }
+    const Csr& csr = *csrp;
     const int64_t n = c->g.n, nnz = c->g.nnz;
     std::vector<int32_t> rp(n + 1);
     NTP_CUDA(cudaMemcpy(rp.data(), csr.row_ptr.p, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
@@ -303,8 +310,10 @@ ntp_status ntp_copy_dinv(const ntp_ctx* cc, float* dinv_in, float* dinv_out) {
     need_graph(c);
     NTP_CUDA(cudaSetDevice(c->device));
     const int64_t n = c->g.n;
-    if (dinv_in && n) NTP_CUDA(cudaMemcpy(dinv_in, c->g.dinv_in_p(), n * sizeof(float), cudaMemcpyDeviceToHost));
-    if (dinv_out && n) NTP_CUDA(cudaMemcpy(dinv_out, c->g.dinv_out_p(), n * sizeof(float), cudaMemcpyDeviceToHost));
+    const float* di = c->g.dinv_in_orig();     // original vertex order either way
+    const float* dout = c->g.dinv_out_orig();
+    if (dinv_in && n) NTP_CUDA(cudaMemcpy(dinv_in, di, n * sizeof(float), cudaMemcpyDeviceToHost));
+    if (dinv_out && n) NTP_CUDA(cudaMemcpy(dinv_out, dout, n * sizeof(float), cudaMemcpyDeviceToHost));
     NTP_API_END(c)
 }
 

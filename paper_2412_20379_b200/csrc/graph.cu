@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ntp_internal.cuh"
 
@@ -246,9 +247,95 @@ static void make_partition(ntp_ctx* c, Csr& csr, int64_t n, int64_t nnz, int64_t
     NTP_CUDA(cudaStreamSynchronize(s));
 }
 
+// ---- degree-ordered internal vertex numbering (NTP_G_REORDER)
+__global__ void key_degrees_kernel(const uint64_t* __restrict__ keys, int64_t nnz, int32_t* __restrict__ deg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        atomicAdd(&deg[k >> 32], 1);                  // in-degree of the destination
+        atomicAdd(&deg[k & 0xFFFFFFFFull], 1);        // out-degree of the source
+    }
+}
+__global__ void order_keys_kernel(const int32_t* __restrict__ deg, int64_t n, uint64_t* __restrict__ keys, int mode) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t d = (uint32_t)deg[v] + 1u;
+        uint32_t cls = d;                                        // mode 0: exact degree
+        if (mode >= 1) {                                         // 1: octave, 2: quarter octave
+            const int lz = 31 - __clz(d);
+            cls = (uint32_t)lz << 2;
+            if (mode == 2 && lz >= 2) cls |= (d >> (lz - 2)) & 3u;
+        }
+        keys[v] = ((uint64_t)(0xFFFFFFFFu - cls) << 32) | (uint64_t)v;   // stable within a class
+    }
+}
+__global__ void order_maps_kernel(const uint64_t* __restrict__ sorted, int64_t n, int32_t* __restrict__ perm,
+                                  int32_t* __restrict__ inv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = (int32_t)(sorted[i] & 0xFFFFFFFFull);
+        inv[i] = v;
+        perm[v] = (int32_t)i;
+    }
+}
+__global__ void relabel_keys_kernel(const uint64_t* __restrict__ in, int64_t nnz, const int32_t* __restrict__ map,
+                                    uint64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = in[i];
+        out[i] = ((uint64_t)(uint32_t)map[k >> 32] << 32) | (uint64_t)(uint32_t)map[k & 0xFFFFFFFFull];
+    }
+}
+
+// Internal ids by descending total degree (in + out, ties by id): the rows the hops gather most
+// often become contiguous, so their lines stay resident in L2/L1.  g.perm maps
+// original -> internal, g.inv internal -> original.  `sorted` (nnz keys, original ids) is
+// relabelled and re-sorted into `out_sorted` (alt buffer).
+static uint64_t* reorder_vertices(ntp_ctx* c, uint64_t* sorted, uint64_t* spare, int64_t nnz, int64_t n, cudaStream_t s) {
+    Graph& g = c->g;
+    g.perm.ensure(std::max<int64_t>(n, 1) * sizeof(int32_t));
+    g.inv.ensure(std::max<int64_t>(n, 1) * sizeof(int32_t));
+    {
+        DevBuf deg, ok, oalt, tmp;
+        deg.ensure(std::max<int64_t>(n, 1) * sizeof(int32_t));
+        ok.ensure(std::max<int64_t>(n, 1) * sizeof(uint64_t));
+        oalt.ensure(std::max<int64_t>(n, 1) * sizeof(uint64_t));
+        NTP_CUDA(cudaMemsetAsync(deg.p, 0, std::max<int64_t>(n, 1) * sizeof(int32_t), s));
+        key_degrees_kernel<<<grid_for(nnz), 256, 0, s>>>(sorted, nnz, deg.as<int32_t>());
+        static const int mode = [] { const char* e = getenv("NTP_REORDER_MODE"); return e ? atoi(e) : 1; }();
+        order_keys_kernel<<<grid_for(n), 256, 0, s>>>(deg.as<int32_t>(), n, ok.as<uint64_t>(), mode);
+        NTP_LAUNCH_CHECK();
+        cub::DoubleBuffer<uint64_t> db(ok.as<uint64_t>(), oalt.as<uint64_t>());
+        size_t tb = 0;
+        NTP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int64_t)n, 0, 64, s));
+        tmp.ensure(tb + 256);
+        NTP_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, db, (int64_t)n, 0, 64, s));
+        order_maps_kernel<<<grid_for(n), 256, 0, s>>>(db.Current(), n, g.perm.as<int32_t>(), g.inv.as<int32_t>());
+        NTP_LAUNCH_CHECK();
+        count_launch(c, 12);
+        NTP_CUDA(cudaStreamSynchronize(s));
+    }
+    relabel_keys_kernel<<<grid_for(nnz), 256, 0, s>>>(sorted, nnz, g.perm.as<int32_t>(), spare);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    uint64_t* out = nullptr;
+    sort_unique(c, spare, sorted, nnz, n, false, &out, s);   // a permutation: no duplicates appear
+    g.reordered = true;
+    return out;
+}
+
+__global__ void original_keys_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t n,
+                                     const int32_t* __restrict__ inv, uint64_t* __restrict__ keys) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t hi = (uint64_t)(uint32_t)inv[r] << 32;
+        for (int32_t e = rp[r]; e < rp[r + 1]; ++e) keys[e] = hi | (uint64_t)(uint32_t)inv[col[e]];
+    }
+}
+__global__ void gather_f32_kernel(const float* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                                  float* __restrict__ dst) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        dst[v] = src[idx[v]];
+}
+
 // keys: device buffer with m keys and room for an alternate buffer of m keys at keys + m_cap.
 void build_graph_from_keys(ntp_ctx* c, uint64_t* keys, int64_t m, int64_t n, bool symmetric,
-                           DevBuf& owner) {
+                           DevBuf& owner, bool reorder) {
     cudaStream_t s = c->s_comp;
     Graph& g = c->g;
     g.reset();   // drops the previous graph
@@ -264,6 +351,7 @@ void build_graph_from_keys(ntp_ctx* c, uint64_t* keys, int64_t m, int64_t n, boo
     const int64_t nnz = sort_unique(c, keys, alt.as<uint64_t>(), m, n, true, &sorted, s);
     NTP_CHECK(nnz < (int64_t(1) << 31), NTP_ERR_CONFIG, "nnz = %lld >= 2^31 is not supported", (long long)nnz);
     g.nnz = nnz;
+    if (reorder && n > 0 && nnz > 0) sorted = reorder_vertices(c, sorted, (sorted == keys) ? alt.as<uint64_t>() : keys, nnz, n, s);
     fill_csr(c, sorted, nnz, n, g.in, s);
     make_partition(c, g.in, n, nnz, g.unit_items, s);
     g.dinv_in.ensure(std::max<int64_t>(n, 1) * sizeof(float));
@@ -287,9 +375,35 @@ void build_graph_from_keys(ntp_ctx* c, uint64_t* keys, int64_t m, int64_t n, boo
         NTP_LAUNCH_CHECK();
         count_launch(c);
     }
+    if (g.reordered) {   // original-order copies of the scales for the layout kernels
+        g.dinv_orig.ensure(2 * std::max<int64_t>(n, 1) * sizeof(float));
+        gather_f32_kernel<<<grid_for(n), 256, 0, s>>>(g.dinv_in_p(), g.perm.as<int32_t>(), n, g.dinv_orig.as<float>());
+        gather_f32_kernel<<<grid_for(n), 256, 0, s>>>(g.dinv_out_p(), g.perm.as<int32_t>(), n,
+                                                      g.dinv_orig.as<float>() + n);
+        NTP_LAUNCH_CHECK();
+        count_launch(c, 2);
+    }
     NTP_CUDA(cudaStreamSynchronize(s));
     g.loaded = true;
     (void)owner;
+}
+
+// The CSR `csr` of a reordered graph expressed in ORIGINAL ids (rows and columns), columns ascending
+// per row, into `out` (row_ptr / col only): what ntp_copy_csr returns.
+void export_original_csr(ntp_ctx* c, const Csr& csr, Csr& out) {
+    const Graph& g = c->g;
+    cudaStream_t s = c->s_comp;
+    const int64_t n = g.n, nnz = g.nnz;
+    DevBuf keys, alt;
+    keys.ensure(std::max<int64_t>(nnz, 1) * sizeof(uint64_t));
+    alt.ensure(std::max<int64_t>(nnz, 1) * sizeof(uint64_t));
+    original_keys_kernel<<<grid_for(n), 256, 0, s>>>(csr.row_ptr.as<int32_t>(), csr.col.as<int32_t>(), n,
+                                                     g.inv.as<int32_t>(), keys.as<uint64_t>());
+    NTP_LAUNCH_CHECK();
+    uint64_t* sorted = keys.as<uint64_t>();
+    if (nnz) sort_unique(c, keys.as<uint64_t>(), alt.as<uint64_t>(), nnz, n, false, &sorted, s);
+    fill_csr(c, sorted, nnz, n, out, s);
+    NTP_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace ntp

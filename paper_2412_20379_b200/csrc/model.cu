@@ -430,7 +430,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd done
 
     // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
-    pack_v2f(c, prop_src, ld_src, w, c->send.p, V_p, d_s, P, g.dinv_out_p(), row0, n, NTP_F32, dt, s);
+    pack_v2f(c, prop_src, ld_src, w, c->send.p, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s);
     alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E2 v2f done
 
@@ -454,7 +454,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     NTP_CUDA(record_timing(c, E[ei++], s));   // E3 prop fwd + f2v done
 
     // a6: loss + gradient, written straight into the backward split's send buffer
-    const float* gscale_bwd = g.dinv_in_p();   // backward column side
+    const float* gscale_bwd = g.dinv_in_orig();   // backward column side (original vertex order)
     int64_t nb_loss = 0;
     if (!after) {
         if (dt == NTP_F32)
@@ -569,6 +569,8 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     const size_t es = esize(m->dtype);
     const bool timed = true;
     cudaEvent_t* E = c->ev;
+    NTP_CHECK(!((m->flags & NTP_M_OVERLAP) && g.reordered), NTP_ERR_CONFIG,
+              "NTP_M_OVERLAP sends last-hop chunks by destination block: needs a graph without NTP_G_REORDER");
 
     // ---- order after the caller's stream
     NTP_CUDA(cudaEventRecord(c->ev[40], user ? user : (cudaStream_t)0));

@@ -93,10 +93,21 @@ struct Graph {
     Csr in;                         // rows = destinations (A^)
     Csr out;                        // rows = sources (A^T); unused if symmetric
     DevBuf dinv_in, dinv_out;       // fp32 [n]
+    // NTP_G_REORDER: the CSRs and D~^{-1/2} use internal ids (descending total degree); slices
+    // handed across the ABI stay in original vertex order (perm: original -> internal, inv:
+    // internal -> original; the first hop gathers through inv, the last hop scatters through it).
+    bool reordered = false;
+    DevBuf perm, inv;               // int32 [n]
+    DevBuf dinv_orig;               // fp32 [2n]: D~_in^{-1/2}, D~_out^{-1/2} in ORIGINAL order (reordered only)
     void reset() {
-        n = nnz = 0; symmetric = false; loaded = false; unit_items = 2048;
-        in.reset(); out.reset(); dinv_in.release(); dinv_out.release();
+        n = nnz = 0; symmetric = false; loaded = false; unit_items = 2048; reordered = false;
+        in.reset(); out.reset(); dinv_in.release(); dinv_out.release(); perm.release(); inv.release();
+        dinv_orig.release();
     }
+    const int32_t* inv_p() const { return reordered ? inv.as<int32_t>() : nullptr; }
+    // per-vertex scales indexed by ORIGINAL vertex id (what the layout kernels use)
+    const float* dinv_in_orig() const { return reordered ? dinv_orig.as<float>() : dinv_in_p(); }
+    const float* dinv_out_orig() const { return reordered ? dinv_orig.as<float>() + n : dinv_out_p(); }
     const Csr& fwd() const { return in; }
     const Csr& bwd() const { return symmetric ? in : out; }
     const float* dinv_in_p() const { return dinv_in.as<float>(); }
@@ -147,7 +158,8 @@ namespace ntp {
 
 // -------------------------------------------------------------- internal API
 void build_graph_from_keys(ntp_ctx* c, uint64_t* keys, int64_t m, int64_t n, bool symmetric,
-                           DevBuf& keybuf_owner);
+                           DevBuf& keybuf_owner, bool reorder = false);
+void export_original_csr(ntp_ctx* c, const Csr& csr, Csr& out);
 void rmat_keys(ntp_ctx* c, int scale, const uint32_t thr[3], uint64_t seed, int64_t i0, int64_t count,
                int64_t n, bool symmetric, uint64_t* keys, cudaStream_t s);
 void rmat_raw(ntp_ctx* c, int scale, const uint32_t thr[3], uint64_t seed, int64_t i0, int64_t count,
@@ -198,9 +210,11 @@ void csr_to_keys(ntp_ctx* c, const int64_t* row_ptr, const int32_t* col, int64_t
 void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, const void* S_in,
               void* S_out, const void* H, int64_t ld_in, int64_t ld_out, int64_t ld_h, int32_t cols,
               ntp_dtype dt, float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi,
-              cudaStream_t s);
+              cudaStream_t s, const int32_t* out_rows = nullptr);
+// S[r] = scale[r] * H[src_rows ? src_rows[r] : r] (scale may be null: plain copy / permutation)
 void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, int32_t cols,
-              const float* scale, int64_t rows, ntp_dtype dt, cudaStream_t s);
+              const float* scale, int64_t rows, ntp_dtype dt, cudaStream_t s,
+              const int32_t* src_rows = nullptr);
 
 // layouts
 void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, int64_t V_p,

@@ -133,6 +133,7 @@ struct HopParams {
     float gamma, alpha;
     int mode;                          // 0 intermediate, 1 last
     int64_t nnz;
+    const int32_t* __restrict__ out_rows;   // last hop of a reordered graph: output row r goes to out_rows[r]
 };
 
 // Lane layout ("full row per edge"): a group of L lanes works on one unit.  Lane
@@ -230,7 +231,8 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
                         out[i] = (p.alpha != 0.f) ? sig * (tot + self) + beta * (0.f + Vec<T, VB>::elem(s0_raw, i))
                                                   : sig * (tot + self);
                     }
-                    if (cok) stv<VB>(p.S_out + (int64_t)my_r * p.ld_out + voff, Vec<T, VB>::pack(out));
+                    const int64_t orow = p.out_rows ? (int64_t)__ldg(p.out_rows + my_r) : (int64_t)my_r;
+                    if (cok) stv<VB>(p.S_out + orow * p.ld_out + voff, Vec<T, VB>::pack(out));
                     r += E - 1;
                     continue;
                 }
@@ -344,7 +346,8 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
 #pragma unroll
                 for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + (0.f + Vec<T, VB>::elem(self_raw, i)));
             }
-            stv<VB>(p.S_out + (int64_t)r * p.ld_out + (int64_t)vcol * VB, Vec<T, VB>::pack(out));
+            const int64_t orow = p.out_rows ? (int64_t)__ldg(p.out_rows + r) : (int64_t)r;
+            stv<VB>(p.S_out + orow * p.ld_out + (int64_t)vcol * VB, Vec<T, VB>::pack(out));
         }
     }
 }
@@ -365,6 +368,7 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
     const int row_vals = p.nvec * VALS;
     const float a = p.rs[r];
     const float b = p.cs[r];
+    const int64_t orow = p.out_rows ? (int64_t)p.out_rows[r] : (int64_t)r;
     for (int k = lane; k < row_vals; k += 32) {
         float acc = p.carry[(u * 2 + 1) * (int64_t)row_vals + k];
         for (int64_t v = u + 1;; ++v) {
@@ -382,24 +386,26 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
             out += ((p.mode == 0) ? p.alpha : p.alpha / b) * h[comp];
         }
         if (sizeof(T) == 4) {
-            reinterpret_cast<float*>(p.S_out + (int64_t)r * p.ld_out)[k] = out;
+            reinterpret_cast<float*>(p.S_out + orow * p.ld_out)[k] = out;
         } else {
-            reinterpret_cast<__nv_bfloat16*>(p.S_out + (int64_t)r * p.ld_out)[k] = __float2bfloat16_rn(out);
+            reinterpret_cast<__nv_bfloat16*>(p.S_out + orow * p.ld_out)[k] = __float2bfloat16_rn(out);
         }
     }
 }
 
 template <typename T>
 __global__ void prescale_kernel(const char* __restrict__ H, int64_t ld_h, char* __restrict__ S, int64_t ld_s,
-                                int32_t nvec, const float* __restrict__ scale, int64_t rows) {
+                                int32_t nvec, const float* __restrict__ scale, int64_t rows,
+                                const int32_t* __restrict__ src_rows) {
     constexpr int VALS = 16 / sizeof(T);
     const int64_t total = rows * nvec;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = i / nvec;
         const int64_t vc = i % nvec;
+        const int64_t hr = src_rows ? (int64_t)src_rows[r] : r;    // reordered graph: gather in original order
         float v[VALS];
-        load16<T>(H + r * ld_h + vc * 16, v);
-        const float s = scale[r];
+        load16<T>(H + hr * ld_h + vc * 16, v);
+        const float s = scale ? scale[r] : 1.f;
 #pragma unroll
         for (int k = 0; k < VALS; ++k) v[k] *= s;
         store16<T>(S + r * ld_s + vc * 16, v);
@@ -460,7 +466,8 @@ static void unit_range(const Csr& csr, int64_t row_lo, int64_t row_hi, int64_t& 
 
 void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, const void* S_in, void* S_out,
               const void* S0, int64_t ld_in, int64_t ld_out, int64_t ld_s0, int32_t cols, ntp_dtype dt,
-              float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi, cudaStream_t s) {
+              float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi, cudaStream_t s,
+              const int32_t* out_rows) {
     const Graph& g = c->g;
     if (row_hi < 0) row_hi = g.n;
     row_lo = std::max<int64_t>(row_lo, 0);
@@ -484,6 +491,7 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     p.ld_s0 = ld_s0 * es;
     p.n = g.n;
     p.nnz = g.nnz;
+    p.out_rows = out_rows;
 
     unit_range(csr, row_lo, row_hi, p.u_begin, p.u_end);
     p.row_lo = row_lo;
@@ -516,17 +524,18 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
 }
 
 void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, int32_t cols, const float* scale,
-              int64_t rows, ntp_dtype dt, cudaStream_t s) {
+              int64_t rows, ntp_dtype dt, cudaStream_t s, const int32_t* src_rows) {
     if (rows <= 0) return;
     const size_t es = esize(dt);
     const int32_t nvec = (int32_t)(cols * es / 16);
     const int64_t total = rows * nvec;
     const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
     if (dt == NTP_F32)
-        prescale_kernel<float><<<blocks, 256, 0, s>>>((const char*)H, ld_h * es, (char*)S, ld_s * es, nvec, scale, rows);
+        prescale_kernel<float><<<blocks, 256, 0, s>>>((const char*)H, ld_h * es, (char*)S, ld_s * es, nvec, scale, rows,
+                                                      src_rows);
     else
         prescale_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>((const char*)H, ld_h * es, (char*)S, ld_s * es, nvec,
-                                                              scale, rows);
+                                                              scale, rows, src_rows);
     NTP_LAUNCH_CHECK();
     count_launch(c);
 }
@@ -554,19 +563,24 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
     c->prop_tmp.ensure((size_t)n * ld_t * es + 16);
     void* bufs[2] = {a.Z, c->prop_tmp.p};
     const int64_t lds[2] = {a.ld_z, ld_t};
+    // reordered graph: the slice arrives in original vertex order; S^0 is formed in internal order
+    // (gather through inv; a pre-scaled input is only permuted) and the last hop scatters back
+    const int32_t* inv = g.inv_p();
+    NTP_CHECK(!(inv && defer_last), NTP_ERR_CONFIG, "chunked overlap needs original vertex order (no NTP_G_REORDER)");
     const void* S0;
     int64_t ld_s0;
-    if (prescaled_input) {
+    const float* pre = prescaled_input ? nullptr : cs;
+    if (prescaled_input && !inv) {
         S0 = a.H;
         ld_s0 = a.ld_h;
     } else if (a.alpha != 0.f) {
         c->prop_s0.ensure((size_t)n * ld_t * es + 16);
-        prescale(c, a.H, a.ld_h, c->prop_s0.p, ld_t, a.cols, cs, n, a.dtype, s);
+        prescale(c, a.H, a.ld_h, c->prop_s0.p, ld_t, a.cols, pre, n, a.dtype, s, inv);
         S0 = c->prop_s0.p;
         ld_s0 = ld_t;
     } else {
         const int b0 = a.K % 2;       // hop 1 writes bufs[(K-1)%2], so S^0 may live in bufs[K%2]
-        prescale(c, a.H, a.ld_h, bufs[b0], lds[b0], a.cols, cs, n, a.dtype, s);
+        prescale(c, a.H, a.ld_h, bufs[b0], lds[b0], a.cols, pre, n, a.dtype, s, inv);
         S0 = bufs[b0];
         ld_s0 = lds[b0];
     }
@@ -583,7 +597,7 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
         const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
         if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
         spmm_hop(c, csr, rs, cs, sin, bufs[nxt], S0, ld_sin, lds[nxt], ld_s0, a.cols, a.dtype, a.gamma, a.alpha,
-                 last ? 1 : 0, 0, -1, s);
+                 last ? 1 : 0, 0, -1, s, last ? inv : nullptr);
         if (timed) {
             NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used + 1], s));
             c->hop_ev_used += 2;

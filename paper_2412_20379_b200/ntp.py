@@ -26,7 +26,7 @@ NTP_OK, NTP_ERR_ARG, NTP_ERR_SHAPE, NTP_ERR_CONFIG, NTP_ERR_GRAPH, NTP_ERR_STATE
     NTP_ERR_CUDA, NTP_ERR_NCCL, NTP_ERR_TIMEOUT = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9
 NTP_F32, NTP_BF16 = 0, 1
 NTP_LAYOUT_VERTEX, NTP_LAYOUT_FEATURE = 0, 1
-NTP_G_SYMMETRIC, NTP_G_VALIDATE = 1, 2
+NTP_G_SYMMETRIC, NTP_G_VALIDATE, NTP_G_REORDER = 1, 2, 4
 NTP_M_W1_AFTER_PROP, NTP_M_OVERLAP, NTP_M_HOST_INPUTS = 1, 2, 4
 PHASES = ["mlp_fwd", "v2f_fwd", "prop_fwd", "f2v_fwd", "loss", "v2f_bwd", "prop_bwd", "f2v_bwd",
           "mlp_bwd", "allreduce", "sgd", "total"]
@@ -178,22 +178,26 @@ class Context:
             raise NtpError(st, _lib.ntp_last_error(self._h).decode())
 
     # -------------------------------------------------------------- graph
-    def load_graph(self, row_ptr, col_idx, n: int, symmetric: bool = False, validate: bool = False):
+    def load_graph(self, row_ptr, col_idx, n: int, symmetric: bool = False, validate: bool = False,
+                   reorder: bool = False):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         cl = np.ascontiguousarray(col_idx, dtype=np.int32)
-        flags = (NTP_G_SYMMETRIC if symmetric else 0) | (NTP_G_VALIDATE if validate else 0)
+        flags = ((NTP_G_SYMMETRIC if symmetric else 0) | (NTP_G_VALIDATE if validate else 0)
+                 | (NTP_G_REORDER if reorder else 0))
         self._chk(_lib.ntp_load_graph(self._h, rp.ctypes.data, cl.ctypes.data, n, int(rp[-1]) if n >= 0 else 0,
                                       flags))
 
-    def build_graph(self, src, dst, n: int, symmetric: bool = False):
+    def build_graph(self, src, dst, n: int, symmetric: bool = False, reorder: bool = False):
         s = np.ascontiguousarray(src, dtype=np.int64)
         d = np.ascontiguousarray(dst, dtype=np.int64)
         self._chk(_lib.ntp_build_graph(self._h, s.ctypes.data, d.ctypes.data, s.size, n,
-                                       NTP_G_SYMMETRIC if symmetric else 0))
+                                       (NTP_G_SYMMETRIC if symmetric else 0) | (NTP_G_REORDER if reorder else 0)))
 
-    def generate_rmat(self, n: int, scale: int, m_raw: int, thresholds, seed: int, symmetric: bool):
+    def generate_rmat(self, n: int, scale: int, m_raw: int, thresholds, seed: int, symmetric: bool,
+                      reorder: bool = False):
         thr = (C.c_uint32 * 3)(*[int(t) for t in thresholds])
-        self._chk(_lib.ntp_generate_rmat(self._h, n, scale, m_raw, thr, seed, NTP_G_SYMMETRIC if symmetric else 0))
+        self._chk(_lib.ntp_generate_rmat(self._h, n, scale, m_raw, thr, seed,
+                                         (NTP_G_SYMMETRIC if symmetric else 0) | (NTP_G_REORDER if reorder else 0)))
 
     def rmat_arcs(self, scale: int, thresholds, seed: int, i0: int, count: int):
         thr = (C.c_uint32 * 3)(*[int(t) for t in thresholds])

@@ -26,10 +26,12 @@ def main():
     ap.add_argument("--K", type=int, default=1)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--bwd", action="store_true")
+    ap.add_argument("--reorder", action="store_true")
     args = ap.parse_args()
     cfg = synth.get_config(args.config)
     ctx = ntp.Context()
-    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric)
+    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric,
+                      reorder=args.reorder)
     n, nnz, sym = ctx.graph_info()
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     esz = 2 if args.dtype == "bf16" else 4
@@ -53,7 +55,7 @@ def main():
         rec = dict(config=args.config, d=d, dtype=args.dtype, ms_per_hop=round(ms, 4),
                    GE_per_s=round(nnz * d / (ms * 1e-3) / 1e9, 1),
                    gather_TBps=round((nnz + n) * rs / (ms * 1e-3) / 1e12, 2),
-                   edges_per_ns=round(nnz / (ms * 1e6), 2), nnz=nnz, n=n,
+                   edges_per_ns=round(nnz / (ms * 1e6), 2), nnz=nnz, n=n, reorder=args.reorder,
                    env={k: v for k, v in os.environ.items() if k.startswith("NTP_")})
         out.append(rec)
         print(json.dumps(rec), flush=True)

@@ -14,12 +14,14 @@ def oracle_graph(name: str):
     return oracle.graph.graph_from_config(synth.get_config(name))
 
 
-def ntp_ctx_for(name: str, device: int = 0, slice_align: int = 16):
-    """A world-1 context with the config's R-MAT graph generated ON THE DEVICE."""
+def ntp_ctx_for(name: str, device: int = 0, slice_align: int = 16, reorder: bool = False):
+    """A world-1 context with the config's R-MAT graph generated ON THE DEVICE
+    (reorder: the library's internal degree-ordered numbering, NTP_G_REORDER)."""
     from paper_2412_20379_b200 import ntp
     cfg = synth.get_config(name)
     ctx = ntp.Context(device=device, slice_align=slice_align)
-    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric)
+    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric,
+                      reorder=reorder)
     return ctx
 
 

@@ -7,7 +7,9 @@ Per rank, through the C ABI with the library's own NCCL communicator:
   2. K-hop propagation of this rank's FEATURE slice vs the oracle (R10, 1e-5) and
      bitwise vs the same columns of a single-GPU (P = 1) propagation;
   3. 3 training epochs with the overlap scheduler on and off: losses vs the oracle
-     (1e-4), and on == off bitwise (scheduling neutrality).
+     (1e-4), and on == off bitwise (scheduling neutrality, S:533);
+  4. the same on a degree-reordered graph (NTP_G_REORDER): slice propagation bitwise vs P = 1,
+     epochs vs the oracle.
 """
 import os
 import sys
@@ -105,6 +107,30 @@ def main(name):
         results.append((losses, W0.cpu(), W1.cpu()))
     assert results[0][0] == results[1][0], "overlap changed the loss"
     assert torch.equal(results[0][1], results[1][1]) and torch.equal(results[0][2], results[1][2])
+
+    # ---- 4. degree-reordered graph (NTP_G_REORDER): slice propagation bitwise vs P = 1 on the same
+    # reordered graph, epochs vs the oracle
+    uid2 = pd.broadcast_unique_id(dist, rank)
+    ctxr = ntp.Context(device=local, rank=rank, world=world, unique_id=uid2)
+    ctxr.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric, reorder=True)
+    ctxr1 = ntp.Context(device=local)
+    ctxr1.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric, reorder=True)
+    Ht = torch.from_numpy(Hs).cuda()
+    Zt = torch.empty_like(Ht)
+    ctxr.propagate_fwd(Ht, Zt, cfg.K, cfg.gamma, cfg.alpha)
+    H1 = torch.from_numpy(Hp1).cuda()
+    Z1 = torch.empty_like(H1)
+    ctxr1.propagate_fwd(H1, Z1, cfg.K, cfg.gamma, cfg.alpha)
+    torch.cuda.synchronize()
+    assert torch.equal(Z1[:, rank * d_s:(rank + 1) * d_s], Zt[:n]), f"reordered P-invariance rank {rank}"
+    W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+    model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
+                 dtype=ntp.NTP_F32, chunks=1, flags=ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0)
+    for e in range(3):
+        rep = ctxr.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
+        assert abs(rep["loss"] - ref_losses[e]) <= 1e-4, f"reordered loss {rep['loss']} vs {ref_losses[e]}"
+    ctxr.close()
+    ctxr1.close()
     dist.barrier()
     if rank == 0:
         print(f"MP OK world={world} config={name} losses={results[1][0]}", flush=True)

@@ -63,6 +63,28 @@ def test_epoch_loss_parity_fp32(name):
     assert losses[-1] < losses[0]
 
 
+@pytest.mark.parametrize("name", ["cora", "small_dir", "small_appnp"])
+def test_epoch_loss_parity_reordered(name):
+    """Epochs on a degree-reordered graph (NTP_G_REORDER) match the oracle like the plain ones."""
+    from paper_2412_20379_b200 import ntp
+    cfg = synth.get_config(name)
+    ctx = ntp_ctx_for(name, reorder=True)
+    X, y, m = synth.config_inputs(cfg)
+    W0, W1 = synth.model_weights(cfg)
+    model = _model(cfg)
+    Xd, yd, md = (torch.from_numpy(a).cuda() for a in (X, y, m))
+    W0d, W1d = torch.from_numpy(W0).cuda(), torch.from_numpy(W1).cuda()
+    losses = [ctx.train_epoch(model, Xd, yd, md, W0d, W1d)["loss"] for _ in range(3)]
+    ref_losses, rW0, rW1 = _train_oracle(name, 3, model["lr"])
+    for e, (a, b) in enumerate(zip(losses, ref_losses)):
+        assert abs(a - b) <= 1e-4, f"epoch {e}: gpu {a} oracle {b}"
+    for got, ref in ((W0d.cpu().numpy(), rW0), (W1d.cpu().numpy(), rW1)):
+        assert np.abs(got - ref).max() <= 1e-4 * max(1.0, np.abs(ref).max())
+    # the chunked overlap needs destination blocks in original order: refused, not wrong
+    with pytest.raises(RuntimeError):
+        ctx.train_epoch(dict(model, flags=model["flags"] | ntp.NTP_M_OVERLAP, chunks=2), Xd, yd, md, W0d, W1d)
+
+
 def test_epoch_host_inputs_same_result():
     a, W0a, W1a, _, _ = _train_gpu("tiny_dir", 2)
     b, W0b, W1b, _, _ = _train_gpu("tiny_dir", 2, host_inputs=True)

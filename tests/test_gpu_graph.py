@@ -50,6 +50,14 @@ def test_generate_rmat_graph_bit_exact(name):
     _check_graph(ctx, oracle_graph(name))
 
 
+@pytest.mark.parametrize("name", ["cora", "tiny_sym", "tiny_dir", "small_appnp", "small_dir"])
+def test_reordered_graph_is_invisible(name):
+    """NTP_G_REORDER stores the graph under a degree-ordered numbering; everything read back
+    through the ABI (CSR both ways, degrees, D~^{-1/2}) is still in original ids, bit-exact."""
+    ctx = ntp_ctx_for(name, reorder=True)
+    _check_graph(ctx, oracle_graph(name))
+
+
 def test_load_graph_and_build_graph(ntp):
     g = oracle_graph("small_dir")
     ctx = ntp.Context()
@@ -65,6 +73,10 @@ def test_load_graph_and_build_graph(ntp):
     _check_graph(ctx, oracle.graph.build_graph(src, dst, 600, True))
     ctx.build_graph(src, dst, 600, symmetric=False)
     _check_graph(ctx, oracle.graph.build_graph(src, dst, 600, False))
+    ctx.build_graph(src, dst, 600, symmetric=False, reorder=True)
+    _check_graph(ctx, oracle.graph.build_graph(src, dst, 600, False))
+    ctx.load_graph(g.row_ptr, g.col, g.n, symmetric=False, reorder=True)
+    _check_graph(ctx, g)
 
 
 def test_degenerate_graphs(ntp):

@@ -48,6 +48,39 @@ def test_fp32_parity(name, d, transposed):
     assert_r10(Zd.cpu().numpy()[:g.n], ref, den, FP32_TOL, f"{name} d={d} T={transposed}")
 
 
+@pytest.mark.parametrize("name", ["cora", "tiny_dir", "small_appnp", "small_dir"])
+@pytest.mark.parametrize("d", [8, 44, 132])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_fp32_parity_reordered(name, d, transposed):
+    """Degree-ordered internal numbering (NTP_G_REORDER): same oracle parity, slices in and out
+    in original vertex order."""
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name, reorder=True)
+    H = _features(g.n, d, 300 + d)
+    Zd, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+    f = oracle.propagate.propagate_bwd if transposed else oracle.propagate.propagate_fwd
+    ref = f(g, H, cfg.K, cfg.gamma, cfg.alpha)
+    den = cond_bound(g, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+    assert_r10(Zd.cpu().numpy()[:g.n], ref, den, FP32_TOL, f"reordered {name} d={d} T={transposed}")
+
+
+def test_reordered_bf16_and_slices():
+    name = "small_appnp"
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name, reorder=True)
+    H = _features(g.n, 48, 77)
+    Zd, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, dtype=torch.bfloat16)
+    ref = oracle.propagate.propagate_fwd(g, H, cfg.K, cfg.gamma, cfg.alpha)
+    den = cond_bound(g, H, cfg.K, cfg.gamma, cfg.alpha)
+    assert_r10(Zd.float().cpu().numpy()[:g.n], ref, den, BF16_TOL, "reordered bf16")
+    # column slices are still bitwise equal to the full-width result
+    Zfull, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha)
+    Zs, _ = _run(ctx, np.ascontiguousarray(H[:, 8:24]), cfg.K, cfg.gamma, cfg.alpha)
+    assert torch.equal(Zs, Zfull[:, 8:24])
+
+
 @pytest.mark.parametrize("K,gamma,alpha", [(0, 1.0, 0.0), (1, 1.0, 0.0), (1, 0.5, 0.5), (3, 0.9, 0.1),
                                            (10, 0.9, 0.1), (7, 1.0, 0.0)])
 def test_fp32_K_gamma_alpha(K, gamma, alpha):
