@@ -175,6 +175,19 @@ ntp_status ntp_propagate_fwd(ntp_ctx* ctx, const ntp_tensor* H, ntp_tensor* Z, i
 ntp_status ntp_propagate_bwd(ntp_ctx* ctx, const ntp_tensor* G, ntp_tensor* dH, int K,
                              float gamma, float alpha, ntp_stream s);
 
+/* Vertex-layout propagation pipeline (a3 -> a4 -> a5, or a7 -> a8 -> a9 when `transposed`;
+ * Alg. 1 lines 9-12 / 22-25): this rank's rows Hv [V_p x w] (fp32,
+ * DEVICE, caller-owned) are split into feature slices with the column-side D~^{-1/2}
+ * pre-scale fused into the pack (one all-to-all), propagated K >= 1 hops in storage dtype
+ * `dt` (fp32 accumulation), and gathered back into Zv [V_p x w] (fp32).  flags & NTP_M_OVERLAP:
+ * the last hop runs per (peer block, sub-chunk) -- `chunks` sub-chunks per block -- and each
+ * finished chunk is exchanged on the comm stream while the next computes (a12, P:855,
+ * Fig. 7(c)); arithmetic is identical either way.  Collective-bearing: every rank calls
+ * it with the same arguments.  NTP_ERR_CONFIG for NTP_M_OVERLAP on an NTP_G_REORDER graph. */
+ntp_status ntp_propagate_pipeline(ntp_ctx* ctx, const ntp_tensor* Hv, ntp_tensor* Zv, int K,
+                                  float gamma, float alpha, int transposed, ntp_dtype dt,
+                                  int32_t chunks, uint32_t flags, ntp_stream s);
+
 /* ------------------------------------------------------ MLP contraction (a2, a10) */
 
 /* C[M x N] = op(A) op(B) on the tensor cores (tcgen05 kind::tf32, 3xTF32 split: fp32-level

@@ -451,6 +451,27 @@ ntp_status ntp_propagate_bwd(ntp_ctx* c, const ntp_tensor* G, ntp_tensor* dH, in
     return do_propagate(c, G, dH, K, gamma, alpha, s, true);
 }
 
+ntp_status ntp_propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K, float gamma, float alpha,
+                                  int transposed, ntp_dtype dt, int32_t chunks, uint32_t flags, ntp_stream st) {
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    check_tensor(Hv, "Hv", false);
+    check_tensor(Zv, "Zv", false);
+    NTP_CHECK(Hv->dtype == NTP_F32 && Zv->dtype == NTP_F32, NTP_ERR_SHAPE, "Hv, Zv must be fp32");
+    NTP_CHECK(dt == NTP_F32 || dt == NTP_BF16, NTP_ERR_ARG, "bad storage dtype");
+    const int64_t V_p = cdiv(c->g.n, c->world);
+    NTP_CHECK(Hv->rows >= V_p && Zv->rows >= V_p && Hv->cols == Zv->cols && Hv->cols > 0, NTP_ERR_SHAPE,
+              "Hv, Zv must be [>= V_p x w], same w");
+    NTP_CHECK(Hv->data != Zv->data, NTP_ERR_ARG, "Zv must not alias Hv");
+    NTP_CHECK(K >= 1, NTP_ERR_ARG, "K >= 1");
+    NTP_CHECK(gamma > 0.f && gamma <= 1.f && alpha >= 0.f && alpha < 1.f, NTP_ERR_ARG, "gamma in (0,1], alpha in [0,1)");
+    NTP_CHECK(chunks >= 1, NTP_ERR_ARG, "chunks >= 1");
+    NTP_CUDA(cudaSetDevice(c->device));
+    propagate_pipeline(c, Hv, Zv, K, gamma, alpha, transposed != 0, dt, chunks, (flags & NTP_M_OVERLAP) != 0,
+                       (cudaStream_t)st);
+    NTP_API_END(c)
+}
+
 // ------------------------------------------------------------------ MLP GEMM
 ntp_status ntp_gemm_f32(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int trans_a,
                         const float* B, int64_t ldb, int trans_b, float* C, int64_t ldc, int epilogue,

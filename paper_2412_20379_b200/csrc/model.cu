@@ -270,8 +270,17 @@ static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool
         alltoall_blocks(c, a.Z, recv, V_p * d_s, a.dtype, s);
         return;
     }
+    // the chunked gather writes `recv` while later chunks of the last hop still read S^0 for the
+    // alpha term: when they are the same buffer, keep S^0 in a copy
+    PropArgs ao = a;
+    if (a.alpha != 0.f && recv == a.H) {
+        const size_t bytes = (size_t)V_pad * a.ld_h * es;
+        c->prop_s0.ensure(bytes + 16);
+        NTP_CUDA(cudaMemcpyAsync(c->prop_s0.p, a.H, bytes, cudaMemcpyDeviceToDevice, s));
+        ao.H = c->prop_s0.p;
+    }
     LastHop lh;
-    propagate(c, a, s, timed, true, &lh);
+    propagate(c, ao, s, timed, true, &lh);
     const int64_t csz = cdiv(V_p, std::max(chunks, 1));
     const ncclDataType_t t = a.dtype == NTP_BF16 ? ncclBfloat16 : ncclFloat32;
     char* zf = static_cast<char*>(a.Z);
@@ -555,6 +564,48 @@ void drop_epoch_graph(ntp_ctx* c) {
 // key (model + every pointer it bakes in) and replayed afterwards: one launch instead of ~60, so
 // the GPU does not idle while the host re-issues the epoch.  Any eager call invalidates the graph
 // (it may have grown scratch buffers the graph points into).  NTP_GRAPH=0 disables capture.
+// Vertex-layout pipeline (a3 -> a4 -> a5; transposed: a7 -> a8 -> a9): this rank's rows Hv [V_p x w]
+// (fp32) -> pack with the column-side pre-scale + block exchange -> K hops on the feature slice
+// (storage dtype dt) -> gather (chunked and overlapped with the last hop when `overlap`) -> Zv.
+void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K, float gamma, float alpha,
+                        bool transposed, ntp_dtype dt, int chunks, bool overlap, cudaStream_t user) {
+    const Graph& g = c->g;
+    NTP_CHECK(!(overlap && g.reordered), NTP_ERR_CONFIG,
+              "the overlapped gather sends last-hop chunks by destination block: needs a graph without NTP_G_REORDER");
+    cudaStream_t s = c->s_comp;
+    const int32_t P = c->world;
+    const int64_t n = g.n;
+    const int64_t V_p = cdiv(n, P);
+    const int64_t row0 = (int64_t)c->rank * V_p;
+    const int32_t w = Hv->cols;
+    const int32_t d_s = slice_width(w, P, dt, c->slice_align);
+    const size_t es = esize(dt);
+    const int64_t feat = (int64_t)P * V_p * d_s;
+    c->send.ensure((size_t)feat * es + 16);
+    c->recv.ensure((size_t)feat * es + 16);
+    c->xfer.ensure((size_t)feat * es + 16);
+    NTP_CUDA(cudaEventRecord(c->ev[40], user));
+    NTP_CUDA(cudaStreamWaitEvent(s, c->ev[40], 0));
+    const float* cs = transposed ? g.dinv_in_orig() : g.dinv_out_orig();   // column side of this direction
+    pack_v2f(c, Hv->data, Hv->ld, w, c->send.p, V_p, d_s, P, cs, row0, n, NTP_F32, dt, s);
+    alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    PropArgs a{};
+    a.H = c->recv.p;
+    a.Z = c->xfer.p;
+    a.ld_h = d_s;
+    a.ld_z = d_s;
+    a.cols = d_s;
+    a.dtype = dt;
+    a.K = K;
+    a.gamma = gamma;
+    a.alpha = alpha;
+    a.transposed = transposed;
+    propagate_and_gather(c, a, c->send.p, overlap, chunks, V_p, d_s, false, s);
+    unpack_f2v(c, c->send.p, V_p, d_s, P, Zv->data, Zv->ld, w, dt, NTP_F32, s);
+    NTP_CUDA(cudaEventRecord(c->ev[41], s));
+    NTP_CUDA(cudaStreamWaitEvent(user, c->ev[41], 0));
+}
+
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user) {
     const Graph& g = c->g;

@@ -197,6 +197,8 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops = f
                bool prescaled_input = false, LastHop* defer_last = nullptr);
 void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi, cudaStream_t s, bool time_hops);
 double collect_hop_ms(ntp_ctx* c, int* n_hops);
+void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K, float gamma, float alpha,
+                        bool transposed, ntp_dtype dt, int chunks, bool overlap, cudaStream_t user);
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
 void drop_epoch_graph(ntp_ctx* c);

@@ -34,8 +34,8 @@ PHASES = ["mlp_fwd", "v2f_fwd", "prop_fwd", "f2v_fwd", "loss", "v2f_bwd", "prop_
 EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_unique_id", "ntp_create",
             "ntp_destroy", "ntp_load_graph", "ntp_build_graph", "ntp_generate_rmat", "ntp_rmat_arcs",
             "ntp_graph_info", "ntp_copy_csr", "ntp_copy_dinv", "ntp_partition", "ntp_scatter_features",
-            "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd", "ntp_gemm_f32",
-            "ntp_train_epoch"]
+            "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd",
+            "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch"]
 
 
 class ntp_tensor(C.Structure):
@@ -83,6 +83,8 @@ _sig = {
     "ntp_layout_f2v": ([_vp, C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), _vp], C.c_int),
     "ntp_propagate_fwd": ([_vp, C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), C.c_int, _f, _f, _vp], C.c_int),
     "ntp_propagate_bwd": ([_vp, C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), C.c_int, _f, _f, _vp], C.c_int),
+    "ntp_propagate_pipeline": ([_vp, C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), C.c_int, _f, _f, C.c_int, C.c_int,
+                                C.c_int32, C.c_uint32, _vp], C.c_int),
     "ntp_gemm_f32": ([_vp, _i64, _i64, _i64, _vp, _i64, C.c_int, _vp, _i64, C.c_int, _vp, _i64, C.c_int, _vp],
                      C.c_int),
     "ntp_train_epoch": ([_vp, C.POINTER(ntp_model), C.POINTER(ntp_tensor), _vp, _vp, C.POINTER(ntp_tensor),
@@ -255,6 +257,14 @@ class Context:
     def propagate_bwd(self, G, dH, K: int, gamma: float = 1.0, alpha: float = 0.0, stream=None):
         a, b = as_ntp_tensor(G, NTP_LAYOUT_FEATURE), as_ntp_tensor(dH, NTP_LAYOUT_FEATURE)
         self._chk(_lib.ntp_propagate_bwd(self._h, C.byref(a), C.byref(b), K, gamma, alpha, _stream_ptr(stream)))
+
+    def propagate_pipeline(self, Hv, Zv, K: int, gamma: float = 1.0, alpha: float = 0.0, transposed: bool = False,
+                           dtype: int = None, chunks: int = 1, overlap: bool = False, stream=None):
+        """Vertex rows -> split -> K hops -> gather (ntp_propagate_pipeline); dtype = slice storage."""
+        a, b = as_ntp_tensor(Hv, NTP_LAYOUT_VERTEX), as_ntp_tensor(Zv, NTP_LAYOUT_VERTEX)
+        dt = NTP_F32 if dtype is None else dtype
+        self._chk(_lib.ntp_propagate_pipeline(self._h, C.byref(a), C.byref(b), K, gamma, alpha, int(transposed), dt,
+                                              chunks, NTP_M_OVERLAP if overlap else 0, _stream_ptr(stream)))
 
     # -------------------------------------------------------------- MLP GEMM
     def gemm(self, A, B, C, trans_a=False, trans_b=False, relu=False, stream=None):

@@ -87,6 +87,29 @@ def main(name):
         torch.cuda.synchronize()
         assert torch.equal(Z1[:, rank * d_s:(rank + 1) * d_s], Zt[:n]), f"P-invariance rank {rank}"
 
+    # ---- 2b. vertex-layout pipeline (split -> K hops -> gather), overlap off / on: vs the oracle
+    # on this rank's rows, and bitwise equal to each other
+    wv = 37
+    Hfull = synth.features(13, n, wv)
+    V_p = part["V_p"]
+    Hv = np.zeros((V_p, wv), np.float32)
+    lo, hi = rank * V_p, min(n, (rank + 1) * V_p)
+    Hv[:hi - lo] = Hfull[lo:hi]
+    outs = []
+    for transposed in (False, True):
+        of = oracle.propagate.propagate_bwd if transposed else oracle.propagate.propagate_fwd
+        ref = of(g, Hfull, cfg.K, cfg.gamma, cfg.alpha)[lo:hi]
+        den = of(g, np.abs(Hfull), cfg.K, cfg.gamma, cfg.alpha)[lo:hi]
+        for overlap in (False, True):
+            Zv = torch.zeros(V_p, wv, device="cuda")
+            ctx.propagate_pipeline(torch.from_numpy(Hv).cuda(), Zv, cfg.K, cfg.gamma, cfg.alpha,
+                                   transposed=transposed, chunks=3, overlap=overlap)
+            torch.cuda.synchronize()
+            z = Zv.double().cpu().numpy()[:hi - lo]
+            assert (np.abs(z - ref) <= 1e-5 * den + 1e-30).all(), f"pipeline parity rank {rank} T={transposed}"
+            outs.append(Zv.cpu())
+        assert torch.equal(outs[-2], outs[-1]), f"pipeline overlap changed bits rank {rank} T={transposed}"
+
     # ---- 3. epochs, overlap off / on
     X, y, m = pd.rank_inputs(cfg, world, rank)
     W0h, W1h = synth.model_weights(cfg)
