@@ -184,6 +184,9 @@ def main():
                     help="chunked last hop with the gather on the comm stream (a12); off by default: on "
                          "reddit the gather moves ~1-10 MB and chunking costs more than it hides")
     ap.add_argument("--slice-align", type=int, default=16)
+    ap.add_argument("--layouts", default="nccl", choices=["p2p", "nccl"],
+                    help="P > 1 layout changes: the NCCL block all-to-all (default) or peer-direct stores into the "
+                         "owners' IPC windows (NTP_M_P2P_LAYOUTS; measured no faster)")
     ap.add_argument("--reorder", default="auto", choices=["auto", "on", "off"],
                     help="NTP_G_REORDER (internal degree-class numbering). auto: on when the vertex table is "
                          "far larger than L2 (n >= 1M: products, orkut, papers), off for the L2-resident Reddit "
@@ -245,7 +248,8 @@ def main():
     msk = torch.from_numpy(mh).cuda()
     W0 = torch.from_numpy(W0h).cuda()
     W1 = torch.from_numpy(W1h).cuda()
-    flags = (ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if args.overlap else 0)
+    flags = ((ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if args.overlap else 0)
+             | (ntp.NTP_M_P2P_LAYOUTS if args.layouts == "p2p" else 0))
     model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=cfg.lr,
                  dtype=dt, chunks=args.chunks, flags=flags)
     stream = torch.cuda.current_stream()
@@ -327,6 +331,8 @@ def main():
                        "gamma": cfg.gamma, "alpha": cfg.alpha, "P": world, "d_s": d_s, "V_p": V_p,
                        "chunks": args.chunks, "overlap": bool(args.overlap),
                        "vertex_order": "degree-ordered internally (NTP_G_REORDER)" if reorder else "R-MAT ids",
+                       "layouts": ("peer-direct IPC stores" if args.layouts == "p2p" and not args.overlap
+                                   else "NCCL all-to-all") if world > 1 else "local",
                        "l2": f"inputs larger than L2 (col_idx {4 * nnz / 1e6:.0f} MB streamed per hop; "
                              f"X_v {Xh.nbytes / 1e6:.0f} MB per rank)",
                        "graph_setup_s": round(t_graph, 3)},

@@ -206,6 +206,11 @@ ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const flo
 #define NTP_M_OVERLAP       2u  /* chunked last hop with the gather on a comm stream (a12) */
 #define NTP_M_HOST_INPUTS   4u  /* X_v/labels_v/train_mask_v are HOST (pinned) pointers;
                                    copied to the device inside the call (e2e path)       */
+#define NTP_M_P2P_LAYOUTS   8u  /* P > 1: peer-direct layout changes instead of the NCCL block
+                                   all-to-all: the producers (pack, last-hop epilogue, loss
+                                   kernel) store into the owners' CUDA-IPC windows over
+                                   NVLink and a barrier replaces each exchange; same bits.
+                                   Opt-in: measured no faster than NCCL */
 
 typedef struct {
     int32_t   d_in, hid, C, K;

@@ -170,6 +170,7 @@ void ntp_destroy(ntp_ctx* c) {
     if (c->s_comp) cudaStreamSynchronize(c->s_comp);
     if (c->s_comm) cudaStreamSynchronize(c->s_comm);
     drop_epoch_graph(c);
+    p2p_shutdown(c);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->blas) cublasDestroy(c->blas);
     for (auto& e : c->ev)

@@ -10,6 +10,8 @@
 //   columns of rank p for my rows) -> unpack into [V_p x w].
 // Pure data movement (plus the optional pre-scale): gather(split(x)) == x bitwise.
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 
 #include "ntp_internal.cuh"
 
@@ -54,7 +56,7 @@ template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) pack_v2f_kernel(const Tin* __restrict__ Hv, int64_t ld_v, int32_t w,
                                                        Tout* __restrict__ send, int64_t V_p, int32_t d_s, int32_t P,
                                                        const float* __restrict__ row_scale, int64_t row0, int64_t n,
-                                                       int vec) {
+                                                       int vec, void* const* __restrict__ peer, int rank) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int wpad = P * d_s;
@@ -76,9 +78,16 @@ __global__ void __launch_bounds__(256) pack_v2f_kernel(const Tin* __restrict__ H
                 for (int i = 0; i < 4; ++i) x[i] *= sc;
             }
             const int q = k / d_s;
-            Q4<Tout>::st(send + ((int64_t)q * V_p + v) * d_s + (k - q * d_s), x);
+            // peer-direct split: block q lands in rank q's window as block `rank` (row row0 + v of
+            // q's feature slice) -- the all-to-all fused into the pack
+            Tout* dst = peer ? static_cast<Tout*>(peer[q]) + ((int64_t)rank * V_p + v) * d_s + (k - q * d_s)
+                             : send + ((int64_t)q * V_p + v) * d_s + (k - q * d_s);
+            Q4<Tout>::st(dst, x);
         }
     }
+#ifndef NTP_NO_P2P_FENCE
+    if (peer) __threadfence_system();
+#endif
 }
 
 // One warp per vertex row: columns [4k, 4k+4) of the row come from block q = 4k / d_s of `recv`.
@@ -112,7 +121,6 @@ __global__ void __launch_bounds__(256) unpack_f2v_kernel(const Tin* __restrict__
     }
 }
 
-int blocks_for(int64_t total) { return (int)std::min<int64_t>(std::max<int64_t>(cdiv(total, 256), 1), 148 * 16); }
 int row_blocks(int64_t rows) { return (int)std::min<int64_t>(std::max<int64_t>(cdiv(rows, 8), 1), 148 * 16); }
 template <typename T> bool quad_ok(const void* p, int64_t ld) {
     return (reinterpret_cast<uintptr_t>(p) % (4 * sizeof(T))) == 0 && (ld % 4) == 0;
@@ -121,21 +129,23 @@ template <typename T> bool quad_ok(const void* p, int64_t ld) {
 }  // namespace
 
 void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, int64_t V_p, int32_t d_s, int32_t P,
-              const float* row_scale, int64_t row0, int64_t n, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s) {
+              const float* row_scale, int64_t row0, int64_t n, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s,
+              void* const* peer) {
+    const int rk = c->rank;
     if (V_p == 0 || d_s == 0) return;
     const int b = row_blocks(V_p);
     const int vec = (dt_in == NTP_F32) ? quad_ok<float>(Hv, ld_v) : quad_ok<__nv_bfloat16>(Hv, ld_v);
     if (dt_in == NTP_F32 && dt_out == NTP_F32)
-        pack_v2f_kernel<float, float><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (float*)send, V_p, d_s, P, row_scale, row0, n, vec);
+        pack_v2f_kernel<float, float><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (float*)send, V_p, d_s, P, row_scale, row0, n, vec, peer, rk);
     else if (dt_in == NTP_F32 && dt_out == NTP_BF16)
         pack_v2f_kernel<float, __nv_bfloat16><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (__nv_bfloat16*)send, V_p, d_s, P,
-                                                                row_scale, row0, n, vec);
+                                                                row_scale, row0, n, vec, peer, rk);
     else if (dt_in == NTP_BF16 && dt_out == NTP_BF16)
         pack_v2f_kernel<__nv_bfloat16, __nv_bfloat16><<<b, 256, 0, s>>>((const __nv_bfloat16*)Hv, ld_v, w,
-                                                                        (__nv_bfloat16*)send, V_p, d_s, P, row_scale, row0, n, vec);
+                                                                        (__nv_bfloat16*)send, V_p, d_s, P, row_scale, row0, n, vec, peer, rk);
     else
         pack_v2f_kernel<__nv_bfloat16, float><<<b, 256, 0, s>>>((const __nv_bfloat16*)Hv, ld_v, w, (float*)send, V_p, d_s,
-                                                                P, row_scale, row0, n, vec);
+                                                                P, row_scale, row0, n, vec, peer, rk);
     NTP_LAUNCH_CHECK();
     count_launch(c);
 }
@@ -157,6 +167,96 @@ void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t 
         unpack_f2v_kernel<float, __nv_bfloat16><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (__nv_bfloat16*)Hv, ld_v, w, vec, keep, ld_keep);
     NTP_LAUNCH_CHECK();
     count_launch(c);
+}
+
+// ---------------------------------------------------------------- peer-direct layouts
+// Each rank exposes two windows by CUDA IPC: the split target ([P][V_p][d_s]: the feature slice the
+// hops read) and the gather target ([P][V_p][d_s]: the last hop's rows for this rank's vertices).
+// Producers store straight into the owner's window over NVLink (pack for the split, the last
+// hop's epilogue for the gather, the loss kernel for the gradient split); a stream-ordered barrier
+// (1-int allreduce) after each producer replaces the all-to-all.  Handles are exchanged with the
+// library's own NCCL communicator whenever a window has to grow (collective, outside capture).
+void p2p_barrier(ntp_ctx* c, cudaStream_t s) {
+    NTP_NCCL(ncclAllReduce(c->p2p_bar.p, c->p2p_bar.p, 1, ncclInt32, ncclSum, c->comm, s));
+}
+
+static void p2p_close(ntp_ctx* c) {
+    for (int q = 0; q < (int)c->p2p_peer_split.size(); ++q) {
+        if (q == c->rank) continue;
+        if (c->p2p_peer_split[q]) cudaIpcCloseMemHandle(c->p2p_peer_split[q]);
+        if (c->p2p_peer_gath[q]) cudaIpcCloseMemHandle(c->p2p_peer_gath[q]);
+    }
+    c->p2p_peer_split.clear();
+    c->p2p_peer_gath.clear();
+}
+
+void p2p_shutdown(ntp_ctx* c) { p2p_close(c); }
+
+bool p2p_ensure(ntp_ctx* c, size_t sb, size_t gb, cudaStream_t s) {
+    const int P = c->world;
+    static const bool enabled = [] { const char* e = getenv("NTP_P2P"); return !(e && atoi(e) == 0); }();
+    if (P <= 1 || c->p2p_state < 0 || !enabled) return false;
+    if (c->p2p_state == 1 && sb <= c->p2p_split_bytes && gb <= c->p2p_gath_bytes) return true;
+    if (c->capturing) return false;
+    c->p2p_bar.ensure(16);
+    NTP_CUDA(cudaMemsetAsync(c->p2p_bar.p, 0, 16, s));
+    p2p_barrier(c, s);                         // nobody writes into the old windows any more
+    NTP_CUDA(cudaStreamSynchronize(s));
+    p2p_close(c);
+    const size_t nsb = std::max(sb, c->p2p_split_bytes), ngb = std::max(gb, c->p2p_gath_bytes);
+    c->p2p_split.release();
+    c->p2p_gath.release();
+    c->p2p_split.ensure(nsb);
+    c->p2p_gath.ensure(ngb);
+    NTP_CUDA(cudaMemsetAsync(c->p2p_split.p, 0, nsb, s));   // padding rows are never written
+    NTP_CUDA(cudaMemsetAsync(c->p2p_gath.p, 0, ngb, s));
+    cudaIpcMemHandle_t own[2];
+    NTP_CUDA(cudaIpcGetMemHandle(&own[0], c->p2p_split.p));
+    NTP_CUDA(cudaIpcGetMemHandle(&own[1], c->p2p_gath.p));
+    const size_t hb = sizeof(own);
+    DevBuf dh;
+    dh.ensure(hb * (P + 1));
+    NTP_CUDA(cudaMemcpyAsync(static_cast<char*>(dh.p) + hb * P, own, hb, cudaMemcpyHostToDevice, s));
+    NTP_NCCL(ncclAllGather(static_cast<char*>(dh.p) + hb * P, dh.p, hb, ncclUint8, c->comm, s));
+    std::vector<cudaIpcMemHandle_t> all(2 * P);
+    NTP_CUDA(cudaMemcpyAsync(all.data(), dh.p, hb * P, cudaMemcpyDeviceToHost, s));
+    NTP_CUDA(cudaStreamSynchronize(s));
+    c->p2p_peer_split.assign(P, nullptr);
+    c->p2p_peer_gath.assign(P, nullptr);
+    int ok = 1;
+    for (int q = 0; q < P; ++q) {
+        if (q == c->rank) {
+            c->p2p_peer_split[q] = c->p2p_split.p;
+            c->p2p_peer_gath[q] = c->p2p_gath.p;
+            continue;
+        }
+        if (cudaIpcOpenMemHandle(&c->p2p_peer_split[q], all[2 * q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&c->p2p_peer_gath[q], all[2 * q + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+        }
+    }
+    // every rank must take the same path: agree on the minimum
+    NTP_CUDA(cudaMemcpyAsync(dh.p, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+    NTP_NCCL(ncclAllReduce(dh.p, dh.p, 1, ncclInt32, ncclMin, c->comm, s));
+    NTP_CUDA(cudaMemcpyAsync(&ok, dh.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NTP_CUDA(cudaStreamSynchronize(s));
+    if (!ok) {
+        p2p_close(c);
+        c->p2p_state = -1;
+        return false;
+    }
+    std::vector<void*> tab(2 * P);
+    for (int q = 0; q < P; ++q) {
+        tab[q] = c->p2p_peer_split[q];
+        tab[P + q] = c->p2p_peer_gath[q];
+    }
+    c->p2p_tab.ensure(2 * P * sizeof(void*));
+    NTP_CUDA(cudaMemcpy(c->p2p_tab.p, tab.data(), 2 * P * sizeof(void*), cudaMemcpyHostToDevice));
+    c->p2p_split_bytes = nsb;
+    c->p2p_gath_bytes = ngb;
+    c->p2p_state = 1;
+    return true;
 }
 
 // Block exchange: block q of `send` goes to rank q and lands as block `rank` of

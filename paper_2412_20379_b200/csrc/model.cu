@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
                                                            const uint8_t* __restrict__ mask, int64_t row0, int64_t n,
                                                            TOut* __restrict__ out, int out_blocked,
                                                            const float* __restrict__ gscale, double* __restrict__ part,
-                                                           int64_t* __restrict__ cnt, int64_t ld_plain) {
+                                                           int64_t* __restrict__ cnt, int64_t ld_plain,
+                                                           void* const* __restrict__ peer, int rank) {
     constexpr int MAXK = 8;
     constexpr int RPB = 256 / LPR;                     // rows per block
     __shared__ double s_loss[RPB];
@@ -113,13 +114,19 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const TIn* __restrict
                 const float gval = train ? (x[k] * inv - (col == yv ? 1.f : 0.f)) * sc : 0.f;
                 if (out_blocked) {
                     const int q = col / d_s;
-                    stf<TOut>(out + ((int64_t)q * V_p + v) * d_s + (col - q * d_s), gval);
+                    // peer-direct: straight into rank q's split window (the gradient v2f fused in)
+                    TOut* dst = peer ? static_cast<TOut*>(peer[q]) + ((int64_t)rank * V_p + v) * d_s + (col - q * d_s)
+                                     : out + ((int64_t)q * V_p + v) * d_s + (col - q * d_s);
+                    stf<TOut>(dst, gval);
                 } else {
                     stf<TOut>(out + v * ld_plain + col, gval);
                 }
             }
         }
     }
+#ifndef NTP_NO_P2P_FENCE
+    if (peer) __threadfence_system();
+#endif
     if (sub == 0) {
         s_loss[rloc] = my_loss;
         s_cnt[rloc] = my_cnt;
@@ -142,13 +149,14 @@ template <typename TIn, typename TOut>
 int64_t launch_softmax_xent(ntp_ctx* c, const TIn* in, int in_blocked, int64_t V_p, int32_t d_s, int32_t C,
                             const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n, TOut* out,
                             int out_blocked, const float* gscale, double* part, int64_t* cnt, int64_t ld_plain,
-                            cudaStream_t s) {
+                            cudaStream_t s, void* const* peer = nullptr) {
     NTP_CHECK(C <= 256, NTP_ERR_CONFIG, "C = %d > 256 classes is not supported", C);
     int64_t nb;
 #define NTP_LOSS_LAUNCH(LPR)                                                                                    \
     nb = std::min<int64_t>(std::max<int64_t>(cdiv(V_p, 256 / LPR), 1), 148 * 8);                              \
     softmax_xent_kernel<TIn, TOut, LPR><<<(unsigned)nb, 256, 0, s>>>(in, in_blocked, V_p, d_s, C, y, mask, row0, n, \
-                                                                     out, out_blocked, gscale, part, cnt, ld_plain)
+                                                                     out, out_blocked, gscale, part, cnt, ld_plain, \
+                                                                     peer, c->rank)
     if (C <= 32) { NTP_LOSS_LAUNCH(4); }
     else if (C <= 64) { NTP_LOSS_LAUNCH(8); }
     else if (C <= 128) { NTP_LOSS_LAUNCH(16); }
@@ -161,14 +169,21 @@ int64_t launch_softmax_xent(ntp_ctx* c, const TIn* in, int in_blocked, int64_t V
 
 // Zero the padded gradient columns [C, P*d_s) of blocked output (left untouched by the loss kernel).
 template <typename T>
-__global__ void zero_pad_cols_kernel(T* __restrict__ buf, int64_t V_p, int32_t d_s, int32_t P, int32_t C) {
+__global__ void zero_pad_cols_kernel(T* __restrict__ buf, int64_t V_p, int32_t d_s, int32_t P, int32_t C,
+                                     void* const* __restrict__ peer, int rank) {
     const int32_t pad = P * d_s - C;
     const int64_t total = V_p * pad;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / pad;
         const int32_t col = C + (int32_t)(i % pad);
-        stf<T>(buf + ((int64_t)(col / d_s) * V_p + v) * d_s + col % d_s, 0.f);
+        const int32_t q = col / d_s;
+        T* dst = peer ? static_cast<T*>(peer[q]) + ((int64_t)rank * V_p + v) * d_s + col % d_s
+                      : buf + ((int64_t)q * V_p + v) * d_s + col % d_s;
+        stf<T>(dst, 0.f);
     }
+#ifndef NTP_NO_P2P_FENCE
+    if (peer) __threadfence_system();
+#endif
 }
 
 // Fixed-order sum of block partials -> scal[0] = loss_sum, scal[1] = n_train (as double).
@@ -438,17 +453,31 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     }
     NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd done
 
+    // Peer-direct layouts (NTP_M_P2P_LAYOUTS, P > 1, CUDA IPC available): the producers store into
+    // the owners' windows and a barrier replaces each all-to-all; otherwise the NCCL block exchange.
+    const bool overlap = (m->flags & NTP_M_OVERLAP) != 0;
+    const size_t win = (size_t)feat_elems * es;
+    const bool p2p = !overlap && (m->flags & NTP_M_P2P_LAYOUTS) && p2p_ensure(c, win, win, s);
+    void* const* tab_split = p2p ? c->p2p_tab.as<void*>() : nullptr;
+    void* const* tab_gath = p2p ? c->p2p_tab.as<void*>() + P : nullptr;
+    void* slice_in = p2p ? c->p2p_split.p : c->recv.p;   // this rank's feature slice after a split
+
     // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
-    pack_v2f(c, prop_src, ld_src, w, c->send.p, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s);
-    alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    if (p2p) {
+        pack_v2f(c, prop_src, ld_src, w, nullptr, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split);
+        p2p_barrier(c, s);
+    } else {
+        pack_v2f(c, prop_src, ld_src, w, c->send.p, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s);
+        alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    }
     NTP_CUDA(record_timing(c, E[ei++], s));   // E2 v2f done
 
-    // a4 + a5: K forward hops on S^0 = recv (pre-scaled) -> Z^K in xfer, gathered into recv
-    const bool overlap = (m->flags & NTP_M_OVERLAP) != 0;
+    // a4 + a5: K forward hops on S^0 (pre-scaled) -> Z^K, gathered into this rank's rows
     c->hop_ev_used = 0;
+    void* gathered = p2p ? c->p2p_gath.p : c->recv.p;
     {
         PropArgs a{};
-        a.H = c->recv.p;
+        a.H = slice_in;
         a.Z = c->xfer.p;
         a.ld_h = d_s;
         a.ld_z = d_s;
@@ -458,40 +487,46 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = false;
-        propagate_and_gather(c, a, c->recv.p, overlap, m->chunks, V_p, d_s, timed, s);
+        if (p2p) {
+            a.po = PeerOut{tab_gath, V_p, c->rank};
+            propagate(c, a, s, timed, true);
+            p2p_barrier(c, s);
+        } else {
+            propagate_and_gather(c, a, c->recv.p, overlap, m->chunks, V_p, d_s, timed, s);
+        }
     }
     NTP_CUDA(record_timing(c, E[ei++], s));   // E3 prop fwd + f2v done
 
-    // a6: loss + gradient, written straight into the backward split's send buffer
+    // a6: loss + gradient, written straight into the backward split's send buffer (or windows)
     const float* gscale_bwd = g.dinv_in_orig();   // backward column side (original vertex order)
     int64_t nb_loss = 0;
     if (!after) {
         if (dt == NTP_F32)
-            nb_loss = launch_softmax_xent(c, (const float*)c->recv.p, 1, V_p, d_s, m->C, lab, msk, row0, n,
-                                          (float*)c->send.p, 1, gscale_bwd, part, cnt, 0, s);
+            nb_loss = launch_softmax_xent(c, (const float*)gathered, 1, V_p, d_s, m->C, lab, msk, row0, n,
+                                          (float*)c->send.p, 1, gscale_bwd, part, cnt, 0, s, tab_split);
         else
-            nb_loss = launch_softmax_xent(c, (const __nv_bfloat16*)c->recv.p, 1, V_p, d_s, m->C, lab, msk, row0, n,
-                                          (__nv_bfloat16*)c->send.p, 1, gscale_bwd, part, cnt, 0, s);
+            nb_loss = launch_softmax_xent(c, (const __nv_bfloat16*)gathered, 1, V_p, d_s, m->C, lab, msk, row0, n,
+                                          (__nv_bfloat16*)c->send.p, 1, gscale_bwd, part, cnt, 0, s, tab_split);
         if (P * d_s > m->C) {
             if (dt == NTP_F32)
                 zero_pad_cols_kernel<float><<<eblocks(V_p * (P * d_s - m->C)), 256, 0, s>>>((float*)c->send.p, V_p, d_s,
-                                                                                          P, m->C);
+                                                                                          P, m->C, tab_split, c->rank);
             else
                 zero_pad_cols_kernel<__nv_bfloat16><<<eblocks(V_p * (P * d_s - m->C)), 256, 0, s>>>(
-                    (__nv_bfloat16*)c->send.p, V_p, d_s, P, m->C);
+                    (__nv_bfloat16*)c->send.p, V_p, d_s, P, m->C, tab_split, c->rank);
             NTP_LAUNCH_CHECK();
             count_launch(c);
         }
     } else {
-        // Z_v = unpack(recv) [V_p x hid]; logits = Z_v W1; dlogits; dZ_v = dlogits W1^T -> pack
+        // Z_v = unpack(gathered) [V_p x hid]; logits = Z_v W1; dlogits; dZ_v = dlogits W1^T -> pack
         float* Zv = dH1;   // reuse [V_p x ldH]
-        unpack_f2v(c, c->recv.p, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s);
+        unpack_f2v(c, gathered, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s);
         mlp_gemm(c, false, false, V_p, m->C, m->hid, Zv, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
         nb_loss = launch_softmax_xent(c, (const float*)L, 0, V_p, d_s, m->C, lab, msk, row0, n, dL, 0, nullptr, part,
                                       cnt, ldL, s);
         mlp_gemm(c, true, false, m->hid, m->C, V_p, Zv, ldH, dL, ldL, dW1, m->C, s);          // dW1 = Z_v^T dlogits
         mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);  // dZ_v -> L
-        pack_v2f(c, L, ldL, m->hid, c->send.p, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s);
+        pack_v2f(c, L, ldL, m->hid, c->send.p, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s, tab_split);
     }
     reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb_loss, scal);
     NTP_LAUNCH_CHECK();
@@ -499,13 +534,15 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     NTP_CUDA(record_timing(c, E[ei++], s));   // E4 loss done
 
     // a7: split the gradient
-    alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    if (p2p) p2p_barrier(c, s);
+    else alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E5 v2f bwd
 
     // a8 + a9: K backward hops on the split gradient, gathered -> dL^ rows [V_p x w]
+    void* gathered_b = p2p ? c->p2p_gath.p : c->send.p;
     {
         PropArgs a{};
-        a.H = c->recv.p;
+        a.H = slice_in;
         a.Z = c->xfer.p;
         a.ld_h = d_s;
         a.ld_z = d_s;
@@ -515,11 +552,17 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = true;
-        propagate_and_gather(c, a, c->send.p, overlap, m->chunks, V_p, d_s, timed, s);
+        if (p2p) {
+            a.po = PeerOut{tab_gath, V_p, c->rank};
+            propagate(c, a, s, timed, true);
+            p2p_barrier(c, s);
+        } else {
+            propagate_and_gather(c, a, c->send.p, overlap, m->chunks, V_p, d_s, timed, s);
+        }
     }
     float* dLw = after ? dH1 : dL;            // gathered dL^ rows (dH1 before the mask when W1 is applied after)
     const int64_t ld_dLw = after ? ldH : ldL;
-    unpack_f2v(c, c->send.p, V_p, d_s, P, dLw, ld_dLw, w, dt, NTP_F32, s, after ? H1 : nullptr, ldH);
+    unpack_f2v(c, gathered_b, V_p, d_s, P, dLw, ld_dLw, w, dt, NTP_F32, s, after ? H1 : nullptr, ldH);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E6 prop bwd + f2v bwd
 
     // a10: MLP backward (ReLU' mask fused into the dH1 GEMM epilogue)

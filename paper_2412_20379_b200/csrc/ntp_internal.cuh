@@ -139,6 +139,13 @@ struct ntp_ctx {
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
     ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit;
+    // peer-direct layouts (CUDA IPC windows over NVLink), see layout.cu
+    int p2p_state = 0;                      // 0 not set up, 1 usable, -1 unavailable
+    ntp::DevBuf p2p_split, p2p_gath;        // this rank's windows (zero-initialised)
+    size_t p2p_split_bytes = 0, p2p_gath_bytes = 0;
+    std::vector<void*> p2p_peer_split, p2p_peer_gath;   // opened peer mappings (own entry = local)
+    ntp::DevBuf p2p_tab;                    // device: [2][P] pointers (split windows, gather windows)
+    ntp::DevBuf p2p_bar;                    // one int for the barrier allreduce
     cudaEvent_t ev[64] = {};
     cudaEvent_t hop_ev[256] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
     int hop_ev_used = 0;
@@ -166,6 +173,15 @@ void rmat_raw(ntp_ctx* c, int scale, const uint32_t thr[3], uint64_t seed, int64
               int64_t* src, int64_t* dst, cudaStream_t s);
 
 // Propagation on one feature slice (dtype-generic storage, fp32 accumulation).
+// Peer-direct output of a layout-changing producer (P2P stores over NVLink into the peers' IPC
+// windows): row v of the global order goes to rank q = v / V_p, into block `rank` of q's
+// [P][V_p][d_s] window, i.e. element offset (rank * V_p + v - q * V_p) * ld.  tab == nullptr:
+// ordinary local output.
+struct PeerOut {
+    void* const* tab = nullptr;   // device array [P] of window base pointers (own = local)
+    int64_t V_p = 0;
+    int rank = 0;
+};
 struct PropArgs {
     const void* H;          // [n x cols] original input (alpha term)
     void* Z;                // output
@@ -175,6 +191,7 @@ struct PropArgs {
     int K;
     float gamma, alpha;
     bool transposed;        // backward (A^T)
+    PeerOut po;             // last hop: write straight into the peers' gather windows (f2v fused)
 };
 // State needed to run the last hop later, chunk by chunk (overlap scheduler, a12).
 struct LastHop {
@@ -212,7 +229,7 @@ void csr_to_keys(ntp_ctx* c, const int64_t* row_ptr, const int32_t* col, int64_t
 void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, const void* S_in,
               void* S_out, const void* H, int64_t ld_in, int64_t ld_out, int64_t ld_h, int32_t cols,
               ntp_dtype dt, float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi,
-              cudaStream_t s, const int32_t* out_rows = nullptr);
+              cudaStream_t s, const int32_t* out_rows = nullptr, const PeerOut* po = nullptr);
 // S[r] = scale[r] * H[src_rows ? src_rows[r] : r] (scale may be null: plain copy / permutation)
 void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, int32_t cols,
               const float* scale, int64_t rows, ntp_dtype dt, cudaStream_t s,
@@ -221,7 +238,12 @@ void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, in
 // layouts
 void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, int64_t V_p,
               int32_t d_s, int32_t P, const float* row_scale, int64_t row0, int64_t n,
-              ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s);
+              ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s, void* const* peer_tab = nullptr);
+// Peer-direct layouts: IPC windows of this rank ([P][V_p][d_s] split target and gather target),
+// exchanged once per size (collective); false when P2P is unavailable (NCCL all-to-all path).
+bool p2p_ensure(ntp_ctx* c, size_t split_bytes, size_t gather_bytes, cudaStream_t s);
+void p2p_barrier(ntp_ctx* c, cudaStream_t s);   // stream-ordered all-rank barrier (tiny allreduce)
+void p2p_shutdown(ntp_ctx* c);                  // closes the peer mappings (ntp_destroy)
 void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t P, void* Hv,
                 int64_t ld_v, int32_t w, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s,
                 const float* keep = nullptr, int64_t ld_keep = 0);

@@ -134,7 +134,21 @@ struct HopParams {
     int mode;                          // 0 intermediate, 1 last
     int64_t nnz;
     const int32_t* __restrict__ out_rows;   // last hop of a reordered graph: output row r goes to out_rows[r]
+    void* const* __restrict__ peer_out;     // last hop, peer-direct gather: window table [P] (else null)
+    int64_t po_V_p;
+    int po_rank;
 };
+
+// Where output row r (internal order) is stored: its original row (out_rows), locally or -- peer-direct
+// gather -- in block po_rank of the owner's window: the f2v all-to-all fused into the epilogue.
+__device__ __forceinline__ char* out_row_ptr(const HopParams& p, int64_t r) {
+    const int64_t orow = p.out_rows ? (int64_t)__ldg(p.out_rows + r) : r;
+    if (p.peer_out) {
+        const int64_t q = orow / p.po_V_p;
+        return static_cast<char*>(p.peer_out[q]) + ((int64_t)p.po_rank * p.po_V_p + orow - q * p.po_V_p) * p.ld_out;
+    }
+    return p.S_out + orow * p.ld_out;
+}
 
 // Lane layout ("full row per edge"): a group of L lanes works on one unit.  Lane
 // gl = e*VP + c holds edge slot e in [0, E) and VB-byte column vector c in [0, VP):
@@ -231,8 +245,7 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
                         out[i] = (p.alpha != 0.f) ? sig * (tot + self) + beta * (0.f + Vec<T, VB>::elem(s0_raw, i))
                                                   : sig * (tot + self);
                     }
-                    const int64_t orow = p.out_rows ? (int64_t)__ldg(p.out_rows + my_r) : (int64_t)my_r;
-                    if (cok) stv<VB>(p.S_out + orow * p.ld_out + voff, Vec<T, VB>::pack(out));
+                    if (cok) stv<VB>(out_row_ptr(p, my_r) + voff, Vec<T, VB>::pack(out));
                     r += E - 1;
                     continue;
                 }
@@ -346,10 +359,12 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
 #pragma unroll
                 for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + (0.f + Vec<T, VB>::elem(self_raw, i)));
             }
-            const int64_t orow = p.out_rows ? (int64_t)__ldg(p.out_rows + r) : (int64_t)r;
-            stv<VB>(p.S_out + orow * p.ld_out + (int64_t)vcol * VB, Vec<T, VB>::pack(out));
+            stv<VB>(out_row_ptr(p, r) + (int64_t)vcol * VB, Vec<T, VB>::pack(out));
         }
     }
+#ifndef NTP_NO_P2P_FENCE
+    if (p.peer_out) __threadfence_system();
+#endif
 }
 
 // Fix-up: one warp per unit that STARTS a split row (its tail).  Sums tail[u],
@@ -368,7 +383,7 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
     const int row_vals = p.nvec * VALS;
     const float a = p.rs[r];
     const float b = p.cs[r];
-    const int64_t orow = p.out_rows ? (int64_t)p.out_rows[r] : (int64_t)r;
+    char* orow_p = out_row_ptr(p, r);
     for (int k = lane; k < row_vals; k += 32) {
         float acc = p.carry[(u * 2 + 1) * (int64_t)row_vals + k];
         for (int64_t v = u + 1;; ++v) {
@@ -386,11 +401,14 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
             out += ((p.mode == 0) ? p.alpha : p.alpha / b) * h[comp];
         }
         if (sizeof(T) == 4) {
-            reinterpret_cast<float*>(p.S_out + orow * p.ld_out)[k] = out;
+            reinterpret_cast<float*>(orow_p)[k] = out;
         } else {
-            reinterpret_cast<__nv_bfloat16*>(p.S_out + orow * p.ld_out)[k] = __float2bfloat16_rn(out);
+            reinterpret_cast<__nv_bfloat16*>(orow_p)[k] = __float2bfloat16_rn(out);
         }
     }
+#ifndef NTP_NO_P2P_FENCE
+    if (p.peer_out) __threadfence_system();
+#endif
 }
 
 template <typename T>
@@ -467,7 +485,7 @@ static void unit_range(const Csr& csr, int64_t row_lo, int64_t row_hi, int64_t& 
 void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, const void* S_in, void* S_out,
               const void* S0, int64_t ld_in, int64_t ld_out, int64_t ld_s0, int32_t cols, ntp_dtype dt,
               float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi, cudaStream_t s,
-              const int32_t* out_rows) {
+              const int32_t* out_rows, const PeerOut* po) {
     const Graph& g = c->g;
     if (row_hi < 0) row_hi = g.n;
     row_lo = std::max<int64_t>(row_lo, 0);
@@ -492,6 +510,9 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     p.n = g.n;
     p.nnz = g.nnz;
     p.out_rows = out_rows;
+    p.peer_out = (po && po->tab) ? po->tab : nullptr;
+    p.po_V_p = po ? po->V_p : 0;
+    p.po_rank = po ? po->rank : 0;
 
     unit_range(csr, row_lo, row_hi, p.u_begin, p.u_end);
     p.row_lo = row_lo;
@@ -597,7 +618,7 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
         const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
         if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
         spmm_hop(c, csr, rs, cs, sin, bufs[nxt], S0, ld_sin, lds[nxt], ld_s0, a.cols, a.dtype, a.gamma, a.alpha,
-                 last ? 1 : 0, 0, -1, s, last ? inv : nullptr);
+                 last ? 1 : 0, 0, -1, s, last ? inv : nullptr, last ? &a.po : nullptr);
         if (timed) {
             NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used + 1], s));
             c->hop_ev_used += 2;

@@ -116,9 +116,13 @@ def main(name):
     lr = cfg.lr * 50
     ref_losses, _, _ = oracle.model.train(g, *synth.config_inputs(cfg), W0h, W1h, cfg.K, cfg.gamma, cfg.alpha, lr, 3)
     results = []
-    for overlap in (False, True):
+    # peer-direct layouts (producers store into the owners' IPC windows), the NCCL block exchange
+    # (default) and the overlapped NCCL gather: all three bitwise equal
+    for mode in ("p2p", "nccl", "overlap"):
+        overlap = mode == "overlap"
         W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
-        flags = (ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if overlap else 0)
+        flags = ((ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if overlap else 0)
+                 | (ntp.NTP_M_P2P_LAYOUTS if mode == "p2p" else 0))
         model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
                      dtype=ntp.NTP_F32, chunks=3, flags=flags)
         losses = []
@@ -126,10 +130,11 @@ def main(name):
             rep = ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
             losses.append(rep["loss"])
         for a, b in zip(losses, ref_losses):
-            assert abs(a - b) <= 1e-4, f"loss {a} vs oracle {b} (overlap={overlap})"
+            assert abs(a - b) <= 1e-4, f"loss {a} vs oracle {b} (mode={mode})"
         results.append((losses, W0.cpu(), W1.cpu()))
-    assert results[0][0] == results[1][0], "overlap changed the loss"
-    assert torch.equal(results[0][1], results[1][1]) and torch.equal(results[0][2], results[1][2])
+    for k in (1, 2):
+        assert results[0][0] == results[k][0], f"layout mode {k} changed the loss"
+        assert torch.equal(results[0][1], results[k][1]) and torch.equal(results[0][2], results[k][2])
 
     # ---- 4. degree-reordered graph (NTP_G_REORDER): slice propagation bitwise vs P = 1 on the same
     # reordered graph, epochs vs the oracle
@@ -148,7 +153,8 @@ def main(name):
     assert torch.equal(Z1[:, rank * d_s:(rank + 1) * d_s], Zt[:n]), f"reordered P-invariance rank {rank}"
     W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
     model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
-                 dtype=ntp.NTP_F32, chunks=1, flags=ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0)
+                 dtype=ntp.NTP_F32, chunks=1,
+                 flags=(ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | ntp.NTP_M_P2P_LAYOUTS)
     for e in range(3):
         rep = ctxr.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
         assert abs(rep["loss"] - ref_losses[e]) <= 1e-4, f"reordered loss {rep['loss']} vs {ref_losses[e]}"
