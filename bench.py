@@ -108,6 +108,24 @@ def l2_gather_bytes(nnz, n, d_s, elem):
     return (nnz + n) * r
 
 
+def gather_ceiling(n, row_bytes):
+    """Measured random-row-gather ceiling of this B200 (profiles/gather_ceiling.json, written from
+    scripts/l2_probe.cu): rows/s for the table's residency (L2 if the slice fits, else HBM) at the
+    smallest probed row size >= row_bytes."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "gather_ceiling.json")))
+    except Exception:
+        return None
+    tab = d["l2_resident"] if n * row_bytes <= 100e6 else d["hbm_resident"]
+    sizes = sorted(int(k) for k in tab)
+    fit = [k for k in sizes if k >= row_bytes] or sizes[-1:]
+    if not fit:
+        return None
+    k = fit[0]
+    return {"rows_per_s": tab[str(k)]["Grows_per_s"] * 1e9, "probe_row_bytes": k,
+            "residency": "L2" if n * row_bytes <= 100e6 else "HBM", "source": "profiles/gather_ceiling.json"}
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -322,6 +340,12 @@ def main():
         achieved = bh / (spmm_avg * 1e-3) / 1e9
         traffic = load_traffic(args.config, world, dtype_name)
         l2b = l2_gather_bytes(nnz, n, d_s, esz)
+        gc = gather_ceiling(n, d_s * esz)
+        gather_line = None
+        if gc:
+            rows_ps = (nnz + n) / (spmm_avg * 1e-3)
+            gather_line = dict(gc, achieved_rows_per_s=rows_ps, frac=rows_ps / gc["rows_per_s"],
+                               row_bytes=d_s * esz)
         line = {
             "metric": METRIC, "value": ge, "unit": "GE/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -342,8 +366,11 @@ def main():
                          "launches_timed": spmm_n, "peak_source": peak_src,
                          "l2_gather_bytes_per_launch": l2b,
                          "l2_gather_GBps": l2b / (spmm_avg * 1e-3) / 1e9,
-                         "note": "algorithmic bytes = compulsory HBM bytes (DESIGN.md §6); the gathered "
-                                 "slice rows are re-read through L2 (l2_gather_*)"},
+                         "gather": gather_line,
+                         "note": "algorithmic bytes = compulsory HBM bytes (DESIGN.md §6): every array once. The "
+                                 "gathered slice rows are re-read through L2 (l2_gather_*); when the slice is "
+                                 "L2-resident the hop is bound by the random-row gather rate, reported against "
+                                 "its measured ceiling in `gather`"},
             "prop_GE_per_s": 2 * cfg.K * nnz * w / (spmm_ms / len(reps) * 1e-3) / 1e9 * 1.0,
             "phase_ms": {k: round(v, 4) for k, v in phase.items()},
             "clocks": clk,

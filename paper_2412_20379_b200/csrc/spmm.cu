@@ -111,8 +111,13 @@ template <typename T> __device__ __forceinline__ void store16(void* p, const flo
 
 
 // resident 256-thread CTAs per SM (register budget)
+// MODE bits 2-3 (OCC, high-degree graphs): 1 = half-length batches at 3 CTAs/SM, 2 = half-length batches
+// at 4 CTAs/SM -- the same bytes in flight per warp spread over more warps, so row ends, butterflies
+// and epilogues of one warp hide behind the loads of the others.
 template <int E, int VB, int MODE>
-__host__ __device__ constexpr int hop_ctas() { return ((MODE & 1) && E == 8 && VB == 16) ? 3 : 2; }
+__host__ __device__ constexpr int hop_ctas() {
+    return ((MODE >> 2) & 3) == 2 ? 4 : ((MODE >> 2) & 3) == 1 ? 3 : ((MODE & 1) && E == 8 && VB == 16) ? 3 : 2;
+}
 
 struct HopParams {
     const int32_t* __restrict__ rp;
@@ -176,8 +181,10 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
     constexpr int VALS = Vec<T, VB>::N;
     // edges per pipeline batch (a multiple of 8); loads per lane per batch LPB = BATCH / E:
     // 8 x 16 B (2-4 x 16 B short), or 4 x 32 B (2 x 32 B short) -- the same bytes in flight
-    constexpr int BATCH = (VB == 16) ? (SHORT ? ((E >= 4) ? 16 : 8) : ((E == 8) ? 64 : (E == 4) ? 32 : 8 * E))
-                                     : (SHORT ? ((E >= 4) ? 2 * E : 8) : ((E >= 2) ? 4 * E : 8));
+    constexpr bool OCC = ((MODE >> 2) & 3) != 0;
+    constexpr int BATCH0 = (VB == 16) ? (SHORT ? ((E >= 4) ? 16 : 8) : ((E == 8) ? 64 : (E == 4) ? 32 : 8 * E))
+                                      : (SHORT ? ((E >= 4) ? 2 * E : 8) : ((E >= 2) ? 4 * E : 8));
+    constexpr int BATCH = (OCC && !SHORT && BATCH0 >= 16) ? BATCH0 / 2 : BATCH0;
     constexpr int LPB = BATCH / E;                        // loads per lane per batch
     constexpr int ISL = (BATCH + L - 1) / L;              // column indices held per lane
     static_assert(BATCH % 8 == 0, "batch must preserve the (j - eb) mod 8 grouping");
@@ -453,7 +460,13 @@ void launch_hop(const HopParams& p, cudaStream_t s) {
     // low-degree variants when the average degree is below 32 (products, papers shapes)
     const bool low_deg = short_env >= 0 ? short_env != 0 : (p.nnz < 32 * std::max<int64_t>(p.n, 1));
     constexpr int LOW = (E >= 4) ? 3 : (E >= 2) ? 2 : 0;   // short batches where E >= 4, tiny rows where E >= 2
+    // high-degree graphs: rows of <= 4 vectors (<= 64 B) run the 4-CTA/SM half-batch variant (OCC 2:
+    // measured 9-10% faster per hop at 32-64 B rows on the Reddit shape, 4-5% slower at 96-176 B)
+    static const int occ_env = [] { const char* v = getenv("NTP_SPMM_OCC"); return v ? atoi(v) : -1; }();
+    const int occ = occ_env >= 0 ? occ_env : (p.nvec * 16 / VB <= 4 ? 2 : 0);
     if (low_deg) launch_variant<T, VB, E, L, LOW>(p, s);
+    else if (occ == 1) launch_variant<T, VB, E, L, 4>(p, s);
+    else if (occ == 2) launch_variant<T, VB, E, L, 8>(p, s);
     else launch_variant<T, VB, E, L, 0>(p, s);
 }
 
