@@ -52,19 +52,24 @@ template <> struct Q4<__nv_bfloat16> {
 // gets columns [q*d_s, (q+1)*d_s) of the row (d_s is a multiple of 4, so a quad never straddles
 // two blocks), pre-scaled by row_scale[row0 + v] and cast; columns >= w and rows >= n are zero.
 // `vec`: Hv rows are 16-byte aligned with ld % 4 == 0 (quad loads), else element loads.
+// Row chunk: Hv holds `rows` rows that are rows [vofs, vofs + rows) of this rank's block.
+// `bits` (optional): [V_p][nw] words, bit k of row vofs + v = (Hv[v][k] > 0) -- the ReLU' mask of
+// the MLP backward kept as 1 bit per element instead of the fp32 H1 (memory-lean epoch).
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) pack_v2f_kernel(const Tin* __restrict__ Hv, int64_t ld_v, int32_t w,
                                                        Tout* __restrict__ send, int64_t V_p, int32_t d_s, int32_t P,
                                                        const float* __restrict__ row_scale, int64_t row0, int64_t n,
-                                                       int vec, void* const* __restrict__ peer, int rank) {
+                                                       int vec, void* const* __restrict__ peer, int rank, int64_t rows,
+                                                       int64_t vofs, uint32_t* __restrict__ bits, int32_t nw) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int wpad = P * d_s;
-    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < V_p; v += warps) {
+    for (int64_t vl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; vl < rows; vl += warps) {
+        const int64_t v = vofs + vl;
         const int64_t gr = row0 + v;
         const bool real = gr < n;
         const float sc = (real && row_scale) ? row_scale[gr] : 1.f;
-        const Tin* src = Hv + v * ld_v;
+        const Tin* src = Hv + vl * ld_v;
         for (int k = lane * 4; k < wpad; k += 128) {
             float x[4] = {0.f, 0.f, 0.f, 0.f};
             if (real) {
@@ -74,6 +79,19 @@ __global__ void __launch_bounds__(256) pack_v2f_kernel(const Tin* __restrict__ H
 #pragma unroll
                     for (int i = 0; i < 4; ++i) x[i] = (k + i < w) ? cvt<Tin, float>(src[k + i]) : 0.f;
                 }
+            }
+            if (bits) {   // 4 bits per lane, 8 lanes per 32-column word (k advances by 128 per pass)
+                uint32_t nib = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) nib |= (x[i] > 0.f ? 1u : 0u) << i;
+                uint32_t word = nib << (4 * (lane & 7));
+                word |= __shfl_xor_sync(0xffffffffu, word, 1);
+                word |= __shfl_xor_sync(0xffffffffu, word, 2);
+                word |= __shfl_xor_sync(0xffffffffu, word, 4);
+                const int wi = k >> 5;
+                if ((lane & 7) == 0 && wi < nw) bits[v * nw + wi] = word;
+            }
+            if (real) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) x[i] *= sc;
             }
@@ -93,14 +111,19 @@ __global__ void __launch_bounds__(256) pack_v2f_kernel(const Tin* __restrict__ H
 // One warp per vertex row: columns [4k, 4k+4) of the row come from block q = 4k / d_s of `recv`.
 // `keep` (optional, same row/column indexing as Hv, ld_keep): zero where keep <= 0 (the fused
 // ReLU' mask of the MLP backward, reading R12).
+// Row chunk: rows [vofs, vofs + rows) of the block layout -> Hv rows [0, rows).  `keep_bits`
+// ([V_p][nw] words, block-row indexed): the same mask as `keep`, one bit per element.
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) unpack_f2v_kernel(const Tin* __restrict__ recv, int64_t V_p, int32_t d_s,
                                                          Tout* __restrict__ Hv, int64_t ld_v, int32_t w, int vec,
-                                                         const float* __restrict__ keep, int64_t ld_keep) {
+                                                         const float* __restrict__ keep, int64_t ld_keep, int64_t rows,
+                                                         int64_t vofs, const uint32_t* __restrict__ keep_bits,
+                                                         int32_t nw) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < V_p; v += warps) {
-        Tout* dst = Hv + v * ld_v;
+    for (int64_t vl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; vl < rows; vl += warps) {
+        const int64_t v = vofs + vl;
+        Tout* dst = Hv + vl * ld_v;
         for (int k = lane * 4; k < w; k += 128) {
             const int q = k / d_s;
             float x[4];
@@ -108,7 +131,13 @@ __global__ void __launch_bounds__(256) unpack_f2v_kernel(const Tin* __restrict__
             if (keep) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if (k + i < w && !(keep[v * ld_keep + k + i] > 0.f)) x[i] = 0.f;
+                    if (k + i < w && !(keep[vl * ld_keep + k + i] > 0.f)) x[i] = 0.f;
+            }
+            if (keep_bits) {
+                const uint32_t word = keep_bits[v * nw + (k >> 5)];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (!((word >> ((k + i) & 31)) & 1u)) x[i] = 0.f;
             }
             if (vec && k + 3 < w) {
                 Q4<Tout>::st(dst + k, x);
@@ -130,41 +159,44 @@ template <typename T> bool quad_ok(const void* p, int64_t ld) {
 
 void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, int64_t V_p, int32_t d_s, int32_t P,
               const float* row_scale, int64_t row0, int64_t n, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s,
-              void* const* peer) {
+              void* const* peer, int64_t rows, int64_t vofs, uint32_t* bits, int32_t nw) {
     const int rk = c->rank;
-    if (V_p == 0 || d_s == 0) return;
-    const int b = row_blocks(V_p);
+    if (rows < 0) rows = V_p;
+    if (rows == 0 || d_s == 0) return;
+    const int b = row_blocks(rows);
     const int vec = (dt_in == NTP_F32) ? quad_ok<float>(Hv, ld_v) : quad_ok<__nv_bfloat16>(Hv, ld_v);
     if (dt_in == NTP_F32 && dt_out == NTP_F32)
-        pack_v2f_kernel<float, float><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (float*)send, V_p, d_s, P, row_scale, row0, n, vec, peer, rk);
+        pack_v2f_kernel<float, float><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (float*)send, V_p, d_s, P, row_scale, row0, n, vec, peer, rk, rows, vofs, bits, nw);
     else if (dt_in == NTP_F32 && dt_out == NTP_BF16)
         pack_v2f_kernel<float, __nv_bfloat16><<<b, 256, 0, s>>>((const float*)Hv, ld_v, w, (__nv_bfloat16*)send, V_p, d_s, P,
-                                                                row_scale, row0, n, vec, peer, rk);
+                                                                row_scale, row0, n, vec, peer, rk, rows, vofs, bits, nw);
     else if (dt_in == NTP_BF16 && dt_out == NTP_BF16)
         pack_v2f_kernel<__nv_bfloat16, __nv_bfloat16><<<b, 256, 0, s>>>((const __nv_bfloat16*)Hv, ld_v, w,
-                                                                        (__nv_bfloat16*)send, V_p, d_s, P, row_scale, row0, n, vec, peer, rk);
+                                                                        (__nv_bfloat16*)send, V_p, d_s, P, row_scale, row0, n, vec, peer, rk, rows, vofs, bits, nw);
     else
         pack_v2f_kernel<__nv_bfloat16, float><<<b, 256, 0, s>>>((const __nv_bfloat16*)Hv, ld_v, w, (float*)send, V_p, d_s,
-                                                                P, row_scale, row0, n, vec, peer, rk);
+                                                                P, row_scale, row0, n, vec, peer, rk, rows, vofs, bits, nw);
     NTP_LAUNCH_CHECK();
     count_launch(c);
 }
 
 void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t P, void* Hv, int64_t ld_v, int32_t w,
-                ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s, const float* keep, int64_t ld_keep) {
+                ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s, const float* keep, int64_t ld_keep, int64_t rows,
+                int64_t vofs, const uint32_t* keep_bits, int32_t nw) {
     (void)P;
-    if (V_p == 0 || w == 0) return;
-    const int b = row_blocks(V_p);
+    if (rows < 0) rows = V_p;
+    if (rows == 0 || w == 0) return;
+    const int b = row_blocks(rows);
     const int vec = (dt_out == NTP_F32) ? quad_ok<float>(Hv, ld_v) : quad_ok<__nv_bfloat16>(Hv, ld_v);
     if (dt_in == NTP_F32 && dt_out == NTP_F32)
-        unpack_f2v_kernel<float, float><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (float*)Hv, ld_v, w, vec, keep, ld_keep);
+        unpack_f2v_kernel<float, float><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (float*)Hv, ld_v, w, vec, keep, ld_keep, rows, vofs, keep_bits, nw);
     else if (dt_in == NTP_BF16 && dt_out == NTP_F32)
-        unpack_f2v_kernel<__nv_bfloat16, float><<<b, 256, 0, s>>>((const __nv_bfloat16*)recv, V_p, d_s, (float*)Hv, ld_v, w, vec, keep, ld_keep);
+        unpack_f2v_kernel<__nv_bfloat16, float><<<b, 256, 0, s>>>((const __nv_bfloat16*)recv, V_p, d_s, (float*)Hv, ld_v, w, vec, keep, ld_keep, rows, vofs, keep_bits, nw);
     else if (dt_in == NTP_BF16 && dt_out == NTP_BF16)
         unpack_f2v_kernel<__nv_bfloat16, __nv_bfloat16><<<b, 256, 0, s>>>((const __nv_bfloat16*)recv, V_p, d_s,
-                                                                          (__nv_bfloat16*)Hv, ld_v, w, vec, keep, ld_keep);
+                                                                          (__nv_bfloat16*)Hv, ld_v, w, vec, keep, ld_keep, rows, vofs, keep_bits, nw);
     else
-        unpack_f2v_kernel<float, __nv_bfloat16><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (__nv_bfloat16*)Hv, ld_v, w, vec, keep, ld_keep);
+        unpack_f2v_kernel<float, __nv_bfloat16><<<b, 256, 0, s>>>((const float*)recv, V_p, d_s, (__nv_bfloat16*)Hv, ld_v, w, vec, keep, ld_keep, rows, vofs, keep_bits, nw);
     NTP_LAUNCH_CHECK();
     count_launch(c);
 }

@@ -223,6 +223,15 @@ __global__ void sgd_kernel(float* __restrict__ W0, int64_t n0, float* __restrict
     }
 }
 
+// out[i] = sum_ch part[ch][i] in chunk order (deterministic weight gradients of the chunked epoch)
+__global__ void sum_chunks_kernel(const float* __restrict__ part, int64_t nch, int64_t len, float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        float acc = part[i];
+        for (int64_t ch = 1; ch < nch; ++ch) acc += part[ch * len + i];
+        out[i] = acc;
+    }
+}
+
 int eblocks(int64_t total) { return (int)std::min<int64_t>(std::max<int64_t>(cdiv(total, 256), 1), 148 * 16); }
 
 // C[M x N] = op(A) op(B), all row-major fp32 (column-major cuBLAS on the transposes).
@@ -418,18 +427,33 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         W1s = Split{w1h, w1l};
     }
 
-    // ---- scratch
-    c->m_H1.ensure((size_t)V_p * ldH * sizeof(float));
-    c->m_L.ensure((size_t)V_p * ldL * sizeof(float));
-    c->m_dL.ensure((size_t)V_p * ldL * sizeof(float));
-    c->m_dH1.ensure((size_t)V_p * ldH * sizeof(float));
+    // ---- scratch.  One GPU (P = 1): the layout changes are identities, so the producers write the
+    // feature slice directly and the hops ping-pong between two slices (propagate_consume) -- no
+    // exchange copies, no send buffer, no scratch slice.  W1 after propagation (R3, papers shape):
+    // the vertex-side work runs in row chunks of `hc` rows (H1, logits, gradients chunk-sized; the
+    // ReLU' mask kept as bits) so the epoch's footprint is the slices plus X (memory-lean plan).
+    const bool local = (P == 1);
+    const char* hce = getenv("NTP_HEAD_CHUNK");   // read per call (tests vary it)
+    const int64_t head_chunk_env = hce ? atoll(hce) : 0;
+    const int64_t hc = after ? std::max<int64_t>(1, std::min<int64_t>(V_p, head_chunk_env > 0 ? head_chunk_env
+                                                                                               : (int64_t)1 << 23))
+                             : V_p;
+    const int64_t nch = after ? cdiv(V_p, hc) : 1;
+    const int32_t nwb = (m->hid + 31) / 32;          // mask words per row
+    const int64_t rowsH = after ? hc : V_p;
+    c->m_H1.ensure((size_t)rowsH * ldH * sizeof(float));
+    c->m_L.ensure((size_t)rowsH * ldL * sizeof(float));
+    c->m_dL.ensure((size_t)rowsH * ldL * sizeof(float));
+    c->m_dH1.ensure((size_t)rowsH * ldH * sizeof(float));
+    if (after) c->m_bits.ensure((size_t)V_p * nwb * sizeof(uint32_t) + 16);
     const int64_t n_w = (int64_t)m->d_in * m->hid + (int64_t)m->hid * m->C;
     c->m_dW.ensure((size_t)n_w * sizeof(float));
+    if (nch > 1) c->m_dWp.ensure((size_t)nch * n_w * sizeof(float));
     c->m_scal.ensure(4 * sizeof(double));
-    c->send.ensure((size_t)feat_elems * es + 16);
+    if (!local) c->send.ensure((size_t)feat_elems * es + 16);
     c->recv.ensure((size_t)feat_elems * es + 16);
     c->xfer.ensure((size_t)feat_elems * es + 16);     // propagation output (feature slice)
-    const int64_t loss_blocks = cdiv(V_p, 8);        // upper bound on loss-kernel blocks (>= 8 rows per block)
+    const int64_t loss_blocks = std::min<int64_t>(cdiv(V_p, 8), 148 * 8) * nch;   // loss-kernel grid bound per chunk
     c->m_part.ensure((size_t)loss_blocks * (sizeof(double) + sizeof(int64_t)) + 16);
     double* part = c->m_part.as<double>();
     int64_t* cnt = reinterpret_cast<int64_t*>(part + loss_blocks);
@@ -437,39 +461,48 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     float* L = c->m_L.as<float>();
     float* dL = c->m_dL.as<float>();
     float* dH1 = c->m_dH1.as<float>();
+    uint32_t* bits = after ? c->m_bits.as<uint32_t>() : nullptr;
     float* dW0 = c->m_dW.as<float>();
     float* dW1 = dW0 + (int64_t)m->d_in * m->hid;
     double* scal = c->m_scal.as<double>();
+    // chunk ch's weight-gradient partials (dW0 | dW1), summed in chunk order afterwards
+    auto dw0_at = [&](int64_t ch) { return nch > 1 ? c->m_dWp.as<float>() + ch * n_w : dW0; };
+    auto dw1_at = [&](int64_t ch) { return dw0_at(ch) + (int64_t)m->d_in * m->hid; };
     NTP_BLAS(cublasSetStream(c->blas, s));
-
-    // a2: MLP forward (ReLU fused into the GEMM epilogue)
-    mlp_gemm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0g, ldw0, H1, ldH, s, /*relu*/ 1, nullptr, 0, W0s);
-    const float* prop_src = H1;             // rows propagated (w columns)
-    int64_t ld_src = ldH;
-    if (!after) {
-        mlp_gemm(c, false, false, V_p, m->C, m->hid, H1, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
-        prop_src = L;
-        ld_src = ldL;
-    }
-    NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd done
 
     // Peer-direct layouts (NTP_M_P2P_LAYOUTS, P > 1, CUDA IPC available): the producers store into
     // the owners' windows and a barrier replaces each all-to-all; otherwise the NCCL block exchange.
     const bool overlap = (m->flags & NTP_M_OVERLAP) != 0;
     const size_t win = (size_t)feat_elems * es;
-    const bool p2p = !overlap && (m->flags & NTP_M_P2P_LAYOUTS) && p2p_ensure(c, win, win, s);
+    const bool p2p = !local && !overlap && (m->flags & NTP_M_P2P_LAYOUTS) && p2p_ensure(c, win, win, s);
     void* const* tab_split = p2p ? c->p2p_tab.as<void*>() : nullptr;
     void* const* tab_gath = p2p ? c->p2p_tab.as<void*>() + P : nullptr;
     void* slice_in = p2p ? c->p2p_split.p : c->recv.p;   // this rank's feature slice after a split
+    void* split_dst = p2p ? nullptr : (local ? c->recv.p : c->send.p);   // where the split's producer writes
+
+    // a2 (+ a3's pack): MLP forward (ReLU fused into the GEMM epilogue)
+    const float* prop_src = H1;             // rows propagated (w columns)
+    int64_t ld_src = ldH;
+    if (!after) {
+        mlp_gemm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0g, ldw0, H1, ldH, s, /*relu*/ 1, nullptr, 0, W0s);
+        mlp_gemm(c, false, false, V_p, m->C, m->hid, H1, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
+        prop_src = L;
+        ld_src = ldL;
+        NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd done
+        pack_v2f(c, prop_src, ld_src, w, split_dst, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split);
+    } else {
+        for (int64_t r = 0; r < V_p; r += hc) {      // H1 chunk -> pre-scaled slice rows + ReLU' bits
+            const int64_t h = std::min(hc, V_p - r);
+            mlp_gemm(c, false, false, h, m->hid, m->d_in, X + r * ldx, ldx, W0g, ldw0, H1, ldH, s, 1, nullptr, 0, W0s);
+            pack_v2f(c, H1, ldH, w, split_dst, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split, h, r,
+                     bits, nwb);
+        }
+        NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd (+ pack) done
+    }
 
     // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
-    if (p2p) {
-        pack_v2f(c, prop_src, ld_src, w, nullptr, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split);
-        p2p_barrier(c, s);
-    } else {
-        pack_v2f(c, prop_src, ld_src, w, c->send.p, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s);
-        alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
-    }
+    if (p2p) p2p_barrier(c, s);
+    else if (!local) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E2 v2f done
 
     // a4 + a5: K forward hops on S^0 (pre-scaled) -> Z^K, gathered into this rank's rows
@@ -487,7 +520,9 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = false;
-        if (p2p) {
+        if (local) {
+            gathered = propagate_consume(c, a, s, timed);
+        } else if (p2p) {
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
             p2p_barrier(c, s);
@@ -496,6 +531,9 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         }
     }
     NTP_CUDA(record_timing(c, E[ei++], s));   // E3 prop fwd + f2v done
+    // the gradient split's producer target: the send buffer, or on one GPU the slice the forward no
+    // longer needs
+    void* gsend = local ? (gathered == c->recv.p ? c->xfer.p : c->recv.p) : c->send.p;
 
     // a6: loss + gradient, written straight into the backward split's send buffer (or windows)
     const float* gscale_bwd = g.dinv_in_orig();   // backward column side (original vertex order)
@@ -503,30 +541,35 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     if (!after) {
         if (dt == NTP_F32)
             nb_loss = launch_softmax_xent(c, (const float*)gathered, 1, V_p, d_s, m->C, lab, msk, row0, n,
-                                          (float*)c->send.p, 1, gscale_bwd, part, cnt, 0, s, tab_split);
+                                          (float*)gsend, 1, gscale_bwd, part, cnt, 0, s, tab_split);
         else
             nb_loss = launch_softmax_xent(c, (const __nv_bfloat16*)gathered, 1, V_p, d_s, m->C, lab, msk, row0, n,
-                                          (__nv_bfloat16*)c->send.p, 1, gscale_bwd, part, cnt, 0, s, tab_split);
+                                          (__nv_bfloat16*)gsend, 1, gscale_bwd, part, cnt, 0, s, tab_split);
         if (P * d_s > m->C) {
             if (dt == NTP_F32)
-                zero_pad_cols_kernel<float><<<eblocks(V_p * (P * d_s - m->C)), 256, 0, s>>>((float*)c->send.p, V_p, d_s,
+                zero_pad_cols_kernel<float><<<eblocks(V_p * (P * d_s - m->C)), 256, 0, s>>>((float*)gsend, V_p, d_s,
                                                                                           P, m->C, tab_split, c->rank);
             else
                 zero_pad_cols_kernel<__nv_bfloat16><<<eblocks(V_p * (P * d_s - m->C)), 256, 0, s>>>(
-                    (__nv_bfloat16*)c->send.p, V_p, d_s, P, m->C, tab_split, c->rank);
+                    (__nv_bfloat16*)gsend, V_p, d_s, P, m->C, tab_split, c->rank);
             NTP_LAUNCH_CHECK();
             count_launch(c);
         }
     } else {
-        // Z_v = unpack(gathered) [V_p x hid]; logits = Z_v W1; dlogits; dZ_v = dlogits W1^T -> pack
-        float* Zv = dH1;   // reuse [V_p x ldH]
-        unpack_f2v(c, gathered, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s);
-        mlp_gemm(c, false, false, V_p, m->C, m->hid, Zv, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
-        nb_loss = launch_softmax_xent(c, (const float*)L, 0, V_p, d_s, m->C, lab, msk, row0, n, dL, 0, nullptr, part,
-                                      cnt, ldL, s);
-        mlp_gemm(c, true, false, m->hid, m->C, V_p, Zv, ldH, dL, ldL, dW1, m->C, s);          // dW1 = Z_v^T dlogits
-        mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);  // dZ_v -> L
-        pack_v2f(c, L, ldL, m->hid, c->send.p, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s, tab_split);
+        // per row chunk: Z_v = unpack(gathered) [h x hid]; logits = Z_v W1; dlogits; dW1 += Z_v^T dlogits;
+        // dZ_v = dlogits W1^T -> pack into the gradient split
+        float* Zv = dH1;   // reuse [hc x ldH]
+        for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
+            const int64_t h = std::min(hc, V_p - r);
+            unpack_f2v(c, gathered, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s, nullptr, 0, h, r);
+            mlp_gemm(c, false, false, h, m->C, m->hid, Zv, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
+            nb_loss += launch_softmax_xent(c, (const float*)L, 0, h, d_s, m->C, lab + r, msk + r, row0 + r, n, dL, 0,
+                                           nullptr, part + nb_loss, cnt + nb_loss, ldL, s);
+            mlp_gemm(c, true, false, m->hid, m->C, h, Zv, ldH, dL, ldL, dw1_at(ch), m->C, s);          // dW1 = Z_v^T dlogits
+            mlp_gemm(c, false, true, h, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);  // dZ_v -> L
+            pack_v2f(c, L, ldL, m->hid, p2p ? nullptr : gsend, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s,
+                     tab_split, h, r);
+        }
     }
     reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb_loss, scal);
     NTP_LAUNCH_CHECK();
@@ -535,15 +578,15 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
 
     // a7: split the gradient
     if (p2p) p2p_barrier(c, s);
-    else alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    else if (!local) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E5 v2f bwd
 
     // a8 + a9: K backward hops on the split gradient, gathered -> dL^ rows [V_p x w]
     void* gathered_b = p2p ? c->p2p_gath.p : c->send.p;
     {
         PropArgs a{};
-        a.H = slice_in;
-        a.Z = c->xfer.p;
+        a.H = local ? gsend : slice_in;
+        a.Z = local ? (gsend == c->recv.p ? c->xfer.p : c->recv.p) : c->xfer.p;
         a.ld_h = d_s;
         a.ld_z = d_s;
         a.cols = d_s;
@@ -552,7 +595,9 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = true;
-        if (p2p) {
+        if (local) {
+            gathered_b = propagate_consume(c, a, s, timed);
+        } else if (p2p) {
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
             p2p_barrier(c, s);
@@ -560,19 +605,26 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             propagate_and_gather(c, a, c->send.p, overlap, m->chunks, V_p, d_s, timed, s);
         }
     }
-    float* dLw = after ? dH1 : dL;            // gathered dL^ rows (dH1 before the mask when W1 is applied after)
-    const int64_t ld_dLw = after ? ldH : ldL;
-    unpack_f2v(c, gathered_b, V_p, d_s, P, dLw, ld_dLw, w, dt, NTP_F32, s, after ? H1 : nullptr, ldH);
+    if (!after) unpack_f2v(c, gathered_b, V_p, d_s, P, dL, ldL, w, dt, NTP_F32, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E6 prop bwd + f2v bwd
 
-    // a10: MLP backward (ReLU' mask fused into the dH1 GEMM epilogue)
+    // a10: MLP backward (ReLU' mask fused into the dH1 GEMM epilogue, or into the unpack from bits)
     if (!after) {
         mlp_gemm(c, true, false, m->hid, m->C, V_p, H1, ldH, dL, ldL, dW1, m->C, s);              // dW1 = H1^T dL^
         mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, dH1, ldH, s, 2, H1, ldH, W1s);  // dH1
+        mlp_gemm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, ldH, dW0, m->hid, s);            // dW0 = X^T dH1
     } else {
-        // ReLU' mask fused into the gather's unpack above
+        for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
+            const int64_t h = std::min(hc, V_p - r);
+            unpack_f2v(c, gathered_b, V_p, d_s, P, dH1, ldH, w, dt, NTP_F32, s, nullptr, 0, h, r, bits, nwb);
+            mlp_gemm(c, true, false, m->d_in, m->hid, h, X + r * ldx, ldx, dH1, ldH, dw0_at(ch), m->hid, s);
+        }
+        if (nch > 1) {
+            sum_chunks_kernel<<<eblocks(n_w), 256, 0, s>>>(c->m_dWp.as<float>(), nch, n_w, dW0);
+            NTP_LAUNCH_CHECK();
+            count_launch(c);
+        }
     }
-    mlp_gemm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, ldH, dW0, m->hid, s);            // dW0 = X^T dH1
     NTP_CUDA(record_timing(c, E[ei++], s));   // E7 mlp bwd
 
     // a11: allreduce (sync_and_update)
@@ -679,6 +731,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     key.ptrs[4] = W1->data;
     key.ld = X_v->ld;
     key.graph_version = c->g_version;
+    key.head_chunk = getenv("NTP_HEAD_CHUNK") ? atoll(getenv("NTP_HEAD_CHUNK")) : 0;
     int64_t epoch_launches = 0;
     if (graphs_enabled() && c->graph_valid && c->graph_key == key) {
         NTP_CUDA(cudaGraphLaunch(c->graph_exec, s));

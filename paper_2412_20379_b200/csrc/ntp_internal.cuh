@@ -123,9 +123,10 @@ struct EpochKey {
     const void* ptrs[5];
     int64_t ld;
     int64_t graph_version;
+    int64_t head_chunk;     // NTP_HEAD_CHUNK (row chunk of the W1-after-propagation epoch)
     bool operator==(const EpochKey& o) const {
         return std::memcmp(&m, &o.m, sizeof(m)) == 0 && std::memcmp(ptrs, o.ptrs, sizeof(ptrs)) == 0 && ld == o.ld &&
-               graph_version == o.graph_version;
+               graph_version == o.graph_version && head_chunk == o.head_chunk;
     }
 };
 
@@ -138,7 +139,7 @@ struct ntp_ctx {
     // scratch
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
-    ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit;
+    ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp;
     // peer-direct layouts (CUDA IPC windows over NVLink), see layout.cu
     int p2p_state = 0;                      // 0 not set up, 1 usable, -1 unavailable
     ntp::DevBuf p2p_split, p2p_gath;        // this rank's windows (zero-initialised)
@@ -213,6 +214,10 @@ struct LastHop {
 void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops = false,
                bool prescaled_input = false, LastHop* defer_last = nullptr);
 void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi, cudaStream_t s, bool time_hops);
+// Pre-scaled input that may be consumed (alpha == 0: S^0 is dead after hop 1): the hops ping-pong
+// between a.H and a.Z (same ld) with no scratch slice; returns the buffer holding Z^K (a.H or a.Z).
+// alpha != 0 falls back to propagate() (S^0 must live through every hop) and returns a.Z.
+void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops);
 double collect_hop_ms(ntp_ctx* c, int* n_hops);
 void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K, float gamma, float alpha,
                         bool transposed, ntp_dtype dt, int chunks, bool overlap, cudaStream_t user);
@@ -238,7 +243,8 @@ void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, in
 // layouts
 void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, int64_t V_p,
               int32_t d_s, int32_t P, const float* row_scale, int64_t row0, int64_t n,
-              ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s, void* const* peer_tab = nullptr);
+              ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s, void* const* peer_tab = nullptr,
+              int64_t rows = -1, int64_t vofs = 0, uint32_t* bits = nullptr, int32_t nw = 0);
 // Peer-direct layouts: IPC windows of this rank ([P][V_p][d_s] split target and gather target),
 // exchanged once per size (collective); false when P2P is unavailable (NCCL all-to-all path).
 bool p2p_ensure(ntp_ctx* c, size_t split_bytes, size_t gather_bytes, cudaStream_t s);
@@ -246,7 +252,8 @@ void p2p_barrier(ntp_ctx* c, cudaStream_t s);   // stream-ordered all-rank barri
 void p2p_shutdown(ntp_ctx* c);                  // closes the peer mappings (ntp_destroy)
 void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t P, void* Hv,
                 int64_t ld_v, int32_t w, ntp_dtype dt_in, ntp_dtype dt_out, cudaStream_t s,
-                const float* keep = nullptr, int64_t ld_keep = 0);
+                const float* keep = nullptr, int64_t ld_keep = 0, int64_t rows = -1, int64_t vofs = 0,
+                const uint32_t* keep_bits = nullptr, int32_t nw = 0);
 void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_elems, ntp_dtype dt,
                      cudaStream_t s);
 

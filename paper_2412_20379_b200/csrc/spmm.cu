@@ -641,6 +641,37 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
     }
 }
 
+void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops) {
+    if (a.alpha != 0.f || a.K == 0 || a.ld_h != a.ld_z || a.po.tab) {
+        propagate(c, a, s, time_hops, true);
+        return a.Z;
+    }
+    const Graph& g = c->g;
+    const Csr& csr = a.transposed ? g.bwd() : g.fwd();
+    const float* rs = a.transposed ? g.dinv_out_p() : g.dinv_in_p();
+    const float* cs = a.transposed ? g.dinv_in_p() : g.dinv_out_p();
+    const int32_t* inv = g.inv_p();
+    void* cur = const_cast<void*>(a.H);
+    void* oth = a.Z;
+    if (inv) {   // reordered graph: S^0 permuted into internal order first (into the other buffer)
+        prescale(c, cur, a.ld_h, oth, a.ld_z, a.cols, nullptr, g.n, a.dtype, s, inv);
+        std::swap(cur, oth);
+    }
+    for (int k = 1; k <= a.K; ++k) {
+        const bool last = (k == a.K);
+        const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
+        if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
+        spmm_hop(c, csr, rs, cs, cur, oth, cur, a.ld_h, a.ld_z, a.ld_h, a.cols, a.dtype, a.gamma, 0.f, last ? 1 : 0, 0,
+                 -1, s, last ? inv : nullptr, nullptr);
+        if (timed) {
+            NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used + 1], s));
+            c->hop_ev_used += 2;
+        }
+        std::swap(cur, oth);
+    }
+    return cur;
+}
+
 void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi, cudaStream_t s, bool time_hops) {
     const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
     if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));

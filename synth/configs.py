@@ -71,6 +71,10 @@ _add(Config("tiny_dir", 12, 3001, 12, 40_000, GRAPH500, False, 33, 20, 7, 3, 0.9
             w_after_prop=True))
 _add(Config("small_appnp", 13, 20_011, 15, 300_000, GRAPH500, True, 50, 32, 13, 10, 0.9, 0.1))
 _add(Config("small_dir", 14, 50_000, 16, 800_000, REDDIT_ABC, False, 64, 48, 19, 2, 1.0, 0.0))
+# High-degree parity cases (average degree >= 32, like the Reddit shape): the kernels' high-degree
+# variants (streaming narrow-row hop) only run on these; hubs span several merge-path units
+_add(Config("dense_sym", 16, 8_000, 13, 260_000, REDDIT_ABC, True, 40, 24, 9, 3, 0.9, 0.1))
+_add(Config("dense_dir", 17, 6_007, 13, 420_000, REDDIT_ABC, False, 36, 16, 11, 2, 1.0, 0.0))
 
 
 def get_config(name: str) -> Config:

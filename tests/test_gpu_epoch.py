@@ -49,7 +49,7 @@ def _train_oracle(name, epochs, lr):
     return oracle.model.train(g, X, y, m, W0, W1, cfg.K, cfg.gamma, cfg.alpha, lr, epochs)
 
 
-@pytest.mark.parametrize("name", ["cora", "tiny_sym", "tiny_dir", "small_appnp", "small_dir"])
+@pytest.mark.parametrize("name", ["cora", "tiny_sym", "tiny_dir", "small_appnp", "small_dir", "dense_sym", "dense_dir"])
 def test_epoch_loss_parity_fp32(name):
     cfg = synth.get_config(name)
     losses, W0, W1, reps, model = _train_gpu(name, 5)
@@ -111,3 +111,19 @@ def test_zero_weights_loss_ln_C():
     rep = ctx.train_epoch(_model(cfg), *(torch.from_numpy(a).cuda() for a in (X, y, m)),
                           torch.from_numpy(W0).cuda(), torch.from_numpy(W1).cuda())
     assert abs(rep["loss"] - np.log(cfg.C)) < 1e-6
+
+
+@pytest.mark.parametrize("chunk", [700, 1024, 4096])
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_epoch_chunked_head(chunk, dtype, monkeypatch):
+    """W1 after propagation (R3): the vertex-side work (MLP forward, logits/loss/gradient head, dW0)
+    runs in row chunks of NTP_HEAD_CHUNK rows with the ReLU' mask kept as bits; 1, 3 or 5 chunks on
+    the 3,001-vertex directed graph give the oracle's losses and weights (fp32: 1e-4; bf16: 2e-2)."""
+    monkeypatch.setenv("NTP_HEAD_CHUNK", str(chunk))
+    losses, W0, W1, reps, model = _train_gpu("tiny_dir", 3, dtype=dtype)
+    ref_losses, rW0, rW1 = _train_oracle("tiny_dir", 3, model["lr"])
+    for e, (a, b) in enumerate(zip(losses, ref_losses)):
+        assert abs(a - b) <= (1e-4 if dtype == 0 else 2e-2 * abs(b)), f"epoch {e}: gpu {a} oracle {b}"
+    if dtype == 0:
+        for got, ref in ((W0, rW0), (W1, rW1)):
+            assert np.abs(got - ref).max() <= 1e-4 * max(1.0, np.abs(ref).max())

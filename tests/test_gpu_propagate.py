@@ -33,8 +33,8 @@ def _run(ctx, H, K, gamma, alpha, transposed=False, dtype=torch.float32, rows=No
     return Zd, Hd
 
 
-@pytest.mark.parametrize("name", ["cora", "tiny_sym", "tiny_dir", "small_appnp", "small_dir"])
-@pytest.mark.parametrize("d", [4, 8, 12, 44, 48, 132])
+@pytest.mark.parametrize("name", ["cora", "tiny_sym", "tiny_dir", "small_appnp", "small_dir", "dense_sym", "dense_dir"])
+@pytest.mark.parametrize("d", [4, 8, 12, 16, 44, 48, 132])
 @pytest.mark.parametrize("transposed", [False, True])
 def test_fp32_parity(name, d, transposed):
     cfg = synth.get_config(name)
@@ -216,8 +216,9 @@ def ntp():
 # ------------------------------------------------------------------ full size (BASELINE configs[1])
 
 @pytest.mark.slow
-def test_reddit_full_size_sampled_rows():
-    """c2 at the bench's P=1 slice width (44 fp32 columns), K=2: sampled output rows
+@pytest.mark.parametrize("d", [44, 8])
+def test_reddit_full_size_sampled_rows(d):
+    """c2 at the bench's P=1 slice width (44 fp32 columns) and the P=8 width (8; streaming kernel), K=2: sampled output rows
     vs the oracle hop by hop (the GPU's hop-1 output is fed to the oracle's hop 2),
     plus the sqrt(d~) fixed point A^ sqrt(d~) = sqrt(d~) (symmetric graph)."""
     name = "reddit"
@@ -225,7 +226,7 @@ def test_reddit_full_size_sampled_rows():
     g = oracle_graph(name)
     ctx = ntp_ctx_for(name)
     n = g.n
-    H = _features(n, 44, 11)
+    H = _features(n, d, 11)
     Z1, _ = _run(ctx, H, 1, 1.0, 0.0)
     Z2, _ = _run(ctx, H, 2, 1.0, 0.0)
     rng = np.random.default_rng(0)
@@ -272,3 +273,20 @@ def test_full_size_sampled_rows(name, d):
     np.testing.assert_allclose(Zs.cpu().numpy(), sq, rtol=5e-5)
     Ys, _ = _run(ctx, sq, cfg.K, gam, cfg.alpha, transposed=True)
     np.testing.assert_allclose(Ys.cpu().numpy(), sq, rtol=5e-5)
+
+
+@pytest.mark.parametrize("name", ["dense_sym", "dense_dir"])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_high_degree_variants_bitwise(name, transposed):
+    """High-degree graphs: narrow slices (<= 64-byte rows) run the 4-CTA/SM half-batch hop variant,
+    wide ones the default variant; the reduction order is the same, so every narrow slice equals the
+    matching columns of the full-width result bitwise (fp32 and bf16 storage)."""
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    for dtype, widths in ((torch.float32, (4, 8, 12, 16)), (torch.bfloat16, (8, 16, 24, 32))):
+        H = _features(g.n, 48, 9)
+        Zfull, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, transposed, dtype=dtype)
+        for d in widths:
+            Zs, _ = _run(ctx, np.ascontiguousarray(H[:, :d]), cfg.K, cfg.gamma, cfg.alpha, transposed, dtype=dtype)
+            assert torch.equal(Zs, Zfull[:, :d]), (dtype, d)
