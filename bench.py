@@ -95,13 +95,18 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ algorithmic bytes
-def hop_bytes(n, nnz, d_s, elem, symmetric, alpha):
-    """Compulsory HBM bytes of one SpMM hop on one GPU (every array touched once):
-    col_idx 4*nnz + row_ptr 4*(n+1) + D~^{-1/2} (4n, or 8n directed) + row slices:
-    gathered rows read once (n*r), self/S^0 rows (already counted in the gathered set),
-    output written once (n*r), S^0 read once more if alpha > 0 (n*r).  r = row-slice bytes."""
+def hop_bytes(n, nnz, d_s, elem, symmetric, alpha, l2_bytes):
+    """Algorithmic HBM bytes of one SpMM hop on one GPU, by residency:
+    B_lo = col_idx 4*nnz + row_ptr 4*(n+1) + D~^{-1/2} (4n, or 8n directed) + slice rows read once,
+           output written once, S^0 once more if alpha > 0 (n*r*(2 + [alpha > 0]));
+    slice (n*r) <= L2: B_lo (perfect reuse: the gathered rows are re-read from L2, not HBM);
+    slice  >  L2: B_hi = B_lo + nnz*r_s (SURVEY's no-reuse per-edge figure: every arc's row slice,
+           sector-rounded r_s = ceil(r/32)*32, comes from HBM).  Returns (bytes, model)."""
     r = d_s * elem
-    return 4 * nnz + 4 * (n + 1) + (4 if symmetric else 8) * n + n * r * (2 + (1 if alpha > 0 else 0))
+    lo = 4 * nnz + 4 * (n + 1) + (4 if symmetric else 8) * n + n * r * (2 + (1 if alpha > 0 else 0))
+    if n * r <= l2_bytes:
+        return lo, "perfect reuse (slice fits L2)"
+    return lo + nnz * (-(-r // 32) * 32), "no reuse (slice larger than L2)"
 
 
 def l2_gather_bytes(nnz, n, d_s, elem):
@@ -255,17 +260,19 @@ def main():
     V_p, d_s = part["V_p"], part["d_s"]
     row0 = rank * V_p
     rows = max(0, min(V_p, n - row0))
-    Xh = np.zeros((V_p, cfg.d_in), np.float32)
-    yh = np.zeros(V_p, np.int32)
-    mh = np.zeros(V_p, np.uint8)
-    if rows:
-        Xh[:rows], yh[:rows], mh[:rows] = synth.config_inputs(cfg, row0, rows)
     W0h, W1h = synth.model_weights(cfg)
     ldx = (cfg.d_in + 3) // 4 * 4          # 16-byte row pitch: the MLP GEMMs read X_v with TMA, no staging copy
     X = torch.zeros(V_p, ldx, dtype=torch.float32, device="cuda")[:, :cfg.d_in]
-    X.copy_(torch.from_numpy(Xh))
-    y = torch.from_numpy(yh).cuda()
-    msk = torch.from_numpy(mh).cuda()
+    y = torch.zeros(V_p, dtype=torch.int32, device="cuda")
+    msk = torch.zeros(V_p, dtype=torch.uint8, device="cuda")
+    if rows:
+        # the same formulas evaluated on the device (synth.config_inputs_device, pinned bitwise against
+        # the numpy version in tests/test_synth.py): papers-scale inputs in seconds instead of minutes
+        synth.config_inputs_device(cfg, row0, rows, device="cuda", out=(X, y, msk))
+    Xh = yh = mh = None
+    if not args.no_e2e:
+        Xh, yh, mh = X.cpu().contiguous().numpy(), y.cpu().numpy(), msk.cpu().numpy()
+    x_bytes = V_p * cfg.d_in * 4
     W0 = torch.from_numpy(W0h).cuda()
     W1 = torch.from_numpy(W1h).cuda()
     flags = ((ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if args.overlap else 0)
@@ -303,7 +310,7 @@ def main():
 
     # ---- e2e: same call with HOST (pinned) inputs copied in every step, loss read back
     e2e_ms = None
-    h2d = Xh.nbytes + yh.nbytes + mh.nbytes
+    h2d = x_bytes + V_p * 4 + V_p
     if not args.no_e2e:
         Xp = torch.from_numpy(Xh).pin_memory()   # host layout [V_p x d_in]; staged into a 16-B pitch on copy
         yp = torch.from_numpy(yh).pin_memory()
@@ -340,7 +347,8 @@ def main():
             peak, peak_src = peaks["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)"
         else:
             peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-        bh = hop_bytes(n, nnz, d_s, esz, sym, cfg.alpha)
+        l2_size = torch.cuda.get_device_properties(local).L2_cache_size
+        bh, bmodel = hop_bytes(n, nnz, d_s, esz, sym, cfg.alpha, l2_size)
         achieved = bh / (spmm_avg * 1e-3) / 1e9
         traffic = load_traffic(args.config, world, dtype_name)
         l2b = l2_gather_bytes(nnz, n, d_s, esz)
@@ -362,19 +370,22 @@ def main():
                        "layouts": ("peer-direct IPC stores" if args.layouts == "p2p" and not args.overlap
                                    else "NCCL all-to-all") if world > 1 else "local",
                        "l2": f"inputs larger than L2 (col_idx {4 * nnz / 1e6:.0f} MB streamed per hop; "
-                             f"X_v {Xh.nbytes / 1e6:.0f} MB per rank)",
+                             f"X_v {x_bytes / 1e6:.0f} MB per rank)",
                        "graph_setup_s": round(t_graph, 3), "hbm_used_GB_max_rank": round(hbm_used_gb, 1)},
             "roofline": {"kernel": "spmm_hop_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": bh, "avg_launch_ms": spmm_avg,
+                         "algorithmic_bytes_per_launch": bh, "bytes_model": bmodel, "l2_bytes": l2_size,
+                         "avg_launch_ms": spmm_avg,
                          "launches_timed": spmm_n, "peak_source": peak_src,
                          "l2_gather_bytes_per_launch": l2b,
                          "l2_gather_GBps": l2b / (spmm_avg * 1e-3) / 1e9,
                          "gather": gather_line,
-                         "note": "algorithmic bytes = compulsory HBM bytes (DESIGN.md §6): every array once. The "
-                                 "gathered slice rows are re-read through L2 (l2_gather_*); when the slice is "
-                                 "L2-resident the hop is bound by the random-row gather rate, reported against "
-                                 "its measured ceiling in `gather`"},
+                         "note": "algorithmic bytes (DESIGN.md §6, SURVEY §8(d)) by residency: a slice that fits "
+                                 "L2 is read from HBM once (gathered rows re-read through L2: l2_gather_*, and the "
+                                 "hop is bound by the random-row gather rate, reported against its measured ceiling "
+                                 "in `gather`); a slice larger than L2 costs every arc's row slice from HBM "
+                                 "(SURVEY's no-reuse per-edge figure). traffic = ncu dram read+write per launch of "
+                                 "this kernel on this workload (profiles/spmm_traffic.json)"},
             "prop_GE_per_s": 2 * cfg.K * nnz * w / (spmm_ms / len(reps) * 1e-3) / 1e9 * 1.0,
             "phase_ms": {k: round(v, 4) for k, v in phase.items()},
             "clocks": clk,

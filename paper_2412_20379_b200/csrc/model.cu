@@ -559,6 +559,13 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         // per row chunk: Z_v = unpack(gathered) [h x hid]; logits = Z_v W1; dlogits; dW1 += Z_v^T dlogits;
         // dZ_v = dlogits W1^T -> pack into the gradient split
         float* Zv = dH1;   // reuse [hc x ldH]
+        if (head_fused_supported(P, d_s, m->hid, m->C, dt)) {
+            // one tcgen05 pass over all rows (head.cu): logits, dl and dZ stay on chip
+            nb_loss = head_fused(c, gathered, V_p, d_s, P, m->hid, m->C, W1g, ldw1, lab, msk, row0, n, gscale_bwd,
+                                 p2p ? nullptr : gsend, tab_split, dw1_at(0), part, cnt, s);
+            for (int64_t ch = 1; ch < nch; ++ch)
+                NTP_CUDA(cudaMemsetAsync(dw1_at(ch), 0, (size_t)m->hid * m->C * sizeof(float), s));
+        } else
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
             unpack_f2v(c, gathered, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s, nullptr, 0, h, r);
@@ -732,6 +739,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     key.ld = X_v->ld;
     key.graph_version = c->g_version;
     key.head_chunk = getenv("NTP_HEAD_CHUNK") ? atoll(getenv("NTP_HEAD_CHUNK")) : 0;
+    key.head_fused = getenv("NTP_HEAD_FUSED") ? atoll(getenv("NTP_HEAD_FUSED")) : 1;
     int64_t epoch_launches = 0;
     if (graphs_enabled() && c->graph_valid && c->graph_key == key) {
         NTP_CUDA(cudaGraphLaunch(c->graph_exec, s));

@@ -124,9 +124,10 @@ struct EpochKey {
     int64_t ld;
     int64_t graph_version;
     int64_t head_chunk;     // NTP_HEAD_CHUNK (row chunk of the W1-after-propagation epoch)
+    int64_t head_fused;     // NTP_HEAD_FUSED (fused tcgen05 head on/off)
     bool operator==(const EpochKey& o) const {
         return std::memcmp(&m, &o.m, sizeof(m)) == 0 && std::memcmp(ptrs, o.ptrs, sizeof(ptrs)) == 0 && ld == o.ld &&
-               graph_version == o.graph_version && head_chunk == o.head_chunk;
+               graph_version == o.graph_version && head_chunk == o.head_chunk && head_fused == o.head_fused;
     }
 };
 
@@ -139,7 +140,7 @@ struct ntp_ctx {
     // scratch
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
-    ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp;
+    ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp, m_head;
     // peer-direct layouts (CUDA IPC windows over NVLink), see layout.cu
     int p2p_state = 0;                      // 0 not set up, 1 usable, -1 unavailable
     ntp::DevBuf p2p_split, p2p_gath;        // this rank's windows (zero-initialised)
@@ -265,6 +266,13 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
 // B_lo != nullptr: B is already rn_tf32-rounded and B_lo holds the residual (tf32_split), e.g. weights.
 void tf32_split(ntp_ctx* c, const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
                 cudaStream_t s);
+
+// Fused W1-after-propagation head (head.cu): bf16 gathered slice, P*d_s == 128, C <= 192.
+bool head_fused_supported(int32_t P, int32_t d_s, int32_t hid, int32_t C, ntp_dtype dt);
+int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, int32_t P, int32_t hid, int32_t C,
+                   const float* W1, int64_t ldw1, const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n,
+                   const float* gscale, void* out, void* const* peer, float* dW1, double* part, int64_t* cnt,
+                   cudaStream_t s);
 
 inline size_t esize(ntp_dtype d) { return d == NTP_BF16 ? 2 : 4; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -140,3 +140,69 @@ def config_inputs(cfg: "Config", row0: int = 0, rows: int | None = None):
     y = labels(cfg.seed, cfg.n, cfg.C, row0, rows)
     m = train_mask(cfg.seed, cfg.n, row0, rows)
     return X, y, m
+
+
+# ---------------------------------------------------------------- the same formulas on a torch device
+# (bench inputs at papers scale: 14 G feature hashes take minutes in numpy).  int64 two's-complement
+# arithmetic wraps like uint64; right shifts are made logical with a mask; unsigned compare / modulo
+# are rewritten in signed terms.  Pinned against the numpy versions above (tests/test_gpu_graph.py).
+def _i64(x: int) -> int:
+    x &= (1 << 64) - 1
+    return x - (1 << 64) if x >= 1 << 63 else x
+
+
+def _srl(z, k: int):
+    import torch
+    return torch.bitwise_and(torch.bitwise_right_shift(z, k), (1 << (64 - k)) - 1)
+
+
+def hash64_torch(seed: int, stream: int, idx):
+    """h(seed, stream, i) for an int64 torch tensor of counters (result: int64 bit pattern of the uint64)."""
+    base = _i64(seed * 0x9E3779B97F4A7C15 + stream * 0xD1B54A32D192ED03)
+    z = idx + base
+    z = torch_xor(z, _srl(z, 30)) * _i64(0xBF58476D1CE4E5B9)
+    z = torch_xor(z, _srl(z, 27)) * _i64(0x94D049BB133111EB)
+    return torch_xor(z, _srl(z, 31))
+
+
+def torch_xor(a, b):
+    import torch
+    return torch.bitwise_xor(a, b)
+
+
+def _ult(a, t: int):
+    """unsigned a < t for int64 bit patterns a and a python int threshold t in [0, 2^64)."""
+    return (a ^ _i64(1 << 63)) < _i64(t ^ (1 << 63))
+
+
+def config_inputs_device(cfg: "Config", row0: int = 0, rows: int | None = None, device="cuda", ld: int | None = None,
+                         out=None):
+    """config_inputs() computed on a torch device: (X [rows x ld][:, :d_in] fp32, y int32, train mask uint8).
+    out=(X, y, m): write into these (first `rows` rows) instead of allocating."""
+    import torch
+    if rows is None:
+        rows = cfg.n - row0
+    d = cfg.d_in
+    ld = ld or d
+    X = out[0] if out is not None else torch.zeros(rows, ld, dtype=torch.float32, device=device)[:, :d]
+    cols = torch.arange(d, dtype=torch.int64, device=device)
+    step = max(1, (1 << 25) // max(d, 1))
+    for r in range(0, rows, step):
+        rr = min(step, rows - r)
+        idx = (torch.arange(row0 + r, row0 + r + rr, dtype=torch.int64, device=device)[:, None] * d + cols[None, :])
+        h = hash64_torch(cfg.seed, S_FEAT, idx)
+        if cfg.binary_density is None:
+            X[r:r + rr] = (_srl(h, 40).to(torch.float64) / float(1 << 23) - 1.0).to(torch.float32)
+        else:
+            X[r:r + rr] = _ult(h, int(cfg.binary_density * float(1 << 64))).to(torch.float32)
+    v = torch.arange(row0, row0 + rows, dtype=torch.int64, device=device)
+    hl = hash64_torch(cfg.seed, S_LABEL, v)
+    hi, lo = _srl(hl, 32), torch.bitwise_and(hl, 0xFFFFFFFF)
+    y = (((hi % cfg.C) * ((1 << 32) % cfg.C) + lo) % cfg.C).to(torch.int32)
+    hm = hash64_torch(cfg.seed, S_MASK, v)
+    m = _ult(hm, int(0.65 * float(1 << 64))).to(torch.uint8)
+    if out is not None:
+        out[1][:rows] = y
+        out[2][:rows] = m
+        return out
+    return X, y, m

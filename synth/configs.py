@@ -75,6 +75,10 @@ _add(Config("small_dir", 14, 50_000, 16, 800_000, REDDIT_ABC, False, 64, 48, 19,
 # variants (streaming narrow-row hop) only run on these; hubs span several merge-path units
 _add(Config("dense_sym", 16, 8_000, 13, 260_000, REDDIT_ABC, True, 40, 24, 9, 3, 0.9, 0.1))
 _add(Config("dense_dir", 17, 6_007, 13, 420_000, REDDIT_ABC, False, 36, 16, 11, 2, 1.0, 0.0))
+# W1-after-propagation with the papers head shape (hid 128 = P*d_s at every P, C = 172 over three
+# 64-class boxes; C = 41 ragged in one box): the fused tcgen05 head (head.cu) runs on bf16 storage
+_add(Config("head_dir", 18, 5_003, 13, 60_000, GRAPH500, False, 32, 128, 172, 2, 1.0, 0.0, w_after_prop=True))
+_add(Config("head_sym", 19, 3_001, 12, 30_000, REDDIT_ABC, True, 24, 128, 41, 3, 0.9, 0.1, w_after_prop=True))
 
 
 def get_config(name: str) -> Config:

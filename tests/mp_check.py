@@ -160,6 +160,24 @@ def main(name):
         assert abs(rep["loss"] - ref_losses[e]) <= 1e-4, f"reordered loss {rep['loss']} vs {ref_losses[e]}"
     ctxr.close()
     ctxr1.close()
+
+    # ---- 5. bf16 storage epochs (the fused tcgen05 head where P*d_s = 128, e.g. head_dir): losses vs
+    # the oracle within 2e-2 relative; peer-direct and NCCL layouts bitwise equal
+    bres = []
+    for mode in ("nccl", "p2p"):
+        W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+        model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
+                     dtype=ntp.NTP_BF16, chunks=1,
+                     flags=(ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0)
+                     | (ntp.NTP_M_P2P_LAYOUTS if mode == "p2p" else 0))
+        losses = []
+        for e in range(2):
+            rep = ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
+            losses.append(rep["loss"])
+            assert abs(rep["loss"] - ref_losses[e]) <= 2e-2 * abs(ref_losses[e]), \
+                f"bf16 loss {rep['loss']} vs oracle {ref_losses[e]} (mode={mode})"
+        bres.append((losses, W0.cpu(), W1.cpu()))
+    assert bres[0][0] == bres[1][0] and torch.equal(bres[0][1], bres[1][1]) and torch.equal(bres[0][2], bres[1][2])
     dist.barrier()
     if rank == 0:
         print(f"MP OK world={world} config={name} losses={results[1][0]}", flush=True)

@@ -127,3 +127,37 @@ def test_epoch_chunked_head(chunk, dtype, monkeypatch):
     if dtype == 0:
         for got, ref in ((W0, rW0), (W1, rW1)):
             assert np.abs(got - ref).max() <= 1e-4 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("name", ["head_dir", "head_sym"])
+@pytest.mark.parametrize("fused", [1, 0])
+def test_epoch_head_bf16(name, fused, monkeypatch):
+    """W1 after propagation on bf16 storage with the papers head shape (hid 128, C 172 / 41): the fused
+    tcgen05 head (head.cu: logits, softmax-xent, dl, dW1 = Z^T dl, dZ = dl W1^T packed into the
+    gradient split) and the unfused path both give the oracle's losses within 2e-2 relative, and the
+    weight CHANGES after 2 SGD steps (which carry dW1 and, through the backward hops, dW0) within 2e-2
+    of the oracle's normwise -- a transposed or dropped operand in the head fails here."""
+    from paper_2412_20379_b200 import ntp
+    monkeypatch.setenv("NTP_HEAD_FUSED", str(fused))
+    cfg = synth.get_config(name)
+    W0i, W1i = synth.model_weights(cfg)
+    losses, W0, W1, reps, model = _train_gpu(name, 2, dtype=ntp.NTP_BF16)
+    ref_losses, rW0, rW1 = _train_oracle(name, 2, model["lr"])
+    for e, (a, b) in enumerate(zip(losses, ref_losses)):
+        assert abs(a - b) <= 2e-2 * abs(b), f"epoch {e}: gpu {a} oracle {b}"
+    for got, ref, init in ((W0, rW0, W0i), (W1, rW1, W1i)):
+        d_ref = ref.astype(np.float64) - init
+        d_got = got.astype(np.float64) - init
+        assert np.linalg.norm(d_got - d_ref) <= 2e-2 * np.linalg.norm(d_ref)
+
+
+def test_epoch_head_fused_matches_unfused(monkeypatch):
+    """The fused head and the unfused chunked path agree on the loss of the first epoch to bf16-level
+    (both consume the same gathered bf16 slice; they differ in dl rounding and summation order)."""
+    from paper_2412_20379_b200 import ntp
+    out = []
+    for fused in (1, 0):
+        monkeypatch.setenv("NTP_HEAD_FUSED", str(fused))
+        losses, _, _, _, _ = _train_gpu("head_dir", 1, dtype=ntp.NTP_BF16)
+        out.append(losses[0])
+    assert abs(out[0] - out[1]) <= 1e-3 * abs(out[1])

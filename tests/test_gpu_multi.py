@@ -19,7 +19,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name", ["small_dir", "small_appnp", "tiny_dir", "cora"])
+@pytest.mark.parametrize("name", ["small_dir", "small_appnp", "tiny_dir", "cora", "head_dir"])
 def test_multi_gpu(name):
     ngpu = torch.cuda.device_count()
     if ngpu < 2:
