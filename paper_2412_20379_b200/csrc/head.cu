@@ -16,14 +16,18 @@
 // (2^-17 relative); dl is rounded to bf16 once (2^-9 relative, the same rounding the gradient slice
 // gets when it is stored).  fp32 accumulation in TMEM.
 //
-// CTA: 12 warps, 1 CTA/SM, persistent over tiles (tile t → CTA t mod grid).
-//   warp 0    : TMEM allocation (512 columns) + MMA issuer (one lane)
-//   warps 1-3 : Z loader (16-byte global loads → 128B-swizzled K-major smem tile, double-buffered)
-//   warps 4-7 : softmax epilogue (thread = tile row: tcgen05.ld logits → loss, dl → smem)
-//   warps 8-11: dZ epilogue (tcgen05.ld dZ → scale, bf16 → gradient slice), final dW1 read-out
+// CTA: 16 warps, 1 CTA/SM, persistent over tiles (tile t → CTA t mod grid).
+//   warp 0     : TMEM allocation (512 columns) + MMA issuer (one lane)
+//   warps 1-3  : Z loader (16-byte global loads → 128B-swizzled K-major smem tile, double-buffered)
+//   warps 4-11 : softmax epilogue, two warps per TMEM lane quarter (thread = tile row, each warp half
+//                of the 32-column chunks; row max / sum combined through shared memory): loss, dl → smem
+//   warps 12-15: dZ epilogue (tcgen05.ld dZ → scale, bf16 → gradient slice), final dW1 read-out
+// MMA order per tile i: MMA1(i+1) is issued before MMA2(i)/MMA3(i), so the softmax of tile i+1 starts
+// while the tensor core still works on tile i's gradients.
 // TMEM columns: [0, 192) logits, [192, 320) dZ, [320, 512) dW1 (lanes = hidden index).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "ntp_internal.cuh"
 #include "ptx.cuh"
@@ -32,7 +36,7 @@ namespace ntp {
 
 namespace {
 
-constexpr int kHeadThreads = 384;
+constexpr int kHeadThreads = 512;
 constexpr int HP = 128;             // padded hidden width P·d_s (K of MMA1, N of MMA2, M of MMA3)
 constexpr int kBox = 128 * 128;     // one 128-row × 128-byte swizzled box (64 bf16 columns)
 constexpr uint32_t kColLogits = 0, kColDZ = 192, kColDW = 320;
@@ -40,7 +44,7 @@ constexpr uint32_t kColLogits = 0, kColDZ = 192, kColDW = 320;
 struct HeadParams {
     const __nv_bfloat16* Z;     // gathered [P][V_p][d_s]
     int64_t V_p;
-    int d_s, P;
+    int d_s, P, lds;            // lds = log2(d_s) (d_s = 128 / P, P a power of two)
     int C, CB, n1, kc;          // classes, 64-class boxes, N of MMA1/3 (C rounded to 16), K steps of MMA2
     const __nv_bfloat16* W1s;   // [2][HP][CB*64] bf16: hi then lo, zero padded
     const int32_t* y;
@@ -56,6 +60,7 @@ struct HeadParams {
     int64_t* cnt;               // [grid]
     int64_t tiles;
     uint32_t idesc1, idesc2, idesc3;
+    int tma;                    // d_s >= 64: Z tiles by TMA (3-D map [P][V_p][d_s], 64-column boxes)
 };
 
 __device__ __forceinline__ uint32_t swz(int r, int col) {   // byte offset of (row, col) in a box set
@@ -93,12 +98,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ float ex2(float x) {   // 2^x (MUFU.EX2; ex2(-inf) = 0)
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-__global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadParams p) {
+__global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __grid_constant__ CUtensorMap tmZ,
+                                                                     const HeadParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sZ = smem;                              // [2][2 boxes]
@@ -117,18 +128,19 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadP
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 12);
     double* s_loss = reinterpret_cast<double*>(bars + 16);      // [128]
     int64_t* s_cnt = reinterpret_cast<int64_t*>(s_loss + 128);  // [128]
+    float* s_stat = reinterpret_cast<float*>(s_cnt + 128);      // [tile parity][half][m, s, xy][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nloc = (int)((p.tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);   // tiles of this CTA
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&zfull[b], 96);
+            ptx::mbar_init(&zfull[b], p.tma ? 1 : 96);
             ptx::mbar_init(&zfree[b], 1);
         }
         ptx::mbar_init(lfull, 1);
-        ptx::mbar_init(lfree, 128);
-        ptx::mbar_init(dlfull, 128);
+        ptx::mbar_init(lfree, 256);
+        ptx::mbar_init(dlfull, 256);
         ptx::mbar_init(dlfree, 1);
         ptx::mbar_init(dzfull, 1);
         ptx::mbar_init(dzfree, 128);
@@ -163,20 +175,24 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadP
         if (lane == 0 && nloc > 0) {
             // ------------------------------------------------ MMA issuer
             const uint32_t zb = ptx::smem_u32(sZ), dlb = ptx::smem_u32(sDL), wb = ptx::smem_u32(sW);
-            for (int i = 0; i < nloc; ++i) {
-                const int b = i & 1;
-                const uint32_t za = zb + b * 2 * kBox;
-                ptx::mbar_wait(&zfull[b], (i >> 1) & 1);
-                if (i > 0) ptx::mbar_wait(lfree, (i - 1) & 1);
+            // MMA1: logits[128 x n1] = Z[128 x 128] . W1[128 x n1]   (A K-major, B MN-major)
+            auto mma1 = [&](int t) {
+                const uint32_t za = zb + (t & 1) * 2 * kBox;
+                ptx::mbar_wait(&zfull[t & 1], (t >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                // MMA1: logits[128 x n1] = Z[128 x 128] . W1[128 x n1]   (A K-major, B MN-major)
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
                     for (int k = 0; k < HP / 16; ++k)
                         mma_bf16(tmem + kColLogits, desc_k(za + (k >> 2) * kBox + (k & 3) * 32),
                                  desc_mn(wb + h * p.CB * kBox + k * 2048), p.idesc1, (h | k) ? 1u : 0u);
                 commit(lfull);
-                ptx::mbar_wait(dlfull, i & 1);
+            };
+            mma1(0);
+            for (int i = 0; i < nloc; ++i) {
+                const uint32_t za = zb + (i & 1) * 2 * kBox;
+                ptx::mbar_wait(lfree, i & 1);      // logits of tile i drained (softmax pass 2 done)
+                ptx::mbar_wait(dlfull, i & 1);     // dl of tile i in shared memory
+                if (i + 1 < nloc) mma1(i + 1);
                 if (i > 0) ptx::mbar_wait(dzfree, (i - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 // MMA2: dZ[128 x 128] = dl[128 x C] . W1^T   (A K-major dl, B K-major W1 rows)
@@ -192,21 +208,42 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadP
                     mma_bf16(tmem + kColDW, desc_mn(za + k * 2048), desc_mn(dlb + k * 2048), p.idesc3,
                              (i > 0 || k > 0) ? 1u : 0u);
                 commit(dlfree);
-                commit(&zfree[b]);
+                commit(&zfree[i & 1]);
             }
             commit(dwfull);
         }
+    } else if (warp < 4 && p.tma) {
+        // ---------------------------------------------------- Z producer: TMA (one lane)
+        if (warp == 1 && lane == 0) {
+            for (int i = 0; i < nloc; ++i) {
+                const int b = i & 1;
+                if (i >= 2) ptx::mbar_wait(&zfree[b], ((i >> 1) - 1) & 1);
+                const int v0 = (int)((blockIdx.x + (int64_t)i * gridDim.x) * 128);
+                uint8_t* za = sZ + b * 2 * kBox;
+                ptx::mbar_expect_tx(&zfull[b], 2 * kBox);
+#pragma unroll
+                for (int bx = 0; bx < 2; ++bx) {   // 64-column box bx = columns [64 bx, 64 bx + 64)
+                    const int col = 64 * bx;
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+                        "%5}], [%2];" ::"r"(ptx::smem_u32(za + bx * kBox)),
+                        "l"(reinterpret_cast<uint64_t>(&tmZ)), "r"(ptx::smem_u32(&zfull[b])), "r"(col & (p.d_s - 1)),
+                        "r"(v0), "r"(col >> p.lds)
+                        : "memory");
+                }
+            }
+        }
     } else if (warp < 4) {
-        // ---------------------------------------------------- Z loader
+        // ---------------------------------------------------- Z loader (d_s < 64: 16-byte loads)
         const int t = threadIdx.x - 32;
-        const int cpr = p.d_s / 8;                 // 16-byte chunks per row of a block
-        const int per_block = 128 * cpr;
+        const int lcpr = p.lds - 3;                // log2(16-byte chunks per row of a block)
+        const int lpb = 7 + lcpr;                  // log2(chunks per 128-row block tile)
         for (int i = 0; i < nloc; ++i) {
             const int b = i & 1;
             if (i >= 2) ptx::mbar_wait(&zfree[b], ((i >> 1) - 1) & 1);
             const int64_t v0 = (blockIdx.x + (int64_t)i * gridDim.x) * 128;
             uint8_t* za = sZ + b * 2 * kBox;
-            constexpr int U = 8;
+            constexpr int U = 22;                  // 2048 chunks / 96 threads: one round per tile
             for (int f0 = t; f0 < 2048; f0 += 96 * U) {
                 uint4 x[U];
 #pragma unroll
@@ -214,8 +251,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadP
                     const int f = f0 + u * 96;
                     x[u] = make_uint4(0, 0, 0, 0);
                     if (f < 2048) {
-                        const int q = f / per_block, rem = f - q * per_block;
-                        const int r = rem / cpr, jc = rem - r * cpr;
+                        const int q = f >> lpb, rem = f & ((1 << lpb) - 1);
+                        const int r = rem >> lcpr, jc = rem & ((1 << lcpr) - 1);
                         if (v0 + r < p.V_p)
                             x[u] = __ldg(reinterpret_cast<const uint4*>(p.Z + ((int64_t)q * p.V_p + v0 + r) * p.d_s) + jc);
                     }
@@ -224,57 +261,85 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadP
                 for (int u = 0; u < U; ++u) {
                     const int f = f0 + u * 96;
                     if (f < 2048) {
-                        const int q = f / per_block, rem = f - q * per_block;
-                        const int r = rem / cpr, jc = rem - r * cpr;
-                        *reinterpret_cast<uint4*>(za + swz(r, q * p.d_s + jc * 8)) = x[u];
+                        const int q = f >> lpb, rem = f & ((1 << lpb) - 1);
+                        const int r = rem >> lcpr, jc = rem & ((1 << lcpr) - 1);
+                        *reinterpret_cast<uint4*>(za + swz(r, (q << p.lds) + jc * 8)) = x[u];
                     }
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             ptx::mbar_arrive(&zfull[b]);
         }
-    } else if (warp < 8) {
-        // ---------------------------------------------------- softmax epilogue (thread = row)
+    } else if (warp < 12) {
+        // ---------------------------------------------------- softmax epilogue (thread = row; two warps
+        // per lane quarter, warp half hf takes the 32-column chunks cc with cc % 2 == hf)
         const int qd = warp & 3;
+        const int hf = (warp - 4) >> 2;
         const int r = qd * 32 + lane;
         const uint32_t lrow = tmem + ((uint32_t)(qd * 32) << 16);
+        constexpr float L2E = 1.4426950408889634f;
         double my_loss = 0.0;
         int64_t my_cnt = 0;
         const int nch = (p.C + 31) / 32;
+        // mask and label of tile i+1 are loaded while tile i is processed (two independent loads, off
+        // the per-tile critical path)
+        auto row_of = [&](int t) { return (blockIdx.x + (int64_t)t * gridDim.x) * 128 + r; };
+        auto real_row = [&](int64_t v) { return v < p.V_p && p.row0 + v < p.n; };
+        uint8_t mk_n = 0;
+        int y_n = 0;
+        if (nloc > 0 && real_row(row_of(0))) {
+            mk_n = __ldg(p.mask + row_of(0));
+            y_n = __ldg(p.y + row_of(0));
+        }
         for (int i = 0; i < nloc; ++i) {
-            const int64_t v = (blockIdx.x + (int64_t)i * gridDim.x) * 128 + r;
-            const bool real = v < p.V_p && p.row0 + v < p.n;
-            const bool train = real && p.mask[v] != 0;
-            const int yv = train ? p.y[v] : -1;
+            const int64_t v = row_of(i);
+            const bool train = real_row(v) && mk_n != 0;
+            const int yv = train ? y_n : -1;
+            if (i + 1 < nloc && real_row(row_of(i + 1))) {
+                mk_n = __ldg(p.mask + row_of(i + 1));
+                y_n = __ldg(p.y + row_of(i + 1));
+            }
             ptx::mbar_wait(lfull, i & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            float m = -INFINITY, s = 0.f, xy = 0.f;
-            for (int cc = 0; cc < nch; ++cc) {
+            // pass 1: online max / sum of exp over my chunks (masked columns are -inf: exp -> 0)
+            float m = -INFINITY, sum = 0.f, xy = 0.f;
+            for (int cc = hf; cc < nch; cc += 2) {
                 uint32_t x[32];
                 tmem_ld32(lrow + kColLogits + cc * 32, x);
+                float f[32];
                 float cm = -INFINITY;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const int col = cc * 32 + j;
-                    const float f = __uint_as_float(x[j]);
-                    if (col < p.C) cm = fmaxf(cm, f);
-                    if (col == yv) xy = f;
+                    f[j] = col < p.C ? __uint_as_float(x[j]) : -INFINITY;
+                    cm = fmaxf(cm, f[j]);
+                    xy = col == yv ? f[j] : xy;
                 }
                 const float mn = fmaxf(m, cm);
+                const float mnl = mn * L2E;
                 float add = 0.f;
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (cc * 32 + j < p.C) add += __expf(__uint_as_float(x[j]) - mn);
-                s = s * __expf(m - mn) + add;
+                for (int j = 0; j < 32; ++j) add += ex2(fmaf(f[j], L2E, -mnl));
+                sum = sum * ex2((m - mn) * L2E) + add;
                 m = mn;
             }
-            if (train) {
-                my_loss += (double)(logf(s) + m - xy);
+            float* st = s_stat + (i & 1) * 768;
+            st[hf * 384 + r] = m;
+            st[hf * 384 + 128 + r] = sum;
+            st[hf * 384 + 256 + r] = xy;
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + qd) : "memory");
+            const float m0 = st[r], s0 = st[128 + r], m1 = st[384 + r], s1 = st[384 + 128 + r];
+            const float mx = fmaxf(m0, m1);
+            const float se = s0 * ex2((m0 - mx) * L2E) + s1 * ex2((m1 - mx) * L2E);   // same order in both halves
+            if (hf == 0 && train) {
+                const float ly = st[(((yv >> 5) & 1) ? 384 : 0) + 256 + r];
+                my_loss += (double)(logf(se) + mx - ly);
                 my_cnt += 1;
             }
-            const float inv = 1.f / s;
+            const float inv = 1.f / se;
+            const float mxl = mx * L2E;
             if (i > 0) ptx::mbar_wait(dlfree, (i - 1) & 1);
-            for (int cc = 0; cc < 2 * p.CB; ++cc) {
+            for (int cc = hf; cc < 2 * p.CB; cc += 2) {
                 uint32_t x[32];
                 if (cc < nch) tmem_ld32(lrow + kColLogits + cc * 32, x);
                 uint32_t w[16];
@@ -284,9 +349,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadP
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int col = cc * 32 + 2 * j + e;
-                        g[e] = (train && col < p.C)
-                                   ? __expf(__uint_as_float(x[2 * j + e]) - m) * inv - (col == yv ? 1.f : 0.f)
-                                   : 0.f;
+                        const float pr = ex2(fmaf(__uint_as_float(x[2 * j + e]), L2E, -mxl)) * inv;
+                        g[e] = (train && col < p.C) ? pr - (col == yv ? 1.f : 0.f) : 0.f;
                     }
                     w[j] = pack_bf16(g[0], g[1]);
                 }
@@ -300,17 +364,25 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadP
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             ptx::mbar_arrive(dlfull);
         }
-        s_loss[r] = my_loss;
-        s_cnt[r] = my_cnt;
+        if (hf == 0) {
+            s_loss[r] = my_loss;
+            s_cnt[r] = my_cnt;
+        }
     } else {
-        // ---------------------------------------------------- dZ epilogue (thread = row)
+        // ---------------------------------------------------- dZ epilogue (thread = row, warps 12-15)
         const int qd = warp & 3;
         const int r = qd * 32 + lane;
         const uint32_t lrow = tmem + ((uint32_t)(qd * 32) << 16);
+        auto scale_of = [&](int t) {
+            const int64_t v = (blockIdx.x + (int64_t)t * gridDim.x) * 128 + r;
+            return (v < p.V_p && p.row0 + v < p.n) ? __ldg(p.gscale + p.row0 + v) : 0.f;
+        };
+        float sc_n = nloc > 0 ? scale_of(0) : 0.f;
         for (int i = 0; i < nloc; ++i) {
             const int64_t v = (blockIdx.x + (int64_t)i * gridDim.x) * 128 + r;
             const bool inb = v < p.V_p;
-            const float sc = (inb && p.row0 + v < p.n) ? __ldg(p.gscale + p.row0 + v) : 0.f;
+            const float sc = sc_n;
+            if (i + 1 < nloc) sc_n = scale_of(i + 1);
             ptx::mbar_wait(dzfull, i & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int cc = 0; cc < HP / 32; ++cc) {
@@ -320,7 +392,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const HeadP
 #pragma unroll
                 for (int c8 = 0; c8 < 4; ++c8) {
                     const int col = cc * 32 + c8 * 8;
-                    const int q = col / p.d_s, j = col - q * p.d_s;
+                    const int q = col >> p.lds, j = col & (p.d_s - 1);
                     uint4 o;
                     o.x = pack_bf16(__uint_as_float(x[c8 * 8 + 0]) * sc, __uint_as_float(x[c8 * 8 + 1]) * sc);
                     o.y = pack_bf16(__uint_as_float(x[c8 * 8 + 2]) * sc, __uint_as_float(x[c8 * 8 + 3]) * sc);
@@ -402,7 +474,8 @@ constexpr uint32_t idesc_bf16(int N, bool a_mn, bool b_mn) {
 
 bool head_fused_supported(int32_t P, int32_t d_s, int32_t hid, int32_t C, ntp_dtype dt) {
     const char* v = getenv("NTP_HEAD_FUSED");   // read per call (part of the epoch graph key)
-    return !(v && atoi(v) == 0) && dt == NTP_BF16 && (int64_t)P * d_s == HP && hid <= HP && d_s % 8 == 0 && C >= 1 && C <= 192;
+    return !(v && atoi(v) == 0) && dt == NTP_BF16 && (int64_t)P * d_s == HP && hid <= HP && d_s >= 8 &&
+           (d_s & (d_s - 1)) == 0 && C >= 1 && C <= 192;
 }
 
 int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, int32_t P, int32_t hid, int32_t C,
@@ -414,6 +487,8 @@ int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, i
     p.V_p = V_p;
     p.d_s = d_s;
     p.P = P;
+    p.lds = 0;
+    while ((1 << p.lds) < d_s) ++p.lds;
     p.C = C;
     p.CB = (C + 63) / 64;
     p.n1 = (C + 15) / 16 * 16;
@@ -442,16 +517,32 @@ int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, i
     p.idesc1 = idesc_bf16(p.n1, false, true);
     p.idesc2 = idesc_bf16(HP, false, false);
     p.idesc3 = idesc_bf16(p.n1, true, true);
+    const char* te = getenv("NTP_HEAD_TMA");   // 0: force the 16-byte-load Z loader (tests cover both paths)
+    p.tma = (d_s >= 64 && !(te && atoi(te) == 0)) ? 1 : 0;
+    CUtensorMap tmZ;
+    std::memset(&tmZ, 0, sizeof(tmZ));
+    if (p.tma) {
+        const cuuint64_t dims[3] = {(cuuint64_t)d_s, (cuuint64_t)V_p, (cuuint64_t)P};
+        const cuuint64_t strides[2] = {(cuuint64_t)d_s * 2, (cuuint64_t)V_p * d_s * 2};
+        const cuuint32_t box[3] = {64, 128, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        NTP_CHECK(((uintptr_t)gathered % 16) == 0, NTP_ERR_SHAPE, "fused head: gathered slice not 16-byte aligned");
+        CUresult r = tensor_map_encoder()(&tmZ, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(gathered), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        NTP_CHECK(r == CUDA_SUCCESS, NTP_ERR_CUDA, "cuTensorMapEncodeTiled (head Z) failed (%d)", (int)r);
+    }
     head_w1_split_kernel<<<(HP * cols + 255) / 256, 256, 0, s>>>(W1, ldw1, hid, C, cols, w1s);
     NTP_LAUNCH_CHECK();
-    const size_t smem = 1024 + (size_t)(4 + 3 * p.CB) * kBox + 16 * 8 + 256 * 8 + 64;
+    const size_t smem = 1024 + (size_t)(4 + 3 * p.CB) * kBox + 16 * 8 + 256 * 8 + 2 * 768 * 4 + 64;
     static bool attr = false;
     if (!attr) {
         NTP_CUDA(cudaFuncSetAttribute(head_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
     NTP_CHECK(smem <= 227 * 1024, NTP_ERR_CONFIG, "fused head needs %zu B of shared memory", smem);
-    head_fused_kernel<<<grid, kHeadThreads, smem, s>>>(p);
+    head_fused_kernel<<<grid, kHeadThreads, smem, s>>>(tmZ, p);
     NTP_LAUNCH_CHECK();
     const int64_t total = (int64_t)hid * C;
     head_dw1_reduce_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 4), 256, 0, s>>>(dwp, grid, total, dW1);

@@ -739,7 +739,8 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     key.ld = X_v->ld;
     key.graph_version = c->g_version;
     key.head_chunk = getenv("NTP_HEAD_CHUNK") ? atoll(getenv("NTP_HEAD_CHUNK")) : 0;
-    key.head_fused = getenv("NTP_HEAD_FUSED") ? atoll(getenv("NTP_HEAD_FUSED")) : 1;
+    key.head_fused = (getenv("NTP_HEAD_FUSED") ? atoll(getenv("NTP_HEAD_FUSED")) : 1) +
+                     2 * (getenv("NTP_HEAD_TMA") ? atoll(getenv("NTP_HEAD_TMA")) : 1);
     int64_t epoch_launches = 0;
     if (graphs_enabled() && c->graph_valid && c->graph_key == key) {
         NTP_CUDA(cudaGraphLaunch(c->graph_exec, s));

@@ -130,8 +130,8 @@ def test_epoch_chunked_head(chunk, dtype, monkeypatch):
 
 
 @pytest.mark.parametrize("name", ["head_dir", "head_sym"])
-@pytest.mark.parametrize("fused", [1, 0])
-def test_epoch_head_bf16(name, fused, monkeypatch):
+@pytest.mark.parametrize("fused,tma", [(1, 1), (1, 0), (0, 1)])
+def test_epoch_head_bf16(name, fused, tma, monkeypatch):
     """W1 after propagation on bf16 storage with the papers head shape (hid 128, C 172 / 41): the fused
     tcgen05 head (head.cu: logits, softmax-xent, dl, dW1 = Z^T dl, dZ = dl W1^T packed into the
     gradient split) and the unfused path both give the oracle's losses within 2e-2 relative, and the
@@ -139,6 +139,7 @@ def test_epoch_head_bf16(name, fused, monkeypatch):
     of the oracle's normwise -- a transposed or dropped operand in the head fails here."""
     from paper_2412_20379_b200 import ntp
     monkeypatch.setenv("NTP_HEAD_FUSED", str(fused))
+    monkeypatch.setenv("NTP_HEAD_TMA", str(tma))     # 0: the 16-byte-load Z loader (the P >= 4 path)
     cfg = synth.get_config(name)
     W0i, W1i = synth.model_weights(cfg)
     losses, W0, W1, reps, model = _train_gpu(name, 2, dtype=ntp.NTP_BF16)
