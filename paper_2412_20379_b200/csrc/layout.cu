@@ -228,7 +228,20 @@ bool p2p_ensure(ntp_ctx* c, size_t sb, size_t gb, cudaStream_t s) {
     const int P = c->world;
     static const bool enabled = [] { const char* e = getenv("NTP_P2P"); return !(e && atoi(e) == 0); }();
     if (P <= 1 || c->p2p_state < 0 || !enabled) return false;
-    if (c->p2p_state == 1 && sb <= c->p2p_split_bytes && gb <= c->p2p_gath_bytes) return true;
+    if (c->p2p_state == 1 && sb <= c->p2p_split_bytes && gb <= c->p2p_gath_bytes) {
+        if (sb == c->p2p_used_sb && gb == c->p2p_used_gb) return true;
+        if (c->capturing) return false;
+        // same windows, new layout (another dtype or slice width): bytes of the old layout would show
+        // through as this layout's never-written padding rows (a bf16 view of fp32 data can hold NaN
+        // patterns), so the windows are cleared -- collectively, between two barriers
+        p2p_barrier(c, s);
+        NTP_CUDA(cudaMemsetAsync(c->p2p_split.p, 0, c->p2p_split_bytes, s));
+        NTP_CUDA(cudaMemsetAsync(c->p2p_gath.p, 0, c->p2p_gath_bytes, s));
+        p2p_barrier(c, s);
+        c->p2p_used_sb = sb;
+        c->p2p_used_gb = gb;
+        return true;
+    }
     if (c->capturing) return false;
     c->p2p_bar.ensure(16);
     NTP_CUDA(cudaMemsetAsync(c->p2p_bar.p, 0, 16, s));
@@ -287,6 +300,8 @@ bool p2p_ensure(ntp_ctx* c, size_t sb, size_t gb, cudaStream_t s) {
     NTP_CUDA(cudaMemcpy(c->p2p_tab.p, tab.data(), 2 * P * sizeof(void*), cudaMemcpyHostToDevice));
     c->p2p_split_bytes = nsb;
     c->p2p_gath_bytes = ngb;
+    c->p2p_used_sb = sb;
+    c->p2p_used_gb = gb;
     c->p2p_state = 1;
     return true;
 }

@@ -477,6 +477,18 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     const bool p2p = !local && !overlap && (m->flags & NTP_M_P2P_LAYOUTS) && p2p_ensure(c, win, win, s);
     void* const* tab_split = p2p ? c->p2p_tab.as<void*>() : nullptr;
     void* const* tab_gath = p2p ? c->p2p_tab.as<void*>() + P : nullptr;
+    // Rows [n, V_pad) of every buffer that serves as a feature slice are padding: no hop writes them,
+    // and every consumer multiplies them by zero (dl = 0, X = 0, mask bits 0) -- so they must hold
+    // zeros, not stale bytes of an earlier allocation (a bf16 view of old fp32 data can be NaN, and
+    // 0 * NaN = NaN in dW1).  Cleared every epoch (< P rows per buffer).
+    if (!local && V_pad > n) {
+        const size_t off = (size_t)n * d_s * es, len = (size_t)(V_pad - n) * d_s * es;
+        for (void* b : {c->recv.p, c->xfer.p, c->send.p})
+            NTP_CUDA(cudaMemsetAsync(static_cast<char*>(b) + off, 0, len, s));
+        if (p2p)
+            for (void* b : {c->p2p_split.p, c->p2p_gath.p})
+                NTP_CUDA(cudaMemsetAsync(static_cast<char*>(b) + off, 0, len, s));
+    }
     void* slice_in = p2p ? c->p2p_split.p : c->recv.p;   // this rank's feature slice after a split
     void* split_dst = p2p ? nullptr : (local ? c->recv.p : c->send.p);   // where the split's producer writes
 

@@ -145,6 +145,7 @@ struct ntp_ctx {
     int p2p_state = 0;                      // 0 not set up, 1 usable, -1 unavailable
     ntp::DevBuf p2p_split, p2p_gath;        // this rank's windows (zero-initialised)
     size_t p2p_split_bytes = 0, p2p_gath_bytes = 0;
+    size_t p2p_used_sb = 0, p2p_used_gb = 0;   // layout the windows currently hold (cleared on change)
     std::vector<void*> p2p_peer_split, p2p_peer_gath;   // opened peer mappings (own entry = local)
     ntp::DevBuf p2p_tab;                    // device: [2][P] pointers (split windows, gather windows)
     ntp::DevBuf p2p_bar;                    // one int for the barrier allreduce

@@ -187,4 +187,10 @@ def main(name):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "small_dir")
+    try:
+        main(sys.argv[1] if len(sys.argv) > 1 else "small_dir")
+    except Exception as e:  # the failing assertion on stdout (torchrun's stderr is long)
+        import traceback
+        print(f"MP FAIL rank {os.environ.get('RANK')}: {type(e).__name__}: {e}\n{traceback.format_exc()[-1500:]}",
+              flush=True)
+        raise
