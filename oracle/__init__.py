@@ -13,9 +13,10 @@ Modules
   propagate  O3/O4: K-hop forward / backward (adjoint) propagation
   model      O5–O9: MLP, decoupled model function, loss, gradients, SGD epoch
   layout     a1/a3/a5: partition maps, vertex <-> feature layouts (definitions)
+  coupled    NEXT-1: the coupled L-layer GCN that naive tensor parallelism trains (baseline)
 
 Parity pins live in tests/test_oracle_*.py.  Functions without a pin say
 "parity unpinned" in their docstring (none at present).
 """
 from ._lib import lib, build_oracle_lib  # noqa: F401
-from . import graph, propagate, model, layout  # noqa: F401
+from . import graph, propagate, model, layout, coupled  # noqa: F401
