@@ -250,7 +250,40 @@ ntp_status ntp_train_epoch(ntp_ctx* ctx, const ntp_model* m, const ntp_tensor* X
                            const int32_t* labels_v, const uint8_t* train_mask_v,
                            ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, ntp_stream s);
 
+/* NEXT-1: naive (coupled) GNN tensor parallelism, the paper's baseline for the
+ * decoupled epoch ("twice per layer", Fig. 6).  One epoch of the L-layer GCN
+ *   H^0 = X_v;  H^l = ReLU(A^ H^{l-1} W^l) (l < L);  logits = A^ H^{L-1} W^L
+ * (Eq. 3-4, two-sided A^ of reading R1, no bias) with every aggregation on this rank's
+ * feature slice: a split before and a gather after each layer's hop, forward and (layers 2..L)
+ * backward -> 4L - 2 layout changes per epoch.  Loss / gradients / SGD as ntp_train_epoch
+ * (O7-O9: softmax cross-entropy over the global train rows, ReLU'(0) = 0, W -= lr dW).
+ *   m->widths[0..L]: d_in, hidden widths..., C (C <= 256); 1 <= L <= NTP_MAX_LAYERS; dtype = slice
+ *   storage (fp32 accumulation).  X_v: this rank's rows [V_p x d_in] fp32 (device).  W[l]: dense
+ *   [widths[l] x widths[l+1]] fp32 device tensors, updated in place.  Synchronous; eager (no graph).
+ * Errors: NTP_ERR_ARG / NTP_ERR_SHAPE before any device work; NTP_ERR_STATE without a graph. */
+#define NTP_MAX_LAYERS 8
+typedef struct {
+    int32_t L;
+    int32_t widths[NTP_MAX_LAYERS + 1];
+    float lr;
+    ntp_dtype dtype;
+    uint32_t flags;            /* reserved, 0 */
+} ntp_coupled_model;
+typedef struct {
+    double loss;               /* pre-update loss of this epoch                              */
+    int64_t n_train;
+    int32_t layout_changes;    /* split / gather all-to-alls issued (4L - 2 when P > 1)      */
+    int32_t hops;              /* SpMM hop launches                                          */
+    int64_t bytes_sent, bytes_recv;   /* per rank, over all layout changes                   */
+    double ms_total, ms_agg;   /* CUDA-event times: whole epoch, SpMM hops                    */
+    int64_t kernel_launches;
+} ntp_coupled_report;
+ntp_status ntp_train_epoch_coupled(ntp_ctx* ctx, const ntp_coupled_model* m, const ntp_tensor* X_v,
+                                   const int32_t* labels_v, const uint8_t* train_mask_v,
+                                   ntp_tensor* const* W, ntp_coupled_report* rep, ntp_stream s);
+
 #ifdef __cplusplus
 }
 #endif
+
 #endif /* NTP_H */

@@ -511,4 +511,28 @@ ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v
     NTP_API_END(c)
 }
 
+ntp_status ntp_train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tensor* X_v,
+                                   const int32_t* labels_v, const uint8_t* train_mask_v, ntp_tensor* const* W,
+                                   ntp_coupled_report* rep, ntp_stream st) {
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    NTP_CHECK(m && X_v && labels_v && train_mask_v && W, NTP_ERR_ARG, "null argument");
+    NTP_CHECK(m->L >= 1 && m->L <= NTP_MAX_LAYERS, NTP_ERR_ARG, "L must be in [1, %d]", NTP_MAX_LAYERS);
+    for (int l = 0; l <= m->L; ++l) NTP_CHECK(m->widths[l] > 0, NTP_ERR_ARG, "widths must be positive");
+    NTP_CHECK(m->widths[m->L] <= 256, NTP_ERR_CONFIG, "C > 256 classes is not supported");
+    NTP_CHECK(m->dtype == NTP_F32 || m->dtype == NTP_BF16, NTP_ERR_ARG, "bad dtype");
+    const int64_t V_p = cdiv(c->g.n, c->world);
+    NTP_CHECK(X_v->dtype == NTP_F32 && X_v->rows >= V_p && X_v->cols == m->widths[0] && X_v->ld >= m->widths[0],
+              NTP_ERR_SHAPE, "X_v must be fp32 [V_p x d_in]");
+    for (int l = 0; l < m->L; ++l) {
+        NTP_CHECK(W[l] != nullptr, NTP_ERR_ARG, "null weight");
+        NTP_CHECK(W[l]->dtype == NTP_F32 && W[l]->rows == m->widths[l] && W[l]->cols == m->widths[l + 1] &&
+                      W[l]->ld == m->widths[l + 1],
+                  NTP_ERR_SHAPE, "W[%d] must be dense fp32 [%d x %d]", l, m->widths[l], m->widths[l + 1]);
+    }
+    NTP_CUDA(cudaSetDevice(c->device));
+    train_epoch_coupled(c, m, X_v, labels_v, train_mask_v, W, rep, (cudaStream_t)st);
+    NTP_API_END(c)
+}
+
 }  // extern "C"

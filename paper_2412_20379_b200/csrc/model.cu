@@ -825,4 +825,174 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     }
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// NEXT-1: naive (coupled) GNN tensor parallelism, the paper's baseline (P:574,
+// Fig. 6).  An L-layer GCN  H^l = ReLU(A^ H^{l-1} W^l)  (logits = A^ H^{L-1} W^L) trained
+// layer by layer with each aggregation on feature slices: every layer pays a split before and a
+// gather after its hop -- 2L layout changes forward and 2(L-1) backward, 4L - 2 per epoch against
+// the decoupled epoch's 4.  Reuses the decoupled path's kernels unchanged: pack (split with
+// the column-side pre-scale), block all-to-all, one-hop propagation, unpack (gather; with the ReLU'
+// mask on the backward), tensor-core GEMMs, loss, fixed-order reductions, SGD.
+void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                         const uint8_t* mask_v, ntp_tensor* const* W, ntp_coupled_report* rep, cudaStream_t user) {
+    const Graph& g = c->g;
+    cudaStream_t s = c->s_comp;
+    const int64_t launches0 = c->launches;
+    const int32_t P = c->world;
+    const int64_t n = g.n;
+    const int64_t V_p = cdiv(n, P);
+    const int64_t row0 = (int64_t)c->rank * V_p;
+    const int L = m->L;
+    const ntp_dtype dt = m->dtype;
+    const size_t es = esize(dt);
+    const bool local = (P == 1);
+    drop_epoch_graph(c);   // the buffers below may move ones a captured decoupled epoch points into
+    NTP_CUDA(cudaEventRecord(c->ev[40], user ? user : (cudaStream_t)0));
+    NTP_CUDA(cudaStreamWaitEvent(s, c->ev[40], 0));
+    cudaEvent_t* E = c->ev;
+    NTP_CUDA(record_timing(c, E[0], s));
+    c->hop_ev_used = 0;
+
+    // ---- buffers: Z^l [V_p x w_{l-1}], H^l [V_p x w_l] (l < L), logits / dA [V_p x w_L], dZ / dA scratch
+    int64_t ldw[kMaxLayers + 1];
+    for (int l = 0; l <= L; ++l) ldw[l] = round4(m->widths[l]);
+    int64_t maxw = 0, nw = 0, nwp = 0;
+    for (int l = 0; l <= L; ++l) maxw = std::max<int64_t>(maxw, ldw[l]);
+    for (int l = 1; l <= L; ++l) nw += (int64_t)m->widths[l - 1] * m->widths[l];
+    for (int l = 1; l <= L; ++l) nwp += (int64_t)m->widths[l - 1] * ldw[l];
+    for (int l = 1; l <= L; ++l) c->cp_Z[l].ensure((size_t)V_p * ldw[l - 1] * sizeof(float) + 16);
+    for (int l = 1; l < L; ++l) c->cp_H[l].ensure((size_t)V_p * ldw[l] * sizeof(float) + 16);
+    c->cp_A.ensure((size_t)V_p * maxw * sizeof(float) + 16);     // logits, then dA^l
+    c->cp_B.ensure((size_t)V_p * maxw * sizeof(float) + 16);     // dZ^l
+    c->cp_W.ensure((size_t)nwp * sizeof(float) + 16);            // 16-byte-pitch copies of W^l
+    c->m_dW.ensure((size_t)nw * sizeof(float) + 16);
+    c->m_scal.ensure(4 * sizeof(double));
+    int64_t maxfeat = 0;
+    for (int l = 0; l < L; ++l)
+        maxfeat = std::max<int64_t>(maxfeat, (int64_t)P * V_p * slice_width(m->widths[l], P, dt, c->slice_align));
+    if (!local) c->send.ensure((size_t)maxfeat * es + 16);
+    c->recv.ensure((size_t)maxfeat * es + 16);
+    c->xfer.ensure((size_t)maxfeat * es + 16);
+    const int64_t loss_blocks = std::min<int64_t>(cdiv(V_p, 8), 148 * 8);
+    c->m_part.ensure((size_t)loss_blocks * (sizeof(double) + sizeof(int64_t)) + 16);
+    double* part = c->m_part.as<double>();
+    int64_t* cnt = reinterpret_cast<int64_t*>(part + loss_blocks);
+    double* scal = c->m_scal.as<double>();
+    float* Wp[kMaxLayers + 1];
+    float* dWl[kMaxLayers + 1];
+    {
+        float* w = c->cp_W.as<float>();
+        float* d = c->m_dW.as<float>();
+        for (int l = 1; l <= L; ++l) {
+            Wp[l] = w;
+            dWl[l] = d;
+            // padded GEMM copy (16-byte pitch) of the caller's dense W^l (ld == cols)
+            NTP_CUDA(cudaMemcpy2DAsync(w, ldw[l] * sizeof(float), W[l - 1]->data, m->widths[l] * sizeof(float),
+                                       m->widths[l] * sizeof(float), m->widths[l - 1], cudaMemcpyDeviceToDevice, s));
+            w += (int64_t)m->widths[l - 1] * ldw[l];
+            d += (int64_t)m->widths[l - 1] * m->widths[l];
+        }
+    }
+    const float* X = static_cast<const float*>(X_v->data);
+    int64_t ldx = X_v->ld;
+    if ((ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(X) % 16) != 0) {
+        c->m_Xs.ensure((size_t)V_p * ldw[0] * sizeof(float));
+        NTP_CUDA(cudaMemcpy2DAsync(c->m_Xs.p, ldw[0] * sizeof(float), X, ldx * sizeof(float), m->widths[0] * sizeof(float),
+                                   V_p, cudaMemcpyDeviceToDevice, s));
+        X = c->m_Xs.as<float>();
+        ldx = ldw[0];
+    }
+    int changes = 0;
+    int64_t wire = 0;
+    // one layout round trip around a single hop: vertex rows Hv [V_p x w] -> split (pre-scaled) -> hop
+    // (transposed = backward) -> gather -> out [V_p x w] (with keep: the ReLU' mask)
+    auto agg = [&](const float* Hv, int64_t ldh, int w, bool transposed, float* out, int64_t ldo, const float* keep,
+                   int64_t ldk) {
+        const int32_t d_s = slice_width(w, P, dt, c->slice_align);
+        const float* cs = transposed ? g.dinv_in_orig() : g.dinv_out_orig();
+        pack_v2f(c, Hv, ldh, w, local ? c->recv.p : c->send.p, V_p, d_s, P, cs, row0, n, NTP_F32, dt, s);
+        if (!local) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+        PropArgs a{};
+        a.H = c->recv.p;
+        a.Z = c->xfer.p;
+        a.ld_h = d_s;
+        a.ld_z = d_s;
+        a.cols = d_s;
+        a.dtype = dt;
+        a.K = 1;
+        a.gamma = 1.f;
+        a.alpha = 0.f;
+        a.transposed = transposed;
+        void* gathered = c->recv.p;
+        if (local) gathered = propagate_consume(c, a, s, true);
+        else propagate_and_gather(c, a, c->recv.p, false, 1, V_p, d_s, true, s);
+        unpack_f2v(c, gathered, V_p, d_s, P, out, ldo, w, dt, NTP_F32, s, keep, ldk);
+        if (!local) {
+            changes += 2;
+            wire += 2 * (int64_t)(P - 1) * V_p * d_s * (int64_t)es;
+        }
+    };
+    // ---- forward: Z^l = A^ H^{l-1} (sliced), H^l = ReLU(Z^l W^l), logits = Z^L W^L
+    float* logits = c->cp_B.as<float>();
+    for (int l = 1; l <= L; ++l) {
+        const float* Hin = (l == 1) ? X : c->cp_H[l - 1].as<float>();
+        const int64_t ldin = (l == 1) ? ldx : ldw[l - 1];
+        agg(Hin, ldin, m->widths[l - 1], false, c->cp_Z[l].as<float>(), ldw[l - 1], nullptr, 0);
+        float* out = (l < L) ? c->cp_H[l].as<float>() : logits;
+        mlp_gemm(c, false, false, V_p, m->widths[l], m->widths[l - 1], c->cp_Z[l].as<float>(), ldw[l - 1], Wp[l],
+                 ldw[l], out, ldw[l], s, l < L ? 1 : 0);
+    }
+    // ---- loss and dA^L (softmax - onehot on train rows; 1/N_train folded into SGD, R12), in place
+    float* dA = c->cp_A.as<float>();
+    const int64_t nb = launch_softmax_xent(c, (const float*)logits, 0, V_p, 0, m->widths[L], labels_v, mask_v, row0, n,
+                                           dA, 0, nullptr, part, cnt, ldw[L], s);
+    reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb, scal);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    // ---- backward (dA^l in cp_A, dZ^l in cp_B: the logits are consumed by the loss)
+    for (int l = L; l >= 1; --l) {
+        mlp_gemm(c, true, false, m->widths[l - 1], m->widths[l], V_p, c->cp_Z[l].as<float>(), ldw[l - 1], dA, ldw[l],
+                 dWl[l], m->widths[l], s);                                               // dW^l = Z^l^T dA^l
+        if (l == 1) break;
+        float* dZ = c->cp_B.as<float>();
+        mlp_gemm(c, false, true, V_p, m->widths[l - 1], m->widths[l], dA, ldw[l], Wp[l], ldw[l], dZ, ldw[l - 1], s);
+        // dA^{l-1} = (A^T dZ^l) * [H^{l-1} > 0], into the logits / dA buffer (dA^l is consumed)
+        agg(dZ, ldw[l - 1], m->widths[l - 1], true, dA, ldw[l - 1], c->cp_H[l - 1].as<float>(), ldw[l - 1]);
+    }
+    if (P > 1) {
+        NTP_NCCL(ncclGroupStart());
+        NTP_NCCL(ncclAllReduce(c->m_dW.p, c->m_dW.p, nw, ncclFloat32, ncclSum, c->comm, s));
+        NTP_NCCL(ncclAllReduce(scal, scal, 2, ncclFloat64, ncclSum, c->comm, s));
+        NTP_NCCL(ncclGroupEnd());
+    }
+    for (int l = 1; l <= L; ++l) {
+        const int64_t len = (int64_t)m->widths[l - 1] * m->widths[l];
+        sgd_kernel<<<eblocks(len), 256, 0, s>>>(static_cast<float*>(W[l - 1]->data), len, nullptr, 0, dWl[l], scal,
+                                                m->lr);
+        NTP_LAUNCH_CHECK();
+        count_launch(c);
+    }
+    NTP_CUDA(record_timing(c, E[1], s));
+    double h_scal[2] = {0, 0};
+    NTP_CUDA(cudaMemcpyAsync(h_scal, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NTP_CUDA(cudaEventRecord(c->ev[41], s));
+    NTP_CUDA(cudaStreamWaitEvent(user ? user : (cudaStream_t)0, c->ev[41], 0));
+    NTP_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->loss = h_scal[1] > 0 ? h_scal[0] / h_scal[1] : 0.0;
+        rep->n_train = (int64_t)h_scal[1];
+        rep->layout_changes = changes;
+        rep->bytes_sent = wire;
+        rep->bytes_recv = wire;
+        float tot = 0.f;
+        NTP_CUDA(cudaEventElapsedTime(&tot, E[0], E[1]));
+        rep->ms_total = tot;
+        int nh = 0;
+        rep->ms_agg = collect_hop_ms(c, &nh);
+        rep->hops = nh;
+        rep->kernel_launches = c->launches - launches0;
+    }
+}
+
 }  // namespace ntp

@@ -141,6 +141,8 @@ struct ntp_ctx {
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
     ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp, m_head;
+    // coupled (naive TP) epoch: Z^l, H^l per layer, dA / dZ scratch, padded weights
+    ntp::DevBuf cp_Z[NTP_MAX_LAYERS + 1], cp_H[NTP_MAX_LAYERS + 1], cp_A, cp_B, cp_W;
     // peer-direct layouts (CUDA IPC windows over NVLink), see layout.cu
     int p2p_state = 0;                      // 0 not set up, 1 usable, -1 unavailable
     ntp::DevBuf p2p_split, p2p_gath;        // this rank's windows (zero-initialised)
@@ -226,6 +228,9 @@ void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K,
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
 void drop_epoch_graph(ntp_ctx* c);
+constexpr int kMaxLayers = NTP_MAX_LAYERS;
+void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                         const uint8_t* mask_v, ntp_tensor* const* W, ntp_coupled_report* rep, cudaStream_t user);
 void arcs_to_keys(ntp_ctx* c, const int64_t* src, const int64_t* dst, int64_t m, int64_t n, bool sym,
                   uint64_t* keys, cudaStream_t s);
 void csr_to_keys(ntp_ctx* c, const int64_t* row_ptr, const int32_t* col, int64_t n, uint64_t* keys,

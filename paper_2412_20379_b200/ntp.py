@@ -35,7 +35,7 @@ EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_u
             "ntp_destroy", "ntp_load_graph", "ntp_build_graph", "ntp_generate_rmat", "ntp_rmat_arcs",
             "ntp_graph_info", "ntp_copy_csr", "ntp_copy_dinv", "ntp_partition", "ntp_scatter_features",
             "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd",
-            "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch"]
+            "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch", "ntp_train_epoch_coupled"]
 
 
 class ntp_tensor(C.Structure):
@@ -60,6 +60,20 @@ class ntp_epoch_report(C.Structure):
                 ("bytes_sent", C.c_int64 * 4), ("bytes_recv", C.c_int64 * 4), ("collectives", C.c_int64),
                 ("kernel_launches", C.c_int64), ("spmm_ms", C.c_double), ("spmm_launches", C.c_int32),
                 ("pad_", C.c_int32)]
+
+
+NTP_MAX_LAYERS = 8
+
+
+class ntp_coupled_model(C.Structure):
+    _fields_ = [("L", C.c_int32), ("widths", C.c_int32 * (NTP_MAX_LAYERS + 1)), ("lr", C.c_float),
+                ("dtype", C.c_int), ("flags", C.c_uint32)]
+
+
+class ntp_coupled_report(C.Structure):
+    _fields_ = [("loss", C.c_double), ("n_train", C.c_int64), ("layout_changes", C.c_int32), ("hops", C.c_int32),
+                ("bytes_sent", C.c_int64), ("bytes_recv", C.c_int64), ("ms_total", C.c_double),
+                ("ms_agg", C.c_double), ("kernel_launches", C.c_int64)]
 
 
 _vp, _i64, _i32, _u32, _u64, _f = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32, C.c_uint64, C.c_float
@@ -89,6 +103,8 @@ _sig = {
                      C.c_int),
     "ntp_train_epoch": ([_vp, C.POINTER(ntp_model), C.POINTER(ntp_tensor), _vp, _vp, C.POINTER(ntp_tensor),
                          C.POINTER(ntp_tensor), C.POINTER(ntp_epoch_report), _vp], C.c_int),
+    "ntp_train_epoch_coupled": ([_vp, C.POINTER(ntp_coupled_model), C.POINTER(ntp_tensor), _vp, _vp,
+                                 C.POINTER(C.POINTER(ntp_tensor)), C.POINTER(ntp_coupled_report), _vp], C.c_int),
 }
 for _name, (_args, _res) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -276,6 +292,28 @@ class Context:
                                     _stream_ptr(stream)))
 
     # -------------------------------------------------------------- epoch
+    def train_epoch_coupled(self, widths, lr: float, X_v, labels_v, mask_v, Ws, dtype: int = NTP_F32,
+                            stream=None) -> dict:
+        """NEXT-1: one naive-tensor-parallel epoch of the coupled GCN (ntp_train_epoch_coupled);
+        Ws (device fp32 [widths[l] x widths[l+1]]) are updated in place."""
+        L = len(widths) - 1
+        m = ntp_coupled_model()
+        m.L = L
+        for i, w in enumerate(widths):
+            m.widths[i] = int(w)
+        m.lr = float(lr)
+        m.dtype = int(dtype)
+        m.flags = 0
+        xt = as_ntp_tensor(X_v, NTP_LAYOUT_VERTEX)
+        wts = [as_ntp_tensor(W) for W in Ws]
+        arr = (C.POINTER(ntp_tensor) * L)(*[C.pointer(w) for w in wts])
+        rep = ntp_coupled_report()
+        self._chk(_lib.ntp_train_epoch_coupled(self._h, C.byref(m), C.byref(xt), _ptr(labels_v), _ptr(mask_v), arr,
+                                               C.byref(rep), _stream_ptr(stream)))
+        return {"loss": rep.loss, "n_train": rep.n_train, "layout_changes": rep.layout_changes, "hops": rep.hops,
+                "bytes_sent": rep.bytes_sent, "bytes_recv": rep.bytes_recv, "ms_total": rep.ms_total,
+                "ms_agg": rep.ms_agg, "kernel_launches": rep.kernel_launches}
+
     def train_epoch(self, model: dict, X_v, labels_v, mask_v, W0, W1, stream=None, host_inputs: bool = False) -> dict:
         m = ntp_model(model["d_in"], model["hid"], model["C"], model["K"], model["gamma"], model["alpha"],
                       model["lr"], model.get("dtype", NTP_F32), model.get("chunks", 1), model.get("flags", 0)

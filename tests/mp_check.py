@@ -178,6 +178,22 @@ def main(name):
                 f"bf16 loss {rep['loss']} vs oracle {ref_losses[e]} (mode={mode})"
         bres.append((losses, W0.cpu(), W1.cpu()))
     assert bres[0][0] == bres[1][0] and torch.equal(bres[0][1], bres[1][1]) and torch.equal(bres[0][2], bres[1][2])
+
+    # ---- 6. NEXT-1: naive (coupled) TP epochs, 2 and 3 layers: losses vs the coupled oracle, and the
+    # communication ledger: 4L - 2 layout changes moving the closed-form bytes
+    from oracle import coupled
+    for mid in ((24,), (24, 16)):
+        widths = (cfg.d_in, *mid, cfg.C)
+        L = len(widths) - 1
+        Ws = [synth.glorot(cfg.seed, widths[i], widths[i + 1], 100_000 * (i + 1)) for i in range(L)]
+        ref_c, _ = coupled.train(g, *synth.config_inputs(cfg), Ws, lr, 2)
+        Wd = [torch.from_numpy(W).cuda() for W in Ws]
+        for e in range(2):
+            rep = ctx.train_epoch_coupled(widths, lr, *(torch.from_numpy(a).cuda() for a in (X, y, m)), Wd)
+            assert abs(rep["loss"] - ref_c[e]) <= 1e-4, f"coupled loss {rep['loss']} vs {ref_c[e]} (L={L})"
+            assert rep["layout_changes"] == coupled.layout_changes(L, world)
+            ds = lambda w: oracle.layout.slice_width(w, world, 4)
+            assert rep["bytes_sent"] == coupled.layout_bytes(widths, V_p, ds, world, 4)
     dist.barrier()
     if rank == 0:
         print(f"MP OK world={world} config={name} losses={results[1][0]}", flush=True)
