@@ -195,6 +195,57 @@ def run_reference(args, cfg, rank):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ NEXT-1: coupled (naive TP) engine
+def run_coupled(args, ctx, cfg, X, y, msk, n, nnz, world, rank, local, dist, barrier, stream, dt, dtype_name, V_p,
+                reorder):
+    """Times ntp_train_epoch_coupled (2-layer GCN d_in -> hid -> C, every layer aggregated on feature slices)
+    and prints its ledger: layout changes and bytes per epoch vs the decoupled epoch's 4 changes."""
+    import torch
+    from paper_2412_20379_b200 import ntp
+    widths = (cfg.d_in, cfg.hid, cfg.C)
+    Ws = [torch.from_numpy(synth.glorot(cfg.seed, widths[i], widths[i + 1], 100_000 * (i + 1))).cuda()
+          for i in range(len(widths) - 1)]
+    for _ in range(args.warmup):
+        ctx.train_epoch_coupled(widths, cfg.lr, X, y, msk, Ws, dtype=dt, stream=stream)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        reps.append(ctx.train_epoch_coupled(widths, cfg.lr, X, y, msk, Ws, dtype=dt, stream=stream))
+    ev1.record(stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank != 0:
+        return
+    L = len(widths) - 1
+    hop_cols = sum(widths[:L]) + sum(widths[1:L])     # forward hops at w_0..w_{L-1}, backward at w_1..w_{L-1}
+    ge = nnz * hop_cols / (ms * 1e-3) / 1e9
+    esz = 2 if dt == ntp.NTP_BF16 else 4
+    d_s_dec = ntp.partition(n, cfg.w, world, dt, 1, args.slice_align)["d_s"]
+    dec_bytes = 0 if world == 1 else 4 * (world - 1) * V_p * d_s_dec * esz
+    r = reps[-1]
+    line = {"metric": METRIC, "engine": "coupled (naive tensor parallelism, NEXT-1)", "value": ge, "unit": "GE/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": dtype_name, "data": "synthetic", "epoch_s": ms / 1e3,
+            "config": {"workload": WORKLOADS.get(args.config, args.config) + "; coupled 2-layer GCN "
+                       f"{widths[0]}->{widths[1]}->{widths[2]}", "n": n, "nnz": nnz, "P": world,
+                       "vertex_order": "degree-ordered internally (NTP_G_REORDER)" if reorder else "R-MAT ids"},
+            "ledger": {"layout_changes_per_epoch": r["layout_changes"], "bytes_sent_per_epoch": r["bytes_sent"],
+                       "decoupled_layout_changes_per_epoch": 0 if world == 1 else 4,
+                       "decoupled_bytes_sent_per_epoch": dec_bytes,
+                       "volume_ratio": (r["bytes_sent"] / dec_bytes) if dec_bytes else None,
+                       "note": "naive TP: a split and a gather around every layer's aggregation (4L-2 = 6 for L=2, "
+                               "P:696); decoupled: 4 per epoch at the propagated width w"},
+            "phase_ms": {"total": r["ms_total"], "aggregation": r["ms_agg"]},
+            "gpu_launches": int(sum(x["kernel_launches"] for x in reps))}
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ main GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -216,6 +267,9 @@ def main():
                     help="NTP_G_REORDER (internal degree-class numbering). auto: on when the vertex table is "
                          "far larger than L2 (n >= 1M: products, orkut, papers), off for the L2-resident Reddit "
                          "shape where it measured slower (DESIGN.md §5); never with --overlap")
+    ap.add_argument("--engine", default="decoupled", choices=["decoupled", "coupled"],
+                    help="coupled: NEXT-1, the naive tensor-parallel 2-layer GCN (d_in -> hid -> C) with its "
+                         "communication ledger, the paper's TP-vs-DTP ablation (P:696, P:1125-1128)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=3)
@@ -287,6 +341,15 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    if args.engine == "coupled":
+        run_coupled(args, ctx, cfg, X, y, msk, n, nnz, world, rank, local, dist, barrier, stream, dt, dtype_name,
+                    V_p, reorder)
+        ctx.close()
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
     # ---- warm-up
     for _ in range(args.warmup):
         ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream)
@@ -309,7 +372,7 @@ def main():
     phase = {k: sum(r["ms"][k] for r in reps) / len(reps) for k in reps[0]["ms"]}
 
     # ---- e2e: same call with HOST (pinned) inputs copied in every step, loss read back
-    e2e_ms = None
+    e2e_ms = e2e_serial_ms = None
     h2d = x_bytes + V_p * 4 + V_p
     if not args.no_e2e:
         Xp = torch.from_numpy(Xh).pin_memory()   # host layout [V_p x d_in]; staged into a 16-B pitch on copy
@@ -321,6 +384,21 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             ctx.train_epoch(model, Xp, yp, mp, W0, W1, stream=stream, host_inputs=True)
+        ev1.record(stream)
+        barrier()
+        e2e_serial_ms = ev0.elapsed_time(ev1) / args.steps
+        # pipelined loop (ntp_stage_inputs): every step still copies its own inputs from pinned host memory
+        # and reads its loss back, but step i+1's copy runs on the copy engine while step i computes
+        for i in range(2):
+            ctx.stage_inputs(i % 2, Xp, yp, mp)
+            ctx.train_epoch(model, Xp, yp, mp, W0, W1, stream=stream, staged_slot=i % 2)
+        barrier()
+        ev0.record(stream)
+        ctx.stage_inputs(0, Xp, yp, mp)
+        for i in range(args.steps):
+            if i + 1 < args.steps:
+                ctx.stage_inputs((i + 1) % 2, Xp, yp, mp)
+            ctx.train_epoch(model, Xp, yp, mp, W0, W1, stream=stream, staged_slot=i % 2)
         ev1.record(stream)
         barrier()
         e2e_ms = ev0.elapsed_time(ev1) / args.steps
@@ -336,6 +414,7 @@ def main():
     hbm_used_gb = allmax((total_b - free_b) / 1e9)
     ms = allmax(ms)
     e2e_ms = allmax(e2e_ms)
+    e2e_serial_ms = allmax(e2e_serial_ms)
     spmm_avg = allmax(spmm_ms / max(spmm_n, 1))
 
     if rank == 0:
@@ -392,7 +471,10 @@ def main():
             "gpu_launches": int(launches),
             "e2e": None if e2e_ms is None else {
                 "value": 2 * cfg.K * nnz * w / (e2e_ms * 1e-3) / 1e9, "unit": "GE/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16},
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
+                "loop": "ntp_stage_inputs: step i+1's host->device copy overlaps step i (two device slots)",
+                "serial_ms_per_step": e2e_serial_ms,
+                "serial_value": 2 * cfg.K * nnz * w / (e2e_serial_ms * 1e-3) / 1e9},
         }
         if world == 1 and not args.no_cpu_baseline and cfg.n > 10_000_000:
             line["cpu_baseline"] = {"value": None, "unit": "GE/s", "cores": os.cpu_count(), "kind": "oracle",

@@ -206,6 +206,11 @@ ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const flo
 #define NTP_M_OVERLAP       2u  /* chunked last hop with the gather on a comm stream (a12) */
 #define NTP_M_HOST_INPUTS   4u  /* X_v/labels_v/train_mask_v are HOST (pinned) pointers;
                                    copied to the device inside the call (e2e path)       */
+#define NTP_M_STAGED       16u  /* inputs come from staging slot (flags >> 8) & 1, filled by
+                                   ntp_stage_inputs (its host->device copy may overlap the
+                                   previous epoch); X_v / labels_v / train_mask_v are ignored
+                                   except for X_v's shape.  Runs eagerly (no epoch graph). */
+#define NTP_M_SLOT_SHIFT    8
 #define NTP_M_P2P_LAYOUTS   8u  /* P > 1: peer-direct layout changes instead of the NCCL block
                                    all-to-all: the producers (pack, last-hop epilogue, loss
                                    kernel) store into the owners' CUDA-IPC windows over
@@ -249,6 +254,16 @@ typedef struct {
 ntp_status ntp_train_epoch(ntp_ctx* ctx, const ntp_model* m, const ntp_tensor* X_v,
                            const int32_t* labels_v, const uint8_t* train_mask_v,
                            ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, ntp_stream s);
+
+/* Input staging for end-to-end training loops: enqueues the host->device copy of one epoch's
+ * inputs (this rank's rows: X_host [V_p x d_in] fp32 with row pitch ldx elements, labels int32[V_p],
+ * train mask uint8[V_p]; pinned host memory for a truly asynchronous copy) into library-owned slot
+ * `slot` (0 or 1) on the library's copy stream and returns at once.  The copy waits until the last
+ * epoch that read the slot has finished with it, so a loop can stage epoch i+1's inputs while epoch
+ * i computes and then call ntp_train_epoch with NTP_M_STAGED | (i+1 % 2) << NTP_M_SLOT_SHIFT.
+ * Host buffers must stay valid until that epoch returns.  NTP_ERR_ARG / NTP_ERR_STATE as usual. */
+ntp_status ntp_stage_inputs(ntp_ctx* ctx, int slot, const float* X_host, int64_t rows, int32_t d_in, int64_t ldx,
+                            const int32_t* labels_host, const uint8_t* train_mask_host);
 
 /* NEXT-1: naive (coupled) GNN tensor parallelism, the paper's baseline for the
  * decoupled epoch ("twice per layer", Fig. 6).  One epoch of the L-layer GCN

@@ -146,6 +146,11 @@ ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint
         NTP_CUDA(cudaSetDevice(device));
         NTP_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
         NTP_CUDA(cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
+        NTP_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            NTP_CUDA(cudaEventCreateWithFlags(&c->st_ready[i], cudaEventDisableTiming));
+            NTP_CUDA(cudaEventCreateWithFlags(&c->st_free[i], cudaEventDisableTiming));
+        }
         for (auto& e : c->ev) NTP_CUDA(cudaEventCreate(&e));
         for (auto& e : c->hop_ev) NTP_CUDA(cudaEventCreate(&e));
         NTP_BLAS(cublasCreate(&c->blas));
@@ -177,8 +182,14 @@ void ntp_destroy(ntp_ctx* c) {
         if (e) cudaEventDestroy(e);
     for (auto& e : c->hop_ev)
         if (e) cudaEventDestroy(e);
+    if (c->s_copy) cudaStreamSynchronize(c->s_copy);
+    for (int i = 0; i < 2; ++i) {
+        if (c->st_ready[i]) cudaEventDestroy(c->st_ready[i]);
+        if (c->st_free[i]) cudaEventDestroy(c->st_free[i]);
+    }
     if (c->s_comp) cudaStreamDestroy(c->s_comp);
     if (c->s_comm) cudaStreamDestroy(c->s_comm);
+    if (c->s_copy) cudaStreamDestroy(c->s_copy);
     delete c;   // DevBufs free themselves
 }
 
@@ -508,6 +519,18 @@ ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v
     NTP_CHECK(W1->rows == m->hid && W1->cols == m->C && W1->ld == m->C, NTP_ERR_SHAPE, "W1 must be dense [hid x C]");
     NTP_CUDA(cudaSetDevice(c->device));
     train_epoch(c, m, X_v, labels_v, train_mask_v, W0, W1, rep, (cudaStream_t)st);
+    NTP_API_END(c)
+}
+
+ntp_status ntp_stage_inputs(ntp_ctx* c, int slot, const float* X_host, int64_t rows, int32_t d_in, int64_t ldx,
+                            const int32_t* labels_host, const uint8_t* train_mask_host) {
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    NTP_CHECK(X_host && labels_host && train_mask_host, NTP_ERR_ARG, "null argument");
+    NTP_CHECK(slot == 0 || slot == 1, NTP_ERR_ARG, "slot must be 0 or 1");
+    NTP_CHECK(d_in > 0 && ldx >= d_in && rows == cdiv(c->g.n, c->world), NTP_ERR_SHAPE, "X_host must be [V_p x d_in]");
+    NTP_CUDA(cudaSetDevice(c->device));
+    stage_inputs(c, slot, X_host, rows, d_in, ldx, labels_host, train_mask_host);
     NTP_API_END(c)
 }
 

@@ -364,7 +364,16 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     int64_t ldx = X_v->ld;
     const int32_t* lab = labels_v;
     const uint8_t* msk = mask_v;
-    if (m->flags & NTP_M_HOST_INPUTS) {
+    if (m->flags & NTP_M_STAGED) {
+        // inputs staged by ntp_stage_inputs (copy stream); this epoch waits for that copy
+        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
+        NTP_CHECK(c->st_rows[slot] == V_p, NTP_ERR_STATE, "staging slot %d holds no inputs of this shape", slot);
+        NTP_CUDA(cudaStreamWaitEvent(s, c->st_ready[slot], 0));
+        X = c->st_X[slot].as<float>();
+        ldx = c->st_ld[slot];
+        lab = c->st_y[slot].as<int32_t>();
+        msk = c->st_m[slot].as<uint8_t>();
+    } else if (m->flags & NTP_M_HOST_INPUTS) {
         c->m_Xs.ensure((size_t)V_p * ldXp * sizeof(float));
         c->m_lab.ensure((size_t)V_p * sizeof(int32_t));
         c->m_mask.ensure((size_t)V_p);
@@ -658,6 +667,11 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                                             m->lr);
     NTP_LAUNCH_CHECK();
     count_launch(c);
+    if (m->flags & NTP_M_STAGED) {   // the slot may be refilled once this epoch is done with it
+        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
+        NTP_CUDA(cudaEventRecord(c->st_free[slot], s));
+        c->st_free_rec[slot] = true;
+    }
     NTP_CUDA(record_timing(c, E[ei++], s));   // E9 sgd
 }
 
@@ -754,7 +768,12 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     key.head_fused = (getenv("NTP_HEAD_FUSED") ? atoll(getenv("NTP_HEAD_FUSED")) : 1) +
                      2 * (getenv("NTP_HEAD_TMA") ? atoll(getenv("NTP_HEAD_TMA")) : 1);
     int64_t epoch_launches = 0;
-    if (graphs_enabled() && c->graph_valid && c->graph_key == key) {
+    if (m->flags & NTP_M_STAGED) {   // slot buffers alternate and the copy stream is outside any graph
+        drop_epoch_graph(c);
+        c->graph_warm = false;
+        enqueue_epoch(c, m, X_v, labels_v, mask_v, W0, W1, timed);
+        epoch_launches = c->launches - launches0;
+    } else if (graphs_enabled() && c->graph_valid && c->graph_key == key) {
         NTP_CUDA(cudaGraphLaunch(c->graph_exec, s));
         c->hop_ev_used = c->graph_hops;
         epoch_launches = c->graph_launches;
@@ -825,6 +844,32 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     }
 }
 
+
+// Input staging (e2e loops): host -> slot copy on the copy stream, after the last epoch that read
+// the slot.  One contiguous DMA in the host pitch, then the 16-byte GEMM pitch on the device (a 2-D
+// host copy with ~2 KB rows runs at a third of the link rate).
+void stage_inputs(ntp_ctx* c, int slot, const float* X, int64_t rows, int32_t d_in, int64_t ldx, const int32_t* y,
+                  const uint8_t* m) {
+    cudaStream_t s = c->s_copy;
+    const int64_t ld = round4(d_in);
+    c->st_X[slot].ensure((size_t)rows * ld * sizeof(float) + 16);
+    c->st_y[slot].ensure((size_t)rows * sizeof(int32_t) + 16);
+    c->st_m[slot].ensure((size_t)rows + 16);
+    if (c->st_free_rec[slot]) NTP_CUDA(cudaStreamWaitEvent(s, c->st_free[slot], 0));
+    if (ldx == ld) {
+        NTP_CUDA(cudaMemcpyAsync(c->st_X[slot].p, X, (size_t)rows * ldx * sizeof(float), cudaMemcpyHostToDevice, s));
+    } else {
+        c->st_raw[slot].ensure((size_t)rows * ldx * sizeof(float) + 16);
+        NTP_CUDA(cudaMemcpyAsync(c->st_raw[slot].p, X, (size_t)rows * ldx * sizeof(float), cudaMemcpyHostToDevice, s));
+        NTP_CUDA(cudaMemcpy2DAsync(c->st_X[slot].p, ld * sizeof(float), c->st_raw[slot].p, ldx * sizeof(float),
+                                   d_in * sizeof(float), rows, cudaMemcpyDeviceToDevice, s));
+    }
+    NTP_CUDA(cudaMemcpyAsync(c->st_y[slot].p, y, (size_t)rows * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    NTP_CUDA(cudaMemcpyAsync(c->st_m[slot].p, m, (size_t)rows, cudaMemcpyHostToDevice, s));
+    NTP_CUDA(cudaEventRecord(c->st_ready[slot], s));
+    c->st_rows[slot] = rows;
+    c->st_ld[slot] = ld;
+}
 
 // ------------------------------------------------------------------------------------------------
 // NEXT-1: naive (coupled) GNN tensor parallelism, the paper's baseline (P:574,

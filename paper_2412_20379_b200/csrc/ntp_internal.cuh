@@ -143,6 +143,12 @@ struct ntp_ctx {
     ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp, m_head;
     // coupled (naive TP) epoch: Z^l, H^l per layer, dA / dZ scratch, padded weights
     ntp::DevBuf cp_Z[NTP_MAX_LAYERS + 1], cp_H[NTP_MAX_LAYERS + 1], cp_A, cp_B, cp_W;
+    // input staging slots (ntp_stage_inputs): X [V_p x round4(d_in)], raw host-pitch copy, labels, mask
+    ntp::DevBuf st_X[2], st_raw[2], st_y[2], st_m[2];
+    cudaStream_t s_copy = nullptr;
+    cudaEvent_t st_ready[2] = {}, st_free[2] = {};
+    bool st_free_rec[2] = {false, false};
+    int64_t st_rows[2] = {0, 0}, st_ld[2] = {0, 0};
     // peer-direct layouts (CUDA IPC windows over NVLink), see layout.cu
     int p2p_state = 0;                      // 0 not set up, 1 usable, -1 unavailable
     ntp::DevBuf p2p_split, p2p_gath;        // this rank's windows (zero-initialised)
@@ -229,6 +235,8 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
 void drop_epoch_graph(ntp_ctx* c);
 constexpr int kMaxLayers = NTP_MAX_LAYERS;
+void stage_inputs(ntp_ctx* c, int slot, const float* X, int64_t rows, int32_t d_in, int64_t ldx, const int32_t* y,
+                  const uint8_t* m);
 void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                          const uint8_t* mask_v, ntp_tensor* const* W, ntp_coupled_report* rep, cudaStream_t user);
 void arcs_to_keys(ntp_ctx* c, const int64_t* src, const int64_t* dst, int64_t m, int64_t n, bool sym,

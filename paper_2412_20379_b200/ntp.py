@@ -28,6 +28,7 @@ NTP_F32, NTP_BF16 = 0, 1
 NTP_LAYOUT_VERTEX, NTP_LAYOUT_FEATURE = 0, 1
 NTP_G_SYMMETRIC, NTP_G_VALIDATE, NTP_G_REORDER = 1, 2, 4
 NTP_M_W1_AFTER_PROP, NTP_M_OVERLAP, NTP_M_HOST_INPUTS, NTP_M_P2P_LAYOUTS = 1, 2, 4, 8
+NTP_M_STAGED, NTP_M_SLOT_SHIFT = 16, 8
 PHASES = ["mlp_fwd", "v2f_fwd", "prop_fwd", "f2v_fwd", "loss", "v2f_bwd", "prop_bwd", "f2v_bwd",
           "mlp_bwd", "allreduce", "sgd", "total"]
 
@@ -35,7 +36,8 @@ EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_u
             "ntp_destroy", "ntp_load_graph", "ntp_build_graph", "ntp_generate_rmat", "ntp_rmat_arcs",
             "ntp_graph_info", "ntp_copy_csr", "ntp_copy_dinv", "ntp_partition", "ntp_scatter_features",
             "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd",
-            "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch", "ntp_train_epoch_coupled"]
+            "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch", "ntp_train_epoch_coupled",
+            "ntp_stage_inputs"]
 
 
 class ntp_tensor(C.Structure):
@@ -103,6 +105,7 @@ _sig = {
                      C.c_int),
     "ntp_train_epoch": ([_vp, C.POINTER(ntp_model), C.POINTER(ntp_tensor), _vp, _vp, C.POINTER(ntp_tensor),
                          C.POINTER(ntp_tensor), C.POINTER(ntp_epoch_report), _vp], C.c_int),
+    "ntp_stage_inputs": ([_vp, C.c_int, _vp, _i64, _i32, _i64, _vp, _vp], C.c_int),
     "ntp_train_epoch_coupled": ([_vp, C.POINTER(ntp_coupled_model), C.POINTER(ntp_tensor), _vp, _vp,
                                  C.POINTER(C.POINTER(ntp_tensor)), C.POINTER(ntp_coupled_report), _vp], C.c_int),
 }
@@ -314,10 +317,21 @@ class Context:
                 "bytes_sent": rep.bytes_sent, "bytes_recv": rep.bytes_recv, "ms_total": rep.ms_total,
                 "ms_agg": rep.ms_agg, "kernel_launches": rep.kernel_launches}
 
-    def train_epoch(self, model: dict, X_v, labels_v, mask_v, W0, W1, stream=None, host_inputs: bool = False) -> dict:
+    def stage_inputs(self, slot: int, X_host, labels_host, mask_host):
+        """ntp_stage_inputs: enqueue the host->device copy of one epoch's inputs into slot 0/1 (returns at
+        once; pinned host tensors give an asynchronous copy that overlaps the running epoch)."""
+        rows, d_in = X_host.shape
+        ldx = X_host.stride(0) if hasattr(X_host, "stride") and callable(X_host.stride) else d_in
+        self._chk(_lib.ntp_stage_inputs(self._h, int(slot), _ptr(X_host), rows, d_in, ldx, _ptr(labels_host),
+                                        _ptr(mask_host)))
+
+    def train_epoch(self, model: dict, X_v, labels_v, mask_v, W0, W1, stream=None, host_inputs: bool = False,
+                    staged_slot: int | None = None) -> dict:
+        flags = model.get("flags", 0) | (NTP_M_HOST_INPUTS if host_inputs else 0)
+        if staged_slot is not None:   # inputs from ntp_stage_inputs slot (X_v gives the shape only)
+            flags |= NTP_M_STAGED | (int(staged_slot) << NTP_M_SLOT_SHIFT)
         m = ntp_model(model["d_in"], model["hid"], model["C"], model["K"], model["gamma"], model["alpha"],
-                      model["lr"], model.get("dtype", NTP_F32), model.get("chunks", 1), model.get("flags", 0)
-                      | (NTP_M_HOST_INPUTS if host_inputs else 0))
+                      model["lr"], model.get("dtype", NTP_F32), model.get("chunks", 1), flags)
         xt = as_ntp_tensor(X_v, NTP_LAYOUT_VERTEX)
         w0, w1 = as_ntp_tensor(W0), as_ntp_tensor(W1)
         rep = ntp_epoch_report()

@@ -162,3 +162,25 @@ def test_epoch_head_fused_matches_unfused(monkeypatch):
         losses, _, _, _, _ = _train_gpu("head_dir", 1, dtype=ntp.NTP_BF16)
         out.append(losses[0])
     assert abs(out[0] - out[1]) <= 1e-3 * abs(out[1])
+
+
+def test_epoch_staged_inputs_same_result():
+    """ntp_stage_inputs + NTP_M_STAGED (the e2e loop: epoch i+1's inputs copied while epoch i runs, two
+    alternating slots) gives bit-identical losses and weights to device-resident inputs."""
+    a, W0a, W1a, _, _ = _train_gpu("tiny_dir", 3)
+    cfg = synth.get_config("tiny_dir")
+    ctx = ntp_ctx_for("tiny_dir")
+    X, y, m = synth.config_inputs(cfg)
+    W0, W1 = synth.model_weights(cfg)
+    model = _model(cfg)
+    model["lr"] = cfg.lr * 50
+    Xp, yp, mp = (torch.from_numpy(t).pin_memory() for t in (X, y, m))
+    W0d, W1d = torch.from_numpy(W0).cuda(), torch.from_numpy(W1).cuda()
+    ctx.stage_inputs(0, Xp, yp, mp)
+    losses = []
+    for i in range(3):
+        if i + 1 < 3:
+            ctx.stage_inputs((i + 1) % 2, Xp, yp, mp)
+        losses.append(ctx.train_epoch(model, Xp, yp, mp, W0d, W1d, staged_slot=i % 2)["loss"])
+    assert losses == a
+    assert np.array_equal(W0d.cpu().numpy(), W0a) and np.array_equal(W1d.cpu().numpy(), W1a)
