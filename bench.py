@@ -256,7 +256,7 @@ def main():
     ap.add_argument("--impl", default="ntp", choices=["ntp", "reference"])
     ap.add_argument("--dtype", default=None, choices=[None, "f32", "bf16"])
     ap.add_argument("--chunks", type=int, default=1)
-    ap.add_argument("--overlap", action="store_true",
+    ap.add_argument("--overlap", action="store_true",  # a12
                     help="chunked last hop with the gather on the comm stream (a12); off by default: on "
                          "reddit the gather moves ~1-10 MB and chunking costs more than it hides")
     ap.add_argument("--slice-align", type=int, default=16)
@@ -302,7 +302,10 @@ def main():
     ctx = ntp.Context(device=local, rank=rank, world=world, unique_id=uid, slice_align=args.slice_align)
 
     t0 = time.time()
-    reorder = (args.reorder == "on" or (args.reorder == "auto" and cfg.n >= 1_000_000)) and not args.overlap
+    # the last-hop chunked gather of --overlap needs original ids; the W1-after-propagation epoch overlaps its
+    # layout changes by row chunk instead and keeps the reorder
+    reorder = (args.reorder == "on" or (args.reorder == "auto" and cfg.n >= 1_000_000)) and \
+        (not args.overlap or cfg.w_after_prop)
     ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric,
                       reorder=reorder)
     n, nnz, sym = ctx.graph_info()

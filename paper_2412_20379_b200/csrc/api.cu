@@ -152,6 +152,7 @@ ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint
             NTP_CUDA(cudaEventCreateWithFlags(&c->st_free[i], cudaEventDisableTiming));
         }
         for (auto& e : c->ev) NTP_CUDA(cudaEventCreate(&e));
+        for (auto& e : c->ov_ev) NTP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         for (auto& e : c->hop_ev) NTP_CUDA(cudaEventCreate(&e));
         NTP_BLAS(cublasCreate(&c->blas));
         NTP_BLAS(cublasSetMathMode(c->blas, CUBLAS_PEDANTIC_MATH));   // fp32 FMA, no TF32 (R11)
@@ -181,6 +182,8 @@ void ntp_destroy(ntp_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->hop_ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->ov_ev)
         if (e) cudaEventDestroy(e);
     if (c->s_copy) cudaStreamSynchronize(c->s_copy);
     for (int i = 0; i < 2; ++i) {

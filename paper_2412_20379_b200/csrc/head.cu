@@ -44,6 +44,7 @@ constexpr uint32_t kColLogits = 0, kColDZ = 192, kColDW = 320;
 struct HeadParams {
     const __nv_bfloat16* Z;     // gathered [P][V_p][d_s]
     int64_t V_p;
+    int64_t v_lo, v_hi;         // this call's rows [v_lo, v_hi) of the V_p (row chunk of the a12 schedule)
     int d_s, P, lds;            // lds = log2(d_s) (d_s = 128 / P, P a power of two)
     int C, CB, n1, kc;          // classes, 64-class boxes, N of MMA1/3 (C rounded to 16), K steps of MMA2
     const __nv_bfloat16* W1s;   // [2][HP][CB*64] bf16: hi then lo, zero padded
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __gri
             for (int i = 0; i < nloc; ++i) {
                 const int b = i & 1;
                 if (i >= 2) ptx::mbar_wait(&zfree[b], ((i >> 1) - 1) & 1);
-                const int v0 = (int)((blockIdx.x + (int64_t)i * gridDim.x) * 128);
+                const int v0 = (int)(p.v_lo + (blockIdx.x + (int64_t)i * gridDim.x) * 128);
                 uint8_t* za = sZ + b * 2 * kBox;
                 ptx::mbar_expect_tx(&zfull[b], 2 * kBox);
 #pragma unroll
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __gri
         for (int i = 0; i < nloc; ++i) {
             const int b = i & 1;
             if (i >= 2) ptx::mbar_wait(&zfree[b], ((i >> 1) - 1) & 1);
-            const int64_t v0 = (blockIdx.x + (int64_t)i * gridDim.x) * 128;
+            const int64_t v0 = p.v_lo + (blockIdx.x + (int64_t)i * gridDim.x) * 128;
             uint8_t* za = sZ + b * 2 * kBox;
             constexpr int U = 22;                  // 2048 chunks / 96 threads: one round per tile
             for (int f0 = t; f0 < 2048; f0 += 96 * U) {
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __gri
                     if (f < 2048) {
                         const int q = f >> lpb, rem = f & ((1 << lpb) - 1);
                         const int r = rem >> lcpr, jc = rem & ((1 << lcpr) - 1);
-                        if (v0 + r < p.V_p)
+                        if (v0 + r < p.v_hi)
                             x[u] = __ldg(reinterpret_cast<const uint4*>(p.Z + ((int64_t)q * p.V_p + v0 + r) * p.d_s) + jc);
                     }
                 }
@@ -283,8 +284,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __gri
         const int nch = (p.C + 31) / 32;
         // mask and label of tile i+1 are loaded while tile i is processed (two independent loads, off
         // the per-tile critical path)
-        auto row_of = [&](int t) { return (blockIdx.x + (int64_t)t * gridDim.x) * 128 + r; };
-        auto real_row = [&](int64_t v) { return v < p.V_p && p.row0 + v < p.n; };
+        auto row_of = [&](int t) { return p.v_lo + (blockIdx.x + (int64_t)t * gridDim.x) * 128 + r; };
+        auto real_row = [&](int64_t v) { return v < p.v_hi && p.row0 + v < p.n; };
         uint8_t mk_n = 0;
         int y_n = 0;
         if (nloc > 0 && real_row(row_of(0))) {
@@ -374,13 +375,13 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __gri
         const int r = qd * 32 + lane;
         const uint32_t lrow = tmem + ((uint32_t)(qd * 32) << 16);
         auto scale_of = [&](int t) {
-            const int64_t v = (blockIdx.x + (int64_t)t * gridDim.x) * 128 + r;
-            return (v < p.V_p && p.row0 + v < p.n) ? __ldg(p.gscale + p.row0 + v) : 0.f;
+            const int64_t v = p.v_lo + (blockIdx.x + (int64_t)t * gridDim.x) * 128 + r;
+            return (v < p.v_hi && p.row0 + v < p.n) ? __ldg(p.gscale + p.row0 + v) : 0.f;
         };
         float sc_n = nloc > 0 ? scale_of(0) : 0.f;
         for (int i = 0; i < nloc; ++i) {
-            const int64_t v = (blockIdx.x + (int64_t)i * gridDim.x) * 128 + r;
-            const bool inb = v < p.V_p;
+            const int64_t v = p.v_lo + (blockIdx.x + (int64_t)i * gridDim.x) * 128 + r;
+            const bool inb = v < p.v_hi;
             const float sc = sc_n;
             if (i + 1 < nloc) sc_n = scale_of(i + 1);
             ptx::mbar_wait(dzfull, i & 1);
@@ -481,10 +482,13 @@ bool head_fused_supported(int32_t P, int32_t d_s, int32_t hid, int32_t C, ntp_dt
 int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, int32_t P, int32_t hid, int32_t C,
                    const float* W1, int64_t ldw1, const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n,
                    const float* gscale, void* out, void* const* peer, float* dW1, double* part, int64_t* cnt,
-                   cudaStream_t s) {
+                   cudaStream_t s, int64_t v_lo, int64_t v_hi) {
+    if (v_hi < 0) v_hi = V_p;
     HeadParams p{};
     p.Z = static_cast<const __nv_bfloat16*>(gathered);
     p.V_p = V_p;
+    p.v_lo = v_lo;
+    p.v_hi = v_hi;
     p.d_s = d_s;
     p.P = P;
     p.lds = 0;
@@ -502,7 +506,7 @@ int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, i
     p.peer = peer;
     p.rank = c->rank;
     p.hid = hid;
-    p.tiles = cdiv(V_p, 128);
+    p.tiles = cdiv(v_hi - v_lo, 128);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(p.tiles, 148));
     const int cols = p.CB * 64;
     const size_t w_bytes = (size_t)2 * HP * cols * sizeof(__nv_bfloat16);

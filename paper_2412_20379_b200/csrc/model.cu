@@ -444,8 +444,10 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     const bool local = (P == 1);
     const char* hce = getenv("NTP_HEAD_CHUNK");   // read per call (tests vary it)
     const int64_t head_chunk_env = hce ? atoll(hce) : 0;
-    const int64_t hc = after ? std::max<int64_t>(1, std::min<int64_t>(V_p, head_chunk_env > 0 ? head_chunk_env
-                                                                                               : (int64_t)1 << 23))
+    // row chunks of the vertex-side work: NTP_HEAD_CHUNK, else the model's chunk count (the a12 schedule's
+    // chunks), capped at 2^23 rows
+    const int64_t hc_def = m->chunks > 1 ? std::min<int64_t>(cdiv(V_p, m->chunks), (int64_t)1 << 23) : (int64_t)1 << 23;
+    const int64_t hc = after ? std::max<int64_t>(1, std::min<int64_t>(V_p, head_chunk_env > 0 ? head_chunk_env : hc_def))
                              : V_p;
     const int64_t nch = after ? cdiv(V_p, hc) : 1;
     const int32_t nwb = (m->hid + 31) / 32;          // mask words per row
@@ -498,6 +500,42 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             for (void* b : {c->p2p_split.p, c->p2p_gath.p})
                 NTP_CUDA(cudaMemsetAsync(static_cast<char*>(b) + off, 0, len, s));
     }
+    // a12 for the W1-after-propagation epoch (P > 1, NCCL layouts): every layout change runs per row chunk
+    // on the comm stream -- split chunk ch while the MLP computes chunk ch+1, gather chunk ch while the head
+    // consumes chunk ch-1, gradient split behind the head, backward gather ahead of the MLP backward --
+    // with the same arithmetic (chunks are the same with and without the overlap).
+    const bool ovl = overlap && after && !local && !p2p;
+    int ovi = 0;                                   // next free overlap event
+    auto ov_event = [&]() -> cudaEvent_t {
+        NTP_CHECK(ovi < kOvEvents, NTP_ERR_CONFIG, "too many overlap chunks (%d events)", kOvEvents);
+        return c->ov_ev[ovi++];
+    };
+    // rows [r, r+h) of every block: block q of `src` -> rank q; rank q's block `rank` -> block q of `dst`
+    auto exchange_rows = [&](const void* src, void* dst, int64_t r, int64_t h, cudaStream_t st) {
+        const ncclDataType_t t = dt == NTP_BF16 ? ncclBfloat16 : ncclFloat32;
+        const size_t cnt = (size_t)h * d_s;
+        NTP_NCCL(ncclGroupStart());
+        for (int q = 0; q < P; ++q) {
+            const size_t off = ((size_t)q * V_p + r) * d_s * es;
+            if (q == c->rank) {
+                NTP_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, cnt * es,
+                                         cudaMemcpyDeviceToDevice, st));
+                continue;
+            }
+            NTP_NCCL(ncclSend(static_cast<const char*>(src) + off, cnt, t, q, c->comm, st));
+            NTP_NCCL(ncclRecv(static_cast<char*>(dst) + off, cnt, t, q, c->comm, st));
+        }
+        NTP_NCCL(ncclGroupEnd());
+    };
+    // comm stream: after `s` reaches this point, exchange rows [r, r+h); returns the completion event
+    auto async_exchange = [&](const void* src, void* dst, int64_t r, int64_t h) -> cudaEvent_t {
+        cudaEvent_t a = ov_event(), b = ov_event();
+        NTP_CUDA(cudaEventRecord(a, s));
+        NTP_CUDA(cudaStreamWaitEvent(c->s_comm, a, 0));
+        exchange_rows(src, dst, r, h, c->s_comm);
+        NTP_CUDA(cudaEventRecord(b, c->s_comm));
+        return b;
+    };
     void* slice_in = p2p ? c->p2p_split.p : c->recv.p;   // this rank's feature slice after a split
     void* split_dst = p2p ? nullptr : (local ? c->recv.p : c->send.p);   // where the split's producer writes
 
@@ -512,18 +550,21 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd done
         pack_v2f(c, prop_src, ld_src, w, split_dst, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split);
     } else {
+        cudaEvent_t last = nullptr;
         for (int64_t r = 0; r < V_p; r += hc) {      // H1 chunk -> pre-scaled slice rows + ReLU' bits
             const int64_t h = std::min(hc, V_p - r);
             mlp_gemm(c, false, false, h, m->hid, m->d_in, X + r * ldx, ldx, W0g, ldw0, H1, ldH, s, 1, nullptr, 0, W0s);
             pack_v2f(c, H1, ldH, w, split_dst, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split, h, r,
                      bits, nwb);
+            if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);   // a3 of chunk ch under a2 of ch+1
         }
+        if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, last, 0));
         NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd (+ pack) done
     }
 
     // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
     if (p2p) p2p_barrier(c, s);
-    else if (!local) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    else if (!local && !ovl) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E2 v2f done
 
     // a4 + a5: K forward hops on S^0 (pre-scaled) -> Z^K, gathered into this rank's rows
@@ -547,10 +588,15 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
             p2p_barrier(c, s);
+        } else if (ovl) {
+            propagate(c, a, s, timed, true);     // a5 per chunk below, consumed chunk by chunk by the head
         } else {
-            propagate_and_gather(c, a, c->recv.p, overlap, m->chunks, V_p, d_s, timed, s);
+            propagate_and_gather(c, a, c->recv.p, overlap && !after, m->chunks, V_p, d_s, timed, s);
         }
     }
+    std::vector<cudaEvent_t> g_ev;                 // forward gather of row chunk ch done (ovl)
+    if (ovl)
+        for (int64_t r = 0; r < V_p; r += hc) g_ev.push_back(async_exchange(c->xfer.p, c->recv.p, r, std::min(hc, V_p - r)));
     NTP_CUDA(record_timing(c, E[ei++], s));   // E3 prop fwd + f2v done
     // the gradient split's producer target: the send buffer, or on one GPU the slice the forward no
     // longer needs
@@ -580,15 +626,19 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         // per row chunk: Z_v = unpack(gathered) [h x hid]; logits = Z_v W1; dlogits; dW1 += Z_v^T dlogits;
         // dZ_v = dlogits W1^T -> pack into the gradient split
         float* Zv = dH1;   // reuse [hc x ldH]
-        if (head_fused_supported(P, d_s, m->hid, m->C, dt)) {
-            // one tcgen05 pass over all rows (head.cu): logits, dl and dZ stay on chip
-            nb_loss = head_fused(c, gathered, V_p, d_s, P, m->hid, m->C, W1g, ldw1, lab, msk, row0, n, gscale_bwd,
-                                 p2p ? nullptr : gsend, tab_split, dw1_at(0), part, cnt, s);
-            for (int64_t ch = 1; ch < nch; ++ch)
-                NTP_CUDA(cudaMemsetAsync(dw1_at(ch), 0, (size_t)m->hid * m->C * sizeof(float), s));
-        } else
+        cudaEvent_t last = nullptr;
+        const bool fused = head_fused_supported(P, d_s, m->hid, m->C, dt);
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
+            if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, g_ev[ch], 0));
+            if (fused) {
+                // one tcgen05 pass over the chunk's rows (head.cu): logits, dl and dZ stay on chip
+                nb_loss += head_fused(c, gathered, V_p, d_s, P, m->hid, m->C, W1g, ldw1, lab, msk, row0, n, gscale_bwd,
+                                      p2p ? nullptr : gsend, tab_split, dw1_at(ch), part + nb_loss, cnt + nb_loss, s,
+                                      r, r + h);
+                if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);   // a7 of chunk ch
+                continue;
+            }
             unpack_f2v(c, gathered, V_p, d_s, P, Zv, ldH, m->hid, dt, NTP_F32, s, nullptr, 0, h, r);
             mlp_gemm(c, false, false, h, m->C, m->hid, Zv, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
             nb_loss += launch_softmax_xent(c, (const float*)L, 0, h, d_s, m->C, lab + r, msk + r, row0 + r, n, dL, 0,
@@ -597,7 +647,9 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             mlp_gemm(c, false, true, h, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);  // dZ_v -> L
             pack_v2f(c, L, ldL, m->hid, p2p ? nullptr : gsend, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s,
                      tab_split, h, r);
+            if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);       // a7 of chunk ch
         }
+        if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, last, 0));
     }
     reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb_loss, scal);
     NTP_LAUNCH_CHECK();
@@ -606,7 +658,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
 
     // a7: split the gradient
     if (p2p) p2p_barrier(c, s);
-    else if (!local) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    else if (!local && !ovl) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E5 v2f bwd
 
     // a8 + a9: K backward hops on the split gradient, gathered -> dL^ rows [V_p x w]
@@ -629,10 +681,15 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
             p2p_barrier(c, s);
+        } else if (ovl) {
+            propagate(c, a, s, timed, true);     // a9 per chunk below, consumed chunk by chunk by a10
         } else {
-            propagate_and_gather(c, a, c->send.p, overlap, m->chunks, V_p, d_s, timed, s);
+            propagate_and_gather(c, a, c->send.p, overlap && !after, m->chunks, V_p, d_s, timed, s);
         }
     }
+    std::vector<cudaEvent_t> b_ev;                 // backward gather of row chunk ch done (ovl)
+    if (ovl)
+        for (int64_t r = 0; r < V_p; r += hc) b_ev.push_back(async_exchange(c->xfer.p, c->send.p, r, std::min(hc, V_p - r)));
     if (!after) unpack_f2v(c, gathered_b, V_p, d_s, P, dL, ldL, w, dt, NTP_F32, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E6 prop bwd + f2v bwd
 
@@ -644,6 +701,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     } else {
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
+            if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, b_ev[ch], 0));
             unpack_f2v(c, gathered_b, V_p, d_s, P, dH1, ldH, w, dt, NTP_F32, s, nullptr, 0, h, r, bits, nwb);
             mlp_gemm(c, true, false, m->d_in, m->hid, h, X + r * ldx, ldx, dH1, ldH, dw0_at(ch), m->hid, s);
         }
@@ -748,8 +806,9 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     const size_t es = esize(m->dtype);
     const bool timed = true;
     cudaEvent_t* E = c->ev;
-    NTP_CHECK(!((m->flags & NTP_M_OVERLAP) && g.reordered), NTP_ERR_CONFIG,
-              "NTP_M_OVERLAP sends last-hop chunks by destination block: needs a graph without NTP_G_REORDER");
+    NTP_CHECK(!((m->flags & NTP_M_OVERLAP) && g.reordered && !after), NTP_ERR_CONFIG,
+              "NTP_M_OVERLAP sends last-hop chunks by destination block: needs a graph without NTP_G_REORDER "
+              "(the W1-after-propagation epoch overlaps its layout changes by row chunk instead)");
 
     // ---- order after the caller's stream
     NTP_CUDA(cudaEventRecord(c->ev[40], user ? user : (cudaStream_t)0));

@@ -158,6 +158,7 @@ struct ntp_ctx {
     ntp::DevBuf p2p_tab;                    // device: [2][P] pointers (split windows, gather windows)
     ntp::DevBuf p2p_bar;                    // one int for the barrier allreduce
     cudaEvent_t ev[64] = {};
+    cudaEvent_t ov_ev[256] = {};    // fork/join events of the chunked layout exchanges (a12)
     cudaEvent_t hop_ev[256] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
     int hop_ev_used = 0;
     int64_t launches = 0;
@@ -235,6 +236,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
 void drop_epoch_graph(ntp_ctx* c);
 constexpr int kMaxLayers = NTP_MAX_LAYERS;
+constexpr int kOvEvents = 256;
 void stage_inputs(ntp_ctx* c, int slot, const float* X, int64_t rows, int32_t d_in, int64_t ldx, const int32_t* y,
                   const uint8_t* m);
 void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
@@ -286,7 +288,7 @@ bool head_fused_supported(int32_t P, int32_t d_s, int32_t hid, int32_t C, ntp_dt
 int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, int32_t P, int32_t hid, int32_t C,
                    const float* W1, int64_t ldw1, const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n,
                    const float* gscale, void* out, void* const* peer, float* dW1, double* part, int64_t* cnt,
-                   cudaStream_t s);
+                   cudaStream_t s, int64_t v_lo = 0, int64_t v_hi = -1);
 
 inline size_t esize(ntp_dtype d) { return d == NTP_BF16 ? 2 : 4; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

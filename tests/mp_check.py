@@ -164,12 +164,13 @@ def main(name):
     # ---- 5. bf16 storage epochs (the fused tcgen05 head where P*d_s = 128, e.g. head_dir): losses vs
     # the oracle within 2e-2 relative; peer-direct and NCCL layouts bitwise equal
     bres = []
-    for mode in ("nccl", "p2p"):
+    # (the W1-after-propagation epoch's overlap runs every layout change per row chunk on the comm stream)
+    for mode in ("nccl", "p2p", "overlap"):
         W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
         model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
-                     dtype=ntp.NTP_BF16, chunks=1,
+                     dtype=ntp.NTP_BF16, chunks=3,
                      flags=(ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0)
-                     | (ntp.NTP_M_P2P_LAYOUTS if mode == "p2p" else 0))
+                     | (ntp.NTP_M_P2P_LAYOUTS if mode == "p2p" else 0) | (ntp.NTP_M_OVERLAP if mode == "overlap" else 0))
         losses = []
         for e in range(2):
             rep = ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
@@ -177,7 +178,19 @@ def main(name):
             assert abs(rep["loss"] - ref_losses[e]) <= 2e-2 * abs(ref_losses[e]), \
                 f"bf16 loss {rep['loss']} vs oracle {ref_losses[e]} (mode={mode})"
         bres.append((losses, W0.cpu(), W1.cpu()))
-    assert bres[0][0] == bres[1][0] and torch.equal(bres[0][1], bres[1][1]) and torch.equal(bres[0][2], bres[1][2])
+    for k in (1, 2):
+        assert bres[0][0] == bres[k][0] and torch.equal(bres[0][1], bres[k][1]) and torch.equal(bres[0][2], bres[k][2]), \
+            f"bf16 mode {k} changed the bits"
+    if cfg.w_after_prop:   # overlap on a degree-reordered graph (the papers configuration): vs the oracle
+        W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+        ctxo = ntp.Context(device=local, rank=rank, world=world, unique_id=pd.broadcast_unique_id(dist, rank))
+        ctxo.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric, reorder=True)
+        model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
+                     dtype=ntp.NTP_BF16, chunks=4, flags=ntp.NTP_M_W1_AFTER_PROP | ntp.NTP_M_OVERLAP)
+        for e in range(2):
+            rep = ctxo.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
+            assert abs(rep["loss"] - ref_losses[e]) <= 2e-2 * abs(ref_losses[e]), f"reordered overlap loss {rep['loss']}"
+        ctxo.close()
 
     # ---- 6. NEXT-1: naive (coupled) TP epochs, 2 and 3 layers: losses vs the coupled oracle, and the
     # communication ledger: 4L - 2 layout changes moving the closed-form bytes
