@@ -49,6 +49,7 @@ struct GemmParams {
     int exp;                            // development timing knob (NTP_GEMM_EXP), 0 in production
     int b_presplit;                     // B arrives as (hi, lo) pair: tmB = hi, tmBlo = lo (weights)
     uint32_t mn_lbo, mn_sbo;            // MN-major descriptor byte offsets (16-byte units)
+    PackEpi pk;                         // epi 3: ReLU -> ReLU' bits + row-scaled bf16 feature-slice blocks
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -313,6 +314,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (n0 + c0 >= p.N) continue;         // warp-uniform
+                if (p.epi == 3) {
+                    // the split's pack fused in (a2 -> a3, W1 after propagation): thread = row, its 32 columns
+                    // ReLU'd, their positivity as one mask word, scaled by the row's D~_out^{-1/2} (0 on padding
+                    // rows) and stored as bf16 into block q = col / d_s of the blocked slice [P][V_p][d_s]
+                    const int64_t row = m0 + 32 * q + lane;
+                    if (row < p.M) {
+                        const int64_t v = p.pk.roff + row;
+                        const bool real = p.pk.row0 + v < p.pk.n;
+                        const float sc = real ? __ldg(p.pk.scale + p.pk.row0 + v) : 0.f;
+                        uint32_t word = 0;
+                        float e[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            e[j] = real ? fmaxf(__uint_as_float(r[j]), 0.f) : 0.f;
+                            word |= (e[j] > 0.f ? 1u : 0u) << j;
+                        }
+                        const int col0 = n0 + c0;
+                        p.pk.bits[v * p.pk.nwb + (col0 >> 5)] = word;
+#pragma unroll
+                        for (int g8 = 0; g8 < 4; ++g8) {
+                            const int col = col0 + 8 * g8;
+                            const int qb = col / p.pk.d_s, jj = col - qb * p.pk.d_s;
+                            uint4 o;
+                            uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const __nv_bfloat162 h2 =
+                                    __floats2bfloat162_rn(e[8 * g8 + 2 * k] * sc, e[8 * g8 + 2 * k + 1] * sc);
+                                ow[k] = *reinterpret_cast<const uint32_t*>(&h2);
+                            }
+                            *reinterpret_cast<uint4*>(p.pk.out + ((int64_t)qb * p.pk.V_p + v) * p.pk.d_s + jj) = o;
+                        }
+                    }
+                    continue;
+                }
                 // row `lane` of the 32 x 32 chunk: 16-byte piece j lands in slot j ^ (lane & 7)
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -457,10 +493,12 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
         splits = (int)std::min<int64_t>(148 / ((int64_t)m_tiles * n_tiles), std::max(1, p.k_tiles_total / 4));
         splits = std::max(splits, 1);
     }
+    if (epi == 3) splits = 1;              // the pack epilogue writes final values (no split-K partials)
     p.k_tiles_per_split = (int)cdiv(p.k_tiles_total, splits);
     splits = (int)cdiv(p.k_tiles_total, p.k_tiles_per_split);
     p.aux = aux;
     p.ldaux = ldaux;
+    if (epi == 3) p.pk = c->pack_epi;
     static const int gemm_exp = [] { const char* v = getenv("NTP_GEMM_EXP"); return v ? atoi(v) : 0; }();
     p.exp = gemm_exp;
     p.mn_lbo = 4096 >> 4;
@@ -504,6 +542,15 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
         NTP_LAUNCH_CHECK();
         count_launch(c);
     }
+}
+
+// C = A B with the pack epilogue (epi 3): see PackEpi.  A [M x K] K-major, B [K x N] MN-major (weights,
+// pre-split), N = P * d_s (no padding columns), N % 32 == 0, d_s % 8 == 0.
+void gemm_tf32x3_pack(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B_hi,
+                      const float* B_lo, int64_t ldb, const PackEpi& pk, cudaStream_t s) {
+    NTP_CHECK(N % 32 == 0 && pk.d_s % 8 == 0, NTP_ERR_CONFIG, "pack epilogue needs N %% 32 == 0 and d_s %% 8 == 0");
+    c->pack_epi = pk;
+    gemm_tf32x3(c, M, N, K, A, lda, false, B_hi, ldb, true, nullptr, 0, 3, nullptr, 0, s, B_lo);
 }
 
 namespace {

@@ -551,11 +551,23 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         pack_v2f(c, prop_src, ld_src, w, split_dst, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split);
     } else {
         cudaEvent_t last = nullptr;
+        // bf16 slice, no padding columns: the split's pack runs in the GEMM epilogue (gemm_tf32x3_pack)
+        const char* pfe = getenv("NTP_PACK_FUSED");
+        const char* ge = getenv("NTP_GEMM");
+        const bool fuse_pack = !(pfe && atoi(pfe) == 0) && !(ge && std::string(ge) == "cublas") && dt == NTP_BF16 &&
+                               (int64_t)P * d_s == m->hid && m->hid % 32 == 0 && d_s % 8 == 0 && !p2p;
         for (int64_t r = 0; r < V_p; r += hc) {      // H1 chunk -> pre-scaled slice rows + ReLU' bits
             const int64_t h = std::min(hc, V_p - r);
-            mlp_gemm(c, false, false, h, m->hid, m->d_in, X + r * ldx, ldx, W0g, ldw0, H1, ldH, s, 1, nullptr, 0, W0s);
-            pack_v2f(c, H1, ldH, w, split_dst, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split, h, r,
-                     bits, nwb);
+            if (fuse_pack) {
+                const PackEpi pk{static_cast<__nv_bfloat16*>(split_dst), V_p, d_s, g.dinv_out_orig(), row0, n, bits,
+                                 nwb, r};
+                gemm_tf32x3_pack(c, h, m->hid, m->d_in, X + r * ldx, ldx, W0s.hi, W0s.lo, ldw0, pk, s);
+            } else {
+                mlp_gemm(c, false, false, h, m->hid, m->d_in, X + r * ldx, ldx, W0g, ldw0, H1, ldH, s, 1, nullptr, 0,
+                         W0s);
+                pack_v2f(c, H1, ldH, w, split_dst, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split,
+                         h, r, bits, nwb);
+            }
             if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);   // a3 of chunk ch under a2 of ch+1
         }
         if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, last, 0));
@@ -825,7 +837,8 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     key.graph_version = c->g_version;
     key.head_chunk = getenv("NTP_HEAD_CHUNK") ? atoll(getenv("NTP_HEAD_CHUNK")) : 0;
     key.head_fused = (getenv("NTP_HEAD_FUSED") ? atoll(getenv("NTP_HEAD_FUSED")) : 1) +
-                     2 * (getenv("NTP_HEAD_TMA") ? atoll(getenv("NTP_HEAD_TMA")) : 1);
+                     2 * (getenv("NTP_HEAD_TMA") ? atoll(getenv("NTP_HEAD_TMA")) : 1) +
+                     4 * (getenv("NTP_PACK_FUSED") ? atoll(getenv("NTP_PACK_FUSED")) : 1);
     int64_t epoch_launches = 0;
     if (m->flags & NTP_M_STAGED) {   // slot buffers alternate and the copy stream is outside any graph
         drop_epoch_graph(c);

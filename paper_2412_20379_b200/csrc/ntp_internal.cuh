@@ -116,6 +116,20 @@ struct Graph {
 
 }  // namespace ntp
 
+// Pack epilogue of the MLP forward GEMM (W1 after propagation): H1 = ReLU(X W0) never reaches HBM in fp32;
+// its ReLU' mask words (bits[v][nwb]) and the row-scaled bf16 blocks of the split are written instead.
+namespace ntp {
+struct PackEpi {
+    __nv_bfloat16* out;        // send buffer [P][V_p][d_s] (bf16)
+    int64_t V_p;
+    int d_s;
+    const float* scale;        // D~_out^{-1/2}, original vertex order
+    int64_t row0, n;           // this rank's first vertex, graph size
+    uint32_t* bits;            // [V_p][nwb]
+    int nwb;
+    int64_t roff;              // GEMM row 0 = vertex row roff of this rank (row chunk)
+};
+}  // namespace ntp
 // ---------------------------------------------------------------- context
 // Everything a captured epoch graph bakes in.
 struct EpochKey {
@@ -159,6 +173,7 @@ struct ntp_ctx {
     ntp::DevBuf p2p_bar;                    // one int for the barrier allreduce
     cudaEvent_t ev[64] = {};
     cudaEvent_t ov_ev[256] = {};    // fork/join events of the chunked layout exchanges (a12)
+    ntp::PackEpi pack_epi{};        // parameters of the next pack-epilogue GEMM launch
     cudaEvent_t hop_ev[256] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
     int hop_ev_used = 0;
     int64_t launches = 0;
@@ -274,6 +289,8 @@ void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t 
 void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_elems, ntp_dtype dt,
                      cudaStream_t s);
 
+void gemm_tf32x3_pack(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B_hi,
+                      const float* B_lo, int64_t ldb, const PackEpi& pk, cudaStream_t s);
 // Tensor-core (tcgen05 kind::tf32, 3xTF32) GEMM, gemm.cu.  A stored [K][M] if a_mn else [M][K];
 // B stored [K][N] if b_mn else [N][K]; lda/ldb multiples of 4.  epi: 0 store, 1 ReLU, 2 keep where aux > 0.
 void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, bool a_mn,

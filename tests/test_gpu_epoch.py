@@ -184,3 +184,20 @@ def test_epoch_staged_inputs_same_result():
         losses.append(ctx.train_epoch(model, Xp, yp, mp, W0d, W1d, staged_slot=i % 2)["loss"])
     assert losses == a
     assert np.array_equal(W0d.cpu().numpy(), W0a) and np.array_equal(W1d.cpu().numpy(), W1a)
+
+
+@pytest.mark.parametrize("chunk", ["0", "1000"])
+def test_epoch_pack_epilogue_bitwise(chunk, monkeypatch):
+    """bf16 W1-after-propagation epochs: the split's pack fused into the MLP GEMM epilogue (ReLU, mask
+    words, D~_out^{-1/2} scale, bf16 blocks) computes the very values of GEMM + pack_v2f, so losses and
+    weights are bit-identical with and without it (whole epoch and row-chunked)."""
+    from paper_2412_20379_b200 import ntp
+    if chunk != "0":
+        monkeypatch.setenv("NTP_HEAD_CHUNK", chunk)
+    out = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("NTP_PACK_FUSED", fused)
+        losses, W0, W1, _, _ = _train_gpu("head_dir", 2, dtype=ntp.NTP_BF16)
+        out.append((losses, W0, W1))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
