@@ -376,9 +376,11 @@ def main():
 
     # ---- e2e: same call with HOST (pinned) inputs copied in every step, loss read back
     e2e_ms = e2e_serial_ms = None
-    h2d = x_bytes + V_p * 4 + V_p
+    h2d = V_p * ldx * 4 + V_p * 4 + V_p      # the padded host rows are what crosses PCIe
     if not args.no_e2e:
-        Xp = torch.from_numpy(Xh).pin_memory()   # host layout [V_p x d_in]; staged into a 16-B pitch on copy
+        # pinned host rows in the 16-byte pitch the GEMMs read (ldx floats), so each step is one plain DMA
+        Xp = torch.zeros(V_p, ldx, dtype=torch.float32).pin_memory()[:, :cfg.d_in]
+        Xp.copy_(torch.from_numpy(Xh))
         yp = torch.from_numpy(yh).pin_memory()
         mp = torch.from_numpy(mh).pin_memory()
         for _ in range(2):
@@ -392,7 +394,7 @@ def main():
         e2e_serial_ms = ev0.elapsed_time(ev1) / args.steps
         # pipelined loop (ntp_stage_inputs): every step still copies its own inputs from pinned host memory
         # and reads its loss back, but step i+1's copy runs on the copy engine while step i computes
-        for i in range(2):
+        for i in range(4):   # eager run per slot, then each slot's epoch graph is captured
             ctx.stage_inputs(i % 2, Xp, yp, mp)
             ctx.train_epoch(model, Xp, yp, mp, W0, W1, stream=stream, staged_slot=i % 2)
         barrier()

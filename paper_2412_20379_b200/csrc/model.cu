@@ -368,7 +368,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         // inputs staged by ntp_stage_inputs (copy stream); this epoch waits for that copy
         const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
         NTP_CHECK(c->st_rows[slot] == V_p, NTP_ERR_STATE, "staging slot %d holds no inputs of this shape", slot);
-        NTP_CUDA(cudaStreamWaitEvent(s, c->st_ready[slot], 0));
+        NTP_CUDA(cudaStreamWaitEvent(s, c->st_ready[slot], c->capturing ? cudaEventWaitExternal : 0));
         X = c->st_X[slot].as<float>();
         ldx = c->st_ld[slot];
         lab = c->st_y[slot].as<int32_t>();
@@ -739,7 +739,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     count_launch(c);
     if (m->flags & NTP_M_STAGED) {   // the slot may be refilled once this epoch is done with it
         const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
-        NTP_CUDA(cudaEventRecord(c->st_free[slot], s));
+        NTP_CUDA(cudaEventRecordWithFlags(c->st_free[slot], s, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
         c->st_free_rec[slot] = true;
     }
     NTP_CUDA(record_timing(c, E[ei++], s));   // E9 sgd
@@ -756,6 +756,11 @@ void drop_epoch_graph(ntp_ctx* c) {
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     c->graph_exec = nullptr;
     c->graph_valid = false;
+    for (int i = 0; i < 2; ++i) {
+        if (c->sg_exec[i]) cudaGraphExecDestroy(c->sg_exec[i]);
+        c->sg_exec[i] = nullptr;
+        c->sg_valid[i] = false;
+    }
 }
 
 // One epoch.  The enqueue sequence is captured into a CUDA graph on the second call with the same
@@ -839,18 +844,32 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     key.head_fused = (getenv("NTP_HEAD_FUSED") ? atoll(getenv("NTP_HEAD_FUSED")) : 1) +
                      2 * (getenv("NTP_HEAD_TMA") ? atoll(getenv("NTP_HEAD_TMA")) : 1) +
                      4 * (getenv("NTP_PACK_FUSED") ? atoll(getenv("NTP_PACK_FUSED")) : 1);
+    // graph cache entry: the plain epoch, or one per staging slot (whose buffers the graph bakes in; the
+    // copy stream's ready / free events become external event nodes)
+    const bool staged = (m->flags & NTP_M_STAGED) != 0;
+    const int sl = staged ? (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u) : 0;
+    if (staged) {
+        key.ptrs[0] = c->st_X[sl].p;
+        key.ptrs[1] = c->st_y[sl].p;
+        key.ptrs[2] = c->st_m[sl].p;
+        key.ld = c->st_ld[sl];
+    }
+    EpochKey& gkey = staged ? c->sg_key[sl] : c->graph_key;
+    bool& gwarm = staged ? c->sg_warm[sl] : c->graph_warm;
+    bool& gvalid = staged ? c->sg_valid[sl] : c->graph_valid;
+    cudaGraphExec_t& gexec = staged ? c->sg_exec[sl] : c->graph_exec;
+    int& ghops = staged ? c->sg_hops[sl] : c->graph_hops;
+    int64_t& glaunches = staged ? c->sg_launches[sl] : c->graph_launches;
     int64_t epoch_launches = 0;
-    if (m->flags & NTP_M_STAGED) {   // slot buffers alternate and the copy stream is outside any graph
-        drop_epoch_graph(c);
-        c->graph_warm = false;
-        enqueue_epoch(c, m, X_v, labels_v, mask_v, W0, W1, timed);
-        epoch_launches = c->launches - launches0;
-    } else if (graphs_enabled() && c->graph_valid && c->graph_key == key) {
-        NTP_CUDA(cudaGraphLaunch(c->graph_exec, s));
-        c->hop_ev_used = c->graph_hops;
-        epoch_launches = c->graph_launches;
-    } else if (graphs_enabled() && c->graph_warm && c->graph_key == key) {
-        drop_epoch_graph(c);
+    if (graphs_enabled() && gvalid && gkey == key) {
+        NTP_CUDA(cudaGraphLaunch(gexec, s));
+        c->hop_ev_used = ghops;
+        epoch_launches = glaunches;
+        if (staged) c->st_free_rec[sl] = true;
+    } else if (graphs_enabled() && gwarm && gkey == key) {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+        gvalid = false;
         cudaGraph_t graph = nullptr;
         NTP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
         c->capturing = true;
@@ -860,25 +879,25 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
             c->capturing = false;
             cudaStreamEndCapture(s, &graph);
             if (graph) cudaGraphDestroy(graph);
-            c->graph_warm = false;
+            gwarm = false;
             throw;
         }
         c->capturing = false;
         NTP_CUDA(cudaStreamEndCapture(s, &graph));
-        cudaError_t ie = cudaGraphInstantiate(&c->graph_exec, graph, 0);
+        cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
         cudaGraphDestroy(graph);
         NTP_CUDA(ie);
-        c->graph_valid = true;
-        c->graph_hops = c->hop_ev_used;
-        c->graph_launches = c->launches - launches0;
-        epoch_launches = c->graph_launches;
-        NTP_CUDA(cudaGraphLaunch(c->graph_exec, s));
+        gvalid = true;
+        ghops = c->hop_ev_used;
+        glaunches = c->launches - launches0;
+        epoch_launches = glaunches;
+        NTP_CUDA(cudaGraphLaunch(gexec, s));
     } else {
-        drop_epoch_graph(c);
+        drop_epoch_graph(c);   // an eager run may grow scratch buffers that captured graphs point into
         enqueue_epoch(c, m, X_v, labels_v, mask_v, W0, W1, timed);
         epoch_launches = c->launches - launches0;
-        c->graph_warm = true;
-        c->graph_key = key;
+        gwarm = true;
+        gkey = key;
     }
     double* scal = c->m_scal.as<double>();
     double h_scal[2] = {0, 0};

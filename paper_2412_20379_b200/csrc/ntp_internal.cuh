@@ -183,6 +183,12 @@ struct ntp_ctx {
     EpochKey graph_key{};
     bool graph_warm = false, graph_valid = false;
     cudaGraphExec_t graph_exec = nullptr;
+    // captured staged epochs, one per input slot (NTP_M_STAGED; the slot's buffers are baked in)
+    EpochKey sg_key[2]{};
+    bool sg_warm[2] = {false, false}, sg_valid[2] = {false, false};
+    cudaGraphExec_t sg_exec[2] = {nullptr, nullptr};
+    int sg_hops[2] = {0, 0};
+    int64_t sg_launches[2] = {0, 0};
     bool capturing = false;         // timing events become external event nodes while capturing
     int graph_hops = 0;
     int64_t graph_launches = 0;

@@ -167,7 +167,7 @@ def test_epoch_head_fused_matches_unfused(monkeypatch):
 def test_epoch_staged_inputs_same_result():
     """ntp_stage_inputs + NTP_M_STAGED (the e2e loop: epoch i+1's inputs copied while epoch i runs, two
     alternating slots) gives bit-identical losses and weights to device-resident inputs."""
-    a, W0a, W1a, _, _ = _train_gpu("tiny_dir", 3)
+    a, W0a, W1a, _, _ = _train_gpu("tiny_dir", 6)
     cfg = synth.get_config("tiny_dir")
     ctx = ntp_ctx_for("tiny_dir")
     X, y, m = synth.config_inputs(cfg)
@@ -178,8 +178,8 @@ def test_epoch_staged_inputs_same_result():
     W0d, W1d = torch.from_numpy(W0).cuda(), torch.from_numpy(W1).cuda()
     ctx.stage_inputs(0, Xp, yp, mp)
     losses = []
-    for i in range(3):
-        if i + 1 < 3:
+    for i in range(6):   # eager per slot, then each slot's captured epoch graph, then replays
+        if i + 1 < 6:
             ctx.stage_inputs((i + 1) % 2, Xp, yp, mp)
         losses.append(ctx.train_epoch(model, Xp, yp, mp, W0d, W1d, staged_slot=i % 2)["loss"])
     assert losses == a
