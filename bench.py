@@ -267,9 +267,10 @@ def main():
                     help="NTP_G_REORDER (internal degree-class numbering). auto: on when the vertex table is "
                          "far larger than L2 (n >= 1M: products, orkut, papers), off for the L2-resident Reddit "
                          "shape where it measured slower (DESIGN.md §5); never with --overlap")
-    ap.add_argument("--engine", default="decoupled", choices=["decoupled", "coupled"],
+    ap.add_argument("--engine", default="decoupled", choices=["decoupled", "coupled", "dp"],
                     help="coupled: NEXT-1, the naive tensor-parallel 2-layer GCN (d_in -> hid -> C) with its "
-                         "communication ledger, the paper's TP-vs-DTP ablation (P:696, P:1125-1128)")
+                         "communication ledger, the paper's TP-vs-DTP ablation (P:696, P:1125-1128); dp: NEXT-4, the "
+                         "data-parallel baseline (full-width rows, all-gather before each hop; load imbalance)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=3)
@@ -304,7 +305,7 @@ def main():
     t0 = time.time()
     # the last-hop chunked gather of --overlap needs original ids; the W1-after-propagation epoch overlaps its
     # layout changes by row chunk instead and keeps the reorder
-    reorder = (args.reorder == "on" or (args.reorder == "auto" and cfg.n >= 1_000_000)) and \
+    reorder = args.engine != "dp" and (args.reorder == "on" or (args.reorder == "auto" and cfg.n >= 1_000_000)) and \
         (not args.overlap or cfg.w_after_prop)
     ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric,
                       reorder=reorder)
@@ -315,6 +316,8 @@ def main():
     dt = ntp.NTP_BF16 if dtype_name == "bf16" else ntp.NTP_F32
     part = ntp.partition(n, cfg.w, world, dt, args.chunks, args.slice_align)
     V_p, d_s = part["V_p"], part["d_s"]
+    if args.engine == "dp":   # every rank aggregates full-width rows
+        d_s = ntp.partition(n, cfg.w, 1, dt, 1, args.slice_align)["d_s"]
     row0 = rank * V_p
     rows = max(0, min(V_p, n - row0))
     W0h, W1h = synth.model_weights(cfg)
@@ -333,6 +336,7 @@ def main():
     W0 = torch.from_numpy(W0h).cuda()
     W1 = torch.from_numpy(W1h).cuda()
     flags = ((ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if args.overlap else 0)
+             | (ntp.NTP_M_DATA_PARALLEL if args.engine == "dp" else 0)
              | (ntp.NTP_M_P2P_LAYOUTS if args.layouts == "p2p" else 0))
     model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=cfg.lr,
                  dtype=dt, chunks=args.chunks, flags=flags)
@@ -420,7 +424,9 @@ def main():
     ms = allmax(ms)
     e2e_ms = allmax(e2e_ms)
     e2e_serial_ms = allmax(e2e_serial_ms)
-    spmm_avg = allmax(spmm_ms / max(spmm_n, 1))
+    own_hop = spmm_ms / max(spmm_n, 1)
+    spmm_avg = allmax(own_hop)
+    hop_min = own_hop if dist is None else -allmax(-own_hop)   # per-rank hop time spread (load balance)
 
     if rank == 0:
         w = cfg.w
@@ -447,6 +453,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32" if dt == ntp.NTP_F32 else "bf16", "data": "synthetic",
             "epoch_s": ms / 1e3,
+            "engine": {"decoupled": "decoupled tensor parallelism (NeutronTP)",
+                       "dp": "data-parallel baseline (NEXT-4): full-width rows, all-gather before every hop"}[args.engine],
+            "load_balance": {"hop_ms_max_rank": spmm_avg, "hop_ms_min_rank": hop_min,
+                             "max_over_min": spmm_avg / hop_min if hop_min else None},
             "config": {"workload": WORKLOADS.get(args.config, args.config), "n": n, "nnz": nnz, "w": w, "K": cfg.K,
                        "gamma": cfg.gamma, "alpha": cfg.alpha, "P": world, "d_s": d_s, "V_p": V_p,
                        "chunks": args.chunks, "overlap": bool(args.overlap),

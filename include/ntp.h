@@ -211,6 +211,10 @@ ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const flo
                                    previous epoch); X_v / labels_v / train_mask_v are ignored
                                    except for X_v's shape.  Runs eagerly (no epoch graph). */
 #define NTP_M_SLOT_SHIFT    8
+#define NTP_M_DATA_PARALLEL 32u /* NEXT-4 baseline: each rank aggregates its own vertex rows at
+                                   full width after an all-gather of the state before every hop,
+                                   instead of feature slices (same function; load follows the rows'
+                                   degrees).  W1 before propagation, NCCL, no NTP_G_REORDER */
 #define NTP_M_P2P_LAYOUTS   8u  /* P > 1: peer-direct layout changes instead of the NCCL block
                                    all-to-all: the producers (pack, last-hop epilogue, loss
                                    kernel) store into the owners' CUDA-IPC windows over

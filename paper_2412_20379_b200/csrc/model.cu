@@ -336,6 +336,10 @@ static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool
     NTP_CUDA(cudaStreamWaitEvent(s, c->ev[51], 0));
 }
 
+static void enqueue_epoch_dp(ntp_ctx* c, const ntp_model* m, const float* X, int64_t ldx, const int32_t* lab,
+                             const uint8_t* msk, float* W0u, float* W1u, const float* W0g, int64_t ldw0,
+                             const float* W1g, int64_t ldw1, Split W0s, Split W1s, bool timed);
+
 // Enqueues one epoch (everything between events E0 and E9) on c->s_comp; capturable.
 static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                           const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, bool timed) {
@@ -434,6 +438,14 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         tf32_split(c, W1g, m->hid, m->C, ldw1, w1h, w1l, s);
         W0s = Split{w0h, w0l};
         W1s = Split{w1h, w1l};
+    }
+
+    if (m->flags & NTP_M_DATA_PARALLEL) {   // NEXT-4 baseline: full-width rows, all-gather before each hop
+        NTP_CHECK(!after && !(m->flags & (NTP_M_OVERLAP | NTP_M_P2P_LAYOUTS)) && !g.reordered, NTP_ERR_CONFIG,
+                  "NTP_M_DATA_PARALLEL: W1 before propagation, NCCL layouts, original vertex order only");
+        c->hop_ev_used = 0;
+        enqueue_epoch_dp(c, m, X, ldx, lab, msk, W0u, W1u, W0g, ldw0, W1g, ldw1, W0s, W1s, timed);
+        return;
     }
 
     // ---- scratch.  One GPU (P = 1): the layout changes are identities, so the producers write the
@@ -928,6 +940,12 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
             rep->bytes_recv[i] = wire;
         }
         rep->collectives = P > 1 ? 5 : 0;
+        if ((m->flags & NTP_M_DATA_PARALLEL) && P > 1) {   // 2K all-gathers of full-width rows + 1 allreduce
+            const int64_t ag = (int64_t)(P - 1) * V_p * slice_width(m->C, 1, m->dtype, c->slice_align) * (int64_t)es;
+            for (int i = 0; i < 4; ++i) rep->bytes_sent[i] = rep->bytes_recv[i] = 0;
+            rep->bytes_sent[0] = rep->bytes_recv[0] = 2 * m->K * ag;
+            rep->collectives = 2 * m->K + 1;
+        }
         rep->kernel_launches = epoch_launches;
         int nh = 0;
         rep->spmm_ms = collect_hop_ms(c, &nh);
@@ -935,6 +953,141 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     }
 }
 
+
+// NEXT-4: the data-parallel baseline the paper compares against (P:338-368,
+// "DepComm"-style).  Each rank owns the vertex rows R_q at FULL width and computes the
+// same decoupled model: before every hop the current state is all-gathered (every rank needs the
+// rows of all in-neighbours), then the rank aggregates only its own destination rows.  Same
+// function as the tensor-parallel epoch -- parity against the same oracle -- but the work per rank
+// follows the degree distribution of its rows (load imbalance, Fig. 10) and the traffic is 2K
+// all-gathers of full-width rows instead of 4 exchanges of slices.  Non-W1-after path, original
+// vertex order, fp32 or bf16 storage.
+static void enqueue_epoch_dp(ntp_ctx* c, const ntp_model* m, const float* X, int64_t ldx, const int32_t* lab,
+                             const uint8_t* msk, float* W0u, float* W1u, const float* W0g, int64_t ldw0,
+                             const float* W1g, int64_t ldw1, Split W0s, Split W1s, bool timed) {
+    const Graph& g = c->g;
+    cudaStream_t s = c->s_comp;
+    const int32_t P = c->world;
+    const int64_t n = g.n;
+    const int64_t V_p = cdiv(n, P);
+    const int64_t V_pad = (int64_t)P * V_p;
+    const int64_t row0 = (int64_t)c->rank * V_p;
+    const int64_t row_hi = std::min(row0 + V_p, n);
+    const ntp_dtype dt = m->dtype;
+    const size_t es = esize(dt);
+    const int32_t ws = slice_width(m->C, 1, dt, c->slice_align);   // full row width, 16-byte padded
+    const int64_t ldH = round4(m->hid), ldL = round4(std::max(m->C, m->hid));
+    cudaEvent_t* E = c->ev;
+    int ei = 1;
+    c->m_H1.ensure((size_t)V_p * ldH * sizeof(float));
+    c->m_L.ensure((size_t)V_p * ldL * sizeof(float));
+    c->m_dL.ensure((size_t)V_p * ldL * sizeof(float));
+    c->m_dH1.ensure((size_t)V_p * ldH * sizeof(float));
+    const int64_t n_w = (int64_t)m->d_in * m->hid + (int64_t)m->hid * m->C;
+    c->m_dW.ensure((size_t)n_w * sizeof(float));
+    c->m_scal.ensure(4 * sizeof(double));
+    const size_t full = (size_t)V_pad * ws * es;
+    c->recv.ensure(full + 16);
+    c->xfer.ensure(full + 16);
+    c->send.ensure(full + 16);      // S^0 (alpha term) / gradient rows
+    const int64_t loss_blocks = std::min<int64_t>(cdiv(V_p, 8), 148 * 8);
+    c->m_part.ensure((size_t)loss_blocks * (sizeof(double) + sizeof(int64_t)) + 16);
+    double* part = c->m_part.as<double>();
+    int64_t* cnt = reinterpret_cast<int64_t*>(part + loss_blocks);
+    float* H1 = c->m_H1.as<float>();
+    float* L = c->m_L.as<float>();
+    float* dL = c->m_dL.as<float>();
+    float* dH1 = c->m_dH1.as<float>();
+    float* dW0 = c->m_dW.as<float>();
+    float* dW1 = dW0 + (int64_t)m->d_in * m->hid;
+    double* scal = c->m_scal.as<double>();
+    char* A = static_cast<char*>(c->recv.p);
+    char* B = static_cast<char*>(c->xfer.p);
+    char* S0 = static_cast<char*>(c->send.p);
+    const size_t own = (size_t)row0 * ws * es;
+    if (V_pad > n)   // padding rows: never written by a hop, multiplied by zero downstream -> keep them zero
+        for (char* b : {A, B, S0}) NTP_CUDA(cudaMemsetAsync(b + (size_t)n * ws * es, 0, (V_pad - n) * ws * es, s));
+    const ncclDataType_t t = dt == NTP_BF16 ? ncclBfloat16 : ncclFloat32;
+    auto allgather = [&](char* buf) {   // own rows -> every rank's copy of the full matrix
+        if (P > 1) NTP_NCCL(ncclAllGather(buf + own, buf, (size_t)V_p * ws, t, c->comm, s));
+    };
+    // K hops of one direction on full-width rows: S^0 own rows in `A` (pre-scaled); returns the buffer
+    // holding Z^K own rows (unscaled, storage dtype)
+    auto hops = [&](bool transposed) -> char* {
+        const Csr& csr = transposed ? g.bwd() : g.fwd();
+        const float* rs = transposed ? g.dinv_out_p() : g.dinv_in_p();
+        const float* cs = transposed ? g.dinv_in_p() : g.dinv_out_p();
+        if (m->alpha != 0.f) NTP_CUDA(cudaMemcpyAsync(S0 + own, A + own, (size_t)V_p * ws * es, cudaMemcpyDeviceToDevice, s));
+        char* cur = A;
+        char* nxt = B;
+        for (int k = 1; k <= m->K; ++k) {
+            allgather(cur);
+            const bool tm = timed && c->hop_ev_used + 2 <= 256;
+            if (tm) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
+            spmm_hop(c, csr, rs, cs, cur, nxt, m->alpha != 0.f ? (const void*)S0 : (const void*)cur, ws, ws, ws, ws,
+                     dt, m->gamma, m->alpha, k == m->K ? 1 : 0, row0, row_hi, s);
+            if (tm) {
+                NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used + 1], s));
+                c->hop_ev_used += 2;
+            }
+            std::swap(cur, nxt);
+        }
+        return cur;
+    };
+    // a2: MLP forward on own rows; S^0 own rows = D~_out^{-1/2} L^ (storage dtype)
+    mlp_gemm(c, false, false, V_p, m->hid, m->d_in, X, ldx, W0g, ldw0, H1, ldH, s, 1, nullptr, 0, W0s);
+    mlp_gemm(c, false, false, V_p, m->C, m->hid, H1, ldH, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd
+    pack_v2f(c, L, ldL, m->C, A + own, V_p, ws, 1, g.dinv_out_orig(), row0, n, NTP_F32, dt, s);
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E2 (no split)
+    char* Z = hops(false);
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E3 prop fwd (incl. all-gathers)
+    // a6: loss on own rows; gradient rows (pre-scaled by the backward column side) into A's own rows
+    char* G = (Z == A) ? B : A;
+    int64_t nb = 0;
+    if (dt == NTP_F32)
+        nb = launch_softmax_xent(c, (const float*)(Z + own), 0, V_p, ws, m->C, lab, msk, row0, n, (float*)(G + own), 1,
+                                 g.dinv_in_orig(), part, cnt, ws, s);
+    else
+        nb = launch_softmax_xent(c, (const __nv_bfloat16*)(Z + own), 0, V_p, ws, m->C, lab, msk, row0, n,
+                                 (__nv_bfloat16*)(G + own), 1, g.dinv_in_orig(), part, cnt, ws, s);
+    if (ws > m->C) {
+        if (dt == NTP_F32)
+            zero_pad_cols_kernel<float><<<eblocks(V_p * (ws - m->C)), 256, 0, s>>>((float*)(G + own), V_p, ws, 1, m->C,
+                                                                                  nullptr, 0);
+        else
+            zero_pad_cols_kernel<__nv_bfloat16><<<eblocks(V_p * (ws - m->C)), 256, 0, s>>>(
+                (__nv_bfloat16*)(G + own), V_p, ws, 1, m->C, nullptr, 0);
+        NTP_LAUNCH_CHECK();
+        count_launch(c);
+    }
+    reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb, scal);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E4 loss
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E5 (no split)
+    if (G != A) NTP_CUDA(cudaMemcpyAsync(A + own, G + own, (size_t)V_p * ws * es, cudaMemcpyDeviceToDevice, s));
+    char* dZ = hops(true);
+    unpack_f2v(c, dZ + own, V_p, ws, 1, dL, ldL, m->C, dt, NTP_F32, s);
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E6 prop bwd
+    // a10: MLP backward on own rows
+    mlp_gemm(c, true, false, m->hid, m->C, V_p, H1, ldH, dL, ldL, dW1, m->C, s);
+    mlp_gemm(c, false, true, V_p, m->hid, m->C, dL, ldL, W1g, ldw1, dH1, ldH, s, 2, H1, ldH, W1s);
+    mlp_gemm(c, true, false, m->d_in, m->hid, V_p, X, ldx, dH1, ldH, dW0, m->hid, s);
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E7 mlp bwd
+    if (P > 1) {
+        NTP_NCCL(ncclGroupStart());
+        NTP_NCCL(ncclAllReduce(dW0, dW0, n_w, ncclFloat32, ncclSum, c->comm, s));
+        NTP_NCCL(ncclAllReduce(scal, scal, 2, ncclFloat64, ncclSum, c->comm, s));
+        NTP_NCCL(ncclGroupEnd());
+    }
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E8 allreduce
+    sgd_kernel<<<eblocks(n_w), 256, 0, s>>>(W0u, (int64_t)m->d_in * m->hid, W1u, (int64_t)m->hid * m->C, dW0, scal,
+                                            m->lr);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+    NTP_CUDA(record_timing(c, E[ei++], s));   // E9 sgd
+}
 
 // Input staging (e2e loops): host -> slot copy on the copy stream, after the last epoch that read
 // the slot.  One contiguous DMA in the host pitch, then the 16-byte GEMM pitch on the device (a 2-D

@@ -192,6 +192,20 @@ def main(name):
             assert abs(rep["loss"] - ref_losses[e]) <= 2e-2 * abs(ref_losses[e]), f"reordered overlap loss {rep['loss']}"
         ctxo.close()
 
+    # ---- 7. NEXT-4: the data-parallel baseline (full-width rows, all-gather before every hop) trains the
+    # same model: losses vs the oracle (fp32 1e-4, bf16 2e-2), traffic = 2K all-gathers of full rows
+    if not cfg.w_after_prop:
+        for dtype, tol in ((ntp.NTP_F32, 1e-4), (ntp.NTP_BF16, 2e-2)):
+            W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+            model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
+                         dtype=dtype, chunks=1, flags=ntp.NTP_M_DATA_PARALLEL)
+            for e in range(3):
+                rep = ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
+                bound = tol if dtype == ntp.NTP_F32 else tol * abs(ref_losses[e])
+                assert abs(rep["loss"] - ref_losses[e]) <= bound, f"DP loss {rep['loss']} vs {ref_losses[e]} ({dtype})"
+            eb = 4 if dtype == ntp.NTP_F32 else 2
+            assert rep["bytes_sent"][0] == 2 * cfg.K * (world - 1) * V_p * oracle.layout.slice_width(cfg.C, 1, eb) * eb
+
     # ---- 6. NEXT-1: naive (coupled) TP epochs, 2 and 3 layers: losses vs the coupled oracle, and the
     # communication ledger: 4L - 2 layout changes moving the closed-form bytes
     from oracle import coupled

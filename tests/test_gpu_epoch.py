@@ -201,3 +201,24 @@ def test_epoch_pack_epilogue_bitwise(chunk, monkeypatch):
         out.append((losses, W0, W1))
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
+
+
+@pytest.mark.parametrize("name", ["tiny_sym", "small_appnp", "small_dir"])
+def test_epoch_data_parallel_baseline(name):
+    """NEXT-4: the data-parallel baseline (NTP_M_DATA_PARALLEL: full-width vertex rows, all-gather
+    before each hop) trains the same model as the tensor-parallel epoch: losses and weights vs the oracle
+    (fp32, 1e-4) on one GPU (the multi-GPU case is mp_check step 7)."""
+    from paper_2412_20379_b200 import ntp
+    cfg = synth.get_config(name)
+    ctx = ntp_ctx_for(name)
+    X, y, m = synth.config_inputs(cfg)
+    W0, W1 = synth.model_weights(cfg)
+    model = _model(cfg, 0, ntp.NTP_M_DATA_PARALLEL)
+    W0d, W1d = torch.from_numpy(W0).cuda(), torch.from_numpy(W1).cuda()
+    losses = [ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0d, W1d)["loss"]
+              for _ in range(3)]
+    ref, rW0, rW1 = _train_oracle(name, 3, model["lr"])
+    for a, b in zip(losses, ref):
+        assert abs(a - b) <= 1e-4
+    for got, r in ((W0d.cpu().numpy(), rW0), (W1d.cpu().numpy(), rW1)):
+        assert np.abs(got - r).max() <= 1e-4 * max(1.0, np.abs(r).max())
