@@ -539,15 +539,18 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     if (p.u_end <= p.u_begin) return;
     // 32-byte vectors when every row the hop touches is 32-byte aligned and at most 8 of them wide
     // (E >= 4 edge slots: wider rows would need more accumulator registers than the kernel has)
-    // auto (NTP_SPMM_VB unset): 32-byte vectors on low-degree graphs except 64-byte rows -- measured on the
-    // papers shape (bf16 storage, ms per hop): 128 B rows 61.8 vs 72.1, 256 B 105.0 vs 107.3, 32 B 23.6 vs
-    // 24.5, 64 B 39.4 vs 37.9; neutral-to-slower on fp32 products and the high-degree Reddit shape
+    // auto (NTP_SPMM_VB unset), by row width -- measured ms per hop, 16-byte vs 32-byte vectors:
+    //   papers (bf16): 256 B 107.3 vs 105.0, 128 B 72.1 vs 61.8, 64 B 37.9 vs 39.4, 32 B 24.5 vs 23.6
+    //   products (fp32): 192 B 2.95 vs 2.98, 96 B 2.03 vs 1.75, 32 B 0.89 vs 0.95
+    //   Reddit (fp32): 96 B 1.435 vs 1.409, 32 B 0.85 vs 1.02
     static const int vb_env = [] { const char* v = getenv("NTP_SPMM_VB"); return v ? atoi(v) : -1; }();
     const bool low_deg_g = p.nnz < 32 * std::max<int64_t>(p.n, 1);
     const bool al32 = (nvec % 2) == 0 && nvec <= 16 && p.ld_in % 32 == 0 && p.ld_out % 32 == 0 &&
                       ((uintptr_t)S_in % 32) == 0 && ((uintptr_t)S_out % 32) == 0 &&
                       (S0 == nullptr || (p.ld_s0 % 32 == 0 && ((uintptr_t)S0 % 32) == 0));
-    if (al32 && (vb_env == 32 || (vb_env < 0 && low_deg_g && dt == NTP_BF16 && nvec != 4))) {
+    // rows of 96 / 128 / 256 B (and 32-B bf16 rows on low-degree graphs) measured faster with 32-byte vectors
+    const bool auto32 = nvec == 6 || nvec == 8 || nvec == 16 || (nvec == 2 && dt == NTP_BF16 && low_deg_g);
+    if (al32 && (vb_env == 32 || (vb_env < 0 && auto32))) {
         if (dt == NTP_F32) dispatch_hop<float, 32>(p, nvec / 2, s);
         else dispatch_hop<__nv_bfloat16, 32>(p, nvec / 2, s);
     } else {
