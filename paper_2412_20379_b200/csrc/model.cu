@@ -726,6 +726,10 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
             if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, b_ev[ch], 0));
+            if (wgrad_fused_supported(P, d_s, m->d_in, m->hid, dt)) {   // unpack + dW0 GEMM in one kernel
+                wgrad_fused(c, X, ldx, V_p, m->d_in, gathered_b, d_s, P, m->hid, bits, nwb, r, r + h, dw0_at(ch), s);
+                continue;
+            }
             unpack_f2v(c, gathered_b, V_p, d_s, P, dH1, ldH, w, dt, NTP_F32, s, nullptr, 0, h, r, bits, nwb);
             mlp_gemm(c, true, false, m->d_in, m->hid, h, X + r * ldx, ldx, dH1, ldH, dw0_at(ch), m->hid, s);
         }
@@ -855,7 +859,8 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     key.head_chunk = getenv("NTP_HEAD_CHUNK") ? atoll(getenv("NTP_HEAD_CHUNK")) : 0;
     key.head_fused = (getenv("NTP_HEAD_FUSED") ? atoll(getenv("NTP_HEAD_FUSED")) : 1) +
                      2 * (getenv("NTP_HEAD_TMA") ? atoll(getenv("NTP_HEAD_TMA")) : 1) +
-                     4 * (getenv("NTP_PACK_FUSED") ? atoll(getenv("NTP_PACK_FUSED")) : 1);
+                     4 * (getenv("NTP_PACK_FUSED") ? atoll(getenv("NTP_PACK_FUSED")) : 1) +
+                     8 * (getenv("NTP_WGRAD_FUSED") ? atoll(getenv("NTP_WGRAD_FUSED")) : 1);
     // graph cache entry: the plain epoch, or one per staging slot (whose buffers the graph bakes in; the
     // copy stream's ready / free events become external event nodes)
     const bool staged = (m->flags & NTP_M_STAGED) != 0;

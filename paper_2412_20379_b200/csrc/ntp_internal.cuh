@@ -154,7 +154,7 @@ struct ntp_ctx {
     // scratch
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
-    ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp, m_head;
+    ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp, m_head, m_wgrad;
     // coupled (naive TP) epoch: Z^l, H^l per layer, dA / dZ scratch, padded weights
     ntp::DevBuf cp_Z[NTP_MAX_LAYERS + 1], cp_H[NTP_MAX_LAYERS + 1], cp_A, cp_B, cp_W;
     // input staging slots (ntp_stage_inputs): X [V_p x round4(d_in)], raw host-pitch copy, labels, mask
@@ -306,6 +306,12 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
 void tf32_split(ntp_ctx* c, const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
                 cudaStream_t s);
 
+// dW0 = X^T (G .* ReLU') straight from the bf16 gradient slice (wgrad.cu): bf16 slices, hid = P*d_s = 128,
+// d_s >= 64, d_in <= 128.
+bool wgrad_fused_supported(int32_t P, int32_t d_s, int32_t d_in, int32_t hid, ntp_dtype dt);
+void wgrad_fused(ntp_ctx* c, const float* X, int64_t ldx, int64_t V_p, int32_t d_in, const void* G, int32_t d_s,
+                 int32_t P, int32_t hid, const uint32_t* bits, int32_t nwb, int64_t r_begin, int64_t r_end, float* dW0,
+                 cudaStream_t s);
 // Fused W1-after-propagation head (head.cu): bf16 gathered slice, P*d_s == 128, C <= 192.
 bool head_fused_supported(int32_t P, int32_t d_s, int32_t hid, int32_t C, ntp_dtype dt);
 int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, int32_t P, int32_t hid, int32_t C,
