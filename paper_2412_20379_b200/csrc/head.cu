@@ -111,8 +111,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 
 __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __grid_constant__ CUtensorMap tmZ,
                                                                      const HeadParams p) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);   // stays a shared pointer
     uint8_t* sZ = smem;                              // [2][2 boxes]
     uint8_t* sDL = sZ + 4 * kBox;                    // [CB boxes]
     uint8_t* sW = sDL + p.CB * kBox;                 // [hi, lo][CB boxes]
