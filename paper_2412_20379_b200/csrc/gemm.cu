@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                     __floats2bfloat162_rn(e[8 * g8 + 2 * k] * sc, e[8 * g8 + 2 * k + 1] * sc);
                                 ow[k] = *reinterpret_cast<const uint32_t*>(&h2);
                             }
-                            *reinterpret_cast<uint4*>(p.pk.out + ((int64_t)qb * p.pk.V_p + v) * p.pk.d_s + jj) = o;
+                            const int64_t orow = p.pk.perm ? (int64_t)__ldg(p.pk.perm + v) : v;
+                            *reinterpret_cast<uint4*>(p.pk.out + ((int64_t)qb * p.pk.V_p + orow) * p.pk.d_s + jj) = o;
                         }
                     }
                     continue;

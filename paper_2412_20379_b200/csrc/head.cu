@@ -61,6 +61,7 @@ struct HeadParams {
     int64_t* cnt;               // [grid]
     int64_t tiles;
     uint32_t idesc1, idesc2, idesc3;
+    const int32_t* out_perm;    // one GPU, reordered graph: gradient row of vertex v goes to slice row out_perm[v]
     int tma;                    // d_s >= 64: Z tiles by TMA (3-D map [P][V_p][d_s], 64-column boxes)
 };
 
@@ -399,9 +400,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __gri
                     o.y = pack_bf16(__uint_as_float(x[c8 * 8 + 2]) * sc, __uint_as_float(x[c8 * 8 + 3]) * sc);
                     o.z = pack_bf16(__uint_as_float(x[c8 * 8 + 4]) * sc, __uint_as_float(x[c8 * 8 + 5]) * sc);
                     o.w = pack_bf16(__uint_as_float(x[c8 * 8 + 6]) * sc, __uint_as_float(x[c8 * 8 + 7]) * sc);
+                    const int64_t ov = p.out_perm ? (int64_t)__ldg(p.out_perm + v) : v;
                     __nv_bfloat16* dst = p.peer ? static_cast<__nv_bfloat16*>(p.peer[q]) +
                                                       ((int64_t)p.rank * p.V_p + v) * p.d_s + j
-                                                : p.out + ((int64_t)q * p.V_p + v) * p.d_s + j;
+                                                : p.out + ((int64_t)q * p.V_p + ov) * p.d_s + j;
                     *reinterpret_cast<uint4*>(dst) = o;
                 }
             }
@@ -482,13 +484,14 @@ bool head_fused_supported(int32_t P, int32_t d_s, int32_t hid, int32_t C, ntp_dt
 int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, int32_t P, int32_t hid, int32_t C,
                    const float* W1, int64_t ldw1, const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n,
                    const float* gscale, void* out, void* const* peer, float* dW1, double* part, int64_t* cnt,
-                   cudaStream_t s, int64_t v_lo, int64_t v_hi) {
+                   cudaStream_t s, int64_t v_lo, int64_t v_hi, const int32_t* out_perm) {
     if (v_hi < 0) v_hi = V_p;
     HeadParams p{};
     p.Z = static_cast<const __nv_bfloat16*>(gathered);
     p.V_p = V_p;
     p.v_lo = v_lo;
     p.v_hi = v_hi;
+    p.out_perm = out_perm;
     p.d_s = d_s;
     p.P = P;
     p.lds = 0;

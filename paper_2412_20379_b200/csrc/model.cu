@@ -551,6 +551,11 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     void* slice_in = p2p ? c->p2p_split.p : c->recv.p;   // this rank's feature slice after a split
     void* split_dst = p2p ? nullptr : (local ? c->recv.p : c->send.p);   // where the split's producer writes
 
+    // one GPU on a reordered graph: producers that can scatter write S^0 / the gradient straight into the
+    // internal vertex order, so the hops skip the permutation pass (propagate_consume input_internal)
+    const int32_t* perm_local = (local && g.reordered && m->alpha == 0.f) ? g.perm.as<int32_t>() : nullptr;
+    bool fwd_internal = false, bwd_internal = false;
+
     // a2 (+ a3's pack): MLP forward (ReLU fused into the GEMM epilogue)
     const float* prop_src = H1;             // rows propagated (w columns)
     int64_t ld_src = ldH;
@@ -572,7 +577,8 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             const int64_t h = std::min(hc, V_p - r);
             if (fuse_pack) {
                 const PackEpi pk{static_cast<__nv_bfloat16*>(split_dst), V_p, d_s, g.dinv_out_orig(), row0, n, bits,
-                                 nwb, r};
+                                 nwb, r, perm_local};
+                fwd_internal = perm_local != nullptr;
                 gemm_tf32x3_pack(c, h, m->hid, m->d_in, X + r * ldx, ldx, W0s.hi, W0s.lo, ldw0, pk, s);
             } else {
                 mlp_gemm(c, false, false, h, m->hid, m->d_in, X + r * ldx, ldx, W0g, ldw0, H1, ldH, s, 1, nullptr, 0,
@@ -607,7 +613,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         a.alpha = m->alpha;
         a.transposed = false;
         if (local) {
-            gathered = propagate_consume(c, a, s, timed);
+            gathered = propagate_consume(c, a, s, timed, fwd_internal);
         } else if (p2p) {
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
@@ -659,7 +665,8 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                 // one tcgen05 pass over the chunk's rows (head.cu): logits, dl and dZ stay on chip
                 nb_loss += head_fused(c, gathered, V_p, d_s, P, m->hid, m->C, W1g, ldw1, lab, msk, row0, n, gscale_bwd,
                                       p2p ? nullptr : gsend, tab_split, dw1_at(ch), part + nb_loss, cnt + nb_loss, s,
-                                      r, r + h);
+                                      r, r + h, perm_local);
+                bwd_internal = perm_local != nullptr;
                 if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);   // a7 of chunk ch
                 continue;
             }
@@ -700,7 +707,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         a.alpha = m->alpha;
         a.transposed = true;
         if (local) {
-            gathered_b = propagate_consume(c, a, s, timed);
+            gathered_b = propagate_consume(c, a, s, timed, bwd_internal);
         } else if (p2p) {
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);

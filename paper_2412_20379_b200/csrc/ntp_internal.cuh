@@ -128,6 +128,7 @@ struct PackEpi {
     uint32_t* bits;            // [V_p][nwb]
     int nwb;
     int64_t roff;              // GEMM row 0 = vertex row roff of this rank (row chunk)
+    const int32_t* perm;       // one GPU, reordered graph: slice row of vertex v = perm[v] (internal order)
 };
 }  // namespace ntp
 // ---------------------------------------------------------------- context
@@ -249,7 +250,8 @@ void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi,
 // Pre-scaled input that may be consumed (alpha == 0: S^0 is dead after hop 1): the hops ping-pong
 // between a.H and a.Z (same ld) with no scratch slice; returns the buffer holding Z^K (a.H or a.Z).
 // alpha != 0 falls back to propagate() (S^0 must live through every hop) and returns a.Z.
-void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops);
+// input_internal: a.H already holds S^0 in the graph's internal vertex order (the producer scattered it)
+void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bool input_internal = false);
 double collect_hop_ms(ntp_ctx* c, int* n_hops);
 void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K, float gamma, float alpha,
                         bool transposed, ntp_dtype dt, int chunks, bool overlap, cudaStream_t user);
@@ -317,7 +319,7 @@ bool head_fused_supported(int32_t P, int32_t d_s, int32_t hid, int32_t C, ntp_dt
 int64_t head_fused(ntp_ctx* c, const void* gathered, int64_t V_p, int32_t d_s, int32_t P, int32_t hid, int32_t C,
                    const float* W1, int64_t ldw1, const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n,
                    const float* gscale, void* out, void* const* peer, float* dW1, double* part, int64_t* cnt,
-                   cudaStream_t s, int64_t v_lo = 0, int64_t v_hi = -1);
+                   cudaStream_t s, int64_t v_lo = 0, int64_t v_hi = -1, const int32_t* out_perm = nullptr);
 
 inline size_t esize(ntp_dtype d) { return d == NTP_BF16 ? 2 : 4; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

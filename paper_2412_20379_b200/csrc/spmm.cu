@@ -648,7 +648,7 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
     }
 }
 
-void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops) {
+void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bool input_internal) {
     if (a.alpha != 0.f || a.K == 0 || a.ld_h != a.ld_z || a.po.tab) {
         propagate(c, a, s, time_hops, true);
         return a.Z;
@@ -660,7 +660,7 @@ void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time
     const int32_t* inv = g.inv_p();
     void* cur = const_cast<void*>(a.H);
     void* oth = a.Z;
-    if (inv) {   // reordered graph: S^0 permuted into internal order first (into the other buffer)
+    if (inv && !input_internal) {   // reordered graph: S^0 permuted into internal order first (other buffer)
         prescale(c, cur, a.ld_h, oth, a.ld_z, a.cols, nullptr, g.n, a.dtype, s, inv);
         std::swap(cur, oth);
     }

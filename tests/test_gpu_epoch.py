@@ -240,3 +240,25 @@ def test_epoch_wgrad_fused_matches(name, monkeypatch):
     assert out[0][0] == out[1][0]
     rel = np.linalg.norm(out[0][1] - out[1][1]) / np.linalg.norm(out[1][1])
     assert rel <= 1e-4, f"dW0 fused vs unfused: normwise relative difference {rel:.3e}"
+
+
+@pytest.mark.parametrize("name", ["head_dir", "head_sym"])
+def test_epoch_head_bf16_reordered(name):
+    """One GPU on a degree-reordered graph: the pack epilogue and the fused head scatter S^0 and the
+    gradient straight into the internal vertex order (no permutation pass before the hops); losses and
+    weight updates still match the oracle within the bf16 tolerance."""
+    from paper_2412_20379_b200 import ntp
+    cfg = synth.get_config(name)
+    ctx = ntp_ctx_for(name, reorder=True)
+    X, y, m = synth.config_inputs(cfg)
+    W0i, W1i = synth.model_weights(cfg)
+    model = _model(cfg, ntp.NTP_BF16)
+    W0d, W1d = torch.from_numpy(W0i).cuda(), torch.from_numpy(W1i).cuda()
+    losses = [ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0d, W1d)["loss"]
+              for _ in range(2)]
+    ref, rW0, rW1 = _train_oracle(name, 2, model["lr"])
+    for a, b in zip(losses, ref):
+        assert abs(a - b) <= 2e-2 * abs(b)
+    for got, r, init in ((W0d.cpu().numpy(), rW0, W0i), (W1d.cpu().numpy(), rW1, W1i)):
+        d_ref, d_got = r - init, got.astype(np.float64) - init
+        assert np.linalg.norm(d_got - d_ref) <= 2e-2 * np.linalg.norm(d_ref)
