@@ -115,22 +115,23 @@ def l2_gather_bytes(nnz, n, d_s, elem):
     return (nnz + n) * r
 
 
-def gather_ceiling(n, row_bytes):
+def gather_ceiling(n, row_bytes, l2_bytes):
     """Measured random-row-gather ceiling of this B200 (profiles/gather_ceiling.json, written from
-    scripts/l2_probe.cu): rows/s for the table's residency (L2 if the slice fits, else HBM) at the
-    smallest probed row size >= row_bytes."""
+    scripts/l2_probe.cu): rows/s for the table's residency (L2 if the slice fits the device's L2, the same
+    test as hop_bytes, else HBM) at the smallest probed row size >= row_bytes."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "gather_ceiling.json")))
     except Exception:
         return None
-    tab = d["l2_resident"] if n * row_bytes <= 100e6 else d["hbm_resident"]
+    l2_res = n * row_bytes <= l2_bytes
+    tab = d["l2_resident"] if l2_res else d["hbm_resident"]
     sizes = sorted(int(k) for k in tab)
     fit = [k for k in sizes if k >= row_bytes] or sizes[-1:]
     if not fit:
         return None
     k = fit[0]
     return {"rows_per_s": tab[str(k)]["Grows_per_s"] * 1e9, "probe_row_bytes": k,
-            "residency": "L2" if n * row_bytes <= 100e6 else "HBM", "source": "profiles/gather_ceiling.json"}
+            "residency": "L2" if l2_res else "HBM", "source": "profiles/gather_ceiling.json"}
 
 
 def load_peaks():
@@ -151,19 +152,52 @@ def load_traffic(config, P, dtype):
 
 
 # ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
+def host_info():
+    """nproc, CPU model and RAM of this host (SURVEY §8(d) oracle timing)."""
+    info = {"nproc": os.cpu_count(), "cpu_model": None, "ram_GB": None}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["ram_GB"] = round(int(line.split()[1]) / 1e6, 1)
+                break
+    except Exception:
+        pass
+    return info
+
+
 def oracle_epoch_time(cfg, epochs=1):
-    """Times the fp64 oracle (as it stands) for `epochs` full epochs on this host."""
+    """Times the fp64 oracle (as it stands) for `epochs` full epochs on this host, from the same initial
+    weights the GPU run starts from; returns its per-epoch losses too (the bench line's parity check), and
+    a single-thread one-hop timing on a 2% row sample, extrapolated to the whole graph."""
     import oracle
     t0 = time.time()
     g = oracle.graph.graph_from_config(cfg)
     t_graph = time.time() - t0
     X, y, m = synth.config_inputs(cfg)
     W0, W1 = synth.model_weights(cfg)
+    losses = []
     t0 = time.time()
     for _ in range(epochs):
         loss, W0, W1 = oracle.model.train_epoch(g, X, y, m, W0, W1, cfg.K, cfg.gamma, cfg.alpha, cfg.lr)
+        losses.append(loss)
     dt = (time.time() - t0) / epochs
-    return dt, g.nnz, oracle.lib.oracle_num_threads(), t_graph
+    threads = oracle.lib.oracle_num_threads()
+    one = None
+    try:
+        rng = np.random.default_rng(0)
+        rows = np.sort(rng.choice(g.n, size=max(1, g.n // 50), replace=False))
+        zin = synth.features(cfg.seed, g.n, cfg.w)
+        oracle.lib.oracle_set_num_threads(1)
+        t1 = time.time()
+        oracle.propagate.hop_rows(g, zin, None, rows, cfg.gamma, 0.0)
+        one = (time.time() - t1) * g.n / rows.size
+    finally:
+        oracle.lib.oracle_set_num_threads(threads)
+    return dt, g.nnz, threads, t_graph, losses, one
 
 
 def run_reference(args, cfg, rank):
@@ -357,9 +391,10 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- warm-up
+    # ---- warm-up (the first epochs start from the same weights as the oracle leg: parity check below)
+    warm_losses = []
     for _ in range(args.warmup):
-        ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream)
+        warm_losses.append(ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream)["loss"])
     # ---- timed (device events on the caller's stream; the library orders its streams after it)
     clocks = ClockSampler(local)
     clocks.start()
@@ -442,7 +477,7 @@ def main():
         achieved = bh / (spmm_avg * 1e-3) / 1e9
         traffic = load_traffic(args.config, world, dtype_name)
         l2b = l2_gather_bytes(nnz, n, d_s, esz)
-        gc = gather_ceiling(n, d_s * esz)
+        gc = gather_ceiling(n, d_s * esz, l2_size)
         gather_line = None
         if gc:
             rows_ps = (nnz + n) / (spmm_avg * 1e-3)
@@ -468,6 +503,11 @@ def main():
                        "graph_setup_s": round(t_graph, 3), "hbm_used_GB_max_rank": round(hbm_used_gb, 1)},
             "roofline": {"kernel": "spmm_hop_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "binding_resource": ("L2 random-row gather: the slice fits L2, so HBM carries the compulsory "
+                                              "bytes only and `gather` is the real bound" if bmodel.startswith("perfect")
+                                              else "HBM: the slice exceeds L2, every arc's row slice streams from HBM"),
+                         "hbm_frac_measured": (traffic / (spmm_avg * 1e-3) / 1e9 / peak) if traffic else None,
+                         "timed_span": "spmm_hop_kernel + its spmm_fixup_kernel (cut-row carries, ~1% of the span)",
                          "algorithmic_bytes_per_launch": bh, "bytes_model": bmodel, "l2_bytes": l2_size,
                          "avg_launch_ms": spmm_avg,
                          "launches_timed": spmm_n, "peak_source": peak_src,
@@ -497,11 +537,23 @@ def main():
                                               "(DESIGN.md §10); the default Reddit-shaped bench line carries it"}
         elif world == 1 and not args.no_cpu_baseline:
             try:
-                t_cpu, nnz_o, cores, _ = oracle_epoch_time(cfg, args.cpu_epochs)
+                t_cpu, nnz_o, cores, _, o_losses, hop1 = oracle_epoch_time(cfg, args.cpu_epochs)
                 line["cpu_baseline"] = {"value": 2 * cfg.K * nnz_o * w / t_cpu / 1e9, "unit": "GE/s",
                                         "cores": cores, "kind": "oracle", "epoch_s": t_cpu,
                                         "sample": f"{args.cpu_epochs} full fp64 oracle epochs of the same workload "
-                                                  f"(graph build excluded), OpenMP over rows + numpy BLAS"}
+                                                  f"(graph build excluded), OpenMP over rows + numpy BLAS",
+                                        "host": host_info(),
+                                        "hop_1thread_s": hop1,
+                                        "hop_1thread_note": "one forward hop on 1 thread, timed on a 2% row sample "
+                                                            "and extrapolated linearly to all rows"}
+                # parity of the bench workload itself: the GPU's first epochs (warm-up, same initial weights)
+                # against the oracle's, loss by loss (R10: 1e-4 for fp32 slices, 2e-2 |loss| for bf16)
+                k = min(len(o_losses), len(warm_losses))
+                errs = [abs(warm_losses[i] - o_losses[i]) for i in range(k)]
+                tol = 1e-4 if dt == ntp.NTP_F32 else 2e-2 * abs(o_losses[0])
+                line["parity"] = {"epochs": k, "loss_gpu": warm_losses[:k], "loss_oracle": o_losses[:k],
+                                  "abs_err": max(errs) if errs else None, "tol": tol,
+                                  "pass": bool(errs) and max(errs) <= tol}
             except Exception as e:  # pragma: no cover
                 line["cpu_baseline"] = {"value": None, "unit": "GE/s", "cores": os.cpu_count(), "kind": "oracle",
                                         "sample": f"failed: {e}"}

@@ -101,7 +101,11 @@ int         ntp_abi_version(void);
                                 descending total degree (the hot rows of the gather
                                 become contiguous).  Invisible at the ABI: slices,
                                 ntp_copy_csr and ntp_copy_dinv stay in original ids.
-                                Not combinable with NTP_M_OVERLAP (NTP_ERR_CONFIG). */
+                                Not combinable with the last-hop chunked gather of
+                                NTP_M_OVERLAP (W1 before propagation) or with
+                                ntp_propagate_pipeline's overlap (NTP_ERR_CONFIG); the
+                                W1-after-propagation epoch overlaps its layout changes
+                                by vertex-row chunk and accepts it. */
 
 /* Loads an in-CSR from HOST arrays: row v = destination, columns = sources u
  * of arcs u->v ("N_in(v)", Eq. 1).  Explicit self loops are dropped
@@ -209,7 +213,10 @@ ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const flo
 #define NTP_M_STAGED       16u  /* inputs come from staging slot (flags >> 8) & 1, filled by
                                    ntp_stage_inputs (its host->device copy may overlap the
                                    previous epoch); X_v / labels_v / train_mask_v are ignored
-                                   except for X_v's shape.  Runs eagerly (no epoch graph). */
+                                   except for X_v's shape.  Each slot's epoch is captured as
+                                   its own CUDA graph (the slot's buffers are baked in; the copy
+                                   stream's ready / free events become external event nodes).
+                                   NTP_ERR_STATE if the slot was never staged with [V_p x d_in]. */
 #define NTP_M_SLOT_SHIFT    8
 #define NTP_M_DATA_PARALLEL 32u /* NEXT-4 baseline: each rank aggregates its own vertex rows at
                                    full width after an all-gather of the state before every hop,
@@ -239,8 +246,10 @@ typedef struct {
     double  loss;               /* global mean train loss, before this epoch's update */
     int64_t n_train;            /* global number of train vertices                    */
     double  ms[NTP_PH_COUNT];
-    int64_t bytes_sent[4];      /* per layout change: v2f fwd, f2v fwd, v2f bwd, f2v bwd */
-    int64_t bytes_recv[4];
+    int64_t bytes_sent[4];      /* per layout change: v2f fwd, f2v fwd, v2f bwd, f2v bwd --   */
+    int64_t bytes_recv[4];      /* counted where issued: NCCL send/recv / all-gather counts to
+                                   and from peers, or the peer-store extents of the P2P path
+                                   (NTP_M_DATA_PARALLEL: all its all-gathers in entry 0)      */
     int64_t collectives;        /* logical collective rounds issued (4 layout + allreduce) */
     int64_t kernel_launches;    /* libntp kernels launched in this call                 */
     double  spmm_ms;            /* summed duration of the SpMM hop kernels              */
@@ -248,7 +257,10 @@ typedef struct {
     int32_t pad_;
 } ntp_epoch_report;
 
-/* One training epoch.  X_v [V_p x d_in] fp32 (this rank's VERTEX rows, rows
+/* One training epoch.  The second call with the same model and pointers captures the enqueue
+ * sequence into a CUDA graph; later calls replay it while no library buffer has been
+ * (re)allocated or freed since the capture (any entry point that grows scratch invalidates it).
+ * X_v [V_p x d_in] fp32 (this rank's VERTEX rows, rows
  * >= n zero), labels_v int32 [V_p], train_mask_v uint8 [V_p] (device unless
  * NTP_M_HOST_INPUTS).  The MLP GEMMs read X_v with TMA: pass ld % 4 == 0 and a 16-byte
  * aligned base, otherwise X_v is staged into a padded copy every epoch (561 MB on reddit).  W0 [d_in x hid], W1 [hid x C] fp32 device, replicated
@@ -300,6 +312,20 @@ typedef struct {
 ntp_status ntp_train_epoch_coupled(ntp_ctx* ctx, const ntp_coupled_model* m, const ntp_tensor* X_v,
                                    const int32_t* labels_v, const uint8_t* train_mask_v,
                                    ntp_tensor* const* W, ntp_coupled_report* rep, ntp_stream s);
+
+/* ------------------------------------------------------ development switches
+ * Environment variables read by the library (A/B measurement only; the defaults are the product):
+ *   NTP_GRAPH=0          no CUDA-graph capture of epochs
+ *   NTP_HEAD_CHUNK=r     rows per vertex-side chunk of the W1-after-propagation epoch
+ *   NTP_HEAD_FUSED=0     unfused head (unpack -> GEMM -> loss -> GEMMs -> pack) instead of head.cu
+ *   NTP_HEAD_TMA=0       head.cu loads Z with 16-byte loads instead of TMA
+ *   NTP_PACK_FUSED=0     pack_v2f pass instead of the MLP GEMM's pack epilogue
+ *   NTP_WGRAD_FUSED=0    unpack + 3xTF32 GEMM instead of wgrad.cu
+ *   NTP_SPMM_VB=16|32    force the hop kernel's vector width; NTP_SPMM_SHORT=0|1 low-degree variants;
+ *   NTP_SPMM_OCC=0|1|2   occupancy variant; NTP_UNIT_ITEMS=T merge-path unit size; NTP_L1_CARVEOUT=0
+ *   NTP_REORDER_MODE=m   degree-class granularity of NTP_G_REORDER; NTP_P2P=0 disables peer windows
+ * Every switch keeps the arithmetic of the reduction order except NTP_UNIT_ITEMS (it changes which
+ * rows are cut across units, so results stay within tolerance but not bitwise). */
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,8 @@ def _load():
     L.oracle_rmat_filter.restype = i64
     L.oracle_num_threads.argtypes = []
     L.oracle_num_threads.restype = i32
+    L.oracle_set_num_threads.argtypes = [i32]
+    L.oracle_set_num_threads.restype = None
     return L
 
 

@@ -161,3 +161,13 @@ int oracle_num_threads(void) {
     return 1;
 #endif
 }
+
+/* Thread count of the OpenMP loops above (bench.py's single-thread baseline; results do not depend on it). */
+void oracle_set_num_threads(int t) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
+}

@@ -60,18 +60,3 @@ def hop_rows(g: Graph, zin, h, rows, gamma: float, alpha: float, transposed: boo
                         zin.ctypes.data, None if hh is None else hh.ctypes.data,
                         float(gamma), float(alpha), rows.ctypes.data, rows.size, out.ctypes.data)
     return out
-
-
-def propagation_matrix(g: Graph, K: int, gamma: float, alpha: float) -> np.ndarray:
-    """Dense M = (gamma A^)^K + alpha * sum_{j<K} (gamma A^)^j, by explicit matrix powers (small n)."""
-    from .graph import dense_adjacency_hat
-    A = gamma * dense_adjacency_hat(g)
-    n = g.n
-    M = np.eye(n)
-    S = np.zeros((n, n))
-    P = np.eye(n)
-    for j in range(K):
-        S += P
-        P = A @ P
-    M = P + alpha * S
-    return M

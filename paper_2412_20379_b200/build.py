@@ -26,8 +26,7 @@ def _site() -> str:
 def nvidia_dirs():
     site = _site()
     nccl = os.path.join(site, "nvidia", "nccl")
-    cublas = os.path.join(site, "nvidia", "cublas")
-    return nccl, cublas
+    return nccl
 
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -35,10 +34,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def _flags():
-    nccl, cublas = nvidia_dirs()
+    nccl = nvidia_dirs()
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
                    "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-                   "-I", os.path.join(nccl, "include"), "-I", os.path.join(cublas, "include")]
+                   "-I", os.path.join(nccl, "include")]
 
 
 def _newer(target, deps):
@@ -73,11 +72,10 @@ def build(force: bool = False, verbose: bool = True) -> str:
             pass
     objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or _newer(LIB, objs):
-        nccl, cublas = nvidia_dirs()
+        nccl = nvidia_dirs()
         cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH + [
             "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
-            "-L", os.path.join(cublas, "lib"), "-l:libcublas.so.12",
-            "-Xlinker", "-rpath=" + os.path.join(nccl, "lib") + ":" + os.path.join(cublas, "lib"),
+            "-Xlinker", "-rpath=" + os.path.join(nccl, "lib"),
         ]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <memory>
 
 #include "ntp_internal.cuh"
@@ -21,9 +22,15 @@ void fail(ntp_status st, const char* fmt, ...) {
     throw Error{st, std::string(buf)};
 }
 
+// Bumped whenever any DevBuf is (re)allocated or freed: captured epoch graphs bake scratch pointers in,
+// so a replay is only valid while no buffer has moved since the capture (EpochKey::alloc_gen).
+static std::atomic<int64_t> g_alloc_gen{0};
+int64_t alloc_generation() { return g_alloc_gen.load(); }
+
 void DevBuf::ensure(size_t b) {
     if (b <= bytes && p) return;
     release();
+    ++g_alloc_gen;
     if (b == 0) b = 16;
     cudaError_t e = cudaMalloc(&p, b);
     if (e != cudaSuccess) {
@@ -36,7 +43,10 @@ void DevBuf::ensure(size_t b) {
 }
 
 void DevBuf::release() {
-    if (p) cudaFree(p);
+    if (p) {
+        cudaFree(p);
+        ++g_alloc_gen;
+    }
     p = nullptr;
     bytes = 0;
 }
@@ -154,8 +164,6 @@ ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint
         for (auto& e : c->ev) NTP_CUDA(cudaEventCreate(&e));
         for (auto& e : c->ov_ev) NTP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         for (auto& e : c->hop_ev) NTP_CUDA(cudaEventCreate(&e));
-        NTP_BLAS(cublasCreate(&c->blas));
-        NTP_BLAS(cublasSetMathMode(c->blas, CUBLAS_PEDANTIC_MATH));   // fp32 FMA, no TF32 (R11)
         if (world > 1) {
             ncclUniqueId u;
             memcpy(&u, id, 128);
@@ -178,7 +186,6 @@ void ntp_destroy(ntp_ctx* c) {
     drop_epoch_graph(c);
     p2p_shutdown(c);
     if (c->comm) ncclCommDestroy(c->comm);
-    if (c->blas) cublasDestroy(c->blas);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->hop_ev)
@@ -520,6 +527,18 @@ ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v
     NTP_CHECK(W0->rows == m->d_in && W0->cols == m->hid && W0->ld == m->hid, NTP_ERR_SHAPE,
               "W0 must be dense [d_in x hid]");
     NTP_CHECK(W1->rows == m->hid && W1->cols == m->C && W1->ld == m->C, NTP_ERR_SHAPE, "W1 must be dense [hid x C]");
+    NTP_CHECK(m->C <= 256, NTP_ERR_CONFIG, "C = %d > 256 classes is not supported", m->C);
+    if (m->flags & NTP_M_STAGED) {
+        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
+        NTP_CHECK(c->st_rows[slot] == V_p && c->st_d_in[slot] == m->d_in, NTP_ERR_STATE,
+                  "staging slot %d holds no inputs of shape [%lld x %d] (ntp_stage_inputs first)", slot, (long long)V_p,
+                  m->d_in);
+    }
+    if ((m->flags & NTP_M_OVERLAP) && (m->flags & NTP_M_W1_AFTER_PROP) && c->world > 1) {
+        const int64_t nch = cdiv(V_p, epoch_row_chunk(m, V_p));   // 4 layout changes x 2 events per row chunk
+        NTP_CHECK(8 * nch <= kOvEvents, NTP_ERR_CONFIG, "too many overlap chunks (%lld > %d)", (long long)nch,
+                  kOvEvents / 8);
+    }
     NTP_CUDA(cudaSetDevice(c->device));
     train_epoch(c, m, X_v, labels_v, train_mask_v, W0, W1, rep, (cudaStream_t)st);
     NTP_API_END(c)

@@ -46,45 +46,17 @@ struct GemmParams {
     int64_t ldaux;
     int epi;                            // 0 store, 1 relu, 2 keep where aux > 0
     int vec;                            // C (and aux) rows 16-byte aligned: float4 epilogue
-    int exp;                            // development timing knob (NTP_GEMM_EXP), 0 in production
     int b_presplit;                     // B arrives as (hi, lo) pair: tmB = hi, tmBlo = lo (weights)
     uint32_t mn_lbo, mn_sbo;            // MN-major descriptor byte offsets (16-byte units)
     PackEpi pk;                         // epi 3: ReLU -> ReLU' bits + row-scaled bf16 feature-slice blocks
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity));
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
+using ptx::smem_u32;
+using ptx::mbar_init;
+using ptx::mbar_wait;
+using ptx::mbar_arrive;
+using ptx::mbar_expect_tx;
+using ptx::tma_load_2d;
 
 // 128B-swizzled UMMA smem descriptors (sm_100 format: version 1, layout type 2 = SWIZZLE_128B).
 __device__ __forceinline__ uint64_t desc_kmajor(uint32_t addr) {
@@ -256,10 +228,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         const uint64_t dB = B_MN ? desc_mnmajor(sb + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(sb + bo);
                         const uint64_t dBlo = B_MN ? desc_mnmajor(sblo + bo, p.mn_lbo, p.mn_sbo) : desc_kmajor(sblo + bo);
                         mma_tf32(acc, dA, dB, p.idesc, (i > 0 || k > 0) ? 1u : 0u);
-                        if (p.exp != 2) {   // dev timing knob: exp 2 = one MMA per step (wrong results)
-                            mma_tf32(acc, dA, dBlo, p.idesc, 1u);
-                            mma_tf32(acc, dAlo, dB, p.idesc, 1u);
-                        }
+                        mma_tf32(acc, dA, dBlo, p.idesc, 1u);
+                        mma_tf32(acc, dAlo, dB, p.idesc, 1u);
                     }
                     mma_commit(&empty[s]);
                 }
@@ -277,11 +247,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int s = it % S;
                 mbar_wait(&full[s], (it / S) & 1);
                 uint8_t* sa = smem + s * stage_bytes;
-                if (p.exp != 1) {   // dev timing knob: exp 1 = no split (wrong results)
-                    split_tile(sa, sa + kTileA, kTileA, tid, 128);
-                    uint8_t* sb = sa + 2 * kTileA;
-                    if (!p.b_presplit) split_tile(sb, sb + tileB, tileB, tid, 128);
-                }
+                split_tile(sa, sa + kTileA, kTileA, tid, 128);
+                uint8_t* sb = sa + 2 * kTileA;
+                if (!p.b_presplit) split_tile(sb, sb + tileB, tileB, tid, 128);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&split[s]);
             }
@@ -500,12 +468,8 @@ void gemm_tf32x3(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, in
     p.aux = aux;
     p.ldaux = ldaux;
     if (epi == 3) p.pk = c->pack_epi;
-    static const int gemm_exp = [] { const char* v = getenv("NTP_GEMM_EXP"); return v ? atoi(v) : 0; }();
-    p.exp = gemm_exp;
     p.mn_lbo = 4096 >> 4;
     p.mn_sbo = 512 >> 4;
-    if (const char* v = getenv("NTP_MN_LBO")) p.mn_lbo = (uint32_t)atoi(v) >> 4;
-    if (const char* v = getenv("NTP_MN_SBO")) p.mn_sbo = (uint32_t)atoi(v) >> 4;
     const CUtensorMapSwizzle mnswz = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
     CUtensorMap ta = a_mn ? make_map(A, M, K, lda, 32, 32, mnswz) : make_map(A, K, M, lda, 32, BM);
     CUtensorMap tb = b_mn ? make_map(B, N, K, ldb, 32, 32, mnswz) : make_map(B, K, N, ldb, 32, p.bn_alloc);

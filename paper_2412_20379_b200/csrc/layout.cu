@@ -320,6 +320,7 @@ void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_ele
     for (int q = 0; q < c->world; ++q) {
         NTP_NCCL(ncclSend(static_cast<const char*>(send) + q * block_elems * es, block_elems, t, q, c->comm, s));
         NTP_NCCL(ncclRecv(static_cast<char*>(recv) + q * block_elems * es, block_elems, t, q, c->comm, s));
+        if (q != c->rank) wire_add(c, block_elems * (int64_t)es, block_elems * (int64_t)es);
     }
     NTP_NCCL(ncclGroupEnd());
 }

@@ -10,7 +10,7 @@
 //   a9  gather -> dL^ rows
 //   a10 dW1 = H1^T dL^, dH1 = (dL^ W1^T) .* [H1 > 0], dW0 = X^T dH1
 //   a11 allreduce(dW0 | dW1) + allreduce(loss_sum, n_train) ; W -= lr/N_train * dW
-// Dense GEMMs: cuBLAS SGEMM (fp32 FMA, no TF32: parity reading R11).
+// Dense GEMMs: tcgen05 3xTF32 (gemm.cu; fp32-level accuracy, parity reading R11).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -21,24 +21,6 @@
 namespace ntp {
 
 namespace {
-
-// dH1 = dH1 .* [H1 > 0]  (ReLU'(0) = 0, reading R12), strided rows
-__global__ void relu_grad_kernel(float* __restrict__ g, const float* __restrict__ h, int64_t rows, int32_t cols,
-                                 int64_t ldg, int64_t ldh) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * cols;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / cols, k = i % cols;
-        g[r * ldg + k] = h[r * ldh + k] > 0.f ? g[r * ldg + k] : 0.f;
-    }
-}
-
-__global__ void relu_rows_kernel(float* __restrict__ x, int64_t rows, int32_t cols, int64_t ld) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * cols;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / cols, k = i % cols;
-        x[r * ld + k] = fmaxf(x[r * ld + k], 0.f);
-    }
-}
 
 template <typename T> __device__ __forceinline__ float ldf(const T* p);
 template <> __device__ __forceinline__ float ldf<float>(const float* p) { return *p; }
@@ -234,38 +216,14 @@ __global__ void sum_chunks_kernel(const float* __restrict__ part, int64_t nch, i
 
 int eblocks(int64_t total) { return (int)std::min<int64_t>(std::max<int64_t>(cdiv(total, 256), 1), 148 * 16); }
 
-// C[M x N] = op(A) op(B), all row-major fp32 (column-major cuBLAS on the transposes).
-void gemm_rm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
-             const float* B, int64_t ldb, float* C, int64_t ldc, float beta = 0.f) {
-    if (M == 0 || N == 0) return;
-    const float one = 1.f;
-    NTP_BLAS(cublasSgemm(c->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)N, (int)M,
-                         (int)K, &one, B, (int)ldb, A, (int)lda, &beta, C, (int)ldc));
-}
-
 // MLP GEMM C = op(A) op(B) (+ epilogue: 1 ReLU, 2 keep where aux > 0) on the tensor cores
-// (gemm.cu, tcgen05 3xTF32); NTP_GEMM=cublas selects cuBLAS SGEMM instead (A/B comparison).
-// (Bs: optional pre-split {hi, lo} copy of B for the tensor-core path, same layout and ldb.)
+// (gemm.cu, tcgen05 3xTF32; Bs: optional pre-split {hi, lo} copy of B, same layout and ldb).
 struct Split { const float* hi = nullptr; const float* lo = nullptr; };
 void mlp_gemm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
               const float* B, int64_t ldb, float* C, int64_t ldc, cudaStream_t s, int epi = 0,
               const float* aux = nullptr, int64_t ldaux = 0, Split Bs = Split{}) {
-    static const bool use_cublas = [] {
-        const char* v = getenv("NTP_GEMM");
-        return v && std::string(v) == "cublas";
-    }();
-    if (!use_cublas) {
-        if (Bs.hi) gemm_tf32x3(c, M, N, K, A, lda, ta, Bs.hi, ldb, !tb, C, ldc, epi, aux, ldaux, s, Bs.lo);
-        else gemm_tf32x3(c, M, N, K, A, lda, ta, B, ldb, !tb, C, ldc, epi, aux, ldaux, s);
-        return;
-    }
-    gemm_rm(c, ta, tb, M, N, K, A, lda, B, ldb, C, ldc);
-    if (epi == 1) relu_rows_kernel<<<eblocks(M * N), 256, 0, s>>>(C, M, (int32_t)N, ldc);
-    if (epi == 2) relu_grad_kernel<<<eblocks(M * N), 256, 0, s>>>(C, aux, M, (int32_t)N, ldc, ldaux);
-    if (epi) {
-        NTP_LAUNCH_CHECK();
-        count_launch(c);
-    }
+    if (Bs.hi) gemm_tf32x3(c, M, N, K, A, lda, ta, Bs.hi, ldb, !tb, C, ldc, epi, aux, ldaux, s, Bs.lo);
+    else gemm_tf32x3(c, M, N, K, A, lda, ta, B, ldb, !tb, C, ldc, epi, aux, ldaux, s);
 }
 
 inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
@@ -294,10 +252,11 @@ static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool
         alltoall_blocks(c, a.Z, recv, V_p * d_s, a.dtype, s);
         return;
     }
-    // the chunked gather writes `recv` while later chunks of the last hop still read S^0 for the
-    // alpha term: when they are the same buffer, keep S^0 in a copy
+    // the chunked gather writes `recv` while later chunks of the last hop still read S^0 -- for the
+    // alpha term, and with K == 1 as the gathered state itself: when they are the same buffer, keep
+    // S^0 in a copy
     PropArgs ao = a;
-    if (a.alpha != 0.f && recv == a.H) {
+    if (recv == a.H && (a.alpha != 0.f || a.K == 1)) {
         const size_t bytes = (size_t)V_pad * a.ld_h * es;
         c->prop_s0.ensure(bytes + 16);
         NTP_CUDA(cudaMemcpyAsync(c->prop_s0.p, a.H, bytes, cudaMemcpyDeviceToDevice, s));
@@ -329,6 +288,7 @@ static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool
                 NTP_NCCL(ncclSend(zf + lo * d_s * es, cnt, t, q, c->comm, c->s_comm));
                 NTP_NCCL(ncclRecv(dst, cnt, t, pr, c->comm, c->s_comm));
                 NTP_NCCL(ncclGroupEnd());
+                wire_add(c, cnt * (int64_t)es, cnt * (int64_t)es);
             }
         }
     }
@@ -339,6 +299,16 @@ static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool
 static void enqueue_epoch_dp(ntp_ctx* c, const ntp_model* m, const float* X, int64_t ldx, const int32_t* lab,
                              const uint8_t* msk, float* W0u, float* W1u, const float* W0g, int64_t ldw0,
                              const float* W1g, int64_t ldw1, Split W0s, Split W1s, bool timed);
+
+// Rows per vertex-side chunk of the W1-after-propagation epoch: NTP_HEAD_CHUNK, else the model's chunk count
+// (the a12 schedule's chunks), capped at 2^23 rows; V_p (one chunk) otherwise.
+int64_t epoch_row_chunk(const ntp_model* m, int64_t V_p) {
+    if (!(m->flags & NTP_M_W1_AFTER_PROP) || V_p <= 0) return std::max<int64_t>(V_p, 1);
+    const char* hce = getenv("NTP_HEAD_CHUNK");   // read per call (tests vary it)
+    const int64_t head_chunk_env = hce ? atoll(hce) : 0;
+    const int64_t hc_def = m->chunks > 1 ? std::min<int64_t>(cdiv(V_p, m->chunks), (int64_t)1 << 23) : (int64_t)1 << 23;
+    return std::max<int64_t>(1, std::min<int64_t>(V_p, head_chunk_env > 0 ? head_chunk_env : hc_def));
+}
 
 // Enqueues one epoch (everything between events E0 and E9) on c->s_comp; capturable.
 static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
@@ -359,6 +329,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
 
     cudaEvent_t* E = c->ev;
     int ei = 0;
+    wire_reset(c);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E0 start (input staging counts as mlp_fwd)
 
     // ---- inputs (e2e: copy host inputs in).  GEMM operands need 16-byte row pitch (TMA).
@@ -371,7 +342,8 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     if (m->flags & NTP_M_STAGED) {
         // inputs staged by ntp_stage_inputs (copy stream); this epoch waits for that copy
         const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
-        NTP_CHECK(c->st_rows[slot] == V_p, NTP_ERR_STATE, "staging slot %d holds no inputs of this shape", slot);
+        NTP_CHECK(c->st_rows[slot] == V_p && c->st_d_in[slot] == m->d_in, NTP_ERR_STATE,
+                  "staging slot %d holds no inputs of this shape", slot);
         NTP_CUDA(cudaStreamWaitEvent(s, c->st_ready[slot], c->capturing ? cudaEventWaitExternal : 0));
         X = c->st_X[slot].as<float>();
         ldx = c->st_ld[slot];
@@ -454,14 +426,8 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     // the vertex-side work runs in row chunks of `hc` rows (H1, logits, gradients chunk-sized; the
     // ReLU' mask kept as bits) so the epoch's footprint is the slices plus X (memory-lean plan).
     const bool local = (P == 1);
-    const char* hce = getenv("NTP_HEAD_CHUNK");   // read per call (tests vary it)
-    const int64_t head_chunk_env = hce ? atoll(hce) : 0;
-    // row chunks of the vertex-side work: NTP_HEAD_CHUNK, else the model's chunk count (the a12 schedule's
-    // chunks), capped at 2^23 rows
-    const int64_t hc_def = m->chunks > 1 ? std::min<int64_t>(cdiv(V_p, m->chunks), (int64_t)1 << 23) : (int64_t)1 << 23;
-    const int64_t hc = after ? std::max<int64_t>(1, std::min<int64_t>(V_p, head_chunk_env > 0 ? head_chunk_env : hc_def))
-                             : V_p;
-    const int64_t nch = after ? cdiv(V_p, hc) : 1;
+    const int64_t hc = epoch_row_chunk(m, V_p);
+    const int64_t nch = cdiv(V_p, hc);
     const int32_t nwb = (m->hid + 31) / 32;          // mask words per row
     const int64_t rowsH = after ? hc : V_p;
     c->m_H1.ensure((size_t)rowsH * ldH * sizeof(float));
@@ -491,7 +457,6 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     // chunk ch's weight-gradient partials (dW0 | dW1), summed in chunk order afterwards
     auto dw0_at = [&](int64_t ch) { return nch > 1 ? c->m_dWp.as<float>() + ch * n_w : dW0; };
     auto dw1_at = [&](int64_t ch) { return dw0_at(ch) + (int64_t)m->d_in * m->hid; };
-    NTP_BLAS(cublasSetStream(c->blas, s));
 
     // Peer-direct layouts (NTP_M_P2P_LAYOUTS, P > 1, CUDA IPC available): the producers store into
     // the owners' windows and a barrier replaces each all-to-all; otherwise the NCCL block exchange.
@@ -536,6 +501,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             }
             NTP_NCCL(ncclSend(static_cast<const char*>(src) + off, cnt, t, q, c->comm, st));
             NTP_NCCL(ncclRecv(static_cast<char*>(dst) + off, cnt, t, q, c->comm, st));
+            wire_add(c, (int64_t)(cnt * es), (int64_t)(cnt * es));
         }
         NTP_NCCL(ncclGroupEnd());
     };
@@ -570,8 +536,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         cudaEvent_t last = nullptr;
         // bf16 slice, no padding columns: the split's pack runs in the GEMM epilogue (gemm_tf32x3_pack)
         const char* pfe = getenv("NTP_PACK_FUSED");
-        const char* ge = getenv("NTP_GEMM");
-        const bool fuse_pack = !(pfe && atoi(pfe) == 0) && !(ge && std::string(ge) == "cublas") && dt == NTP_BF16 &&
+        const bool fuse_pack = !(pfe && atoi(pfe) == 0) && dt == NTP_BF16 &&
                                (int64_t)P * d_s == m->hid && m->hid % 32 == 0 && d_s % 8 == 0 && !p2p;
         for (int64_t r = 0; r < V_p; r += hc) {      // H1 chunk -> pre-scaled slice rows + ReLU' bits
             const int64_t h = std::min(hc, V_p - r);
@@ -592,13 +557,16 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd (+ pack) done
     }
 
+    // peer-direct layout change: the producer stored (P-1) blocks of V_p x d_s into the peers' windows
+    const int64_t p2p_wire = (int64_t)(P - 1) * V_p * d_s * (int64_t)es;
     // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
-    if (p2p) p2p_barrier(c, s);
+    if (p2p) p2p_barrier(c, s), wire_add(c, p2p_wire, p2p_wire);
     else if (!local && !ovl) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E2 v2f done
 
     // a4 + a5: K forward hops on S^0 (pre-scaled) -> Z^K, gathered into this rank's rows
     c->hop_ev_used = 0;
+    c->wire_phase = 1;
     void* gathered = p2p ? c->p2p_gath.p : c->recv.p;
     {
         PropArgs a{};
@@ -618,6 +586,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
             p2p_barrier(c, s);
+            wire_add(c, p2p_wire, p2p_wire);
         } else if (ovl) {
             propagate(c, a, s, timed, true);     // a5 per chunk below, consumed chunk by chunk by the head
         } else {
@@ -633,6 +602,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     void* gsend = local ? (gathered == c->recv.p ? c->xfer.p : c->recv.p) : c->send.p;
 
     // a6: loss + gradient, written straight into the backward split's send buffer (or windows)
+    c->wire_phase = 2;
     const float* gscale_bwd = g.dinv_in_orig();   // backward column side (original vertex order)
     int64_t nb_loss = 0;
     if (!after) {
@@ -688,11 +658,12 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     NTP_CUDA(record_timing(c, E[ei++], s));   // E4 loss done
 
     // a7: split the gradient
-    if (p2p) p2p_barrier(c, s);
+    if (p2p) p2p_barrier(c, s), wire_add(c, p2p_wire, p2p_wire);
     else if (!local && !ovl) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E5 v2f bwd
 
     // a8 + a9: K backward hops on the split gradient, gathered -> dL^ rows [V_p x w]
+    c->wire_phase = 3;
     void* gathered_b = p2p ? c->p2p_gath.p : c->send.p;
     {
         PropArgs a{};
@@ -712,6 +683,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
             p2p_barrier(c, s);
+            wire_add(c, p2p_wire, p2p_wire);
         } else if (ovl) {
             propagate(c, a, s, timed, true);     // a9 per chunk below, consumed chunk by chunk by a10
         } else {
@@ -884,17 +856,23 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     cudaGraphExec_t& gexec = staged ? c->sg_exec[sl] : c->graph_exec;
     int& ghops = staged ? c->sg_hops[sl] : c->graph_hops;
     int64_t& glaunches = staged ? c->sg_launches[sl] : c->graph_launches;
+    int64_t* gwire = staged ? c->sg_wire[sl] : c->graph_wire;
+    int64_t& ggen = staged ? c->sg_gen[sl] : c->graph_gen;
     int64_t epoch_launches = 0;
-    if (graphs_enabled() && gvalid && gkey == key) {
+    // A captured graph bakes in every scratch pointer: it is replayed only while no library buffer has been
+    // (re)allocated or freed since its capture (alloc_generation), whatever entry point moved it.
+    if (graphs_enabled() && gvalid && gkey == key && ggen == alloc_generation()) {
         NTP_CUDA(cudaGraphLaunch(gexec, s));
         c->hop_ev_used = ghops;
         epoch_launches = glaunches;
+        for (int i = 0; i < 4; ++i) c->wire_sent[i] = gwire[i], c->wire_recv[i] = gwire[4 + i];
         if (staged) c->st_free_rec[sl] = true;
     } else if (graphs_enabled() && gwarm && gkey == key) {
         if (gexec) cudaGraphExecDestroy(gexec);
         gexec = nullptr;
         gvalid = false;
         cudaGraph_t graph = nullptr;
+        const int64_t gen0 = alloc_generation();
         NTP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
         c->capturing = true;
         try {
@@ -908,16 +886,25 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         }
         c->capturing = false;
         NTP_CUDA(cudaStreamEndCapture(s, &graph));
-        cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
-        cudaGraphDestroy(graph);
-        NTP_CUDA(ie);
-        gvalid = true;
-        ghops = c->hop_ev_used;
-        glaunches = c->launches - launches0;
-        epoch_launches = glaunches;
-        NTP_CUDA(cudaGraphLaunch(gexec, s));
+        if (alloc_generation() != gen0) {
+            // a buffer moved while the epoch was being recorded: earlier nodes may hold the old pointer.
+            // Discard the recording and run the epoch eagerly (the buffers now have their final size).
+            cudaGraphDestroy(graph);
+            enqueue_epoch(c, m, X_v, labels_v, mask_v, W0, W1, timed);
+            epoch_launches = c->launches - launches0;
+        } else {
+            cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
+            cudaGraphDestroy(graph);
+            NTP_CUDA(ie);
+            gvalid = true;
+            ggen = gen0;
+            ghops = c->hop_ev_used;
+            glaunches = c->launches - launches0;
+            for (int i = 0; i < 4; ++i) gwire[i] = c->wire_sent[i], gwire[4 + i] = c->wire_recv[i];
+            epoch_launches = glaunches;
+            NTP_CUDA(cudaGraphLaunch(gexec, s));
+        }
     } else {
-        drop_epoch_graph(c);   // an eager run may grow scratch buffers that captured graphs point into
         enqueue_epoch(c, m, X_v, labels_v, mask_v, W0, W1, timed);
         epoch_launches = c->launches - launches0;
         gwarm = true;
@@ -946,18 +933,13 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         float tot = 0.f;
         NTP_CUDA(cudaEventElapsedTime(&tot, E[0], E[9]));
         rep->ms[NTP_PH_TOTAL] = tot;
-        const int64_t wire = (int64_t)(P - 1) * V_p * d_s * (int64_t)es;
+        // counted where the transfers are issued (NCCL counts, peer-store extents); DP: all in entry 0
         for (int i = 0; i < 4; ++i) {
-            rep->bytes_sent[i] = wire;
-            rep->bytes_recv[i] = wire;
+            rep->bytes_sent[i] = c->wire_sent[i];
+            rep->bytes_recv[i] = c->wire_recv[i];
         }
         rep->collectives = P > 1 ? 5 : 0;
-        if ((m->flags & NTP_M_DATA_PARALLEL) && P > 1) {   // 2K all-gathers of full-width rows + 1 allreduce
-            const int64_t ag = (int64_t)(P - 1) * V_p * slice_width(m->C, 1, m->dtype, c->slice_align) * (int64_t)es;
-            for (int i = 0; i < 4; ++i) rep->bytes_sent[i] = rep->bytes_recv[i] = 0;
-            rep->bytes_sent[0] = rep->bytes_recv[0] = 2 * m->K * ag;
-            rep->collectives = 2 * m->K + 1;
-        }
+        if ((m->flags & NTP_M_DATA_PARALLEL) && P > 1) rep->collectives = 2 * m->K + 1;   // 2K all-gathers + allreduce
         rep->kernel_launches = epoch_launches;
         int nh = 0;
         rep->spmm_ms = collect_hop_ms(c, &nh);
@@ -1021,7 +1003,10 @@ static void enqueue_epoch_dp(ntp_ctx* c, const ntp_model* m, const float* X, int
         for (char* b : {A, B, S0}) NTP_CUDA(cudaMemsetAsync(b + (size_t)n * ws * es, 0, (V_pad - n) * ws * es, s));
     const ncclDataType_t t = dt == NTP_BF16 ? ncclBfloat16 : ncclFloat32;
     auto allgather = [&](char* buf) {   // own rows -> every rank's copy of the full matrix
-        if (P > 1) NTP_NCCL(ncclAllGather(buf + own, buf, (size_t)V_p * ws, t, c->comm, s));
+        if (P > 1) {
+            NTP_NCCL(ncclAllGather(buf + own, buf, (size_t)V_p * ws, t, c->comm, s));
+            wire_add(c, (int64_t)(P - 1) * V_p * ws * (int64_t)es, (int64_t)(P - 1) * V_p * ws * (int64_t)es);
+        }
     };
     // K hops of one direction on full-width rows: S^0 own rows in `A` (pre-scaled); returns the buffer
     // holding Z^K own rows (unscaled, storage dtype)
@@ -1124,6 +1109,7 @@ void stage_inputs(ntp_ctx* c, int slot, const float* X, int64_t rows, int32_t d_
     NTP_CUDA(cudaMemcpyAsync(c->st_m[slot].p, m, (size_t)rows, cudaMemcpyHostToDevice, s));
     NTP_CUDA(cudaEventRecord(c->st_ready[slot], s));
     c->st_rows[slot] = rows;
+    c->st_d_in[slot] = d_in;
     c->st_ld[slot] = ld;
 }
 
@@ -1205,7 +1191,7 @@ void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tenso
         ldx = ldw[0];
     }
     int changes = 0;
-    int64_t wire = 0;
+    wire_reset(c);
     // one layout round trip around a single hop: vertex rows Hv [V_p x w] -> split (pre-scaled) -> hop
     // (transposed = backward) -> gather -> out [V_p x w] (with keep: the ReLU' mask)
     auto agg = [&](const float* Hv, int64_t ldh, int w, bool transposed, float* out, int64_t ldo, const float* keep,
@@ -1229,10 +1215,7 @@ void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tenso
         if (local) gathered = propagate_consume(c, a, s, true);
         else propagate_and_gather(c, a, c->recv.p, false, 1, V_p, d_s, true, s);
         unpack_f2v(c, gathered, V_p, d_s, P, out, ldo, w, dt, NTP_F32, s, keep, ldk);
-        if (!local) {
-            changes += 2;
-            wire += 2 * (int64_t)(P - 1) * V_p * d_s * (int64_t)es;
-        }
+        if (!local) changes += 2;
     };
     // ---- forward: Z^l = A^ H^{l-1} (sliced), H^l = ReLU(Z^l W^l), logits = Z^L W^L
     float* logits = c->cp_B.as<float>();
@@ -1284,8 +1267,8 @@ void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tenso
         rep->loss = h_scal[1] > 0 ? h_scal[0] / h_scal[1] : 0.0;
         rep->n_train = (int64_t)h_scal[1];
         rep->layout_changes = changes;
-        rep->bytes_sent = wire;
-        rep->bytes_recv = wire;
+        rep->bytes_sent = c->wire_sent[0];   // every layout change of the coupled epoch counts in entry 0
+        rep->bytes_recv = c->wire_recv[0];
         float tot = 0.f;
         NTP_CUDA(cudaEventElapsedTime(&tot, E[0], E[1]));
         rep->ms_total = tot;

@@ -3,7 +3,6 @@
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
-#include <cublas_v2.h>
 #include <nccl.h>
 
 #include <cstdint>
@@ -40,14 +39,6 @@ struct Error {
                         ncclGetErrorString(_r));                                           \
     } while (0)
 
-#define NTP_BLAS(expr)                                                                     \
-    do {                                                                                   \
-        cublasStatus_t _s = (expr);                                                        \
-        if (_s != CUBLAS_STATUS_SUCCESS)                                                   \
-            ::ntp::fail(NTP_ERR_CUDA, "%s:%d %s -> cublas status %d", __FILE__, __LINE__,  \
-                        #expr, (int)_s);                                                   \
-    } while (0)
-
 #define NTP_CHECK(cond, st, ...)                                                           \
     do {                                                                                   \
         if (!(cond)) ::ntp::fail((st), __VA_ARGS__);                                       \
@@ -56,6 +47,8 @@ struct Error {
 #define NTP_LAUNCH_CHECK() NTP_CUDA(cudaGetLastError())
 
 // ------------------------------------------------------------- device buffer
+int64_t alloc_generation();        // bumped by every DevBuf (re)allocation / free
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -150,7 +143,6 @@ struct ntp_ctx {
     int device = 0, rank = 0, world = 1, slice_align = 16;
     ncclComm_t comm = nullptr;
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
-    cublasHandle_t blas = nullptr;
     ntp::Graph g;
     // scratch
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
@@ -164,6 +156,7 @@ struct ntp_ctx {
     cudaEvent_t st_ready[2] = {}, st_free[2] = {};
     bool st_free_rec[2] = {false, false};
     int64_t st_rows[2] = {0, 0}, st_ld[2] = {0, 0};
+    int32_t st_d_in[2] = {0, 0};
     // peer-direct layouts (CUDA IPC windows over NVLink), see layout.cu
     int p2p_state = 0;                      // 0 not set up, 1 usable, -1 unavailable
     ntp::DevBuf p2p_split, p2p_gath;        // this rank's windows (zero-initialised)
@@ -190,6 +183,12 @@ struct ntp_ctx {
     cudaGraphExec_t sg_exec[2] = {nullptr, nullptr};
     int sg_hops[2] = {0, 0};
     int64_t sg_launches[2] = {0, 0};
+    int64_t graph_gen = -1, sg_gen[2] = {-1, -1};   // alloc_generation() at capture
+    int64_t graph_wire[8] = {}, sg_wire[2][8] = {};  // wire bytes counted while recording (replays reuse them)
+    // bytes handed to the transport (NCCL send/recv, all-gather, peer stores) per layout change of the
+    // current epoch: 0 v2f fwd, 1 f2v fwd, 2 v2f bwd, 3 f2v bwd (wire_phase selects the entry)
+    int64_t wire_sent[4] = {}, wire_recv[4] = {};
+    int wire_phase = 0;
     bool capturing = false;         // timing events become external event nodes while capturing
     int graph_hops = 0;
     int64_t graph_launches = 0;
@@ -258,6 +257,7 @@ void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K,
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
 void drop_epoch_graph(ntp_ctx* c);
+int64_t epoch_row_chunk(const ntp_model* m, int64_t V_p);
 constexpr int kMaxLayers = NTP_MAX_LAYERS;
 constexpr int kOvEvents = 256;
 void stage_inputs(ntp_ctx* c, int slot, const float* X, int64_t rows, int32_t d_in, int64_t ldx, const int32_t* y,
@@ -327,6 +327,15 @@ int32_t slice_width(int32_t w, int32_t P, ntp_dtype dt, int align);
 
 void count_launch(ntp_ctx* c, int k = 1);
 // Record a TIMING event (phase marks, SpMM hop pairs): external event node under graph capture.
+// Layout-change traffic handed to the transport by this rank (see ntp_ctx::wire_sent).
+inline void wire_add(ntp_ctx* c, int64_t sent, int64_t recv) {
+    c->wire_sent[c->wire_phase & 3] += sent;
+    c->wire_recv[c->wire_phase & 3] += recv;
+}
+inline void wire_reset(ntp_ctx* c) {
+    for (int i = 0; i < 4; ++i) c->wire_sent[i] = c->wire_recv[i] = 0;
+    c->wire_phase = 0;
+}
 inline cudaError_t record_timing(ntp_ctx* c, cudaEvent_t e, cudaStream_t s) {
     return cudaEventRecordWithFlags(e, s, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
 }

@@ -175,6 +175,21 @@ def _ult(a, t: int):
     return (a ^ _i64(1 << 63)) < _i64(t ^ (1 << 63))
 
 
+def features_device(seed: int, n: int, d: int, device="cuda", row0: int = 0, rows: int | None = None):
+    """features() (dense) computed on a torch device: fp32 [rows x d]."""
+    import torch
+    if rows is None:
+        rows = n - row0
+    X = torch.empty(rows, d, dtype=torch.float32, device=device)
+    cols = torch.arange(d, dtype=torch.int64, device=device)
+    step = max(1, (1 << 25) // max(d, 1))
+    for r in range(0, rows, step):
+        rr = min(step, rows - r)
+        idx = (torch.arange(row0 + r, row0 + r + rr, dtype=torch.int64, device=device)[:, None] * d + cols[None, :])
+        X[r:r + rr] = (_srl(hash64_torch(seed, S_FEAT, idx), 40).to(torch.float64) / float(1 << 23) - 1.0).to(torch.float32)
+    return X
+
+
 def config_inputs_device(cfg: "Config", row0: int = 0, rows: int | None = None, device="cuda", ld: int | None = None,
                          out=None):
     """config_inputs() computed on a torch device: (X [rows x ld][:, :d_in] fp32, y int32, train mask uint8).

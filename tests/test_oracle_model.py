@@ -132,3 +132,34 @@ def test_partition_maps():
     assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
     assert layout.slice_width(41, 1, 4) == 44 and layout.slice_width(41, 1, 4, 32) == 48
     assert layout.slice_width(128, 8, 2) == 16 and layout.slice_width(41, 4, 4) == 12
+
+
+def test_softmax_xent_train_mask_hand_computed():
+    """O7/O8 on two hand-computed rows (masks P:919): a masked-out row -- even with extreme
+    logits -- contributes neither loss, count nor gradient; an unmasked one does.  A consistent omission
+    of the mask from loss, count and dlogits fails the first case, a wrong N_train the second."""
+    y = np.array([0, 1])
+    # row 0: uniform over 2 classes -> -log(1/2) = ln 2, dlogits = (1/2 - 1, 1/2)
+    # row 1: extreme logits, masked out
+    logits = np.array([[0.0, 0.0], [1000.0, -1000.0]])
+    loss_sum, n_train, d = model.softmax_xent(logits, y, np.array([1, 0], dtype=np.uint8))
+    assert n_train == 1
+    assert loss_sum == pytest.approx(np.log(2.0), abs=1e-15)
+    np.testing.assert_allclose(d, [[-0.5, 0.5], [0.0, 0.0]], atol=1e-15)
+    # row 1 = (ln 3, 0), label 1, now in the train set: -log(1/4) = ln 4, dlogits = (3/4, 1/4 - 1)
+    logits = np.array([[0.0, 0.0], [np.log(3.0), 0.0]])
+    loss_sum, n_train, d = model.softmax_xent(logits, y, np.array([1, 1], dtype=np.uint8))
+    assert n_train == 2
+    assert loss_sum == pytest.approx(np.log(8.0), abs=1e-14)
+    np.testing.assert_allclose(d, [[-0.5, 0.5], [0.75, -0.75]], atol=1e-15)
+
+
+def test_forward_loss_divides_by_train_count():
+    """O7's 1/N_train: on the empty graph (A^ = I) with K = 1, gamma = 1, alpha = 0 and W chosen so the
+    logits are the hand-computed rows above, the mean loss over the one train row is ln 2."""
+    g = build_graph(np.zeros(0, np.int64), np.zeros(0, np.int64), 2, symmetric=True)
+    X = np.array([[0.0], [1.0]])
+    W0 = np.array([[1.0]])
+    W1 = np.array([[1000.0, -1000.0]])   # row 0: logits (0, 0); row 1: (1000, -1000), masked out
+    loss = model.forward_loss(g, X, np.array([0, 1]), np.array([1, 0], np.uint8), W0, W1, 1, 1.0, 0.0)
+    assert loss == pytest.approx(np.log(2.0), abs=1e-15)

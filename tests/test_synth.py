@@ -30,3 +30,8 @@ def test_config_inputs_cuda_matches_numpy():
     Xn, yn, mn = synth.config_inputs(cfg, 50_000_000, 4096)
     assert np.array_equal(X.cpu().numpy(), Xn) and np.array_equal(y.cpu().numpy(), yn)
     assert np.array_equal(m.cpu().numpy(), mn)
+
+
+def test_features_device_matches_numpy():
+    a = synth.features_device(27, 10_000, 4, device="cpu", row0=9_000, rows=1000).numpy()
+    assert np.array_equal(a, synth.features(27, 10_000, 4, row0=9_000, rows=1000))
