@@ -13,7 +13,8 @@
  *            feature slices -> gather -> loss -> split -> K backward hops ->
  *            gather -> MLP backward -> allreduce(dW) -> SGD.
  *
- * Layouts (P = number of feature slices = world size):
+ * Layouts (P = number of feature slices = world size, or world * vs after ntp_set_slices;
+ * SURVEY §8(a) a1):
  *   V_p   = ceil(n / P),  V_pad = P * V_p
  *   d_s   = ceil(w / P) rounded up so d_s*elem_bytes % slice_align == 0 (16 or 32)
  *   VERTEX  layout on rank q: rows [q*V_p, (q+1)*V_p) of the padded matrix at width w
@@ -91,6 +92,21 @@ void        ntp_destroy(ntp_ctx* ctx);
 const char* ntp_last_error(const ntp_ctx* ctx);
 const char* ntp_status_string(ntp_status s);
 int         ntp_abi_version(void);
+
+/* Virtual slices (SURVEY §8(b) "P > world with P % world == 0"): from now on the context splits the
+ * propagated width into P = world * vs feature slices, vs per rank, processed in sequence on this GPU
+ * (every slice is aggregated independently; the paper's workers become virtual).  All
+ * layout definitions below then use P: V_p = ceil(n / P), V_pad = P * V_p, d_s = slice width for P;
+ * this rank's VERTEX rows are the vs*V_p rows from rank*vs*V_p, its FEATURE tensor stacks its vs slices
+ * [vs*V_pad x d_s] (slice j = global slice rank*vs + j), and the layout changes exchange per (peer,
+ * slice) blocks (world == 1: device-local, the exchange is the identity).  Collective: every rank calls it
+ * with the same P.  NTP_ERR_ARG unless P >= world and P % world == 0.  Default P = world. */
+ntp_status ntp_set_slices(ntp_ctx* ctx, int32_t P);
+
+/* CUDA-event duration (ms, summed) and count of the SpMM hop launches -- each spmm_hop_kernel with its
+ * spmm_fixup_kernel -- enqueued by the last ntp_propagate_fwd / _bwd / _pipeline or ntp_train_epoch
+ * call; waits for the last of them.  The events are recorded on the stream the hops run on. */
+ntp_status ntp_hop_timing(ntp_ctx* ctx, double* ms, int32_t* launches);
 
 /* -------------------------------------------------------------- graph (a0) */
 

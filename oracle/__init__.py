@@ -14,9 +14,10 @@ Modules
   model      O5–O9: MLP, decoupled model function, loss, gradients, SGD epoch
   layout     a1/a3/a5: partition maps, vertex <-> feature layouts (definitions)
   coupled    NEXT-1: the coupled L-layer GCN that naive tensor parallelism trains (baseline)
+  gat        NEXT-2: decoupled GAT (attention precomputed once per epoch, Eq. 5 / §4.1.1)
 
 Parity pins live in tests/test_oracle_*.py.  Functions without a pin say
 "parity unpinned" in their docstring (none at present).
 """
 from ._lib import lib, build_oracle_lib  # noqa: F401
-from . import graph, propagate, model, layout, coupled  # noqa: F401
+from . import graph, propagate, model, layout, coupled, gat  # noqa: F401

@@ -78,6 +78,10 @@ static void need_graph(const ntp_ctx* c) {
     NTP_CHECK(c->g.loaded, NTP_ERR_STATE, "no graph loaded");
 }
 
+// P = world * vs feature slices: V_pad = P * ceil(n / P); this rank's vertex rows V_pad / world.
+static int64_t pad_rows(const ntp_ctx* c, int64_t n) { return (int64_t)nslices(c) * cdiv(n, nslices(c)); }
+static int64_t rank_rows(const ntp_ctx* c, int64_t n) { return pad_rows(c, n) / c->world; }
+
 }  // namespace ntp
 
 using namespace ntp;
@@ -339,6 +343,28 @@ ntp_status ntp_copy_dinv(const ntp_ctx* cc, float* dinv_in, float* dinv_out) {
     NTP_API_END(c)
 }
 
+ntp_status ntp_set_slices(ntp_ctx* c, int32_t P) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(P >= c->world && P % c->world == 0 && P <= 4096, NTP_ERR_ARG,
+              "P = %d must be a multiple of world = %d (and <= 4096)", P, c->world);
+    NTP_CUDA(cudaSetDevice(c->device));
+    NTP_CUDA(cudaStreamSynchronize(c->s_comp));
+    drop_epoch_graph(c);
+    c->vs = P / c->world;
+    NTP_API_END(c)
+}
+
+ntp_status ntp_hop_timing(ntp_ctx* c, double* ms, int32_t* launches) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(ms && launches, NTP_ERR_ARG, "null output");
+    NTP_CUDA(cudaSetDevice(c->device));
+    if (c->hop_ev_used > 0) NTP_CUDA(cudaEventSynchronize(c->hop_ev[c->hop_ev_used - 1]));
+    int nh = 0;
+    *ms = collect_hop_ms(c, &nh);
+    *launches = nh;
+    NTP_API_END(c)
+}
+
 // ------------------------------------------------------------------ partition maps
 ntp_status ntp_partition(int64_t n, int32_t w, int32_t P, ntp_dtype dtype, int32_t chunks, int slice_align,
                          ntp_partition_info* out) {
@@ -367,24 +393,30 @@ ntp_status ntp_scatter_features(ntp_ctx* c, const void* X_host, ntp_dtype dtype,
     NTP_CHECK(out->dtype == dtype, NTP_ERR_SHAPE, "dtype mismatch");
     NTP_CUDA(cudaSetDevice(c->device));
     const size_t es = esize(dtype);
-    const int64_t V_p = cdiv(n, c->world);
-    NTP_CUDA(cudaMemset2DAsync(out->data, out->ld * es, 0, out->cols * es, out->rows, c->s_comp));
+    const int64_t V_r = rank_rows(c, n), V_pad = pad_rows(c, n);
     if (layout == NTP_LAYOUT_VERTEX) {
-        NTP_CHECK(out->rows >= V_p && out->cols >= d, NTP_ERR_SHAPE, "vertex tensor must be >= [V_p x d]");
-        const int64_t r0 = (int64_t)c->rank * V_p;
-        const int64_t nr = std::max<int64_t>(0, std::min<int64_t>(V_p, n - r0));
+        NTP_CHECK(out->rows >= V_r && out->cols >= d, NTP_ERR_SHAPE, "vertex tensor must be >= [V_p x d] = [%lld x %d]",
+                  (long long)V_r, d);
+        NTP_CUDA(cudaMemset2DAsync(out->data, out->ld * es, 0, out->cols * es, out->rows, c->s_comp));
+        const int64_t r0 = (int64_t)c->rank * V_r;
+        const int64_t nr = std::max<int64_t>(0, std::min<int64_t>(V_r, n - r0));
         if (nr > 0 && d > 0)
             NTP_CUDA(cudaMemcpy2DAsync(out->data, out->ld * es, static_cast<const char*>(X_host) + r0 * d * es, d * es,
                                        d * es, nr, cudaMemcpyHostToDevice, c->s_comp));
     } else {
-        const int32_t d_s = slice_width(d, c->world, dtype, c->slice_align);
-        NTP_CHECK(out->rows >= (int64_t)c->world * V_p && out->cols >= d_s, NTP_ERR_SHAPE,
-                  "feature tensor must be >= [V_pad x d_s] = [%lld x %d]", (long long)(c->world * V_p), d_s);
-        const int32_t c0 = c->rank * d_s;
-        const int32_t nc = std::max(0, std::min(d_s, d - c0));
-        if (nc > 0 && n > 0)
-            NTP_CUDA(cudaMemcpy2DAsync(out->data, out->ld * es, static_cast<const char*>(X_host) + c0 * es, d * es,
-                                       nc * es, n, cudaMemcpyHostToDevice, c->s_comp));
+        // this rank's vs slices stacked: slice j (global slice rank*vs + j) = rows [j*V_pad, (j+1)*V_pad)
+        const int32_t d_s = slice_width(d, nslices(c), dtype, c->slice_align);
+        NTP_CHECK(out->rows >= (int64_t)c->vs * V_pad && out->cols >= d_s, NTP_ERR_SHAPE,
+                  "feature tensor must be >= [vs*V_pad x d_s] = [%lld x %d]", (long long)(c->vs * V_pad), d_s);
+        NTP_CUDA(cudaMemset2DAsync(out->data, out->ld * es, 0, out->cols * es, out->rows, c->s_comp));
+        for (int j = 0; j < c->vs; ++j) {
+            const int32_t c0 = (c->rank * c->vs + j) * d_s;
+            const int32_t nc = std::max(0, std::min(d_s, d - c0));
+            if (nc > 0 && n > 0)
+                NTP_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out->data) + (size_t)j * V_pad * out->ld * es, out->ld * es,
+                                           static_cast<const char*>(X_host) + c0 * es, d * es, nc * es, n,
+                                           cudaMemcpyHostToDevice, c->s_comp));
+        }
     }
     NTP_CUDA(cudaStreamSynchronize(c->s_comp));
     NTP_API_END(c)
@@ -396,17 +428,18 @@ ntp_status ntp_layout_v2f(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Hf, ntp_
     check_tensor(Hv, "Hv", false);
     check_tensor(Hf, "Hf", true);
     NTP_CHECK(Hv->dtype == Hf->dtype, NTP_ERR_SHAPE, "dtype mismatch");
-    const int64_t V_p = cdiv(c->g.n, c->world);
-    const int32_t d_s = slice_width(Hv->cols, c->world, Hv->dtype, c->slice_align);
+    const int32_t P = nslices(c);
+    const int64_t V_p = rank_rows(c, c->g.n), V_pad = pad_rows(c, c->g.n);
+    const int32_t d_s = slice_width(Hv->cols, P, Hv->dtype, c->slice_align);
     NTP_CHECK(Hv->rows >= V_p, NTP_ERR_SHAPE, "Hv rows %lld < V_p %lld", (long long)Hv->rows, (long long)V_p);
-    NTP_CHECK(Hf->rows == (int64_t)c->world * V_p && Hf->cols == d_s && Hf->ld == d_s, NTP_ERR_SHAPE,
-              "Hf must be dense [V_pad x d_s] = [%lld x %d]", (long long)(c->world * V_p), d_s);
+    NTP_CHECK(Hf->rows == (int64_t)c->vs * V_pad && Hf->cols == d_s && Hf->ld == d_s, NTP_ERR_SHAPE,
+              "Hf must be dense [vs*V_pad x d_s] = [%lld x %d]", (long long)(c->vs * V_pad), d_s);
     cudaStream_t s = (cudaStream_t)st;
     const size_t es = esize(Hv->dtype);
-    c->send.ensure((size_t)c->world * V_p * d_s * es + 16);
-    pack_v2f(c, Hv->data, Hv->ld, Hv->cols, c->send.p, V_p, d_s, c->world, nullptr, (int64_t)c->rank * V_p, c->g.n,
+    c->send.ensure((size_t)P * V_p * d_s * es + 16);
+    pack_v2f(c, Hv->data, Hv->ld, Hv->cols, c->send.p, V_p, d_s, P, nullptr, (int64_t)c->rank * V_p, c->g.n,
              Hv->dtype, Hf->dtype, s);
-    alltoall_blocks(c, c->send.p, Hf->data, V_p * d_s, Hf->dtype, s);
+    exchange_v2f(c, c->send.p, Hf->data, V_p * d_s, Hf->dtype, s);
     NTP_API_END(c)
 }
 
@@ -416,16 +449,17 @@ ntp_status ntp_layout_f2v(ntp_ctx* c, const ntp_tensor* Hf, ntp_tensor* Hv, ntp_
     check_tensor(Hf, "Hf", true);
     check_tensor(Hv, "Hv", false);
     NTP_CHECK(Hv->dtype == Hf->dtype, NTP_ERR_SHAPE, "dtype mismatch");
-    const int64_t V_p = cdiv(c->g.n, c->world);
-    const int32_t d_s = slice_width(Hv->cols, c->world, Hv->dtype, c->slice_align);
+    const int32_t P = nslices(c);
+    const int64_t V_p = rank_rows(c, c->g.n), V_pad = pad_rows(c, c->g.n);
+    const int32_t d_s = slice_width(Hv->cols, P, Hv->dtype, c->slice_align);
     NTP_CHECK(Hv->rows >= V_p, NTP_ERR_SHAPE, "Hv rows < V_p");
-    NTP_CHECK(Hf->rows == (int64_t)c->world * V_p && Hf->cols == d_s && Hf->ld == d_s, NTP_ERR_SHAPE,
-              "Hf must be dense [V_pad x d_s] = [%lld x %d]", (long long)(c->world * V_p), d_s);
+    NTP_CHECK(Hf->rows == (int64_t)c->vs * V_pad && Hf->cols == d_s && Hf->ld == d_s, NTP_ERR_SHAPE,
+              "Hf must be dense [vs*V_pad x d_s] = [%lld x %d]", (long long)(c->vs * V_pad), d_s);
     cudaStream_t s = (cudaStream_t)st;
     const size_t es = esize(Hv->dtype);
-    c->recv.ensure((size_t)c->world * V_p * d_s * es + 16);
-    alltoall_blocks(c, Hf->data, c->recv.p, V_p * d_s, Hf->dtype, s);
-    unpack_f2v(c, c->recv.p, V_p, d_s, c->world, Hv->data, Hv->ld, Hv->cols, Hf->dtype, Hv->dtype, s);
+    c->recv.ensure((size_t)P * V_p * d_s * es + 16);
+    exchange_f2v(c, Hf->data, c->recv.p, V_p * d_s, Hf->dtype, s);
+    unpack_f2v(c, c->recv.p, V_p, d_s, P, Hv->data, Hv->ld, Hv->cols, Hf->dtype, Hv->dtype, s);
     NTP_API_END(c)
 }
 
@@ -459,7 +493,8 @@ static ntp_status do_propagate(ntp_ctx* c, const ntp_tensor* H, ntp_tensor* Z, i
     if (Z->rows > c->g.n)
         NTP_CUDA(cudaMemset2DAsync(static_cast<char*>(Z->data) + c->g.n * Z->ld * es, Z->ld * es, 0, Z->cols * es,
                                    Z->rows - c->g.n, s));
-    if (H->cols > 0) propagate(c, a, s);
+    c->hop_ev_used = 0;
+    if (H->cols > 0) propagate(c, a, s, /*time_hops*/ true);
     NTP_API_END(c)
 }
 
@@ -481,7 +516,7 @@ ntp_status ntp_propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* 
     check_tensor(Zv, "Zv", false);
     NTP_CHECK(Hv->dtype == NTP_F32 && Zv->dtype == NTP_F32, NTP_ERR_SHAPE, "Hv, Zv must be fp32");
     NTP_CHECK(dt == NTP_F32 || dt == NTP_BF16, NTP_ERR_ARG, "bad storage dtype");
-    const int64_t V_p = cdiv(c->g.n, c->world);
+    const int64_t V_p = rank_rows(c, c->g.n);
     NTP_CHECK(Hv->rows >= V_p && Zv->rows >= V_p && Hv->cols == Zv->cols && Hv->cols > 0, NTP_ERR_SHAPE,
               "Hv, Zv must be [>= V_p x w], same w");
     NTP_CHECK(Hv->data != Zv->data, NTP_ERR_ARG, "Zv must not alias Hv");
@@ -522,7 +557,7 @@ ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v
     NTP_CHECK(m->dtype == NTP_F32 || m->dtype == NTP_BF16, NTP_ERR_ARG, "bad dtype");
     NTP_CHECK(X_v->dtype == NTP_F32 && W0->dtype == NTP_F32 && W1->dtype == NTP_F32, NTP_ERR_SHAPE,
               "X_v, W0, W1 must be fp32");
-    const int64_t V_p = cdiv(c->g.n, c->world);
+    const int64_t V_p = rank_rows(c, c->g.n);
     NTP_CHECK(X_v->rows >= V_p && X_v->cols == m->d_in && X_v->ld >= m->d_in, NTP_ERR_SHAPE, "X_v must be [V_p x d_in]");
     NTP_CHECK(W0->rows == m->d_in && W0->cols == m->hid && W0->ld == m->hid, NTP_ERR_SHAPE,
               "W0 must be dense [d_in x hid]");
@@ -550,7 +585,7 @@ ntp_status ntp_stage_inputs(ntp_ctx* c, int slot, const float* X_host, int64_t r
     need_graph(c);
     NTP_CHECK(X_host && labels_host && train_mask_host, NTP_ERR_ARG, "null argument");
     NTP_CHECK(slot == 0 || slot == 1, NTP_ERR_ARG, "slot must be 0 or 1");
-    NTP_CHECK(d_in > 0 && ldx >= d_in && rows == cdiv(c->g.n, c->world), NTP_ERR_SHAPE, "X_host must be [V_p x d_in]");
+    NTP_CHECK(d_in > 0 && ldx >= d_in && rows == rank_rows(c, c->g.n), NTP_ERR_SHAPE, "X_host must be [V_p x d_in]");
     NTP_CUDA(cudaSetDevice(c->device));
     stage_inputs(c, slot, X_host, rows, d_in, ldx, labels_host, train_mask_host);
     NTP_API_END(c)
@@ -566,6 +601,7 @@ ntp_status ntp_train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const
     for (int l = 0; l <= m->L; ++l) NTP_CHECK(m->widths[l] > 0, NTP_ERR_ARG, "widths must be positive");
     NTP_CHECK(m->widths[m->L] <= 256, NTP_ERR_CONFIG, "C > 256 classes is not supported");
     NTP_CHECK(m->dtype == NTP_F32 || m->dtype == NTP_BF16, NTP_ERR_ARG, "bad dtype");
+    NTP_CHECK(c->vs == 1, NTP_ERR_CONFIG, "the coupled epoch runs one slice per rank (no virtual slices)");
     const int64_t V_p = cdiv(c->g.n, c->world);
     NTP_CHECK(X_v->dtype == NTP_F32 && X_v->rows >= V_p && X_v->cols == m->widths[0] && X_v->ld >= m->widths[0],
               NTP_ERR_SHAPE, "X_v must be fp32 [V_p x d_in]");

@@ -325,4 +325,43 @@ void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_ele
     NTP_NCCL(ncclGroupEnd());
 }
 
+// Split / gather with vs slices per rank: per (peer q, local slice j) one send/recv of blk elements, issued in
+// the same (q, j) order on every rank so NCCL pairs them.  vs == 1: the block all-to-all above.
+static void exchange_sliced(ntp_ctx* c, const void* src, void* dst, int64_t blk, ntp_dtype dt, cudaStream_t s,
+                            bool v2f) {
+    const int W = c->world, vs = c->vs;
+    const size_t es = esize(dt);
+    if (vs == 1) {
+        alltoall_blocks(c, src, dst, blk, dt, s);
+        return;
+    }
+    if (W == 1) {   // slice j of my rows is block j on both sides
+        if (src != dst && blk > 0)
+            NTP_CUDA(cudaMemcpyAsync(dst, src, (size_t)vs * blk * es, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    const ncclDataType_t t = dt == NTP_BF16 ? ncclBfloat16 : ncclFloat32;
+    const char* sp = static_cast<const char*>(src);
+    char* dp = static_cast<char*>(dst);
+    NTP_NCCL(ncclGroupStart());
+    for (int q = 0; q < W; ++q)
+        for (int j = 0; j < vs; ++j) {
+            // v2f: send block (q*vs + j) of my rows, receive rank q's rows of my slice j (block j*W + q);
+            // f2v: the reverse
+            const int64_t sb = v2f ? (int64_t)q * vs + j : (int64_t)j * W + q;
+            const int64_t rb = v2f ? (int64_t)j * W + q : (int64_t)q * vs + j;
+            NTP_NCCL(ncclSend(sp + sb * blk * es, blk, t, q, c->comm, s));
+            NTP_NCCL(ncclRecv(dp + rb * blk * es, blk, t, q, c->comm, s));
+            if (q != c->rank) wire_add(c, blk * (int64_t)es, blk * (int64_t)es);
+        }
+    NTP_NCCL(ncclGroupEnd());
+}
+
+void exchange_v2f(ntp_ctx* c, const void* send, void* feat, int64_t blk, ntp_dtype dt, cudaStream_t s) {
+    exchange_sliced(c, send, feat, blk, dt, s, true);
+}
+void exchange_f2v(ntp_ctx* c, const void* feat, void* recv, int64_t blk, ntp_dtype dt, cudaStream_t s) {
+    exchange_sliced(c, feat, recv, blk, dt, s, false);
+}
+
 }  // namespace ntp

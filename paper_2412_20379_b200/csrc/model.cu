@@ -315,17 +315,22 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                           const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, bool timed) {
     const Graph& g = c->g;
     cudaStream_t s = c->s_comp;
-    const int32_t P = c->world;
+    // P feature slices over `world` ranks, vs = P / world per rank (virtual slices, processed in sequence).
+    // V_pad = P * ceil(n / P); this rank's vertex rows are the contiguous V_p = V_pad / world = vs * ceil(n/P)
+    // rows from row0, and every blocked buffer is [P][V_p][d_s] (block q = slice q of these rows).
+    const int32_t P = nslices(c);
+    const int32_t vs = c->vs;
     const int64_t n = g.n;
-    const int64_t V_p = cdiv(n, P);
+    const int64_t V_pad = (int64_t)P * cdiv(n, P);
+    const int64_t V_p = V_pad / c->world;
     const int64_t row0 = (int64_t)c->rank * V_p;
     const bool after = (m->flags & NTP_M_W1_AFTER_PROP) != 0;
     const int32_t w = after ? m->hid : m->C;
     const int32_t d_s = slice_width(w, P, m->dtype, c->slice_align);
-    const int64_t V_pad = (int64_t)P * V_p;
     const ntp_dtype dt = m->dtype;
     const size_t es = esize(dt);
-    const int64_t feat_elems = V_pad * d_s;
+    const int64_t feat_elems = (int64_t)vs * V_pad * d_s;   // this rank's slices [vs][V_pad][d_s]
+    auto slice_at = [&](void* base, int j) -> void* { return static_cast<char*>(base) + (size_t)j * V_pad * d_s * es; };
 
     cudaEvent_t* E = c->ev;
     int ei = 0;
@@ -425,7 +430,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     // exchange copies, no send buffer, no scratch slice.  W1 after propagation (R3, papers shape):
     // the vertex-side work runs in row chunks of `hc` rows (H1, logits, gradients chunk-sized; the
     // ReLU' mask kept as bits) so the epoch's footprint is the slices plus X (memory-lean plan).
-    const bool local = (P == 1);
+    const bool local = (c->world == 1);
     const int64_t hc = epoch_row_chunk(m, V_p);
     const int64_t nch = cdiv(V_p, hc);
     const int32_t nwb = (m->hid + 31) / 32;          // mask words per row
@@ -468,11 +473,12 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     // Rows [n, V_pad) of every buffer that serves as a feature slice are padding: no hop writes them,
     // and every consumer multiplies them by zero (dl = 0, X = 0, mask bits 0) -- so they must hold
     // zeros, not stale bytes of an earlier allocation (a bf16 view of old fp32 data can be NaN, and
-    // 0 * NaN = NaN in dW1).  Cleared every epoch (< P rows per buffer).
-    if (!local && V_pad > n) {
+    // 0 * NaN = NaN in dW1).  Cleared every epoch (< P rows per slice).
+    if (V_pad > n) {
         const size_t off = (size_t)n * d_s * es, len = (size_t)(V_pad - n) * d_s * es;
-        for (void* b : {c->recv.p, c->xfer.p, c->send.p})
-            NTP_CUDA(cudaMemsetAsync(static_cast<char*>(b) + off, 0, len, s));
+        for (int j = 0; j < vs; ++j)
+            for (void* b : {c->recv.p, c->xfer.p, local ? nullptr : c->send.p})
+                if (b) NTP_CUDA(cudaMemsetAsync(static_cast<char*>(slice_at(b, j)) + off, 0, len, s));
         if (p2p)
             for (void* b : {c->p2p_split.p, c->p2p_gath.p})
                 NTP_CUDA(cudaMemsetAsync(static_cast<char*>(b) + off, 0, len, s));
@@ -561,7 +567,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     const int64_t p2p_wire = (int64_t)(P - 1) * V_p * d_s * (int64_t)es;
     // a3: split (pre-scaled by the forward column side D~_out^{-1/2})
     if (p2p) p2p_barrier(c, s), wire_add(c, p2p_wire, p2p_wire);
-    else if (!local && !ovl) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    else if (!local && !ovl) exchange_v2f(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E2 v2f done
 
     // a4 + a5: K forward hops on S^0 (pre-scaled) -> Z^K, gathered into this rank's rows
@@ -580,8 +586,21 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         a.gamma = m->gamma;
         a.alpha = m->alpha;
         a.transposed = false;
-        if (local) {
-            gathered = propagate_consume(c, a, s, timed, fwd_internal);
+        if (local) {   // slice j of recv -> slice j of recv / xfer (the same buffer for every slice)
+            for (int j = 0; j < vs; ++j) {
+                PropArgs aj = a;
+                aj.H = slice_at(c->recv.p, j);
+                aj.Z = slice_at(c->xfer.p, j);
+                gathered = propagate_consume(c, aj, s, timed, fwd_internal) == aj.H ? c->recv.p : c->xfer.p;
+            }
+        } else if (vs > 1) {   // every slice in sequence, then one gather
+            for (int j = 0; j < vs; ++j) {
+                PropArgs aj = a;
+                aj.H = slice_at(slice_in, j);
+                aj.Z = slice_at(c->xfer.p, j);
+                propagate(c, aj, s, timed, true);
+            }
+            exchange_f2v(c, c->xfer.p, c->recv.p, V_p * d_s, dt, s);
         } else if (p2p) {
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
@@ -659,7 +678,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
 
     // a7: split the gradient
     if (p2p) p2p_barrier(c, s), wire_add(c, p2p_wire, p2p_wire);
-    else if (!local && !ovl) alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    else if (!local && !ovl) exchange_v2f(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E5 v2f bwd
 
     // a8 + a9: K backward hops on the split gradient, gathered -> dL^ rows [V_p x w]
@@ -678,7 +697,22 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         a.alpha = m->alpha;
         a.transposed = true;
         if (local) {
-            gathered_b = propagate_consume(c, a, s, timed, bwd_internal);
+            void* hb = const_cast<void*>(a.H);
+            void* zb = a.Z;
+            for (int j = 0; j < vs; ++j) {
+                PropArgs aj = a;
+                aj.H = slice_at(hb, j);
+                aj.Z = slice_at(zb, j);
+                gathered_b = propagate_consume(c, aj, s, timed, bwd_internal) == aj.H ? hb : zb;
+            }
+        } else if (vs > 1) {
+            for (int j = 0; j < vs; ++j) {
+                PropArgs aj = a;
+                aj.H = slice_at(slice_in, j);
+                aj.Z = slice_at(c->xfer.p, j);
+                propagate(c, aj, s, timed, true);
+            }
+            exchange_f2v(c, c->xfer.p, c->send.p, V_p * d_s, dt, s);
         } else if (p2p) {
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
@@ -770,15 +804,19 @@ void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K,
     const Graph& g = c->g;
     NTP_CHECK(!(overlap && g.reordered), NTP_ERR_CONFIG,
               "the overlapped gather sends last-hop chunks by destination block: needs a graph without NTP_G_REORDER");
+    NTP_CHECK(!(overlap && c->vs > 1), NTP_ERR_CONFIG, "the overlapped gather needs one slice per rank");
     cudaStream_t s = c->s_comp;
-    const int32_t P = c->world;
+    const int32_t P = nslices(c);
+    const int32_t vs = c->vs;
     const int64_t n = g.n;
-    const int64_t V_p = cdiv(n, P);
+    const int64_t V_pad = (int64_t)P * cdiv(n, P);
+    const int64_t V_p = V_pad / c->world;                 // this rank's rows (vs slice blocks)
     const int64_t row0 = (int64_t)c->rank * V_p;
     const int32_t w = Hv->cols;
     const int32_t d_s = slice_width(w, P, dt, c->slice_align);
     const size_t es = esize(dt);
     const int64_t feat = (int64_t)P * V_p * d_s;
+    c->hop_ev_used = 0;
     c->send.ensure((size_t)feat * es + 16);
     c->recv.ensure((size_t)feat * es + 16);
     c->xfer.ensure((size_t)feat * es + 16);
@@ -786,7 +824,7 @@ void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K,
     NTP_CUDA(cudaStreamWaitEvent(s, c->ev[40], 0));
     const float* cs = transposed ? g.dinv_in_orig() : g.dinv_out_orig();   // column side of this direction
     pack_v2f(c, Hv->data, Hv->ld, w, c->send.p, V_p, d_s, P, cs, row0, n, NTP_F32, dt, s);
-    alltoall_blocks(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
+    exchange_v2f(c, c->send.p, c->recv.p, V_p * d_s, dt, s);
     PropArgs a{};
     a.H = c->recv.p;
     a.Z = c->xfer.p;
@@ -798,7 +836,20 @@ void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K,
     a.gamma = gamma;
     a.alpha = alpha;
     a.transposed = transposed;
-    propagate_and_gather(c, a, c->send.p, overlap, chunks, V_p, d_s, false, s);
+    if (vs == 1) {
+        propagate_and_gather(c, a, c->send.p, overlap, chunks, V_p, d_s, true, s);
+    } else {   // virtual slices: each slice in sequence, then one gather
+        for (int j = 0; j < vs; ++j) {
+            PropArgs aj = a;
+            const size_t off = (size_t)j * V_pad * d_s * es;
+            aj.H = static_cast<char*>(c->recv.p) + off;
+            aj.Z = static_cast<char*>(c->xfer.p) + off;
+            if (V_pad > n)   // padding rows of every slice travel in the gather: keep them zero
+                NTP_CUDA(cudaMemsetAsync(static_cast<char*>(aj.Z) + n * d_s * es, 0, (V_pad - n) * d_s * es, s));
+            propagate(c, aj, s, true, true);
+        }
+        exchange_f2v(c, c->xfer.p, c->send.p, V_p * d_s, dt, s);
+    }
     unpack_f2v(c, c->send.p, V_p, d_s, P, Zv->data, Zv->ld, w, dt, NTP_F32, s);
     NTP_CUDA(cudaEventRecord(c->ev[41], s));
     NTP_CUDA(cudaStreamWaitEvent(user, c->ev[41], 0));
@@ -810,14 +861,12 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     cudaStream_t s = c->s_comp;
     const int64_t launches0 = c->launches;
     const int32_t P = c->world;
-    const int64_t n = g.n;
-    const int64_t V_p = cdiv(n, P);
     const bool after = (m->flags & NTP_M_W1_AFTER_PROP) != 0;
-    const int32_t w = after ? m->hid : m->C;
-    const int32_t d_s = slice_width(w, P, m->dtype, c->slice_align);
-    const size_t es = esize(m->dtype);
     const bool timed = true;
     cudaEvent_t* E = c->ev;
+    NTP_CHECK(c->vs == 1 || !(m->flags & (NTP_M_OVERLAP | NTP_M_P2P_LAYOUTS | NTP_M_DATA_PARALLEL)), NTP_ERR_CONFIG,
+              "virtual slices (ntp_set_slices P > world) run the plain layout path: no NTP_M_OVERLAP, "
+              "NTP_M_P2P_LAYOUTS or NTP_M_DATA_PARALLEL");
     NTP_CHECK(!((m->flags & NTP_M_OVERLAP) && g.reordered && !after), NTP_ERR_CONFIG,
               "NTP_M_OVERLAP sends last-hop chunks by destination block: needs a graph without NTP_G_REORDER "
               "(the W1-after-propagation epoch overlaps its layout changes by row chunk instead)");
@@ -1019,7 +1068,7 @@ static void enqueue_epoch_dp(ntp_ctx* c, const ntp_model* m, const float* X, int
         char* nxt = B;
         for (int k = 1; k <= m->K; ++k) {
             allgather(cur);
-            const bool tm = timed && c->hop_ev_used + 2 <= 256;
+            const bool tm = timed && c->hop_ev_used + 2 <= kHopEvents;
             if (tm) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
             spmm_hop(c, csr, rs, cs, cur, nxt, m->alpha != 0.f ? (const void*)S0 : (const void*)cur, ws, ws, ws, ws,
                      dt, m->gamma, m->alpha, k == m->K ? 1 : 0, row0, row_hi, s);
@@ -1134,6 +1183,7 @@ void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tenso
     const ntp_dtype dt = m->dtype;
     const size_t es = esize(dt);
     const bool local = (P == 1);
+    NTP_CHECK(c->vs == 1, NTP_ERR_CONFIG, "the coupled epoch runs one slice per rank (no virtual slices)");
     drop_epoch_graph(c);   // the buffers below may move ones a captured decoupled epoch points into
     NTP_CUDA(cudaEventRecord(c->ev[40], user ? user : (cudaStream_t)0));
     NTP_CUDA(cudaStreamWaitEvent(s, c->ev[40], 0));

@@ -141,6 +141,7 @@ struct EpochKey {
 
 struct ntp_ctx {
     int device = 0, rank = 0, world = 1, slice_align = 16;
+    int vs = 1;                     // virtual feature slices per rank (ntp_set_slices): P = world * vs
     ncclComm_t comm = nullptr;
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
     ntp::Graph g;
@@ -168,7 +169,7 @@ struct ntp_ctx {
     cudaEvent_t ev[64] = {};
     cudaEvent_t ov_ev[256] = {};    // fork/join events of the chunked layout exchanges (a12)
     ntp::PackEpi pack_epi{};        // parameters of the next pack-epilogue GEMM launch
-    cudaEvent_t hop_ev[256] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
+    cudaEvent_t hop_ev[512] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
     int hop_ev_used = 0;
     int64_t launches = 0;
     std::string err;
@@ -260,6 +261,7 @@ void drop_epoch_graph(ntp_ctx* c);
 int64_t epoch_row_chunk(const ntp_model* m, int64_t V_p);
 constexpr int kMaxLayers = NTP_MAX_LAYERS;
 constexpr int kOvEvents = 256;
+constexpr int kHopEvents = 512;
 void stage_inputs(ntp_ctx* c, int slot, const float* X, int64_t rows, int32_t d_in, int64_t ldx, const int32_t* y,
                   const uint8_t* m);
 void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
@@ -296,6 +298,15 @@ void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t 
                 const uint32_t* keep_bits = nullptr, int32_t nw = 0);
 void alltoall_blocks(ntp_ctx* c, const void* send, void* recv, int64_t block_elems, ntp_dtype dt,
                      cudaStream_t s);
+// Layout exchanges with P = world * vs feature slices (vs virtual slices per rank, processed in sequence).
+// Blocks are blk = V_r * d_s elements (V_r = vs * V_p rows per rank).
+//   split  (v2f): send [P][V_r][d_s] (block s = slice s of my rows)  ->  feature slices [vs][V_pad][d_s]
+//                 (slice j, rows of rank q = block j*world + q)
+//   gather (f2v): feature slices [vs][V_pad][d_s]  ->  recv [P][V_r][d_s] (block s = slice s of my rows)
+// world == 1: both layouts coincide (identity; a copy only if the buffers differ).
+void exchange_v2f(ntp_ctx* c, const void* send, void* feat, int64_t blk, ntp_dtype dt, cudaStream_t s);
+void exchange_f2v(ntp_ctx* c, const void* feat, void* recv, int64_t blk, ntp_dtype dt, cudaStream_t s);
+inline int32_t nslices(const ntp_ctx* c) { return c->world * c->vs; }
 
 void gemm_tf32x3_pack(ntp_ctx* c, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B_hi,
                       const float* B_lo, int64_t ldb, const PackEpi& pk, cudaStream_t s);

@@ -635,7 +635,7 @@ void propagate(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time_hops, bo
                                   a.gamma, a.alpha};
             return;
         }
-        const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
+        const bool timed = time_hops && c->hop_ev_used + 2 <= kHopEvents;
         if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
         spmm_hop(c, csr, rs, cs, sin, bufs[nxt], S0, ld_sin, lds[nxt], ld_s0, a.cols, a.dtype, a.gamma, a.alpha,
                  last ? 1 : 0, 0, -1, s, last ? inv : nullptr, last ? &a.po : nullptr);
@@ -666,7 +666,7 @@ void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time
     }
     for (int k = 1; k <= a.K; ++k) {
         const bool last = (k == a.K);
-        const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
+        const bool timed = time_hops && c->hop_ev_used + 2 <= kHopEvents;
         if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
         spmm_hop(c, csr, rs, cs, cur, oth, cur, a.ld_h, a.ld_z, a.ld_h, a.cols, a.dtype, a.gamma, 0.f, last ? 1 : 0, 0,
                  -1, s, last ? inv : nullptr, nullptr);
@@ -680,7 +680,7 @@ void* propagate_consume(ntp_ctx* c, const PropArgs& a, cudaStream_t s, bool time
 }
 
 void run_last_hop(ntp_ctx* c, const LastHop& lh, int64_t row_lo, int64_t row_hi, cudaStream_t s, bool time_hops) {
-    const bool timed = time_hops && c->hop_ev_used + 2 <= 256;
+    const bool timed = time_hops && c->hop_ev_used + 2 <= kHopEvents;
     if (timed) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
     spmm_hop(c, *lh.csr, lh.rs, lh.cs, lh.sin, lh.out, lh.S0, lh.ld_sin, lh.ld_out, lh.ld_s0, lh.cols, lh.dt, lh.gamma,
              lh.alpha, 1, row_lo, row_hi, s);

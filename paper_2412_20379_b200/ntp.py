@@ -37,7 +37,7 @@ EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_u
             "ntp_graph_info", "ntp_copy_csr", "ntp_copy_dinv", "ntp_partition", "ntp_scatter_features",
             "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd",
             "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch", "ntp_train_epoch_coupled",
-            "ntp_stage_inputs"]
+            "ntp_stage_inputs", "ntp_set_slices", "ntp_hop_timing"]
 
 
 class ntp_tensor(C.Structure):
@@ -106,6 +106,8 @@ _sig = {
     "ntp_train_epoch": ([_vp, C.POINTER(ntp_model), C.POINTER(ntp_tensor), _vp, _vp, C.POINTER(ntp_tensor),
                          C.POINTER(ntp_tensor), C.POINTER(ntp_epoch_report), _vp], C.c_int),
     "ntp_stage_inputs": ([_vp, C.c_int, _vp, _i64, _i32, _i64, _vp, _vp], C.c_int),
+    "ntp_set_slices": ([_vp, _i32], C.c_int),
+    "ntp_hop_timing": ([_vp, C.POINTER(C.c_double), C.POINTER(_i32)], C.c_int),
     "ntp_train_epoch_coupled": ([_vp, C.POINTER(ntp_coupled_model), C.POINTER(ntp_tensor), _vp, _vp,
                                  C.POINTER(C.POINTER(ntp_tensor)), C.POINTER(ntp_coupled_report), _vp], C.c_int),
 }
@@ -182,6 +184,18 @@ class Context:
         if st != NTP_OK:
             raise NtpError(st, _lib.ntp_last_error(None).decode())
         self.device, self.rank, self.world, self.slice_align = device, rank, world, slice_align
+        self.slices = world
+
+    def set_slices(self, P: int):
+        """ntp_set_slices: P = world * vs feature slices (vs virtual slices per rank, in sequence)."""
+        self._chk(_lib.ntp_set_slices(self._h, int(P)))
+        self.slices = int(P)
+
+    def hop_timing(self):
+        """ntp_hop_timing: (summed ms, launches) of the SpMM hops of the last propagation / epoch call."""
+        ms, k = C.c_double(), C.c_int32()
+        self._chk(_lib.ntp_hop_timing(self._h, C.byref(ms), C.byref(k)))
+        return ms.value, k.value
 
     def close(self):
         if self._h:
