@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                     __floats2bfloat162_rn(e[8 * g8 + 2 * k] * sc, e[8 * g8 + 2 * k + 1] * sc);
                                 ow[k] = *reinterpret_cast<const uint32_t*>(&h2);
                             }
-                            const int64_t orow = p.pk.perm ? (int64_t)__ldg(p.pk.perm + v) : v;
+                            const int64_t orow = (p.pk.perm && v < p.pk.n) ? (int64_t)__ldg(p.pk.perm + v) : v;   // padding rows stay
                             *reinterpret_cast<uint4*>(p.pk.out + ((int64_t)qb * p.pk.V_p + orow) * p.pk.d_s + jj) = o;
                         }
                     }

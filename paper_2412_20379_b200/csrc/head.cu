@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_fused_kernel(const __gri
                     o.y = pack_bf16(__uint_as_float(x[c8 * 8 + 2]) * sc, __uint_as_float(x[c8 * 8 + 3]) * sc);
                     o.z = pack_bf16(__uint_as_float(x[c8 * 8 + 4]) * sc, __uint_as_float(x[c8 * 8 + 5]) * sc);
                     o.w = pack_bf16(__uint_as_float(x[c8 * 8 + 6]) * sc, __uint_as_float(x[c8 * 8 + 7]) * sc);
-                    const int64_t ov = p.out_perm ? (int64_t)__ldg(p.out_perm + v) : v;
+                    const int64_t ov = (p.out_perm && v < p.n) ? (int64_t)__ldg(p.out_perm + v) : v;   // padding rows stay
                     __nv_bfloat16* dst = p.peer ? static_cast<__nv_bfloat16*>(p.peer[q]) +
                                                       ((int64_t)p.rank * p.V_p + v) * p.d_s + j
                                                 : p.out + ((int64_t)q * p.V_p + ov) * p.d_s + j;

@@ -755,7 +755,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     NTP_CUDA(record_timing(c, E[ei++], s));   // E7 mlp bwd
 
     // a11: allreduce (sync_and_update)
-    if (P > 1) {
+    if (!local) {
         NTP_NCCL(ncclGroupStart());
         NTP_NCCL(ncclAllReduce(dW0, dW0, n_w, ncclFloat32, ncclSum, c->comm, s));
         NTP_NCCL(ncclAllReduce(scal, scal, 2, ncclFloat64, ncclSum, c->comm, s));
