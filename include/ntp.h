@@ -287,6 +287,21 @@ ntp_status ntp_train_epoch(ntp_ctx* ctx, const ntp_model* m, const ntp_tensor* X
                            const int32_t* labels_v, const uint8_t* train_mask_v,
                            ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, ntp_stream s);
 
+/* NEXT-2: one epoch of decoupled GAT (Eq. 5; §4.1.1: attention
+ * "precomputed ... before the graph aggregation" and shared, then aggregation on feature slices):
+ *   z = ReLU(X W0) W1 (w = C);  s_uv = a_src.z_u + a_dst.z_v over N_in(v) + {v} (A~ = A + I);
+ *   alpha_uv = softmax_v(LeakyReLU(s_uv, slope));  Z^0 = z, Z^k = gamma A_att Z^{k-1};  softmax
+ *   cross-entropy on Z^K;  gradients of W0, W1 and att by the chain rule (through the attention);
+ *   SGD on all three.
+ * att: [2 x C] fp32 device (row 0 a_src, row 1 a_dst), updated in place.  m->alpha must be 0, m->flags 0
+ * (device inputs, W1 before propagation), C <= 256, graph without NTP_G_REORDER; virtual slices allowed.
+ * Per epoch: 4 layout changes, one all-gather of 2 floats per vertex (score halves: every rank then
+ * evaluates every coefficient itself), one allreduce of the n + nnz coefficient gradients, one of
+ * dW0|dW1|da.  Synchronous; eager (no epoch graph).  Errors as ntp_train_epoch. */
+ntp_status ntp_train_epoch_gat(ntp_ctx* ctx, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                               const uint8_t* train_mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_tensor* att,
+                               float slope, ntp_epoch_report* rep, ntp_stream s);
+
 /* Input staging for end-to-end training loops: enqueues the host->device copy of one epoch's
  * inputs (this rank's rows: X_host [V_p x d_in] fp32 with row pitch ldx elements, labels int32[V_p],
  * train mask uint8[V_p]; pinned host memory for a truly asynchronous copy) into library-owned slot

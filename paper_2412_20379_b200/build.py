@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libntp.so")
-SOURCES = ["api.cu", "graph.cu", "spmm.cu", "layout.cu", "model.cu", "gemm.cu", "head.cu", "wgrad.cu"]
+SOURCES = ["api.cu", "graph.cu", "spmm.cu", "layout.cu", "model.cu", "gemm.cu", "head.cu", "wgrad.cu", "gat.cu"]
 HEADERS = ["ntp_internal.cuh"]
 
 

@@ -579,6 +579,31 @@ ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v
     NTP_API_END(c)
 }
 
+ntp_status ntp_train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                               const uint8_t* train_mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_tensor* att, float slope,
+                               ntp_epoch_report* rep, ntp_stream st) {
+    NTP_API_BEGIN(c)
+    need_graph(c);
+    NTP_CHECK(m && X_v && labels_v && train_mask_v && W0 && W1 && att, NTP_ERR_ARG, "null argument");
+    NTP_CHECK(m->d_in > 0 && m->hid > 0 && m->C > 0 && m->K >= 1, NTP_ERR_ARG, "bad model dims / K");
+    NTP_CHECK(m->gamma > 0.f && m->gamma <= 1.f, NTP_ERR_ARG, "gamma in (0,1]");
+    NTP_CHECK(m->alpha == 0.f, NTP_ERR_CONFIG, "the GAT epoch has no alpha mix (reading G3): alpha must be 0");
+    NTP_CHECK(m->dtype == NTP_F32 || m->dtype == NTP_BF16, NTP_ERR_ARG, "bad dtype");
+    NTP_CHECK(m->flags == 0, NTP_ERR_CONFIG, "the GAT epoch takes no epoch flags (device inputs, W1 before propagation)");
+    NTP_CHECK(m->C <= 256, NTP_ERR_CONFIG, "C = %d > 256 classes is not supported", m->C);
+    NTP_CHECK(slope >= 0.f && slope < 1.f, NTP_ERR_ARG, "LeakyReLU slope in [0, 1)");
+    NTP_CHECK(X_v->dtype == NTP_F32 && W0->dtype == NTP_F32 && W1->dtype == NTP_F32 && att->dtype == NTP_F32,
+              NTP_ERR_SHAPE, "X_v, W0, W1, att must be fp32");
+    const int64_t V_p = rank_rows(c, c->g.n);
+    NTP_CHECK(X_v->rows >= V_p && X_v->cols == m->d_in && X_v->ld >= m->d_in, NTP_ERR_SHAPE, "X_v must be [V_p x d_in]");
+    NTP_CHECK(W0->rows == m->d_in && W0->cols == m->hid && W0->ld == m->hid, NTP_ERR_SHAPE, "W0 must be dense [d_in x hid]");
+    NTP_CHECK(W1->rows == m->hid && W1->cols == m->C && W1->ld == m->C, NTP_ERR_SHAPE, "W1 must be dense [hid x C]");
+    NTP_CHECK(att->rows == 2 && att->cols == m->C && att->ld == m->C, NTP_ERR_SHAPE, "att must be dense [2 x C]");
+    NTP_CUDA(cudaSetDevice(c->device));
+    train_epoch_gat(c, m, X_v, labels_v, train_mask_v, W0, W1, att, slope, rep, (cudaStream_t)st);
+    NTP_API_END(c)
+}
+
 ntp_status ntp_stage_inputs(ntp_ctx* c, int slot, const float* X_host, int64_t rows, int32_t d_in, int64_t ldx,
                             const int32_t* labels_host, const uint8_t* train_mask_host) {
     NTP_API_BEGIN(c)

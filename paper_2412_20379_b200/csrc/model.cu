@@ -230,6 +230,48 @@ inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
 
 }  // namespace
 
+// ---- epoch building blocks shared with the GAT epoch (gat.cu)
+void epoch_gemm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                const float* B, int64_t ldb, float* C, int64_t ldc, cudaStream_t s, int epi, const float* aux,
+                int64_t ldaux, const float* B_hi, const float* B_lo) {
+    mlp_gemm(c, ta, tb, M, N, K, A, lda, B, ldb, C, ldc, s, epi, aux, ldaux, Split{B_hi, B_lo});
+}
+
+int64_t epoch_loss(ntp_ctx* c, const void* in, ntp_dtype tin, int in_blocked, int64_t V_p, int32_t d_s, int32_t C,
+                   const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n, void* out, ntp_dtype tout,
+                   int out_blocked, const float* gscale, double* part, int64_t* cnt, int64_t ld_plain, cudaStream_t s) {
+    NTP_CHECK(tin == tout, NTP_ERR_CONFIG, "loss kernel: input and gradient storage must match");
+    if (tin == NTP_F32)
+        return launch_softmax_xent(c, (const float*)in, in_blocked, V_p, d_s, C, y, mask, row0, n, (float*)out,
+                                   out_blocked, gscale, part, cnt, ld_plain, s);
+    return launch_softmax_xent(c, (const __nv_bfloat16*)in, in_blocked, V_p, d_s, C, y, mask, row0, n,
+                               (__nv_bfloat16*)out, out_blocked, gscale, part, cnt, ld_plain, s);
+}
+
+void epoch_zero_pad_cols(ntp_ctx* c, void* buf, ntp_dtype dt, int64_t V_p, int32_t d_s, int32_t P, int32_t C,
+                         cudaStream_t s) {
+    if (P * d_s <= C) return;
+    if (dt == NTP_F32)
+        zero_pad_cols_kernel<float><<<eblocks(V_p * (P * d_s - C)), 256, 0, s>>>((float*)buf, V_p, d_s, P, C, nullptr, 0);
+    else
+        zero_pad_cols_kernel<__nv_bfloat16><<<eblocks(V_p * (P * d_s - C)), 256, 0, s>>>((__nv_bfloat16*)buf, V_p, d_s,
+                                                                                        P, C, nullptr, 0);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+}
+
+void epoch_reduce_loss(ntp_ctx* c, const double* part, const int64_t* cnt, int64_t nb, double* scal, cudaStream_t s) {
+    reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb, scal);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+}
+
+void epoch_sgd(ntp_ctx* c, float* W, int64_t n, const float* dW, const double* scal, float lr, cudaStream_t s) {
+    sgd_kernel<<<eblocks(n), 256, 0, s>>>(W, n, nullptr, 0, dW, scal, lr);
+    NTP_LAUNCH_CHECK();
+    count_launch(c);
+}
+
 // Propagate K hops on this rank's feature slice (a.Z = output slice [V_pad x d_s])
 // and gather the result into `recv` ([P][V_p][d_s], block p = rank p's columns of
 // my rows).  overlap == false: all hops, then one block exchange on `s`.

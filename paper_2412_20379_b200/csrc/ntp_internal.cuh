@@ -147,6 +147,9 @@ struct ntp_ctx {
     ntp::Graph g;
     // scratch
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
+    // decoupled GAT (gat.cu): score halves, coefficients (+ out-CSR order), their gradients, level stack
+    ntp::DevBuf gat_fg, gat_alpha, gat_alpha_t, gat_dalpha, gat_ds, gat_pspd, gat_perm, gat_Z, gat_da;
+    int64_t gat_perm_version = -1;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
     ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp, m_head, m_wgrad;
     // coupled (naive TP) epoch: Z^l, H^l per layer, dA / dZ scratch, padded weights
@@ -258,6 +261,20 @@ void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K,
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
 void drop_epoch_graph(ntp_ctx* c);
+// epoch building blocks (model.cu), shared with the GAT epoch (gat.cu)
+void epoch_gemm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                const float* B, int64_t ldb, float* C, int64_t ldc, cudaStream_t s, int epi, const float* aux,
+                int64_t ldaux, const float* B_hi, const float* B_lo);
+int64_t epoch_loss(ntp_ctx* c, const void* in, ntp_dtype tin, int in_blocked, int64_t V_p, int32_t d_s, int32_t C,
+                   const int32_t* y, const uint8_t* mask, int64_t row0, int64_t n, void* out, ntp_dtype tout,
+                   int out_blocked, const float* gscale, double* part, int64_t* cnt, int64_t ld_plain, cudaStream_t s);
+void epoch_zero_pad_cols(ntp_ctx* c, void* buf, ntp_dtype dt, int64_t V_p, int32_t d_s, int32_t P, int32_t C,
+                         cudaStream_t s);
+void epoch_reduce_loss(ntp_ctx* c, const double* part, const int64_t* cnt, int64_t nb, double* scal, cudaStream_t s);
+void epoch_sgd(ntp_ctx* c, float* W, int64_t n, const float* dW, const double* scal, float lr, cudaStream_t s);
+void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
+                     const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_tensor* att, float slope,
+                     ntp_epoch_report* rep, cudaStream_t user);
 int64_t epoch_row_chunk(const ntp_model* m, int64_t V_p);
 constexpr int kMaxLayers = NTP_MAX_LAYERS;
 constexpr int kOvEvents = 256;
@@ -276,7 +293,8 @@ void csr_to_keys(ntp_ctx* c, const int64_t* row_ptr, const int32_t* col, int64_t
 void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, const void* S_in,
               void* S_out, const void* H, int64_t ld_in, int64_t ld_out, int64_t ld_h, int32_t cols,
               ntp_dtype dt, float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi,
-              cudaStream_t s, const int32_t* out_rows = nullptr, const PeerOut* po = nullptr);
+              cudaStream_t s, const int32_t* out_rows = nullptr, const PeerOut* po = nullptr,
+              const float* ew = nullptr, const float* sw = nullptr);   // weighted hop (GAT): arc / self coefficients
 // S[r] = scale[r] * H[src_rows ? src_rows[r] : r] (scale may be null: plain copy / permutation)
 void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, int32_t cols,
               const float* scale, int64_t rows, ntp_dtype dt, cudaStream_t s,

@@ -98,6 +98,13 @@ __device__ __forceinline__ void vadd(float (&a)[Vec<T, VB>::N], const Raw<VB>& x
 #pragma unroll
     for (int i = 0; i < Vec<T, VB>::N; ++i) a[i] += Vec<T, VB>::elem(x, i);
 }
+// weighted hop (per-arc coefficient, e.g. GAT attention): a += w * x as one rounding (explicit fma, so the
+// accumulation is the same instruction sequence for every slice width)
+template <typename T, int VB>
+__device__ __forceinline__ void vfma(float (&a)[Vec<T, VB>::N], const Raw<VB>& x, float w) {
+#pragma unroll
+    for (int i = 0; i < Vec<T, VB>::N; ++i) a[i] = __fmaf_rn(w, Vec<T, VB>::elem(x, i), a[i]);
+}
 
 // 16-byte element loads for the fix-up / prescale kernels
 template <typename T> __device__ __forceinline__ void load16(const void* p, float (&v)[16 / sizeof(T)]) {
@@ -142,6 +149,8 @@ struct HopParams {
     void* const* __restrict__ peer_out;     // last hop, peer-direct gather: window table [P] (else null)
     int64_t po_V_p;
     int po_rank;
+    const float* __restrict__ ew;      // weighted hop: per-arc coefficients in CSR order (else null)
+    const float* __restrict__ sw;      // weighted hop: per-row self-loop coefficients
 };
 
 // Where output row r (internal order) is stored: its original row (out_rows), locally or -- peer-direct
@@ -172,7 +181,10 @@ __device__ __forceinline__ char* out_row_ptr(const HopParams& p, int64_t r) {
 // SM; bit 1 = tiny-row path (E >= 2, below).  Neither enters the reduction order (groups are
 // (j - eb) mod 8 for any batch that is a multiple of 8), and the tiny path's registers are only
 // paid where it is used.
-template <typename T, int VB, int E, int L, int MODE>
+// WT (weighted hop): the row sum carries a per-arc coefficient p.ew[j] (loaded with the column index and
+// shuffled with it) and the self term p.sw[r]; no row / column D~^{-1/2} (rs = cs = 1).  GAT's attention
+// aggregation (Eq. 5) -- the same merge-path split, pipeline and fixed reduction order.
+template <typename T, int VB, int E, int L, int MODE, bool WT = false>
 __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kernel(const HopParams p) {
     constexpr bool SHORT = (MODE & 1) != 0;
     constexpr bool TINY = (MODE & 2) != 0 && E >= 2;
@@ -187,7 +199,9 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
     constexpr int BATCH = (OCC && !SHORT && BATCH0 >= 16) ? BATCH0 / 2 : BATCH0;
     constexpr int LPB = BATCH / E;                        // loads per lane per batch
     constexpr int ISL = (BATCH + L - 1) / L;              // column indices held per lane
+    constexpr int ISLW = WT ? ISL : 1, LPBW = WT ? LPB : 1;   // arc coefficients held per lane (weighted)
     static_assert(BATCH % 8 == 0, "batch must preserve the (j - eb) mod 8 grouping");
+    static_assert(!(WT && MODE != 0), "the weighted hop has only the general path");
     const int lane = threadIdx.x & 31;
     const int gl = lane % L;
     const int gbase = lane - gl;
@@ -269,62 +283,78 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
             // epilogue operands issued now so their latency hides behind the gather (short rows)
             const bool fin = !(head || tail) && e_raw == 0 && col_ok;
             Raw<VB> self_raw = zero_raw<VB>();
-            float ra = 0.f, rb = 0.f;
+            float ra = 0.f, rb = 0.f, swr = 0.f;
             if (fin) {
                 self_raw = ldv<VB>(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * VB);
-                ra = __ldg(p.rs + r);
-                rb = __ldg(p.cs + r);
+                if constexpr (WT) {
+                    ra = rb = 1.f;
+                    swr = __ldg(p.sw + r);
+                } else {
+                    ra = __ldg(p.rs + r);
+                    rb = __ldg(p.cs + r);
+                }
             }
             float acc[NACC][VALS];
 #pragma unroll
             for (int k = 0; k < NACC; ++k)
 #pragma unroll
                 for (int i = 0; i < VALS; ++i) acc[k][i] = 0.f;
-            // column indices of a batch: lane gl holds edges base + sl*L + gl (0 past the end)
-            auto load_idx = [&](int base, int (&dst)[ISL]) {
+            // column indices of a batch: lane gl holds edges base + sl*L + gl (0 past the end), with their
+            // coefficients when weighted
+            auto load_idx = [&](int base, int (&dst)[ISL], float (&dw)[ISLW]) {
 #pragma unroll
                 for (int sl = 0; sl < ISL; ++sl) {
                     const int j = base + sl * L + gl;
-                    dst[sl] = (sl * L + gl < BATCH && j < ee) ? __ldg(colp + j) : 0;
+                    const bool ok = sl * L + gl < BATCH && j < ee;
+                    dst[sl] = ok ? __ldg(colp + j) : 0;
+                    if constexpr (WT) dw[sl] = ok ? __ldg(p.ew + j) : 0.f;
                 }
             };
             // row loads of a batch; slots past the end read row 0 (never accumulated)
-            auto load_data = [&](const int (&ix)[ISL], Raw<VB> (&dst)[LPB]) {
+            auto load_data = [&](const int (&ix)[ISL], const float (&iw)[ISLW], Raw<VB> (&dst)[LPB],
+                                 float (&wd)[LPBW]) {
 #pragma unroll
                 for (int t = 0; t < LPB; ++t) {
                     // edge t*E + e of the batch: held by lane (t*E % L) + e in slot (t*E)/L (E divides L)
-                    const int src = __shfl_sync(gmask, ix[(t * E) / L], gbase + ((t * E) % L) + e);
+                    const int from = gbase + ((t * E) % L) + e;
+                    const int src = __shfl_sync(gmask, ix[(t * E) / L], from);
+                    if constexpr (WT) wd[t] = __shfl_sync(gmask, iw[(t * E) / L], from);
                     dst[t] = ldv<VB>(vbase + (size_t)(uint32_t)src * ld_in);
                 }
             };
             // edge base + t*E + e belongs to group (t*E + e) mod 8, i.e. acc[t % NACC]
-            auto consume = [&](const Raw<VB> (&v)[LPB], int base) {
+            auto consume = [&](const Raw<VB> (&v)[LPB], const float (&wv)[LPBW], int base) {
                 const int rem = ee - base;
+                auto add = [&](int t) {
+                    if constexpr (WT) vfma<T, VB>(acc[t % NACC], v[t], wv[t]);
+                    else vadd<T, VB>(acc[t % NACC], v[t]);
+                };
                 if (rem >= BATCH) {
 #pragma unroll
-                    for (int t = 0; t < LPB; ++t) vadd<T, VB>(acc[t % NACC], v[t]);
+                    for (int t = 0; t < LPB; ++t) add(t);
                 } else {
 #pragma unroll
                     for (int t = 0; t < LPB; ++t)
-                        if (t * E + e < rem) vadd<T, VB>(acc[t % NACC], v[t]);
+                        if (t * E + e < rem) add(t);
                 }
             };
             // two-deep software pipeline, unrolled by 2 so the buffers ping-pong without copies:
             // while batch b is accumulated, batch b+1's rows and batch b+2's indices are in flight
             int ia[ISL], ib[ISL];
+            float wia[ISLW], wib[ISLW], wva[LPBW], wvb[LPBW];
             Raw<VB> va[LPB], vb[LPB];
-            load_idx(eb, ia);
-            if (eb < ee) load_data(ia, va);
-            load_idx(eb + BATCH, ib);
+            load_idx(eb, ia, wia);
+            if (eb < ee) load_data(ia, wia, va, wva);
+            load_idx(eb + BATCH, ib, wib);
             for (int base = eb; base < ee;) {
-                load_idx(base + 2 * BATCH, ia);
-                if (base + BATCH < ee) load_data(ib, vb);
-                consume(va, base);
+                load_idx(base + 2 * BATCH, ia, wia);
+                if (base + BATCH < ee) load_data(ib, wib, vb, wvb);
+                consume(va, wva, base);
                 base += BATCH;
                 if (base >= ee) break;
-                load_idx(base + 2 * BATCH, ib);
-                if (base + BATCH < ee) load_data(ia, va);
-                consume(vb, base);
+                load_idx(base + 2 * BATCH, ib, wib);
+                if (base + BATCH < ee) load_data(ia, wia, va, wva);
+                consume(vb, wvb, base);
                 base += BATCH;
             }
             // fixed butterfly over the 8 reduction groups
@@ -355,7 +385,11 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
             }
             const float sig = (p.mode == 0) ? p.gamma * ra * rb : p.gamma * ra;
             float out[VALS];
-            if (p.alpha != 0.f) {
+            if constexpr (WT) {   // gamma * (sum_u w_uv S_u + w_vv S_v); no alpha mix (the GAT epoch's reading)
+#pragma unroll
+                for (int i = 0; i < VALS; ++i)
+                    out[i] = sig * __fmaf_rn(swr, Vec<T, VB>::elem(self_raw, i), acc[0][i]);
+            } else if (p.alpha != 0.f) {
                 const Raw<VB> s0_raw = ldv<VB>(p.S0 + (int64_t)r * p.ld_s0 + (int64_t)vcol * VB);
                 const float beta = (p.mode == 0) ? p.alpha : p.alpha / rb;
 #pragma unroll
@@ -388,8 +422,9 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
     if (!(rs_e >= e0 && rs_e < e1)) return;            // row r does not start (with edges) in unit u
     constexpr int VALS = 16 / sizeof(T);
     const int row_vals = p.nvec * VALS;
-    const float a = p.rs[r];
-    const float b = p.cs[r];
+    const float a = p.sw ? 1.f : p.rs[r];
+    const float b = p.sw ? 1.f : p.cs[r];
+    const float swr = p.sw ? p.sw[r] : 0.f;
     char* orow_p = out_row_ptr(p, r);
     for (int k = lane; k < row_vals; k += 32) {
         float acc = p.carry[(u * 2 + 1) * (int64_t)row_vals + k];
@@ -401,7 +436,7 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
         float self[VALS];
         load16<T>(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * 16, self);
         const float sig = (p.mode == 0) ? p.gamma * a * b : p.gamma * a;
-        float out = sig * (acc + self[comp]);
+        float out = p.sw ? sig * __fmaf_rn(swr, self[comp], acc) : sig * (acc + self[comp]);
         if (p.alpha != 0.f) {
             float h[VALS];
             load16<T>(p.S0 + (int64_t)r * p.ld_s0 + (int64_t)vcol * 16, h);
@@ -443,19 +478,26 @@ bool carveout_max_l1() {
 }
 
 // 256-thread CTAs, one unit per lane group, the whole unified array as L1 (no shared memory).
-template <typename T, int VB, int E, int L, int MODE>
+template <typename T, int VB, int E, int L, int MODE, bool WT = false>
 void launch_variant(const HopParams& p, cudaStream_t s) {
     static bool attr = false;
     if (!attr && carveout_max_l1()) {
-        NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, VB, E, L, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+        NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, VB, E, L, MODE, WT>,
+                                      cudaFuncAttributePreferredSharedMemoryCarveout, 0));
         attr = true;
     }
-    spmm_hop_kernel<T, VB, E, L, MODE><<<(unsigned)cdiv((p.u_end - p.u_begin) * L, kBlock), kBlock, 0, s>>>(p);
+    spmm_hop_kernel<T, VB, E, L, MODE, WT><<<(unsigned)cdiv((p.u_end - p.u_begin) * L, kBlock), kBlock, 0, s>>>(p);
     NTP_LAUNCH_CHECK();
 }
 
 template <typename T, int VB, int E, int L>
 void launch_hop(const HopParams& p, cudaStream_t s) {
+    if constexpr (VB == 16) {
+        if (p.ew) {   // weighted (GAT attention): general path only
+            launch_variant<T, VB, E, L, 0, true>(p, s);
+            return;
+        }
+    }
     static const int short_env = [] { const char* v = getenv("NTP_SPMM_SHORT"); return v ? atoi(v) : -1; }();
     // low-degree variants when the average degree is below 32 (products, papers shapes)
     const bool low_deg = short_env >= 0 ? short_env != 0 : (p.nnz < 32 * std::max<int64_t>(p.n, 1));
@@ -498,7 +540,7 @@ static void unit_range(const Csr& csr, int64_t row_lo, int64_t row_hi, int64_t& 
 void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, const void* S_in, void* S_out,
               const void* S0, int64_t ld_in, int64_t ld_out, int64_t ld_s0, int32_t cols, ntp_dtype dt,
               float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi, cudaStream_t s,
-              const int32_t* out_rows, const PeerOut* po) {
+              const int32_t* out_rows, const PeerOut* po, const float* ew, const float* sw) {
     const Graph& g = c->g;
     if (row_hi < 0) row_hi = g.n;
     row_lo = std::max<int64_t>(row_lo, 0);
@@ -526,6 +568,8 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     p.peer_out = (po && po->tab) ? po->tab : nullptr;
     p.po_V_p = po ? po->V_p : 0;
     p.po_rank = po ? po->rank : 0;
+    p.ew = ew;
+    p.sw = sw;
 
     unit_range(csr, row_lo, row_hi, p.u_begin, p.u_end);
     p.row_lo = row_lo;
@@ -550,7 +594,7 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
                       (S0 == nullptr || (p.ld_s0 % 32 == 0 && ((uintptr_t)S0 % 32) == 0));
     // rows of 96 / 128 / 256 B (and 32-B bf16 rows on low-degree graphs) measured faster with 32-byte vectors
     const bool auto32 = nvec == 6 || nvec == 8 || nvec == 16 || (nvec == 2 && dt == NTP_BF16 && low_deg_g);
-    if (al32 && (vb_env == 32 || (vb_env < 0 && auto32))) {
+    if (al32 && !ew && (vb_env == 32 || (vb_env < 0 && auto32))) {
         if (dt == NTP_F32) dispatch_hop<float, 32>(p, nvec / 2, s);
         else dispatch_hop<__nv_bfloat16, 32>(p, nvec / 2, s);
     } else {

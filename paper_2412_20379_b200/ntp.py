@@ -37,7 +37,7 @@ EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_u
             "ntp_graph_info", "ntp_copy_csr", "ntp_copy_dinv", "ntp_partition", "ntp_scatter_features",
             "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd",
             "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch", "ntp_train_epoch_coupled",
-            "ntp_stage_inputs", "ntp_set_slices", "ntp_hop_timing"]
+            "ntp_stage_inputs", "ntp_set_slices", "ntp_hop_timing", "ntp_train_epoch_gat"]
 
 
 class ntp_tensor(C.Structure):
@@ -107,6 +107,9 @@ _sig = {
                          C.POINTER(ntp_tensor), C.POINTER(ntp_epoch_report), _vp], C.c_int),
     "ntp_stage_inputs": ([_vp, C.c_int, _vp, _i64, _i32, _i64, _vp, _vp], C.c_int),
     "ntp_set_slices": ([_vp, _i32], C.c_int),
+    "ntp_train_epoch_gat": ([_vp, C.POINTER(ntp_model), C.POINTER(ntp_tensor), _vp, _vp, C.POINTER(ntp_tensor),
+                             C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), _f, C.POINTER(ntp_epoch_report), _vp],
+                            C.c_int),
     "ntp_hop_timing": ([_vp, C.POINTER(C.c_double), C.POINTER(_i32)], C.c_int),
     "ntp_train_epoch_coupled": ([_vp, C.POINTER(ntp_coupled_model), C.POINTER(ntp_tensor), _vp, _vp,
                                  C.POINTER(C.POINTER(ntp_tensor)), C.POINTER(ntp_coupled_report), _vp], C.c_int),
@@ -338,6 +341,25 @@ class Context:
         ldx = X_host.stride(0) if hasattr(X_host, "stride") and callable(X_host.stride) else d_in
         self._chk(_lib.ntp_stage_inputs(self._h, int(slot), _ptr(X_host), rows, d_in, ldx, _ptr(labels_host),
                                         _ptr(mask_host)))
+
+    def _report(self, rep) -> dict:
+        return {"loss": rep.loss, "n_train": rep.n_train, "ms": dict(zip(PHASES, list(rep.ms))),
+                "bytes_sent": list(rep.bytes_sent), "bytes_recv": list(rep.bytes_recv),
+                "collectives": rep.collectives, "kernel_launches": rep.kernel_launches,
+                "spmm_ms": rep.spmm_ms, "spmm_launches": rep.spmm_launches}
+
+    def train_epoch_gat(self, model: dict, X_v, labels_v, mask_v, W0, W1, att, slope: float = 0.2,
+                        stream=None) -> dict:
+        """NEXT-2: one decoupled-GAT epoch (ntp_train_epoch_gat); W0, W1, att [2 x C] updated in place."""
+        m = ntp_model(model["d_in"], model["hid"], model["C"], model["K"], model["gamma"], model.get("alpha", 0.0),
+                      model["lr"], model.get("dtype", NTP_F32), model.get("chunks", 1), model.get("flags", 0))
+        xt = as_ntp_tensor(X_v, NTP_LAYOUT_VERTEX)
+        w0, w1, at = as_ntp_tensor(W0), as_ntp_tensor(W1), as_ntp_tensor(att)
+        rep = ntp_epoch_report()
+        self._chk(_lib.ntp_train_epoch_gat(self._h, C.byref(m), C.byref(xt), _ptr(labels_v), _ptr(mask_v),
+                                           C.byref(w0), C.byref(w1), C.byref(at), float(slope), C.byref(rep),
+                                           _stream_ptr(stream)))
+        return self._report(rep)
 
     def train_epoch(self, model: dict, X_v, labels_v, mask_v, W0, W1, stream=None, host_inputs: bool = False,
                     staged_slot: int | None = None) -> dict:
