@@ -280,6 +280,85 @@ def run_coupled(args, ctx, cfg, X, y, msk, n, nnz, world, rank, local, dist, bar
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ HBM-bound propagation leg
+def hbm_leg(args, world, rank, local, dist, barrier, allmax, peak, peak_src, l2_size):
+    """The Orkut-shaped pipeline of BASELINE configs[3] (3.07M vertices, ~116M arcs, w = 512 fp32, K = 2): this
+    rank's rows -> split -> K hops on its d_s = 512/N column slice -> gather, forward and backward
+    (ntp_propagate_pipeline), timed with CUDA events; the hop kernel's roofline against HBM (the slice is
+    3.07M x d_s x 4 B >= 786 MB at N <= 8, far above L2, so every arc's row slice streams from HBM)."""
+    import torch
+    from paper_2412_20379_b200 import ntp
+    cfg = synth.get_config("orkut")
+    w, K = cfg.d_in, cfg.K
+    uid = None
+    if world > 1:
+        obj = [ntp.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = ntp.Context(device=local, rank=rank, world=world, unique_id=uid)
+    t0 = time.time()
+    ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric,
+                      reorder=True)
+    n, nnz, sym = ctx.graph_info()
+    t_graph = time.time() - t0
+    part = ntp.partition(n, w, world, ntp.NTP_F32)
+    V_p, d_s = part["V_p"], part["d_s"]
+    rows = max(0, min(V_p, n - rank * V_p))
+    Hv = synth.features_device(cfg.seed, n, w, device="cuda", row0=rank * V_p, rows=rows) if rows else None
+    H = torch.zeros(V_p, w, device="cuda")
+    if rows:
+        H[:rows] = Hv
+    del Hv
+    Z = torch.empty_like(H)
+    G = torch.empty_like(H)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ctx.propagate_pipeline(H, Z, K, cfg.gamma, cfg.alpha, transposed=False, stream=stream)
+        a = ctx.hop_timing()
+        ctx.propagate_pipeline(Z, G, K, cfg.gamma, cfg.alpha, transposed=True, stream=stream)
+        b = ctx.hop_timing()
+        return a[0] + b[0], a[1] + b[1]
+
+    for _ in range(2):
+        step()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hop_ms = hops = 0
+    ev0.record(stream)
+    for _ in range(args.leg_steps):
+        a, b = step()
+        hop_ms += a
+        hops += b
+    ev1.record(stream)
+    barrier()
+    ms = allmax(ev0.elapsed_time(ev1) / args.leg_steps)
+    hop_avg = allmax(hop_ms / max(hops, 1))
+    ctx.close()
+    del H, Z, G
+    torch.cuda.empty_cache()
+    bh, bmodel = hop_bytes(n, nnz, d_s, 4, sym, cfg.alpha, l2_size)
+    traffic = load_traffic("orkut", world, "f32")
+    achieved = bh / (hop_avg * 1e-3) / 1e9
+    return {
+        "workload": "Orkut-shaped R-MAT graph (3.07M vertices, ~116M arcs), w = 512 fp32, K = 2: split -> K hops "
+                    "-> gather, forward + backward (ntp_propagate_pipeline); BASELINE configs[3]",
+        "n": n, "nnz": nnz, "w": w, "K": K, "P": world, "d_s": d_s, "graph_setup_s": round(t_graph, 3),
+        "ms_per_step": ms, "value": 2 * K * nnz * w / (ms * 1e-3) / 1e9, "unit": "GE/s",
+        "steps": args.leg_steps,
+        "roofline": {"kernel": "spmm_hop_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "hbm_frac_measured": (traffic / (hop_avg * 1e-3) / 1e9 / peak) if traffic else None,
+                     "algorithmic_bytes_per_launch": bh, "bytes_model": bmodel, "avg_launch_ms": hop_avg,
+                     "launches_timed": hops, "peak_source": peak_src,
+                     "timed_span": "spmm_hop_kernel + its spmm_fixup_kernel, CUDA events on the hop's stream",
+                     "vs_8TBps": achieved / 8000.0,
+                     "note": "no-reuse bytes (SURVEY §8(d) B_hop): every arc's sector-rounded row slice from HBM, plus "
+                             "col_idx, row_ptr, D~^-1/2, self rows and output rows; traffic = ncu dram read+write per "
+                             "launch (profiles/spmm_traffic.json, orkut/P<N>/f32)"},
+    }
+
+
 # ------------------------------------------------------------------ main GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -308,6 +387,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=3)
+    ap.add_argument("--no-hbm-leg", action="store_true", help="skip the HBM-bound Orkut-shaped propagation leg")
+    ap.add_argument("--leg-steps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -456,6 +537,27 @@ def main():
 
     free_b, total_b = torch.cuda.mem_get_info()
     hbm_used_gb = allmax((total_b - free_b) / 1e9)
+    peaks = load_peaks()
+    if peaks and peaks.get("hbm_gbs"):
+        peak, peak_src = peaks["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    l2_size = torch.cuda.get_device_properties(local).L2_cache_size
+    # layout changes timed inside the epoch (CUDA events): bytes handed to NCCL per rank / phase time
+    nvlink = None
+    if world > 1:
+        names = [("v2f_fwd", 0, "pack + all-to-all"), ("f2v_fwd", 1, "all-to-all"), ("v2f_bwd", 2, "all-to-all"),
+                 ("f2v_bwd", 3, "all-to-all + unpack")]
+        nvlink = {}
+        for ph, i, what in names:
+            t_ph = allmax(phase[ph])
+            b = reps[-1]["bytes_sent"][i]
+            nvlink[ph] = {"ms": t_ph, "bytes_sent_per_rank": b, "what": what,
+                          "GBps_per_direction": (b / (t_ph * 1e-3) / 1e9) if t_ph else None,
+                          "frac_of_900GBps": (b / (t_ph * 1e-3) / 1e9 / 900.0) if t_ph else None}
+    leg = None
+    if not args.no_hbm_leg and args.engine == "decoupled" and args.config == "reddit":
+        leg = hbm_leg(args, world, rank, local, dist, barrier, allmax, peak, peak_src, l2_size)
     ms = allmax(ms)
     e2e_ms = allmax(e2e_ms)
     e2e_serial_ms = allmax(e2e_serial_ms)
@@ -467,12 +569,6 @@ def main():
         w = cfg.w
         esz = 2 if dt == ntp.NTP_BF16 else 4
         ge = 2 * cfg.K * nnz * w / (ms * 1e-3) / 1e9
-        peaks = load_peaks()
-        if peaks and peaks.get("hbm_gbs"):
-            peak, peak_src = peaks["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)"
-        else:
-            peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-        l2_size = torch.cuda.get_device_properties(local).L2_cache_size
         bh, bmodel = hop_bytes(n, nnz, d_s, esz, sym, cfg.alpha, l2_size)
         achieved = bh / (spmm_avg * 1e-3) / 1e9
         traffic = load_traffic(args.config, world, dtype_name)
@@ -522,6 +618,8 @@ def main():
                                  "this kernel on this workload (profiles/spmm_traffic.json)"},
             "prop_GE_per_s": 2 * cfg.K * nnz * w / (spmm_ms / len(reps) * 1e-3) / 1e9 * 1.0,
             "phase_ms": {k: round(v, 4) for k, v in phase.items()},
+            "nvlink": nvlink,
+            "hbm_leg": leg,
             "clocks": clk,
             "gpu_launches": int(launches),
             "e2e": None if e2e_ms is None else {

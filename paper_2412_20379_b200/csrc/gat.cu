@@ -388,6 +388,7 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     };
     for (int k = 1; k <= m->K; ++k)
         for (int j = 0; j < vs; ++j) hop(sl(Zst, (int64_t)(k - 1) * vs + j), sl(Zst, (int64_t)k * vs + j), false);
+    NTP_CUDA(record_timing(c, E[10], s));   // fwd hops done
     // a5: gather Z^K into this rank's rows, blocked [P][V_p][d_s]
     c->wire_phase = 1;
     void* ZK = sl(Zst, (int64_t)m->K * vs);
@@ -437,6 +438,7 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
         }
         std::swap(cur, nxt);
     }
+    NTP_CUDA(record_timing(c, E[11], s));   // bwd hops (+ SDDMM) done
     // a9: gather G^0 -> dz rows
     void* gathered_b = cur;
     if (!local) {
@@ -488,17 +490,7 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     if (rep) {
         rep->loss = h_scal[1] > 0 ? h_scal[0] / h_scal[1] : 0.0;
         rep->n_train = (int64_t)h_scal[1];
-        static const int phase_of[9] = {NTP_PH_MLP_FWD, NTP_PH_V2F_FWD, NTP_PH_PROP_FWD, NTP_PH_LOSS, NTP_PH_V2F_BWD,
-                                        NTP_PH_PROP_BWD, NTP_PH_MLP_BWD, NTP_PH_ALLREDUCE, NTP_PH_SGD};
-        for (int i = 0; i < NTP_PH_COUNT; ++i) rep->ms[i] = 0.0;
-        for (int i = 0; i < 9; ++i) {
-            float ms = 0.f;
-            NTP_CUDA(cudaEventElapsedTime(&ms, E[i], E[i + 1]));
-            rep->ms[phase_of[i]] = ms;
-        }
-        float tot = 0.f;
-        NTP_CUDA(cudaEventElapsedTime(&tot, E[0], E[9]));
-        rep->ms[NTP_PH_TOTAL] = tot;
+        epoch_phases(E, rep->ms);
         for (int i = 0; i < 4; ++i) {
             rep->bytes_sent[i] = c->wire_sent[i];
             rep->bytes_recv[i] = c->wire_recv[i];

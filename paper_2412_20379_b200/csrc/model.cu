@@ -231,6 +231,21 @@ inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
 }  // namespace
 
 // ---- epoch building blocks shared with the GAT epoch (gat.cu)
+// Phase times from the epoch's events: E0 start, E1 mlp fwd, E2 v2f, E[10] fwd hops done, E3 f2v, E4 loss,
+// E5 v2f bwd, E[11] bwd hops done, E6 f2v bwd (+ unpack), E7 mlp bwd, E8 allreduce, E9 sgd.
+void epoch_phases(cudaEvent_t* E, double* ms) {
+    struct { int a, b, ph; } tab[] = {{0, 1, NTP_PH_MLP_FWD}, {1, 2, NTP_PH_V2F_FWD}, {2, 10, NTP_PH_PROP_FWD},
+                                      {10, 3, NTP_PH_F2V_FWD}, {3, 4, NTP_PH_LOSS},    {4, 5, NTP_PH_V2F_BWD},
+                                      {5, 11, NTP_PH_PROP_BWD}, {11, 6, NTP_PH_F2V_BWD}, {6, 7, NTP_PH_MLP_BWD},
+                                      {7, 8, NTP_PH_ALLREDUCE}, {8, 9, NTP_PH_SGD},     {0, 9, NTP_PH_TOTAL}};
+    for (int i = 0; i < NTP_PH_COUNT; ++i) ms[i] = 0.0;
+    for (const auto& t : tab) {
+        float x = 0.f;
+        NTP_CUDA(cudaEventElapsedTime(&x, E[t.a], E[t.b]));
+        ms[t.ph] = x;
+    }
+}
+
 void epoch_gemm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, cudaStream_t s, int epi, const float* aux,
                 int64_t ldaux, const float* B_hi, const float* B_lo) {
@@ -282,7 +297,7 @@ void epoch_sgd(ntp_ctx* c, float* W, int64_t n, const float* dW, const double* s
 // sends block (r+s)%P and receives from (r-s)%P, so each step is a permutation and
 // all ranks issue the same NCCL sequence.  Arithmetic is unchanged.
 static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool overlap, int chunks, int64_t V_p,
-                                 int32_t d_s, bool timed, cudaStream_t s) {
+                                 int32_t d_s, bool timed, cudaStream_t s, cudaEvent_t mid = nullptr) {
     const int P = c->world;
     const size_t es = esize(a.dtype);
     const int64_t n = c->g.n;
@@ -291,6 +306,7 @@ static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool
         NTP_CUDA(cudaMemsetAsync(static_cast<char*>(a.Z) + n * a.ld_z * es, 0, (V_pad - n) * a.ld_z * es, s));
     if (!overlap || P == 1) {
         propagate(c, a, s, timed, true);
+        if (mid) NTP_CUDA(record_timing(c, mid, s));   // hops done, the gather follows
         alltoall_blocks(c, a.Z, recv, V_p * d_s, a.dtype, s);
         return;
     }
@@ -306,6 +322,7 @@ static void propagate_and_gather(ntp_ctx* c, const PropArgs& a, void* recv, bool
     }
     LastHop lh;
     propagate(c, ao, s, timed, true, &lh);
+    if (mid) NTP_CUDA(record_timing(c, mid, s));   // overlap: the "gather" phase holds the chunked last hop
     const int64_t csz = cdiv(V_p, std::max(chunks, 1));
     const ncclDataType_t t = a.dtype == NTP_BF16 ? ncclBfloat16 : ncclFloat32;
     char* zf = static_cast<char*>(a.Z);
@@ -635,6 +652,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                 aj.Z = slice_at(c->xfer.p, j);
                 gathered = propagate_consume(c, aj, s, timed, fwd_internal) == aj.H ? c->recv.p : c->xfer.p;
             }
+            NTP_CUDA(record_timing(c, E[10], s));   // one GPU: the gather is the identity
         } else if (vs > 1) {   // every slice in sequence, then one gather
             for (int j = 0; j < vs; ++j) {
                 PropArgs aj = a;
@@ -642,16 +660,19 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                 aj.Z = slice_at(c->xfer.p, j);
                 propagate(c, aj, s, timed, true);
             }
+            NTP_CUDA(record_timing(c, E[10], s));
             exchange_f2v(c, c->xfer.p, c->recv.p, V_p * d_s, dt, s);
         } else if (p2p) {
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
+            NTP_CUDA(record_timing(c, E[10], s));   // stores done by the last hop; the barrier completes them
             p2p_barrier(c, s);
             wire_add(c, p2p_wire, p2p_wire);
         } else if (ovl) {
             propagate(c, a, s, timed, true);     // a5 per chunk below, consumed chunk by chunk by the head
+            NTP_CUDA(record_timing(c, E[10], s));
         } else {
-            propagate_and_gather(c, a, c->recv.p, overlap && !after, m->chunks, V_p, d_s, timed, s);
+            propagate_and_gather(c, a, c->recv.p, overlap && !after, m->chunks, V_p, d_s, timed, s, E[10]);
         }
     }
     std::vector<cudaEvent_t> g_ev;                 // forward gather of row chunk ch done (ovl)
@@ -747,6 +768,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                 aj.Z = slice_at(zb, j);
                 gathered_b = propagate_consume(c, aj, s, timed, bwd_internal) == aj.H ? hb : zb;
             }
+            NTP_CUDA(record_timing(c, E[11], s));
         } else if (vs > 1) {
             for (int j = 0; j < vs; ++j) {
                 PropArgs aj = a;
@@ -754,16 +776,19 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                 aj.Z = slice_at(c->xfer.p, j);
                 propagate(c, aj, s, timed, true);
             }
+            NTP_CUDA(record_timing(c, E[11], s));
             exchange_f2v(c, c->xfer.p, c->send.p, V_p * d_s, dt, s);
         } else if (p2p) {
             a.po = PeerOut{tab_gath, V_p, c->rank};
             propagate(c, a, s, timed, true);
+            NTP_CUDA(record_timing(c, E[11], s));
             p2p_barrier(c, s);
             wire_add(c, p2p_wire, p2p_wire);
         } else if (ovl) {
             propagate(c, a, s, timed, true);     // a9 per chunk below, consumed chunk by chunk by a10
+            NTP_CUDA(record_timing(c, E[11], s));
         } else {
-            propagate_and_gather(c, a, c->send.p, overlap && !after, m->chunks, V_p, d_s, timed, s);
+            propagate_and_gather(c, a, c->send.p, overlap && !after, m->chunks, V_p, d_s, timed, s, E[11]);
         }
     }
     std::vector<cudaEvent_t> b_ev;                 // backward gather of row chunk ch done (ovl)
@@ -1013,14 +1038,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
         rep->n_train = (int64_t)h_scal[1];
         // E0 start, E1 mlp fwd, E2 v2f, E3 prop fwd (+gather), E4 loss, E5 v2f bwd,
         // E6 prop bwd (+gather, unpack), E7 mlp bwd, E8 allreduce, E9 sgd.
-        static const int phase_of[9] = {NTP_PH_MLP_FWD, NTP_PH_V2F_FWD, NTP_PH_PROP_FWD, NTP_PH_LOSS, NTP_PH_V2F_BWD,
-                                        NTP_PH_PROP_BWD, NTP_PH_MLP_BWD, NTP_PH_ALLREDUCE, NTP_PH_SGD};
-        for (int i = 0; i < NTP_PH_COUNT; ++i) rep->ms[i] = 0.0;
-        for (int i = 0; i < 9; ++i) {
-            float ms = 0.f;
-            NTP_CUDA(cudaEventElapsedTime(&ms, E[i], E[i + 1]));
-            rep->ms[phase_of[i]] = ms;
-        }
+        epoch_phases(E, rep->ms);
         float tot = 0.f;
         NTP_CUDA(cudaEventElapsedTime(&tot, E[0], E[9]));
         rep->ms[NTP_PH_TOTAL] = tot;
@@ -1129,6 +1147,7 @@ static void enqueue_epoch_dp(ntp_ctx* c, const ntp_model* m, const float* X, int
     pack_v2f(c, L, ldL, m->C, A + own, V_p, ws, 1, g.dinv_out_orig(), row0, n, NTP_F32, dt, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E2 (no split)
     char* Z = hops(false);
+    NTP_CUDA(record_timing(c, E[10], s));
     NTP_CUDA(record_timing(c, E[ei++], s));   // E3 prop fwd (incl. all-gathers)
     // a6: loss on own rows; gradient rows (pre-scaled by the backward column side) into A's own rows
     char* G = (Z == A) ? B : A;
@@ -1156,6 +1175,7 @@ static void enqueue_epoch_dp(ntp_ctx* c, const ntp_model* m, const float* X, int
     NTP_CUDA(record_timing(c, E[ei++], s));   // E5 (no split)
     if (G != A) NTP_CUDA(cudaMemcpyAsync(A + own, G + own, (size_t)V_p * ws * es, cudaMemcpyDeviceToDevice, s));
     char* dZ = hops(true);
+    NTP_CUDA(record_timing(c, E[11], s));
     unpack_f2v(c, dZ + own, V_p, ws, 1, dL, ldL, m->C, dt, NTP_F32, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E6 prop bwd
     // a10: MLP backward on own rows

@@ -262,6 +262,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
 void drop_epoch_graph(ntp_ctx* c);
 // epoch building blocks (model.cu), shared with the GAT epoch (gat.cu)
+void epoch_phases(cudaEvent_t* E, double* ms);
 void epoch_gemm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, cudaStream_t s, int epi, const float* aux,
                 int64_t ldaux, const float* B_hi, const float* B_lo);

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--bwd", action="store_true")
     ap.add_argument("--reorder", action="store_true")
+    ap.add_argument("--warmup", type=int, default=3, help="untimed calls per width (0 under ncu: one launch each)")
     args = ap.parse_args()
     cfg = synth.get_config(args.config)
     ctx = ntp.Context()
@@ -40,7 +41,7 @@ def main():
         H = torch.randn(n, d, device="cuda").to(tdt)
         Z = torch.empty_like(H)
         f = ctx.propagate_bwd if args.bwd else ctx.propagate_fwd
-        for _ in range(3):
+        for _ in range(args.warmup):
             f(H, Z, args.K, 1.0, 0.0)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
