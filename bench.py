@@ -200,6 +200,49 @@ def oracle_epoch_time(cfg, epochs=1):
     return dt, g.nnz, threads, t_graph, losses, one
 
 
+def oracle_sampled_estimate(cfg, frac=0.01, cols=4):
+    """SURVEY §8(d) c5 oracle timing: the full fp64 state of the papers shape is ~1 TB, so the oracle (as it
+    stands) propagates a `cols`-column subset over a `frac` row sample -- exact per row and column by column
+    separability -- and runs the MLP forward/backward and the loss on the same row sample; the epoch
+    time is EXTRAPOLATED linearly (x 1/frac rows, x w/cols columns, x 2K hops)."""
+    import oracle
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(cfg.n, size=max(1, int(cfg.n * frac)), replace=False)).astype(np.int64)
+    t0 = time.time()
+    nb = oracle.graph.sampled_rows(cfg, rows, False)       # in-arcs of the sample (arc-stream filter)
+    t_filter = time.time() - t0
+    rp = np.zeros(cfg.n + 1, np.int64)
+    deg = np.zeros(cfg.n, np.int64)
+    deg[rows] = [nb[v].size for v in rows.tolist()]
+    np.cumsum(deg, out=rp[1:])
+    col = np.concatenate([nb[v] for v in rows.tolist()]).astype(np.int32)
+    sample_arcs = int(col.size)
+    ones = np.ones(cfg.n)
+    zin = rng.standard_normal((cfg.n, cols))
+    lib = oracle.lib
+    out = np.empty((rows.size, cols))
+    t0 = time.time()
+    lib.oracle_hop_rows(rp.ctypes.data, col.ctypes.data, ones.ctypes.data, ones.ctypes.data, cols, zin.ctypes.data,
+                        None, 1.0, 0.0, rows.ctypes.data, rows.size, out.ctypes.data)
+    t_hop = time.time() - t0
+    del zin, rp, col
+    X, y, m = synth.config_inputs(cfg, 0, rows.size)        # a row sample of the same shape
+    W0, W1 = synth.model_weights(cfg)
+    t0 = time.time()
+    A1 = X.astype(np.float64) @ W0
+    H1 = np.maximum(A1, 0.0)
+    logits = H1 @ W1 if not cfg.w_after_prop else H1 @ W1   # W1 applied after propagation: same GEMM
+    loss_sum, n_train, d = oracle.model.softmax_xent(logits, y, m)
+    dW1 = H1.T @ d
+    dH1 = (d @ W1.T) * (A1 > 0)
+    dW0 = X.T.astype(np.float64) @ dH1
+    t_mlp = time.time() - t0
+    hop_full = t_hop / frac * (cfg.w / cols)
+    epoch = 2 * cfg.K * hop_full + t_mlp / frac
+    return {"epoch_s": epoch, "hop_s": hop_full, "mlp_s": t_mlp / frac, "filter_s": t_filter,
+            "sample_rows": int(rows.size), "sample_arcs": sample_arcs, "cols": cols, "frac": frac}
+
+
 def run_reference(args, cfg, rank):
     if rank != 0:
         return
@@ -222,7 +265,7 @@ def run_reference(args, cfg, rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS.get(args.config, args.config), "n": cfg.n, "nnz": g.nnz, "w": w,
                        "K": cfg.K},
-            "cpu_baseline": {"value": ge, "unit": "GE/s", "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": ge, "unit": "GE/s", "cores": cores, "kind": "oracle", "host": host_info(),
                              "sample": f"{args.steps} full fp64 oracle epochs of the same workload (after "
                                        f"{args.warmup} warm-up), OpenMP rows + numpy BLAS"},
             "e2e": {"value": ge, "unit": "GE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -630,9 +673,15 @@ def main():
                 "serial_value": 2 * cfg.K * nnz * w / (e2e_serial_ms * 1e-3) / 1e9},
         }
         if world == 1 and not args.no_cpu_baseline and cfg.n > 10_000_000:
-            line["cpu_baseline"] = {"value": None, "unit": "GE/s", "cores": os.cpu_count(), "kind": "oracle",
-                                    "sample": "not run: the fp64 oracle's full state for this graph is ~1 TB "
-                                              "(DESIGN.md §10); the default Reddit-shaped bench line carries it"}
+            import oracle
+            est = oracle_sampled_estimate(cfg)
+            line["cpu_baseline"] = {"value": 2 * cfg.K * nnz * w / est["epoch_s"] / 1e9, "unit": "GE/s",
+                                    "cores": oracle.lib.oracle_num_threads(), "kind": "oracle", "extrapolated": True,
+                                    "epoch_s": est["epoch_s"], "host": host_info(), "detail": est,
+                                    "sample": f"EXTRAPOLATED: fp64 oracle hop on {est['cols']} of {cfg.w} columns over a "
+                                              f"{est['frac']:.0%} row sample ({est['sample_arcs']} arcs) plus the MLP "
+                                              f"and loss on a {est['frac']:.0%} row sample, scaled linearly "
+                                              f"(SURVEY §8(d)); the full fp64 state is ~1 TB"}
         elif world == 1 and not args.no_cpu_baseline:
             try:
                 t_cpu, nnz_o, cores, _, o_losses, hop1 = oracle_epoch_time(cfg, args.cpu_epochs)

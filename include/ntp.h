@@ -103,6 +103,18 @@ int         ntp_abi_version(void);
  * with the same P.  NTP_ERR_ARG unless P >= world and P % world == 0.  Default P = world. */
 ntp_status ntp_set_slices(ntp_ctx* ctx, int32_t P);
 
+/* Collective deadline (SURVEY §8(b) "collective failures or timeouts abort the communicator"; the
+ * analogue of SPEC S:407's round timeout).  Every call that waits for collective-bearing work
+ * (ntp_train_epoch*, ntp_sync, ntp_destroy) polls the stream and ncclCommGetAsyncError; an NCCL error
+ * aborts the communicator (ncclCommAbort) and returns NTP_ERR_NCCL, and work still pending after `ms`
+ * milliseconds (e.g. ranks that issued different collective sequences) aborts it and returns
+ * NTP_ERR_TIMEOUT.  After an abort every collective-bearing call returns NTP_ERR_NCCL; destroy the
+ * context.  ms = 0 (default): wait without a deadline (errors are still detected). */
+ntp_status ntp_set_timeout(ntp_ctx* ctx, int64_t ms);
+
+/* Waits for the work enqueued on `s` (e.g. layout changes, pipelines) under the contract above. */
+ntp_status ntp_sync(ntp_ctx* ctx, ntp_stream s);
+
 /* CUDA-event duration (ms, summed) and count of the SpMM hop launches -- each spmm_hop_kernel with its
  * spmm_fixup_kernel -- enqueued by the last ntp_propagate_fwd / _bwd / _pipeline or ntp_train_epoch
  * call; waits for the last of them.  The events are recorded on the stream the hops run on. */

@@ -5,6 +5,8 @@
 #include <cstring>
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <thread>
 #include <memory>
 
 #include "ntp_internal.cuh"
@@ -76,6 +78,46 @@ static void check_tensor(const ntp_tensor* t, const char* name, bool need_vec) {
 
 static void need_graph(const ntp_ctx* c) {
     NTP_CHECK(c->g.loaded, NTP_ERR_STATE, "no graph loaded");
+}
+
+void need_comm(const ntp_ctx* c) {
+    NTP_CHECK(!(c->world > 1 && (c->comm_aborted || !c->comm)), NTP_ERR_NCCL,
+              "the NCCL communicator was aborted after an error or a timeout; destroy this context");
+}
+
+static void abort_comm(ntp_ctx* c) {
+    if (c->comm) ncclCommAbort(c->comm);   // kernels of the aborted communicator return
+    c->comm = nullptr;
+    c->comm_aborted = true;
+    drop_epoch_graph(c);                    // captured epochs hold its kernels
+}
+
+void wait_stream(ntp_ctx* c, cudaStream_t s) {
+    if (!c->comm) {
+        NTP_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) return;
+        if (e != cudaErrorNotReady) NTP_CUDA(e);
+        ncclResult_t ar = ncclSuccess;
+        if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+            abort_comm(c);
+            cudaStreamSynchronize(s);
+            fail(NTP_ERR_NCCL, "NCCL asynchronous error: %s (communicator aborted)", ncclGetErrorString(ar));
+        }
+        const int64_t ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+        if (c->timeout_ms > 0 && ms > c->timeout_ms) {
+            abort_comm(c);
+            cudaStreamSynchronize(s);
+            cudaGetLastError();
+            fail(NTP_ERR_TIMEOUT, "collective work did not complete within %lld ms (communicator aborted)",
+                 (long long)c->timeout_ms);
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
 }
 
 // P = world * vs feature slices: V_pad = P * ceil(n / P); this rank's vertex rows V_pad / world.
@@ -185,8 +227,11 @@ ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint
 void ntp_destroy(ntp_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    if (c->s_comp) cudaStreamSynchronize(c->s_comp);
-    if (c->s_comm) cudaStreamSynchronize(c->s_comm);
+    try {   // a hung collective (and a timeout set) aborts the communicator instead of blocking here
+        if (c->s_comp) wait_stream(c, c->s_comp);
+        if (c->s_comm) wait_stream(c, c->s_comm);
+    } catch (...) {
+    }
     drop_epoch_graph(c);
     p2p_shutdown(c);
     if (c->comm) ncclCommDestroy(c->comm);
@@ -345,12 +390,27 @@ ntp_status ntp_copy_dinv(const ntp_ctx* cc, float* dinv_in, float* dinv_out) {
 
 ntp_status ntp_set_slices(ntp_ctx* c, int32_t P) {
     NTP_API_BEGIN(c)
+    need_comm(c);
     NTP_CHECK(P >= c->world && P % c->world == 0 && P <= 4096, NTP_ERR_ARG,
               "P = %d must be a multiple of world = %d (and <= 4096)", P, c->world);
     NTP_CUDA(cudaSetDevice(c->device));
     NTP_CUDA(cudaStreamSynchronize(c->s_comp));
     drop_epoch_graph(c);
     c->vs = P / c->world;
+    NTP_API_END(c)
+}
+
+ntp_status ntp_set_timeout(ntp_ctx* c, int64_t ms) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(ms >= 0, NTP_ERR_ARG, "timeout must be >= 0 ms");
+    c->timeout_ms = ms;
+    NTP_API_END(c)
+}
+
+ntp_status ntp_sync(ntp_ctx* c, ntp_stream st) {
+    NTP_API_BEGIN(c)
+    NTP_CUDA(cudaSetDevice(c->device));
+    wait_stream(c, (cudaStream_t)st);
     NTP_API_END(c)
 }
 
@@ -424,6 +484,7 @@ ntp_status ntp_scatter_features(ntp_ctx* c, const void* X_host, ntp_dtype dtype,
 
 ntp_status ntp_layout_v2f(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Hf, ntp_stream st) {
     NTP_API_BEGIN(c)
+    need_comm(c);
     need_graph(c);
     check_tensor(Hv, "Hv", false);
     check_tensor(Hf, "Hf", true);
@@ -445,6 +506,7 @@ ntp_status ntp_layout_v2f(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Hf, ntp_
 
 ntp_status ntp_layout_f2v(ntp_ctx* c, const ntp_tensor* Hf, ntp_tensor* Hv, ntp_stream st) {
     NTP_API_BEGIN(c)
+    need_comm(c);
     need_graph(c);
     check_tensor(Hf, "Hf", true);
     check_tensor(Hv, "Hv", false);
@@ -511,6 +573,7 @@ ntp_status ntp_propagate_bwd(ntp_ctx* c, const ntp_tensor* G, ntp_tensor* dH, in
 ntp_status ntp_propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K, float gamma, float alpha,
                                   int transposed, ntp_dtype dt, int32_t chunks, uint32_t flags, ntp_stream st) {
     NTP_API_BEGIN(c)
+    need_comm(c);
     need_graph(c);
     check_tensor(Hv, "Hv", false);
     check_tensor(Zv, "Zv", false);
@@ -549,6 +612,7 @@ ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v
                            const uint8_t* train_mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep,
                            ntp_stream st) {
     NTP_API_BEGIN(c)
+    need_comm(c);
     need_graph(c);
     NTP_CHECK(m && X_v && labels_v && train_mask_v && W0 && W1, NTP_ERR_ARG, "null argument");
     NTP_CHECK(m->d_in > 0 && m->hid > 0 && m->C > 0 && m->K >= 1, NTP_ERR_ARG, "bad model dims / K");
@@ -583,6 +647,7 @@ ntp_status ntp_train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor*
                                const uint8_t* train_mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_tensor* att, float slope,
                                ntp_epoch_report* rep, ntp_stream st) {
     NTP_API_BEGIN(c)
+    need_comm(c);
     need_graph(c);
     NTP_CHECK(m && X_v && labels_v && train_mask_v && W0 && W1 && att, NTP_ERR_ARG, "null argument");
     NTP_CHECK(m->d_in > 0 && m->hid > 0 && m->C > 0 && m->K >= 1, NTP_ERR_ARG, "bad model dims / K");
@@ -620,6 +685,7 @@ ntp_status ntp_train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const
                                    const int32_t* labels_v, const uint8_t* train_mask_v, ntp_tensor* const* W,
                                    ntp_coupled_report* rep, ntp_stream st) {
     NTP_API_BEGIN(c)
+    need_comm(c);
     need_graph(c);
     NTP_CHECK(m && X_v && labels_v && train_mask_v && W, NTP_ERR_ARG, "null argument");
     NTP_CHECK(m->L >= 1 && m->L <= NTP_MAX_LAYERS, NTP_ERR_ARG, "L must be in [1, %d]", NTP_MAX_LAYERS);

@@ -246,7 +246,7 @@ bool p2p_ensure(ntp_ctx* c, size_t sb, size_t gb, cudaStream_t s) {
     c->p2p_bar.ensure(16);
     NTP_CUDA(cudaMemsetAsync(c->p2p_bar.p, 0, 16, s));
     p2p_barrier(c, s);                         // nobody writes into the old windows any more
-    NTP_CUDA(cudaStreamSynchronize(s));
+    wait_stream(c, s);
     p2p_close(c);
     const size_t nsb = std::max(sb, c->p2p_split_bytes), ngb = std::max(gb, c->p2p_gath_bytes);
     c->p2p_split.release();
@@ -265,7 +265,7 @@ bool p2p_ensure(ntp_ctx* c, size_t sb, size_t gb, cudaStream_t s) {
     NTP_NCCL(ncclAllGather(static_cast<char*>(dh.p) + hb * P, dh.p, hb, ncclUint8, c->comm, s));
     std::vector<cudaIpcMemHandle_t> all(2 * P);
     NTP_CUDA(cudaMemcpyAsync(all.data(), dh.p, hb * P, cudaMemcpyDeviceToHost, s));
-    NTP_CUDA(cudaStreamSynchronize(s));
+    wait_stream(c, s);
     c->p2p_peer_split.assign(P, nullptr);
     c->p2p_peer_gath.assign(P, nullptr);
     int ok = 1;
@@ -285,7 +285,7 @@ bool p2p_ensure(ntp_ctx* c, size_t sb, size_t gb, cudaStream_t s) {
     NTP_CUDA(cudaMemcpyAsync(dh.p, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
     NTP_NCCL(ncclAllReduce(dh.p, dh.p, 1, ncclInt32, ncclMin, c->comm, s));
     NTP_CUDA(cudaMemcpyAsync(&ok, dh.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    NTP_CUDA(cudaStreamSynchronize(s));
+    wait_stream(c, s);
     if (!ok) {
         p2p_close(c);
         c->p2p_state = -1;

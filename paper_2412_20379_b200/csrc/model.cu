@@ -1031,7 +1031,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     NTP_CUDA(cudaMemcpyAsync(h_scal, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     NTP_CUDA(cudaEventRecord(c->ev[41], s));
     NTP_CUDA(cudaStreamWaitEvent(user ? user : (cudaStream_t)0, c->ev[41], 0));
-    NTP_CUDA(cudaStreamSynchronize(s));
+    wait_stream(c, s);
 
     if (rep) {
         rep->loss = h_scal[1] > 0 ? h_scal[0] / h_scal[1] : 0.0;
@@ -1374,7 +1374,7 @@ void train_epoch_coupled(ntp_ctx* c, const ntp_coupled_model* m, const ntp_tenso
     NTP_CUDA(cudaMemcpyAsync(h_scal, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     NTP_CUDA(cudaEventRecord(c->ev[41], s));
     NTP_CUDA(cudaStreamWaitEvent(user ? user : (cudaStream_t)0, c->ev[41], 0));
-    NTP_CUDA(cudaStreamSynchronize(s));
+    wait_stream(c, s);
     if (rep) {
         rep->loss = h_scal[1] > 0 ? h_scal[0] / h_scal[1] : 0.0;
         rep->n_train = (int64_t)h_scal[1];

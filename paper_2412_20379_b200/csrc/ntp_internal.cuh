@@ -142,6 +142,8 @@ struct EpochKey {
 struct ntp_ctx {
     int device = 0, rank = 0, world = 1, slice_align = 16;
     int vs = 1;                     // virtual feature slices per rank (ntp_set_slices): P = world * vs
+    int64_t timeout_ms = 0;         // collective deadline of the synchronising calls (ntp_set_timeout), 0 = none
+    bool comm_aborted = false;      // the communicator was aborted after an error or a timeout
     ncclComm_t comm = nullptr;
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
     ntp::Graph g;
@@ -261,6 +263,11 @@ void propagate_pipeline(ntp_ctx* c, const ntp_tensor* Hv, ntp_tensor* Zv, int K,
 void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                  const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_epoch_report* rep, cudaStream_t user);
 void drop_epoch_graph(ntp_ctx* c);
+// Waits for stream s under the collective contract (the analogue of SPEC S:407's round
+// timeout): polls the stream and ncclCommGetAsyncError; on an NCCL error or after c->timeout_ms it aborts
+// the communicator (ncclCommAbort) and fails with NTP_ERR_NCCL / NTP_ERR_TIMEOUT.
+void wait_stream(ntp_ctx* c, cudaStream_t s);
+void need_comm(const ntp_ctx* c);   // NTP_ERR_NCCL once the communicator has been aborted
 // epoch building blocks (model.cu), shared with the GAT epoch (gat.cu)
 void epoch_phases(cudaEvent_t* E, double* ms);
 void epoch_gemm(ntp_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,

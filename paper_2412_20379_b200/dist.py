@@ -10,21 +10,23 @@ from __future__ import annotations
 import numpy as np
 
 
-def rank_rows(n: int, w: int, world: int, rank: int, dtype: int = 0, slice_align: int = 16):
-    """(row0, rows, V_p, d_s) of `rank`: rows [row0, row0+rows) are real vertices; V_p-rows is padding."""
+def rank_rows(n: int, w: int, world: int, rank: int, dtype: int = 0, slice_align: int = 16, slices: int = 0):
+    """(row0, rows, V_p, d_s) of `rank`: rows [row0, row0+rows) are real vertices; V_p-rows is padding.
+    slices = P feature slices (ntp_set_slices; default world): the rank owns V_pad / world rows."""
     from . import ntp
-    part = ntp.partition(n, w, world, dtype, 1, slice_align)
-    V_p = part["V_p"]
+    P = slices or world
+    part = ntp.partition(n, w, P, dtype, 1, slice_align)
+    V_p = part["V_pad"] // world
     row0 = rank * V_p
     rows = max(0, min(V_p, n - row0))
     return row0, rows, V_p, part["d_s"]
 
 
-def rank_inputs(cfg, world: int, rank: int):
+def rank_inputs(cfg, world: int, rank: int, slices: int = 0):
     """This rank's VERTEX-layout inputs (X_v [V_p x d_in] fp32, labels int32, train mask uint8),
     zero-padded beyond n (padding rows are in no mask)."""
     import synth
-    row0, rows, V_p, _ = rank_rows(cfg.n, cfg.w, world, rank)
+    row0, rows, V_p, _ = rank_rows(cfg.n, cfg.w, world, rank, slices=slices)
     X = np.zeros((V_p, cfg.d_in), np.float32)
     y = np.zeros(V_p, np.int32)
     m = np.zeros(V_p, np.uint8)

@@ -37,7 +37,8 @@ EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_u
             "ntp_graph_info", "ntp_copy_csr", "ntp_copy_dinv", "ntp_partition", "ntp_scatter_features",
             "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd",
             "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch", "ntp_train_epoch_coupled",
-            "ntp_stage_inputs", "ntp_set_slices", "ntp_hop_timing", "ntp_train_epoch_gat"]
+            "ntp_stage_inputs", "ntp_set_slices", "ntp_hop_timing", "ntp_train_epoch_gat",
+            "ntp_set_timeout", "ntp_sync"]
 
 
 class ntp_tensor(C.Structure):
@@ -107,6 +108,8 @@ _sig = {
                          C.POINTER(ntp_tensor), C.POINTER(ntp_epoch_report), _vp], C.c_int),
     "ntp_stage_inputs": ([_vp, C.c_int, _vp, _i64, _i32, _i64, _vp, _vp], C.c_int),
     "ntp_set_slices": ([_vp, _i32], C.c_int),
+    "ntp_set_timeout": ([_vp, _i64], C.c_int),
+    "ntp_sync": ([_vp, _vp], C.c_int),
     "ntp_train_epoch_gat": ([_vp, C.POINTER(ntp_model), C.POINTER(ntp_tensor), _vp, _vp, C.POINTER(ntp_tensor),
                              C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), _f, C.POINTER(ntp_epoch_report), _vp],
                             C.c_int),
@@ -193,6 +196,14 @@ class Context:
         """ntp_set_slices: P = world * vs feature slices (vs virtual slices per rank, in sequence)."""
         self._chk(_lib.ntp_set_slices(self._h, int(P)))
         self.slices = int(P)
+
+    def set_timeout(self, ms: int):
+        """ntp_set_timeout: collective deadline of the synchronising calls (0 = none)."""
+        self._chk(_lib.ntp_set_timeout(self._h, int(ms)))
+
+    def sync(self, stream=None):
+        """ntp_sync: wait for the stream's work under the timeout / abort contract."""
+        self._chk(_lib.ntp_sync(self._h, _stream_ptr(stream)))
 
     def hop_timing(self):
         """ntp_hop_timing: (summed ms, launches) of the SpMM hops of the last propagation / epoch call."""

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--widths", required=True)
     ap.add_argument("--elem", type=int, default=4)
     ap.add_argument("--note", default="")
+    ap.add_argument("--outdir", default=os.path.join(ROOT, "profiles"))
     args = ap.parse_args()
     out = subprocess.run(["ncu", "-i", args.rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -52,7 +53,8 @@ def main():
     widths = [int(x) for x in args.widths.split(",")]
     assert len(recs) == len(keys), (len(recs), keys)
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-    tj = os.path.join(ROOT, "profiles", "spmm_traffic.json")
+    os.makedirs(args.outdir, exist_ok=True)
+    tj = os.path.join(args.outdir, "spmm_traffic.json")
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
     lines = [f"# {args.tag}: spmm_hop_kernel, ncu --set full --clock-control none (one launch per slice width)", "",
              args.note, "",
@@ -73,7 +75,7 @@ def main():
     lines.append("")
     lines.append(f"ncu times are cold-cache, serialised replays (compare against bench CUDA-event times for shares "
                  f"only). Measured copy peak {peak} GB/s (MEASURED_PEAKS.json).")
-    open(os.path.join(ROOT, "profiles", args.tag + ".md"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(args.outdir, args.tag + ".md"), "w").write("\n".join(lines) + "\n")
     json.dump(dict(sorted(traffic.items())), open(tj, "w"), indent=1)
     print("\n".join(lines))
 

@@ -9,7 +9,11 @@ Per rank, through the C ABI with the library's own NCCL communicator:
   3. 3 training epochs with the overlap scheduler on and off: losses vs the oracle
      (1e-4), and on == off bitwise (scheduling neutrality, S:533);
   4. the same on a degree-reordered graph (NTP_G_REORDER): slice propagation bitwise vs P = 1,
-     epochs vs the oracle.
+     epochs vs the oracle;
+  5.-7. bf16 / fused head, NEXT-4 data-parallel baseline, NEXT-1 coupled epochs;
+  8. NEXT-2 decoupled GAT epochs vs the GAT oracle (one and two slices per rank);
+  9. virtual slices across ranks (P = 2 * world): layouts and epochs;
+ 10. a mismatched collective times out (NTP_ERR_TIMEOUT) and aborts the communicator.
 """
 import os
 import sys
@@ -131,6 +135,9 @@ def main(name):
             losses.append(rep["loss"])
         for a, b in zip(losses, ref_losses):
             assert abs(a - b) <= 1e-4, f"loss {a} vs oracle {b} (mode={mode})"
+        # bytes handed to the transport per layout change (counted where issued) = the closed form
+        wire = (world - 1) * V_p * oracle.layout.slice_width(cfg.hid if cfg.w_after_prop else cfg.C, world, 4) * 4
+        assert rep["bytes_sent"] == [wire] * 4, f"wire bytes {rep['bytes_sent']} vs {wire} (mode={mode})"
         results.append((losses, W0.cpu(), W1.cpu()))
     for k in (1, 2):
         assert results[0][0] == results[k][0], f"layout mode {k} changed the loss"
@@ -221,6 +228,91 @@ def main(name):
             assert rep["layout_changes"] == coupled.layout_changes(L, world)
             ds = lambda w: oracle.layout.slice_width(w, world, 4)
             assert rep["bytes_sent"] == coupled.layout_bytes(widths, V_p, ds, world, 4)
+    # ---- 8. NEXT-2: decoupled GAT (score halves all-gathered, coefficients recomputed per rank, dalpha
+    # allreduced): losses and every parameter vs the GAT oracle; then with 2 virtual slices per rank
+    if not cfg.w_after_prop:
+        from oracle import gat
+        a0 = synth.glorot(cfg.seed, 2, cfg.C, 7_000_000)
+        gmodel = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=2, gamma=0.9, alpha=0.0, lr=lr, dtype=ntp.NTP_F32,
+                      chunks=1, flags=0)
+        rl, rW0, rW1, ras, rad = gat.train(g, *synth.config_inputs(cfg), W0h, W1h, a0[0], a0[1], 2, 0.9, lr, 2)
+        for vsl in (1, 2):
+            ctxg = ntp.Context(device=local, rank=rank, world=world, unique_id=pd.broadcast_unique_id(dist, rank))
+            ctxg.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric)
+            ctxg.set_slices(world * vsl)
+            Xg, yg, mg = pd.rank_inputs(cfg, world, rank, slices=world * vsl)
+            W0, W1, A = (torch.from_numpy(a).cuda() for a in (W0h, W1h, a0))
+            for e in range(2):
+                rep = ctxg.train_epoch_gat(gmodel, *(torch.from_numpy(a).cuda() for a in (Xg, yg, mg)), W0, W1, A)
+                assert abs(rep["loss"] - rl[e]) <= 1e-4, f"GAT loss {rep['loss']} vs {rl[e]} (vs={vsl})"
+            for got, ref in ((W0, rW0), (W1, rW1), (A, np.stack([ras, rad]))):
+                got = got.cpu().numpy()
+                assert np.abs(got - ref).max() <= 1e-4 * max(1.0, np.abs(ref).max()), f"GAT weights (vs={vsl})"
+            ctxg.close()
+
+    # ---- 9. virtual slices across ranks (P = 2 * world: two slices per GPU, per-(peer, slice) exchanges):
+    # layouts round trip, epochs vs the oracle
+    ctxv = ntp.Context(device=local, rank=rank, world=world, unique_id=pd.broadcast_unique_id(dist, rank))
+    ctxv.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric)
+    Pv = 2 * world
+    ctxv.set_slices(Pv)
+    partv = oracle.layout.partition(n, 37, Pv, 4)
+    Vr = partv["V_pad"] // world
+    Xfull = synth.features(99, n, 37)
+    Hv_ = np.zeros((Vr, 37), np.float32)
+    lo_, hi_ = rank * Vr, min(n, (rank + 1) * Vr)
+    Hv_[:max(0, hi_ - lo_)] = Xfull[lo_:hi_]
+    Hv_t = torch.from_numpy(Hv_).cuda()
+    Hf = torch.empty(2 * partv["V_pad"], partv["d_s"], device="cuda")
+    ctxv.layout_v2f(Hv_t, Hf)
+    for j in range(2):   # slice j of this rank = global slice rank*2 + j of the matrix
+        q = rank * 2 + j
+        ref = np.zeros((partv["V_pad"], partv["d_s"]), np.float32)
+        c0, c1 = q * partv["d_s"], min(37, (q + 1) * partv["d_s"])
+        if c1 > c0:
+            ref[:n, :c1 - c0] = Xfull[:, c0:c1]
+        torch.cuda.synchronize()
+        assert np.array_equal(Hf[j * partv["V_pad"]:(j + 1) * partv["V_pad"]].cpu().numpy(), ref), f"virtual v2f {rank}/{j}"
+    back = torch.zeros_like(Hv_t)
+    ctxv.layout_f2v(Hf, back)
+    ctxv.sync()
+    assert torch.equal(back, Hv_t), "virtual f2v(v2f(x)) != x"
+    Xv_, yv_, mv_ = pd.rank_inputs(cfg, world, rank, slices=Pv)
+    W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+    model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
+                 dtype=ntp.NTP_F32, chunks=1, flags=ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0)
+    for e in range(3):
+        rep = ctxv.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (Xv_, yv_, mv_)), W0, W1)
+        assert abs(rep["loss"] - ref_losses[e]) <= 1e-4, f"virtual-slice loss {rep['loss']} vs {ref_losses[e]}"
+    ctxv.close()
+
+    # ---- 10. collective timeout: rank 0 issues a layout change the other ranks never join;
+    # its synchronising call must abort the communicator and return NTP_ERR_TIMEOUT, not hang
+    ctxt = ntp.Context(device=local, rank=rank, world=world, unique_id=pd.broadcast_unique_id(dist, rank))
+    ctxt.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric)
+    ctxt.set_timeout(3000)
+    dist.barrier()
+    if rank == 0:
+        part1 = oracle.layout.partition(n, 37, world, 4)
+        Hv1 = torch.zeros(part1["V_p"], 37, device="cuda")
+        Hf1 = torch.empty(part1["V_pad"], part1["d_s"], device="cuda")
+        ctxt.layout_v2f(Hv1, Hf1)
+        import time as _t
+        t0 = _t.time()
+        try:
+            ctxt.sync()
+            raise AssertionError("mismatched collective did not time out")
+        except ntp.NtpError as ex:
+            assert ex.status == ntp.NTP_ERR_TIMEOUT, f"expected NTP_ERR_TIMEOUT, got {ex}"
+        assert _t.time() - t0 < 60, "timeout took too long"
+        try:   # the aborted communicator refuses further collectives
+            ctxt.layout_v2f(Hv1, Hf1)
+            raise AssertionError("collective accepted after abort")
+        except ntp.NtpError as ex:
+            assert ex.status == ntp.NTP_ERR_NCCL
+    dist.barrier()
+    ctxt.close()
+
     dist.barrier()
     if rank == 0:
         print(f"MP OK world={world} config={name} losses={results[1][0]}", flush=True)
