@@ -46,6 +46,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, ui
         : "memory");
 }
 
+// 1-D bulk copy global -> shared (cp.async.bulk, no tensor map): `bytes` (multiple of 16, 16-byte aligned
+// addresses) land at dst, completion counted on `bar` (complete_tx).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // TMA gather4: rows r0..r3 (box width = tensor map box dim 0, starting at column c0) of a 2-D
 // tensor land back to back in shared memory.  Rows outside the tensor are zero-filled.
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int r0, int r1,

@@ -408,6 +408,156 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
 #endif
 }
 
+// Wide rows (>= 1 KB of slice per vertex, e.g. the Orkut c4 pipeline at N <= 2).  The register-staged
+// gather above keeps what the register file allows in flight (ncu, Orkut w = 512 fp32: 22% warps active,
+// DRAM 59% of the copy peak, L2 28%).  Here a producer warp streams every arc's whole row slice into a
+// shared-memory ring with cp.async.bulk -- nothing in flight occupies registers; completion is counted on
+// one mbarrier per stage of A arcs -- and NW = row bytes / 512 consumer warps each own a 512-byte column
+// chunk (one 16-byte vector per lane).  Arc j of a row accumulates into group (j - eb) mod 8 in ascending
+// order and the 8 groups are reduced by the same butterfly ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)): every
+// column is summed exactly as in spmm_hop_kernel, so the two kernels give bitwise equal results and the
+// slice-width (P) invariance holds across them.  One CTA per merge-path unit, all rows (no row range).
+template <typename T, int NW, int A, int S>
+__global__ void __launch_bounds__(32 * (NW + 1)) spmm_hop_bulk_kernel(const HopParams p) {
+    extern __shared__ __align__(1024) uint8_t bulk_smem[];
+    constexpr int RB = NW * 512;
+    constexpr int VALS = Vec<T, 16>::N;
+    uint64_t* full = reinterpret_cast<uint64_t*>(bulk_smem + (size_t)S * A * RB);
+    uint64_t* empty = full + S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u = p.u_begin + blockIdx.x;
+    if (u >= p.u_end) return;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], NW);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    const int r0 = p.unit_row[u], r1 = p.unit_row[u + 1];
+    const int e0 = p.unit_e[u], e1 = p.unit_e[u + 1];
+    const int total = e1 - e0;                     // the unit's arcs, consumed in CSR order
+    if (warp == NW) {                              // ---- producer
+        const int nst = (total + A - 1) / A;
+        for (int st = 0; st < nst; ++st) {
+            const int stage = st % S;
+            const int cnt = min(A, total - st * A);
+            const int j = e0 + st * A + lane;
+            const int src = lane < cnt ? __ldg(p.col + j) : 0;
+            if (lane == 0) {
+                if (st >= S) ptx::mbar_wait(&empty[stage], ((st / S) - 1) & 1);
+                ptx::mbar_expect_tx(&full[stage], (uint32_t)cnt * RB);
+            }
+            __syncwarp();
+            if (lane < cnt)
+                ptx::bulk_load(bulk_smem + ((size_t)stage * A + lane) * RB, p.S_in + (size_t)(uint32_t)src * p.ld_in, RB,
+                               &full[stage]);
+        }
+        return;
+    }
+    // ---- consumers: warp w owns 16-byte vector vcol = 32 w + lane of every row slice
+    const int vcol = warp * 32 + lane;
+    const bool has_tail = (r1 < p.n) && (e1 > max(p.rp[r1], e0));
+    const int r_end = has_tail ? r1 + 1 : r1;
+    const int row_vals = p.nvec * VALS;
+    int k = 0;                                     // arcs consumed so far
+    for (int r = r0; r < r_end; ++r) {
+        const int rs_e = p.rp[r], re_e = p.rp[r + 1];
+        const int eb = max(rs_e, e0), ee = min(re_e, e1);
+        const bool head = (r == r0) && (rs_e < e0);
+        const bool tail = (r == r1);
+        const bool fin = !(head || tail);
+        Raw<16> self_raw = zero_raw<16>();
+        float ra = 0.f, rb = 0.f;
+        if (fin) {
+            self_raw = ldv<16>(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * 16);
+            ra = __ldg(p.rs + r);
+            rb = __ldg(p.cs + r);
+        }
+        float acc[kG][VALS];
+#pragma unroll
+        for (int g = 0; g < kG; ++g)
+#pragma unroll
+            for (int i = 0; i < VALS; ++i) acc[g][i] = 0.f;
+        for (int jb = eb; jb < ee; jb += kG) {   // arc jb + g belongs to group g (static register index)
+#pragma unroll
+            for (int g = 0; g < kG; ++g) {
+                if (jb + g >= ee) break;
+                const int st = k / A, stage = st % S, slot = k - st * A;
+                if (slot == 0) ptx::mbar_wait(&full[stage], (st / S) & 1);
+                const uint4 x =
+                    *reinterpret_cast<const uint4*>(bulk_smem + ((size_t)stage * A + slot) * RB + vcol * 16);
+                const Raw<16> xr{{x.x, x.y, x.z, x.w}};
+                vadd<T, 16>(acc[g], xr);
+                if (slot == A - 1 || k == total - 1) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+                }
+                ++k;
+            }
+        }
+        // fixed butterfly over the 8 reduction groups (in-lane; the E = 1 form of spmm_hop_kernel)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const int kb = 1 << b;
+#pragma unroll
+            for (int g = 0; g < kG; ++g)
+                if ((g & kb) == 0 && (g | kb) < kG) {
+#pragma unroll
+                    for (int i = 0; i < VALS; ++i) acc[g][i] += acc[g | kb][i];
+                }
+        }
+        if (head || tail) {
+            float* dst = p.carry + ((u * 2 + (head ? 0 : 1)) * (int64_t)row_vals) + vcol * VALS;
+#pragma unroll
+            for (int i = 0; i < VALS; ++i) dst[i] = acc[0][i];
+            continue;
+        }
+        const float sig = (p.mode == 0) ? p.gamma * ra * rb : p.gamma * ra;
+        float out[VALS];
+        if (p.alpha != 0.f) {
+            const Raw<16> s0_raw = ldv<16>(p.S0 + (int64_t)r * p.ld_s0 + (int64_t)vcol * 16);
+            const float beta = (p.mode == 0) ? p.alpha : p.alpha / rb;
+#pragma unroll
+            for (int i = 0; i < VALS; ++i)
+                out[i] = sig * (acc[0][i] + (0.f + Vec<T, 16>::elem(self_raw, i))) +
+                         beta * (0.f + Vec<T, 16>::elem(s0_raw, i));
+        } else {
+#pragma unroll
+            for (int i = 0; i < VALS; ++i) out[i] = sig * (acc[0][i] + (0.f + Vec<T, 16>::elem(self_raw, i)));
+        }
+        stv<16>(out_row_ptr(p, r) + (int64_t)vcol * 16, Vec<T, 16>::pack(out));
+    }
+#ifndef NTP_NO_P2P_FENCE
+    if (p.peer_out) __threadfence_system();
+#endif
+}
+
+constexpr int kBulkA = 4, kBulkS = 4;   // arcs per stage, stages in flight per unit
+constexpr int64_t kBulkMinBytes = 1024;  // auto: rows of >= 1 KB take the bulk-copy gather
+
+template <typename T, int NW, int A, int S>
+void launch_bulk_as(const HopParams& p, cudaStream_t s) {
+    constexpr size_t smem = (size_t)S * A * NW * 512 + 2 * S * sizeof(uint64_t);
+    static bool attr = false;
+    if (!attr) {
+        NTP_CUDA(cudaFuncSetAttribute(spmm_hop_bulk_kernel<T, NW, A, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        attr = true;
+    }
+    spmm_hop_bulk_kernel<T, NW, A, S><<<(unsigned)(p.u_end - p.u_begin), 32 * (NW + 1), smem, s>>>(p);
+    NTP_LAUNCH_CHECK();
+}
+
+template <typename T, int NW>
+void launch_bulk(const HopParams& p, cudaStream_t s) {
+    // ring shape measured on the Orkut shape (ms per hop at 4 KB / 2 KB / 1 KB rows): 4 arcs x 4 stages
+    // 61.2 / 28.6 / 15.1; 8 x 3: 65.8 / 31.3 / 15.3; 2 x 8: 63.3 / 30.7 / 16.4; 4 x 6: 66.9 / 32.1 / 16.0;
+    // 2 x 4: 65.1 / 30.5 / 16.1 (register-staged kernel: 81.6 / 38.5 / 18.5; at 512 B rows 9.13 vs 9.49 bulk)
+    launch_bulk_as<T, NW, kBulkA, kBulkS>(p, s);
+}
+
 // Fix-up: one warp per unit that STARTS a split row (its tail).  Sums tail[u],
 // head[u+1], ..., head[u_last] in unit order, then applies the epilogue.
 template <typename T>
@@ -594,7 +744,26 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
                       (S0 == nullptr || (p.ld_s0 % 32 == 0 && ((uintptr_t)S0 % 32) == 0));
     // rows of 96 / 128 / 256 B (and 32-B bf16 rows on low-degree graphs) measured faster with 32-byte vectors
     const bool auto32 = nvec == 6 || nvec == 8 || nvec == 16 || (nvec == 2 && dt == NTP_BF16 && low_deg_g);
-    if (al32 && !ew && (vb_env == 32 || (vb_env < 0 && auto32))) {
+    // wide rows over the whole graph: the bulk-copy gather (NTP_SPMM_BULK: -1 auto, 0 off, 1 any multiple of 512 B)
+    static const int bulk_env = [] { const char* v = getenv("NTP_SPMM_BULK"); return v ? atoi(v) : -1; }();
+    const int64_t row_bytes = (int64_t)nvec * 16;
+    const bool bulk_ok = !ew && row_lo == 0 && row_hi == g.n &&
+                         (row_bytes == 512 || row_bytes == 1024 || row_bytes == 2048 || row_bytes == 4096) &&
+                         (uintptr_t)S_in % 16 == 0 && p.ld_in % 16 == 0;
+    if (bulk_ok && (bulk_env == 1 || (bulk_env < 0 && row_bytes >= kBulkMinBytes))) {
+        const int nw = (int)(row_bytes / 512);
+        if (dt == NTP_F32) {
+            if (nw == 1) launch_bulk<float, 1>(p, s);
+            else if (nw == 2) launch_bulk<float, 2>(p, s);
+            else if (nw == 4) launch_bulk<float, 4>(p, s);
+            else launch_bulk<float, 8>(p, s);
+        } else {
+            if (nw == 1) launch_bulk<__nv_bfloat16, 1>(p, s);
+            else if (nw == 2) launch_bulk<__nv_bfloat16, 2>(p, s);
+            else if (nw == 4) launch_bulk<__nv_bfloat16, 4>(p, s);
+            else launch_bulk<__nv_bfloat16, 8>(p, s);
+        }
+    } else if (al32 && !ew && (vb_env == 32 || (vb_env < 0 && auto32))) {
         if (dt == NTP_F32) dispatch_hop<float, 32>(p, nvec / 2, s);
         else dispatch_hop<__nv_bfloat16, 32>(p, nvec / 2, s);
     } else {
