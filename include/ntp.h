@@ -250,6 +250,13 @@ ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const flo
                                    full width after an all-gather of the state before every hop,
                                    instead of feature slices (same function; load follows the rows'
                                    degrees).  W1 before propagation, NCCL, no NTP_G_REORDER */
+#define NTP_M_HOST_STREAM  64u  /* memory-efficient scheduling (NEXT-3): X_v is a HOST pointer (pinned
+                                   for asynchronous copies, row pitch X_v->ld) that stays in host memory;
+                                   every vertex-row chunk of it is copied into a 2-slot device ring on
+                                   the copy stream right before the MLP forward / dW0 kernels that read
+                                   it (the copy of chunk ch+1 overlaps chunk ch).  Labels and mask stay
+                                   device pointers.  W1 after propagation only; eager (no epoch graph).
+                                   Frees the V_p x d_in fp32 input from HBM (fp32 papers shape at P = 1) */
 #define NTP_M_P2P_LAYOUTS   8u  /* P > 1: peer-direct layout changes instead of the NCCL block
                                    all-to-all: the producers (pack, last-hop epilogue, loss
                                    kernel) store into the owners' CUDA-IPC windows over

@@ -206,6 +206,8 @@ ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint
         for (int i = 0; i < 2; ++i) {
             NTP_CUDA(cudaEventCreateWithFlags(&c->st_ready[i], cudaEventDisableTiming));
             NTP_CUDA(cudaEventCreateWithFlags(&c->st_free[i], cudaEventDisableTiming));
+            NTP_CUDA(cudaEventCreateWithFlags(&c->hs_ready[i], cudaEventDisableTiming));
+            NTP_CUDA(cudaEventCreateWithFlags(&c->hs_free[i], cudaEventDisableTiming));
         }
         for (auto& e : c->ev) NTP_CUDA(cudaEventCreate(&e));
         for (auto& e : c->ov_ev) NTP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -245,6 +247,8 @@ void ntp_destroy(ntp_ctx* c) {
     for (int i = 0; i < 2; ++i) {
         if (c->st_ready[i]) cudaEventDestroy(c->st_ready[i]);
         if (c->st_free[i]) cudaEventDestroy(c->st_free[i]);
+        if (c->hs_ready[i]) cudaEventDestroy(c->hs_ready[i]);
+        if (c->hs_free[i]) cudaEventDestroy(c->hs_free[i]);
     }
     if (c->s_comp) cudaStreamDestroy(c->s_comp);
     if (c->s_comm) cudaStreamDestroy(c->s_comm);
@@ -633,6 +637,9 @@ ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v
                   "staging slot %d holds no inputs of shape [%lld x %d] (ntp_stage_inputs first)", slot, (long long)V_p,
                   m->d_in);
     }
+    if (m->flags & NTP_M_HOST_STREAM)
+        NTP_CHECK((m->flags & NTP_M_W1_AFTER_PROP) && !(m->flags & (NTP_M_STAGED | NTP_M_HOST_INPUTS | NTP_M_DATA_PARALLEL)),
+                  NTP_ERR_CONFIG, "NTP_M_HOST_STREAM: W1-after-propagation epochs with device labels/mask only");
     if ((m->flags & NTP_M_OVERLAP) && (m->flags & NTP_M_W1_AFTER_PROP) && c->world > 1) {
         const int64_t nch = cdiv(V_p, epoch_row_chunk(m, V_p));   // 4 layout changes x 2 events per row chunk
         NTP_CHECK(8 * nch <= kOvEvents, NTP_ERR_CONFIG, "too many overlap chunks (%lld > %d)", (long long)nch,

@@ -433,6 +433,8 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         ldx = ldXp;
         lab = c->m_lab.as<int32_t>();
         msk = c->m_mask.as<uint8_t>();
+    } else if (m->flags & NTP_M_HOST_STREAM) {
+        // X stays in host memory: the row-chunk loops below stream it through c->hs_ring
     } else if ((ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(X) % 16) != 0) {
         c->m_Xs.ensure((size_t)V_p * ldXp * sizeof(float));
         NTP_CUDA(cudaMemcpy2DAsync(c->m_Xs.p, ldXp * sizeof(float), X, ldx * sizeof(float), m->d_in * sizeof(float),
@@ -492,6 +494,37 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     const bool local = (c->world == 1);
     const int64_t hc = epoch_row_chunk(m, V_p);
     const int64_t nch = cdiv(V_p, hc);
+    // NTP_M_HOST_STREAM (memory-efficient scheduling: inputs stay in host memory): every row chunk of
+    // X is copied into one slot of a 2-slot device ring on the copy stream right before the kernel that reads
+    // it; the copy of chunk ch+1 waits only for the slot's previous reader (chunk ch-1), so it runs under the
+    // GEMM of chunk ch.  X_v is read twice per epoch (MLP forward, dW0).
+    const bool hstream = (m->flags & NTP_M_HOST_STREAM) != 0;
+    if (hstream) c->hs_ring.ensure((size_t)2 * hc * ldXp * sizeof(float) + 16);
+    int hs_next = 0;
+    auto x_rows = [&](int64_t r, int64_t h, int& slot) -> const float* {
+        if (!hstream) {
+            slot = -1;
+            return X + r * ldx;
+        }
+        slot = hs_next;
+        hs_next ^= 1;
+        float* dst = c->hs_ring.as<float>() + (size_t)slot * hc * ldXp;
+        if (c->hs_used[slot]) NTP_CUDA(cudaStreamWaitEvent(c->s_copy, c->hs_free[slot], 0));
+        if (ldx == ldXp)
+            NTP_CUDA(cudaMemcpyAsync(dst, X + r * ldx, (size_t)h * ldx * sizeof(float), cudaMemcpyHostToDevice, c->s_copy));
+        else
+            NTP_CUDA(cudaMemcpy2DAsync(dst, ldXp * sizeof(float), X + r * ldx, ldx * sizeof(float), m->d_in * sizeof(float),
+                                       h, cudaMemcpyHostToDevice, c->s_copy));
+        NTP_CUDA(cudaEventRecord(c->hs_ready[slot], c->s_copy));
+        NTP_CUDA(cudaStreamWaitEvent(s, c->hs_ready[slot], 0));
+        return dst;
+    };
+    auto x_done = [&](int slot) {
+        if (slot < 0) return;
+        NTP_CUDA(cudaEventRecord(c->hs_free[slot], s));
+        c->hs_used[slot] = true;
+    };
+    const int64_t ldxc = hstream ? ldXp : ldx;      // row pitch of a chunk as the kernels see it
     const int32_t nwb = (m->hid + 31) / 32;          // mask words per row
     const int64_t rowsH = after ? hc : V_p;
     c->m_H1.ensure((size_t)rowsH * ldH * sizeof(float));
@@ -605,17 +638,19 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                                (int64_t)P * d_s == m->hid && m->hid % 32 == 0 && d_s % 8 == 0 && !p2p;
         for (int64_t r = 0; r < V_p; r += hc) {      // H1 chunk -> pre-scaled slice rows + ReLU' bits
             const int64_t h = std::min(hc, V_p - r);
+            int slot;
+            const float* Xc = x_rows(r, h, slot);
             if (fuse_pack) {
                 const PackEpi pk{static_cast<__nv_bfloat16*>(split_dst), V_p, d_s, g.dinv_out_orig(), row0, n, bits,
                                  nwb, r, perm_local};
                 fwd_internal = perm_local != nullptr;
-                gemm_tf32x3_pack(c, h, m->hid, m->d_in, X + r * ldx, ldx, W0s.hi, W0s.lo, ldw0, pk, s);
+                gemm_tf32x3_pack(c, h, m->hid, m->d_in, Xc, ldxc, W0s.hi, W0s.lo, ldw0, pk, s);
             } else {
-                mlp_gemm(c, false, false, h, m->hid, m->d_in, X + r * ldx, ldx, W0g, ldw0, H1, ldH, s, 1, nullptr, 0,
-                         W0s);
+                mlp_gemm(c, false, false, h, m->hid, m->d_in, Xc, ldxc, W0g, ldw0, H1, ldH, s, 1, nullptr, 0, W0s);
                 pack_v2f(c, H1, ldH, w, split_dst, V_p, d_s, P, g.dinv_out_orig(), row0, n, NTP_F32, dt, s, tab_split,
                          h, r, bits, nwb);
             }
+            x_done(slot);
             if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);   // a3 of chunk ch under a2 of ch+1
         }
         if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, last, 0));
@@ -806,12 +841,15 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
             if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, b_ev[ch], 0));
-            if (wgrad_fused_supported(P, d_s, m->d_in, m->hid, dt)) {   // unpack + dW0 GEMM in one kernel
+            if (!hstream && wgrad_fused_supported(P, d_s, m->d_in, m->hid, dt)) {   // unpack + dW0 GEMM in one kernel
                 wgrad_fused(c, X, ldx, V_p, m->d_in, gathered_b, d_s, P, m->hid, bits, nwb, r, r + h, dw0_at(ch), s);
                 continue;
             }
             unpack_f2v(c, gathered_b, V_p, d_s, P, dH1, ldH, w, dt, NTP_F32, s, nullptr, 0, h, r, bits, nwb);
-            mlp_gemm(c, true, false, m->d_in, m->hid, h, X + r * ldx, ldx, dH1, ldH, dw0_at(ch), m->hid, s);
+            int slot;
+            const float* Xc = x_rows(r, h, slot);
+            mlp_gemm(c, true, false, m->d_in, m->hid, h, Xc, ldxc, dH1, ldH, dw0_at(ch), m->hid, s);
+            x_done(slot);
         }
         if (nch > 1) {
             sum_chunks_kernel<<<eblocks(n_w), 256, 0, s>>>(c->m_dWp.as<float>(), nch, n_w, dW0);
@@ -977,13 +1015,14 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     int64_t epoch_launches = 0;
     // A captured graph bakes in every scratch pointer: it is replayed only while no library buffer has been
     // (re)allocated or freed since its capture (alloc_generation), whatever entry point moved it.
-    if (graphs_enabled() && gvalid && gkey == key && ggen == alloc_generation()) {
+    const bool capturable = graphs_enabled() && !(m->flags & NTP_M_HOST_STREAM);   // host-streamed epochs run eagerly
+    if (capturable && gvalid && gkey == key && ggen == alloc_generation()) {
         NTP_CUDA(cudaGraphLaunch(gexec, s));
         c->hop_ev_used = ghops;
         epoch_launches = glaunches;
         for (int i = 0; i < 4; ++i) c->wire_sent[i] = gwire[i], c->wire_recv[i] = gwire[4 + i];
         if (staged) c->st_free_rec[sl] = true;
-    } else if (graphs_enabled() && gwarm && gkey == key) {
+    } else if (capturable && gwarm && gkey == key) {
         if (gexec) cudaGraphExecDestroy(gexec);
         gexec = nullptr;
         gvalid = false;
@@ -1021,6 +1060,10 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
             NTP_CUDA(cudaGraphLaunch(gexec, s));
         }
     } else {
+        // a different key (or capture disabled): this entry's recording no longer matches it
+        if (gexec) cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+        gvalid = false;
         enqueue_epoch(c, m, X_v, labels_v, mask_v, W0, W1, timed);
         epoch_launches = c->launches - launches0;
         gwarm = true;

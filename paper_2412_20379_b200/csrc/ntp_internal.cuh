@@ -160,6 +160,10 @@ struct ntp_ctx {
     ntp::DevBuf st_X[2], st_raw[2], st_y[2], st_m[2];
     cudaStream_t s_copy = nullptr;
     cudaEvent_t st_ready[2] = {}, st_free[2] = {};
+    // NTP_M_HOST_STREAM: X_v stays in (pinned) host memory; row chunks stream through a 2-slot device ring
+    ntp::DevBuf hs_ring;
+    cudaEvent_t hs_ready[2] = {}, hs_free[2] = {};
+    bool hs_used[2] = {false, false};
     bool st_free_rec[2] = {false, false};
     int64_t st_rows[2] = {0, 0}, st_ld[2] = {0, 0};
     int32_t st_d_in[2] = {0, 0};

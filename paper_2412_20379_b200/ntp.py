@@ -28,7 +28,7 @@ NTP_F32, NTP_BF16 = 0, 1
 NTP_LAYOUT_VERTEX, NTP_LAYOUT_FEATURE = 0, 1
 NTP_G_SYMMETRIC, NTP_G_VALIDATE, NTP_G_REORDER = 1, 2, 4
 NTP_M_W1_AFTER_PROP, NTP_M_OVERLAP, NTP_M_HOST_INPUTS, NTP_M_P2P_LAYOUTS = 1, 2, 4, 8
-NTP_M_STAGED, NTP_M_SLOT_SHIFT, NTP_M_DATA_PARALLEL = 16, 8, 32
+NTP_M_STAGED, NTP_M_SLOT_SHIFT, NTP_M_DATA_PARALLEL, NTP_M_HOST_STREAM = 16, 8, 32, 64
 PHASES = ["mlp_fwd", "v2f_fwd", "prop_fwd", "f2v_fwd", "loss", "v2f_bwd", "prop_bwd", "f2v_bwd",
           "mlp_bwd", "allreduce", "sgd", "total"]
 
@@ -373,8 +373,9 @@ class Context:
         return self._report(rep)
 
     def train_epoch(self, model: dict, X_v, labels_v, mask_v, W0, W1, stream=None, host_inputs: bool = False,
-                    staged_slot: int | None = None) -> dict:
-        flags = model.get("flags", 0) | (NTP_M_HOST_INPUTS if host_inputs else 0)
+                    staged_slot: int | None = None, host_stream: bool = False) -> dict:
+        flags = (model.get("flags", 0) | (NTP_M_HOST_INPUTS if host_inputs else 0)
+                 | (NTP_M_HOST_STREAM if host_stream else 0))
         if staged_slot is not None:   # inputs from ntp_stage_inputs slot (X_v gives the shape only)
             flags |= NTP_M_STAGED | (int(staged_slot) << NTP_M_SLOT_SHIFT)
         m = ntp_model(model["d_in"], model["hid"], model["C"], model["K"], model["gamma"], model["alpha"],

@@ -262,3 +262,38 @@ def test_epoch_head_bf16_reordered(name):
     for got, r, init in ((W0d.cpu().numpy(), rW0, W0i), (W1d.cpu().numpy(), rW1, W1i)):
         d_ref, d_got = r - init, got.astype(np.float64) - init
         assert np.linalg.norm(d_got - d_ref) <= 2e-2 * np.linalg.norm(d_ref)
+
+
+def test_epoch_graph_cache_key_switch_and_scratch_growth():
+    """Captured epoch graphs (ntp_train_epoch) are replayed only for the same key AND while no library buffer
+    moved since the capture: switching models on one context, and growing shared scratch through other entry
+    points (a wide propagation, a large GEMM) between epochs, must give the losses of fresh contexts."""
+    from paper_2412_20379_b200 import ntp
+    name = "small_dir"
+    cfg = synth.get_config(name)
+    X, y, m = (torch.from_numpy(a).cuda() for a in synth.config_inputs(cfg))
+    W0h, W1h = synth.model_weights(cfg)
+
+    def model(dtype):
+        return dict(_model(cfg, dtype), lr=0.0)   # lr = 0: every epoch of a model has the same loss
+
+    def fresh(dtype):
+        ctx = ntp_ctx_for(name)
+        loss = ctx.train_epoch(model(dtype), X, y, m, torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda())["loss"]
+        ctx.close()
+        return loss
+
+    ref = {0: fresh(0), ntp.NTP_BF16: fresh(ntp.NTP_BF16)}
+    ctx = ntp_ctx_for(name)
+    W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+    for dtype in (0, ntp.NTP_BF16, 0):
+        for _ in range(3):   # eager, captured, replayed
+            assert ctx.train_epoch(model(dtype), X, y, m, W0, W1)["loss"] == ref[dtype]
+    # scratch growth through other entry points between captured epochs
+    H = torch.randn(cfg.n, 512, device="cuda")
+    ctx.propagate_fwd(H, torch.empty_like(H), 2)
+    A = torch.randn(4096, 20000, device="cuda")
+    ctx.gemm(A, torch.randn(20000, 64, device="cuda"), torch.empty(4096, 64, device="cuda"))
+    for _ in range(3):
+        assert ctx.train_epoch(model(0), X, y, m, W0, W1)["loss"] == ref[0]
+    ctx.close()
