@@ -112,6 +112,10 @@ ntp_status ntp_set_slices(ntp_ctx* ctx, int32_t P);
  * context.  ms = 0 (default): wait without a deadline (errors are still detected). */
 ntp_status ntp_set_timeout(ntp_ctx* ctx, int64_t ms);
 
+/* Aborts this rank's communicator now (e.g. after a peer reported NTP_ERR_TIMEOUT), so that no call --
+ * including ntp_destroy -- waits for peers any more.  Afterwards as above. */
+ntp_status ntp_abort(ntp_ctx* ctx);
+
 /* Waits for the work enqueued on `s` (e.g. layout changes, pipelines) under the contract above. */
 ntp_status ntp_sync(ntp_ctx* ctx, ntp_stream s);
 

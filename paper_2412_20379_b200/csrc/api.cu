@@ -411,6 +411,13 @@ ntp_status ntp_set_timeout(ntp_ctx* c, int64_t ms) {
     NTP_API_END(c)
 }
 
+ntp_status ntp_abort(ntp_ctx* c) {
+    NTP_API_BEGIN(c)
+    NTP_CUDA(cudaSetDevice(c->device));
+    abort_comm(c);
+    NTP_API_END(c)
+}
+
 ntp_status ntp_sync(ntp_ctx* c, ntp_stream st) {
     NTP_API_BEGIN(c)
     NTP_CUDA(cudaSetDevice(c->device));

@@ -38,7 +38,7 @@ EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_u
             "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd",
             "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch", "ntp_train_epoch_coupled",
             "ntp_stage_inputs", "ntp_set_slices", "ntp_hop_timing", "ntp_train_epoch_gat",
-            "ntp_set_timeout", "ntp_sync"]
+            "ntp_set_timeout", "ntp_sync", "ntp_abort"]
 
 
 class ntp_tensor(C.Structure):
@@ -110,6 +110,7 @@ _sig = {
     "ntp_set_slices": ([_vp, _i32], C.c_int),
     "ntp_set_timeout": ([_vp, _i64], C.c_int),
     "ntp_sync": ([_vp, _vp], C.c_int),
+    "ntp_abort": ([_vp], C.c_int),
     "ntp_train_epoch_gat": ([_vp, C.POINTER(ntp_model), C.POINTER(ntp_tensor), _vp, _vp, C.POINTER(ntp_tensor),
                              C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), _f, C.POINTER(ntp_epoch_report), _vp],
                             C.c_int),
@@ -200,6 +201,10 @@ class Context:
     def set_timeout(self, ms: int):
         """ntp_set_timeout: collective deadline of the synchronising calls (0 = none)."""
         self._chk(_lib.ntp_set_timeout(self._h, int(ms)))
+
+    def abort(self):
+        """ntp_abort: abort this rank's communicator (no further waits on peers)."""
+        self._chk(_lib.ntp_abort(self._h))
 
     def sync(self, stream=None):
         """ntp_sync: wait for the stream's work under the timeout / abort contract."""

@@ -32,6 +32,10 @@ from paper_2412_20379_b200 import ntp  # noqa: E402
 from paper_2412_20379_b200 import dist as pd  # noqa: E402
 
 
+def _step(k, rank):
+    print(f"[mp_check rank {rank}] step {k}", flush=True)
+
+
 def main(name):
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -44,6 +48,7 @@ def main(name):
     g = oracle.graph.graph_from_config(cfg)
     n = g.n
 
+    _step('1', rank)
     # ---- 1. layouts
     for dt, tdt, eb in ((ntp.NTP_F32, torch.float32, 4), (ntp.NTP_BF16, torch.bfloat16, 2)):
         w = 37
@@ -60,6 +65,7 @@ def main(name):
         torch.cuda.synchronize()
         assert torch.equal(back, Xv), f"f2v(v2f(x)) != x rank {rank}"
 
+    _step('2', rank)
     # ---- 2. propagation of this rank's slice
     w = 41
     part = oracle.layout.partition(n, w, world, 4)
@@ -91,6 +97,7 @@ def main(name):
         torch.cuda.synchronize()
         assert torch.equal(Z1[:, rank * d_s:(rank + 1) * d_s], Zt[:n]), f"P-invariance rank {rank}"
 
+    _step('2b', rank)
     # ---- 2b. vertex-layout pipeline (split -> K hops -> gather), overlap off / on: vs the oracle
     # on this rank's rows, and bitwise equal to each other
     wv = 37
@@ -114,6 +121,7 @@ def main(name):
             outs.append(Zv.cpu())
         assert torch.equal(outs[-2], outs[-1]), f"pipeline overlap changed bits rank {rank} T={transposed}"
 
+    _step('3', rank)
     # ---- 3. epochs, overlap off / on
     X, y, m = pd.rank_inputs(cfg, world, rank)
     W0h, W1h = synth.model_weights(cfg)
@@ -143,6 +151,7 @@ def main(name):
         assert results[0][0] == results[k][0], f"layout mode {k} changed the loss"
         assert torch.equal(results[0][1], results[k][1]) and torch.equal(results[0][2], results[k][2])
 
+    _step('4', rank)
     # ---- 4. degree-reordered graph (NTP_G_REORDER): slice propagation bitwise vs P = 1 on the same
     # reordered graph, epochs vs the oracle
     uid2 = pd.broadcast_unique_id(dist, rank)
@@ -168,6 +177,7 @@ def main(name):
     ctxr.close()
     ctxr1.close()
 
+    _step('5', rank)
     # ---- 5. bf16 storage epochs (the fused tcgen05 head where P*d_s = 128, e.g. head_dir): losses vs
     # the oracle within 2e-2 relative; peer-direct and NCCL layouts bitwise equal
     bres = []
@@ -199,6 +209,7 @@ def main(name):
             assert abs(rep["loss"] - ref_losses[e]) <= 2e-2 * abs(ref_losses[e]), f"reordered overlap loss {rep['loss']}"
         ctxo.close()
 
+    _step('7', rank)
     # ---- 7. NEXT-4: the data-parallel baseline (full-width rows, all-gather before every hop) trains the
     # same model: losses vs the oracle (fp32 1e-4, bf16 2e-2), traffic = 2K all-gathers of full rows
     if not cfg.w_after_prop:
@@ -213,6 +224,7 @@ def main(name):
             eb = 4 if dtype == ntp.NTP_F32 else 2
             assert rep["bytes_sent"][0] == 2 * cfg.K * (world - 1) * V_p * oracle.layout.slice_width(cfg.C, 1, eb) * eb
 
+    _step('6', rank)
     # ---- 6. NEXT-1: naive (coupled) TP epochs, 2 and 3 layers: losses vs the coupled oracle, and the
     # communication ledger: 4L - 2 layout changes moving the closed-form bytes
     from oracle import coupled
@@ -228,6 +240,7 @@ def main(name):
             assert rep["layout_changes"] == coupled.layout_changes(L, world)
             ds = lambda w: oracle.layout.slice_width(w, world, 4)
             assert rep["bytes_sent"] == coupled.layout_bytes(widths, V_p, ds, world, 4)
+    _step('8', rank)
     # ---- 8. NEXT-2: decoupled GAT (score halves all-gathered, coefficients recomputed per rank, dalpha
     # allreduced): losses and every parameter vs the GAT oracle; then with 2 virtual slices per rank
     if not cfg.w_after_prop:
@@ -250,6 +263,7 @@ def main(name):
                 assert np.abs(got - ref).max() <= 1e-4 * max(1.0, np.abs(ref).max()), f"GAT weights (vs={vsl})"
             ctxg.close()
 
+    _step('9', rank)
     # ---- 9. virtual slices across ranks (P = 2 * world: two slices per GPU, per-(peer, slice) exchanges):
     # layouts round trip, epochs vs the oracle
     ctxv = ntp.Context(device=local, rank=rank, world=world, unique_id=pd.broadcast_unique_id(dist, rank))
@@ -286,16 +300,19 @@ def main(name):
         assert abs(rep["loss"] - ref_losses[e]) <= 1e-4, f"virtual-slice loss {rep['loss']} vs {ref_losses[e]}"
     ctxv.close()
 
+    _step('10', rank)
     # ---- 10. collective timeout: rank 0 issues a layout change the other ranks never join;
     # its synchronising call must abort the communicator and return NTP_ERR_TIMEOUT, not hang
     ctxt = ntp.Context(device=local, rank=rank, world=world, unique_id=pd.broadcast_unique_id(dist, rank))
     ctxt.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, thr, cfg.seed, cfg.symmetric)
     ctxt.set_timeout(3000)
+    part1 = oracle.layout.partition(n, 37, world, 4)
+    Hv1 = torch.zeros(part1["V_p"], 37, device="cuda")
+    Hf1 = torch.empty(part1["V_pad"], part1["d_s"], device="cuda")
+    ctxt.layout_v2f(Hv1, Hf1)   # a matched exchange first: NCCL connects peers lazily, inside the enqueueing call
+    ctxt.sync()
     dist.barrier()
     if rank == 0:
-        part1 = oracle.layout.partition(n, 37, world, 4)
-        Hv1 = torch.zeros(part1["V_p"], 37, device="cuda")
-        Hf1 = torch.empty(part1["V_pad"], part1["d_s"], device="cuda")
         ctxt.layout_v2f(Hv1, Hf1)
         import time as _t
         t0 = _t.time()
@@ -311,6 +328,8 @@ def main(name):
         except ntp.NtpError as ex:
             assert ex.status == ntp.NTP_ERR_NCCL
     dist.barrier()
+    if rank != 0:
+        ctxt.abort()   # the peer gave up: leave without waiting for it
     ctxt.close()
 
     dist.barrier()
