@@ -431,6 +431,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=3)
     ap.add_argument("--no-hbm-leg", action="store_true", help="skip the HBM-bound Orkut-shaped propagation leg")
+    ap.add_argument("--host-stream", action="store_true",
+                    help="NEXT-3: keep X_v in pinned host memory and stream its row chunks (NTP_M_HOST_STREAM; "
+                         "W1-after-propagation configs, e.g. --config papers --dtype f32)")
     ap.add_argument("--leg-steps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -487,6 +490,13 @@ def main():
         # the same formulas evaluated on the device (synth.config_inputs_device, pinned bitwise against
         # the numpy version in tests/test_synth.py): papers-scale inputs in seconds instead of minutes
         synth.config_inputs_device(cfg, row0, rows, device="cuda", out=(X, y, msk))
+    if args.host_stream:   # NEXT-3: the inputs live in pinned host memory; HBM holds only row chunks of them
+        Xp = torch.zeros(V_p, ldx, dtype=torch.float32).pin_memory()[:, :cfg.d_in]
+        Xp.copy_(X)
+        del X
+        torch.cuda.empty_cache()
+        X = Xp
+        args.no_e2e = True
     Xh = yh = mh = None
     if not args.no_e2e:
         Xh, yh, mh = X.cpu().contiguous().numpy(), y.cpu().numpy(), msk.cpu().numpy()
@@ -518,7 +528,7 @@ def main():
     # ---- warm-up (the first epochs start from the same weights as the oracle leg: parity check below)
     warm_losses = []
     for _ in range(args.warmup):
-        warm_losses.append(ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream)["loss"])
+        warm_losses.append(ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream, host_stream=args.host_stream)["loss"])
     # ---- timed (device events on the caller's stream; the library orders its streams after it)
     clocks = ClockSampler(local)
     clocks.start()
@@ -527,7 +537,7 @@ def main():
     reps = []
     ev0.record(stream)
     for _ in range(args.steps):
-        reps.append(ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream))
+        reps.append(ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream, host_stream=args.host_stream))
     ev1.record(stream)
     barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -634,6 +644,8 @@ def main():
             "config": {"workload": WORKLOADS.get(args.config, args.config), "n": n, "nnz": nnz, "w": w, "K": cfg.K,
                        "gamma": cfg.gamma, "alpha": cfg.alpha, "P": world, "d_s": d_s, "V_p": V_p,
                        "chunks": args.chunks, "overlap": bool(args.overlap),
+                       "inputs": "pinned host memory, streamed per row chunk (NTP_M_HOST_STREAM)" if args.host_stream
+                                 else "device-resident",
                        "vertex_order": "degree-ordered internally (NTP_G_REORDER)" if reorder else "R-MAT ids",
                        "layouts": ("peer-direct IPC stores" if args.layouts == "p2p" and not args.overlap
                                    else "NCCL all-to-all") if world > 1 else "local",
@@ -665,6 +677,7 @@ def main():
             "hbm_leg": leg,
             "clocks": clk,
             "gpu_launches": int(launches),
+            "losses": {"warmup": warm_losses, "timed_last": reps[-1]["loss"]},
             "e2e": None if e2e_ms is None else {
                 "value": 2 * cfg.K * nnz * w / (e2e_ms * 1e-3) / 1e9, "unit": "GE/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,

@@ -18,7 +18,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, out_q):
+def _worker(rank, world, port, name, out_q, slices=0):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -29,7 +29,7 @@ def _worker(rank, world, port, name, out_q):
         import synth
         from paper_2412_20379_b200 import dist as pd
         cfg = synth.get_config(name)
-        X, y, m = pd.rank_inputs(cfg, world, rank)
+        X, y, m = pd.rank_inputs(cfg, world, rank, slices=slices)
         parts = [None] * world
         dist.all_gather_object(parts, (X, y, m))
         # id broadcast through the same object channel the bench uses (library not needed)
@@ -43,8 +43,10 @@ def _worker(rank, world, port, name, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["tiny_dir", "cora"])
-def test_rank_inputs_tile_the_graph(name):
+@pytest.mark.parametrize("name,slices", [("tiny_dir", 0), ("cora", 0), ("tiny_dir", 6), ("cora", 8)])
+def test_rank_inputs_tile_the_graph(name, slices):
+    """Per-rank vertex rows tile [0, n) exactly, for P = world and for virtual slices (P = slices, P % world
+    == 0: each rank owns V_pad / world = (P / world) * ceil(n / P) rows)."""
     import synth
     from paper_2412_20379_b200 import build
     build.build(verbose=False)
@@ -52,7 +54,7 @@ def test_rank_inputs_tile_the_graph(name):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, slices)) for r in range(world)]
     for p in procs:
         p.start()
     parts, uid, mx = q.get(timeout=120)
@@ -65,7 +67,8 @@ def test_rank_inputs_tile_the_graph(name):
     m = np.concatenate([p[2] for p in parts])
     Xf, yf, mf = synth.config_inputs(cfg)
     n = cfg.n
-    assert X.shape[0] == 2 * -(-n // 2)
+    P = slices or world
+    assert X.shape[0] == P * -(-n // P)
     assert np.array_equal(X[:n], Xf) and np.array_equal(y[:n], yf) and np.array_equal(m[:n], mf)
     assert not X[n:].any() and not m[n:].any()
     assert uid == bytes(range(128))
