@@ -10,7 +10,7 @@ if [ "$1" == "--bench" ]; then
   python bench.py --steps 5 --warmup 3 > gpurun_out/bench_r02.log 2>&1; echo bench=$?
   tail -1 gpurun_out/bench_r02.log | cut -c1-3000
 fi
-NCU="ncu --set full --clock-control none -k regex:spmm_hop_kernel"
+NCU="ncu --set full --clock-control none -k regex:spmm_hop"
 SB="python scripts/spmm_bench.py --K 1 --reps 1 --warmup 0"
 SUM="python scripts/profile_hops.py --outdir gpurun_out/prof"
 run() {   # tag, keys, widths, elem, spmm_bench args...

@@ -38,7 +38,7 @@ def main():
     hdr, units = rows[0], rows[1]
     recs = []
     for r in rows[2:]:
-        if "spmm_hop_kernel" not in r[hdr.index("Kernel Name")]:
+        if "spmm_hop" not in r[hdr.index("Kernel Name")]:
             continue
         d = {}
         for w in WANT:
