@@ -272,6 +272,46 @@ def run_reference(args, cfg, rank):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ NEXT-2: decoupled GAT engine
+def run_gat(args, ctx, cfg, X, y, msk, n, nnz, world, rank, dist, barrier, stream, dt, dtype_name, V_p):
+    """Times ntp_train_epoch_gat on the config's graph (w = C propagated, K hops with the precomputed attention)."""
+    import torch
+    W0h, W1h = synth.model_weights(cfg)
+    W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+    A = torch.from_numpy(synth.glorot(cfg.seed, 2, cfg.C, 7_000_000)).cuda()
+    model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=0.0, lr=cfg.lr, dtype=dt,
+                 chunks=1, flags=0)
+    for _ in range(args.warmup):
+        ctx.train_epoch_gat(model, X, y, msk, W0, W1, A, stream=stream)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        reps.append(ctx.train_epoch_gat(model, X, y, msk, W0, W1, A, stream=stream))
+    ev1.record(stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    hop = sum(r["spmm_ms"] for r in reps) / max(1, sum(r["spmm_launches"] for r in reps))
+    if dist is not None:
+        t = torch.tensor([ms, hop], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, hop = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+    w = cfg.C
+    line = {"metric": METRIC, "engine": "decoupled GAT (NEXT-2): attention precomputed once per epoch, weighted hops",
+            "value": 2 * cfg.K * nnz * w / (ms * 1e-3) / 1e9, "unit": "GE/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": dtype_name, "data": "synthetic", "epoch_s": ms / 1e3,
+            "config": {"workload": WORKLOADS.get(args.config, args.config) + "; decoupled GAT (w = C)", "n": n,
+                       "nnz": nnz, "w": w, "K": cfg.K, "gamma": cfg.gamma, "P": world},
+            "hop_ms": hop, "loss": reps[-1]["loss"],
+            "phase_ms": {k: round(sum(r["ms"][k] for r in reps) / len(reps), 4) for k in reps[0]["ms"]},
+            "gpu_launches": int(sum(r["kernel_launches"] for r in reps))}
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ NEXT-1: coupled (naive TP) engine
 def run_coupled(args, ctx, cfg, X, y, msk, n, nnz, world, rank, local, dist, barrier, stream, dt, dtype_name, V_p,
                 reorder):
@@ -429,10 +469,12 @@ def main():
                     help="NTP_G_REORDER (internal degree-class numbering). auto: on when the vertex table is "
                          "far larger than L2 (n >= 1M: products, orkut, papers), off for the L2-resident Reddit "
                          "shape where it measured slower (DESIGN.md §5); never with --overlap")
-    ap.add_argument("--engine", default="decoupled", choices=["decoupled", "coupled", "dp"],
+    ap.add_argument("--engine", default="decoupled", choices=["decoupled", "coupled", "dp", "gat"],
                     help="coupled: NEXT-1, the naive tensor-parallel 2-layer GCN (d_in -> hid -> C) with its "
                          "communication ledger, the paper's TP-vs-DTP ablation (P:696, P:1125-1128); dp: NEXT-4, the "
-                         "data-parallel baseline (full-width rows, all-gather before each hop; load imbalance)")
+                         "data-parallel baseline (full-width rows, all-gather before each hop; load imbalance); gat: "
+                         "NEXT-2, the decoupled GAT epoch (attention precomputed once, weighted hops, W1 before "
+                         "propagation, alpha = 0)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=3)
@@ -472,7 +514,7 @@ def main():
     t0 = time.time()
     # the last-hop chunked gather of --overlap needs original ids; the W1-after-propagation epoch overlaps its
     # layout changes by row chunk instead and keeps the reorder
-    reorder = args.engine != "dp" and (args.reorder == "on" or (args.reorder == "auto" and cfg.n >= 1_000_000)) and \
+    reorder = args.engine not in ("dp", "gat") and (args.reorder == "on" or (args.reorder == "auto" and cfg.n >= 1_000_000)) and \
         (not args.overlap or cfg.w_after_prop)
     ctx.generate_rmat(cfg.n, cfg.scale, cfg.m_raw, synth.rmat_thresholds(*cfg.abc), cfg.seed, cfg.symmetric,
                       reorder=reorder)
@@ -522,6 +564,13 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    if args.engine == "gat":
+        run_gat(args, ctx, cfg, X, y, msk, n, nnz, world, rank, dist, barrier, stream, dt, dtype_name, V_p)
+        ctx.close()
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     if args.engine == "coupled":
         run_coupled(args, ctx, cfg, X, y, msk, n, nnz, world, rank, local, dist, barrier, stream, dt, dtype_name,
                     V_p, reorder)
