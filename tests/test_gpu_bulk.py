@@ -33,10 +33,11 @@ np.save(out, Z.float().cpu().numpy())
 """
 
 
-def _run(tmp_path, bulk, name, d, dt, tr, K, reorder=False):
-    out = str(tmp_path / f"z_{bulk}_{name}_{d}_{dt}_{int(tr)}_{K}_{int(reorder)}.npy")
+def _run(tmp_path, bulk, name, d, dt, tr, K, reorder=False, var="NTP_SPMM_BULK"):
+    out = str(tmp_path / f"z_{var}_{bulk}_{name}_{d}_{dt}_{int(tr)}_{K}_{int(reorder)}.npy")
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"), args=(name, d, dt, tr, K, reorder, out))
-    env = dict(os.environ, NTP_SPMM_BULK=str(bulk))
+    env = dict(os.environ)
+    env[var] = str(bulk)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     return np.load(out)
