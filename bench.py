@@ -702,7 +702,9 @@ def main():
                        "inputs": "pinned host memory, streamed per row chunk (NTP_M_HOST_STREAM)" if args.host_stream
                                  else "device-resident",
                        "vertex_order": "degree-ordered internally (NTP_G_REORDER)" if reorder else "R-MAT ids",
-                       "layouts": ("peer-direct IPC stores" if args.layouts == "p2p" and not args.overlap
+                       "layouts": ("copy-engine peer copies per row chunk (overlapped)"
+                                   if args.layouts == "p2p" and args.overlap and cfg.w_after_prop
+                                   else "peer-direct IPC stores" if args.layouts == "p2p" and not args.overlap
                                    else "NCCL all-to-all") if world > 1 else "local",
                        "l2": f"inputs larger than L2 (col_idx {4 * nnz / 1e6:.0f} MB streamed per hop; "
                              f"X_v {x_bytes / 1e6:.0f} MB per rank)",

@@ -265,7 +265,12 @@ ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const flo
                                    all-to-all: the producers (pack, last-hop epilogue, loss
                                    kernel) store into the owners' CUDA-IPC windows over
                                    NVLink and a barrier replaces each exchange; same bits.
-                                   Opt-in: measured no faster than NCCL */
+                                   Opt-in: measured no faster than NCCL.
+                                   With NTP_M_OVERLAP and NTP_M_W1_AFTER_PROP: the row-chunked
+                                   overlap schedule with copy-engine transfers -- one
+                                   cudaMemcpyAsync per peer and chunk into the owner's window,
+                                   then a fenced flag write into its inbox that the consumer
+                                   waits on (cuStreamWriteValue32 / cuStreamWaitValue32); eager */
 
 typedef struct {
     int32_t   d_in, hid, C, K;

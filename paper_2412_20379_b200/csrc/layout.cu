@@ -13,6 +13,9 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ntp_internal.cuh"
 
 namespace ntp {
@@ -252,9 +255,9 @@ bool p2p_ensure(ntp_ctx* c, size_t sb, size_t gb, cudaStream_t s) {
     c->p2p_split.release();
     c->p2p_gath.release();
     c->p2p_split.ensure(nsb);
-    c->p2p_gath.ensure(ngb);
+    c->p2p_gath.ensure(ngb + kCeFlagBytes);                  // + the copy-engine layout flags (inbox)
     NTP_CUDA(cudaMemsetAsync(c->p2p_split.p, 0, nsb, s));   // padding rows are never written
-    NTP_CUDA(cudaMemsetAsync(c->p2p_gath.p, 0, ngb, s));
+    NTP_CUDA(cudaMemsetAsync(c->p2p_gath.p, 0, ngb + kCeFlagBytes, s));
     cudaIpcMemHandle_t own[2];
     NTP_CUDA(cudaIpcGetMemHandle(&own[0], c->p2p_split.p));
     NTP_CUDA(cudaIpcGetMemHandle(&own[1], c->p2p_gath.p));
@@ -304,6 +307,47 @@ bool p2p_ensure(ntp_ctx* c, size_t sb, size_t gb, cudaStream_t s) {
     c->p2p_used_gb = gb;
     c->p2p_state = 1;
     return true;
+}
+
+uint32_t* ce_flags(ntp_ctx* c, int q) {
+    return reinterpret_cast<uint32_t*>(static_cast<char*>(c->p2p_peer_gath[q]) + c->p2p_gath_bytes);
+}
+
+namespace {
+PFN_cuStreamWriteValue32_v8000 write_u32_fn() {
+    static PFN_cuStreamWriteValue32_v8000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        return (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                   ? reinterpret_cast<PFN_cuStreamWriteValue32_v8000>(f)
+                   : nullptr;
+    }();
+    NTP_CHECK(fn != nullptr, NTP_ERR_CUDA, "cuStreamWriteValue32 not available");
+    return fn;
+}
+PFN_cuStreamWaitValue32_v8000 wait_u32_fn() {
+    static PFN_cuStreamWaitValue32_v8000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        return (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                   ? reinterpret_cast<PFN_cuStreamWaitValue32_v8000>(f)
+                   : nullptr;
+    }();
+    NTP_CHECK(fn != nullptr, NTP_ERR_CUDA, "cuStreamWaitValue32 not available");
+    return fn;
+}
+}  // namespace
+
+void stream_write_u32(cudaStream_t s, void* addr, uint32_t v) {
+    const CUresult r = write_u32_fn()((CUstream)s, (CUdeviceptr)(uintptr_t)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT);
+    NTP_CHECK(r == CUDA_SUCCESS, NTP_ERR_CUDA, "cuStreamWriteValue32 failed: %d", (int)r);
+}
+
+void stream_wait_u32_geq(cudaStream_t s, void* addr, uint32_t v) {
+    const CUresult r = wait_u32_fn()((CUstream)s, (CUdeviceptr)(uintptr_t)addr, v, CU_STREAM_WAIT_VALUE_GEQ);
+    NTP_CHECK(r == CUDA_SUCCESS, NTP_ERR_CUDA, "cuStreamWaitValue32 failed: %d", (int)r);
 }
 
 // Block exchange: block q of `send` goes to rank q and lands as block `rank` of

@@ -560,6 +560,14 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     const bool overlap = (m->flags & NTP_M_OVERLAP) != 0;
     const size_t win = (size_t)feat_elems * es;
     const bool p2p = !local && !overlap && (m->flags & NTP_M_P2P_LAYOUTS) && p2p_ensure(c, win, win, s);
+    // copy-engine layout changes (a12 with NTP_M_OVERLAP | NTP_M_P2P_LAYOUTS, W1 after propagation): every
+    // row chunk of every layout change is one cudaMemcpyAsync per peer straight into the owner's IPC window on
+    // the comm stream -- copy engines over NVLink, no SMs -- followed by a flag write into the owner's inbox
+    // (cuStreamWriteValue32, fenced); consumers wait on their inbox (cuStreamWaitValue32).  Eager epochs only.
+    const bool ce = !local && overlap && after && (m->flags & NTP_M_P2P_LAYOUTS) && vs == 1 && !c->capturing &&
+                    nch <= kCeChunks && c->world <= kCeRanks && p2p_ensure(c, win, win, s);
+    if (ce) ++c->ce_seq;
+    const uint32_t seq = c->ce_seq;
     void* const* tab_split = p2p ? c->p2p_tab.as<void*>() : nullptr;
     void* const* tab_gath = p2p ? c->p2p_tab.as<void*>() + P : nullptr;
     // Rows [n, V_pad) of every buffer that serves as a feature slice are padding: no hop writes them,
@@ -571,7 +579,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         for (int j = 0; j < vs; ++j)
             for (void* b : {c->recv.p, c->xfer.p, local ? nullptr : c->send.p})
                 if (b) NTP_CUDA(cudaMemsetAsync(static_cast<char*>(slice_at(b, j)) + off, 0, len, s));
-        if (p2p)
+        if (p2p || ce)
             for (void* b : {c->p2p_split.p, c->p2p_gath.p})
                 NTP_CUDA(cudaMemsetAsync(static_cast<char*>(b) + off, 0, len, s));
     }
@@ -579,7 +587,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     // on the comm stream -- split chunk ch while the MLP computes chunk ch+1, gather chunk ch while the head
     // consumes chunk ch-1, gradient split behind the head, backward gather ahead of the MLP backward --
     // with the same arithmetic (chunks are the same with and without the overlap).
-    const bool ovl = overlap && after && !local && !p2p;
+    const bool ovl = overlap && after && !local && !p2p;   // (ce: the same chunk schedule, copy-engine transfers)
     int ovi = 0;                                   // next free overlap event
     auto ov_event = [&]() -> cudaEvent_t {
         NTP_CHECK(ovi < kOvEvents, NTP_ERR_CONFIG, "too many overlap chunks (%d events)", kOvEvents);
@@ -603,16 +611,45 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         }
         NTP_NCCL(ncclGroupEnd());
     };
+    // copy-engine variant of exchange_rows: rows [r, r+h) of block q of `src` -> block `rank` of rank q's
+    // window (split windows for phases 0 / 2, gather windows for 1 / 3), then flag (phase, rank, ch) := seq
+    // in every peer's inbox
+    auto ce_rows = [&](const void* src, int phase, int64_t r, int64_t h, int ch, cudaStream_t st) {
+        const std::vector<void*>& dst = (phase == 0 || phase == 2) ? c->p2p_peer_split : c->p2p_peer_gath;
+        const size_t bytes = (size_t)h * d_s * es;
+        for (int k = 1; k <= P; ++k) {   // peers first (rotated, so ranks do not all target the same peer), own last
+            const int q = (c->rank + k) % P;
+            NTP_CUDA(cudaMemcpyAsync(static_cast<char*>(dst[q]) + ((size_t)c->rank * V_p + r) * d_s * es,
+                                     static_cast<const char*>(src) + ((size_t)q * V_p + r) * d_s * es, bytes,
+                                     cudaMemcpyDeviceToDevice, st));
+            if (q != c->rank) wire_add(c, (int64_t)bytes, (int64_t)bytes);
+        }
+        for (int q = 0; q < P; ++q)
+            if (q != c->rank) stream_write_u32(st, ce_flags(c, q) + ce_flag_slot(phase, c->rank, ch), seq);
+    };
+    // this rank's chunk ch of `phase` has landed: own block (event) and every peer's (inbox flags)
+    auto ce_wait = [&](cudaEvent_t own, int phase, int ch) {
+        NTP_CUDA(cudaStreamWaitEvent(s, own, 0));
+        for (int q = 0; q < P; ++q)
+            if (q != c->rank) stream_wait_u32_geq(s, ce_flags(c, c->rank) + ce_flag_slot(phase, q, ch), seq);
+    };
+    int ce_phase = 0, ce_ch = 0;   // phase / chunk of the next async_exchange (copy-engine mode)
     // comm stream: after `s` reaches this point, exchange rows [r, r+h); returns the completion event
     auto async_exchange = [&](const void* src, void* dst, int64_t r, int64_t h) -> cudaEvent_t {
         cudaEvent_t a = ov_event(), b = ov_event();
         NTP_CUDA(cudaEventRecord(a, s));
         NTP_CUDA(cudaStreamWaitEvent(c->s_comm, a, 0));
-        exchange_rows(src, dst, r, h, c->s_comm);
+        if (ce) ce_rows(src, ce_phase, r, h, ce_ch++, c->s_comm);
+        else exchange_rows(src, dst, r, h, c->s_comm);
         NTP_CUDA(cudaEventRecord(b, c->s_comm));
         return b;
     };
-    void* slice_in = p2p ? c->p2p_split.p : c->recv.p;   // this rank's feature slice after a split
+    // consumer side of chunk ch (NCCL: the comm stream's event; copy engines: plus the peers' flags)
+    auto wait_chunk = [&](cudaEvent_t ev, int phase, int ch) {
+        if (ce) ce_wait(ev, phase, ch);
+        else NTP_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    };
+    void* slice_in = (p2p || ce) ? c->p2p_split.p : c->recv.p;   // this rank's feature slice after a split
     void* split_dst = p2p ? nullptr : (local ? c->recv.p : c->send.p);   // where the split's producer writes
 
     // one GPU on a reordered graph: producers that can scatter write S^0 / the gradient straight into the
@@ -653,7 +690,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             x_done(slot);
             if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);   // a3 of chunk ch under a2 of ch+1
         }
-        if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, last, 0));
+        if (ovl) wait_chunk(last, 0, (int)nch - 1);   // every chunk (a peer's copies land in stream order)
         NTP_CUDA(record_timing(c, E[ei++], s));   // E1 mlp_fwd (+ pack) done
     }
 
@@ -667,7 +704,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     // a4 + a5: K forward hops on S^0 (pre-scaled) -> Z^K, gathered into this rank's rows
     c->hop_ev_used = 0;
     c->wire_phase = 1;
-    void* gathered = p2p ? c->p2p_gath.p : c->recv.p;
+    void* gathered = (p2p || ce) ? c->p2p_gath.p : c->recv.p;
     {
         PropArgs a{};
         a.H = slice_in;
@@ -711,8 +748,10 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         }
     }
     std::vector<cudaEvent_t> g_ev;                 // forward gather of row chunk ch done (ovl)
+    ce_phase = 1, ce_ch = 0;
     if (ovl)
         for (int64_t r = 0; r < V_p; r += hc) g_ev.push_back(async_exchange(c->xfer.p, c->recv.p, r, std::min(hc, V_p - r)));
+    ce_phase = 2, ce_ch = 0;
     NTP_CUDA(record_timing(c, E[ei++], s));   // E3 prop fwd + f2v done
     // the gradient split's producer target: the send buffer, or on one GPU the slice the forward no
     // longer needs
@@ -747,7 +786,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         const bool fused = head_fused_supported(P, d_s, m->hid, m->C, dt);
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
-            if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, g_ev[ch], 0));
+            if (ovl) wait_chunk(g_ev[ch], 1, (int)ch);
             if (fused) {
                 // one tcgen05 pass over the chunk's rows (head.cu): logits, dl and dZ stay on chip
                 nb_loss += head_fused(c, gathered, V_p, d_s, P, m->hid, m->C, W1g, ldw1, lab, msk, row0, n, gscale_bwd,
@@ -767,7 +806,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                      tab_split, h, r);
             if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);       // a7 of chunk ch
         }
-        if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, last, 0));
+        if (ovl) wait_chunk(last, 2, (int)nch - 1);
     }
     reduce_partials_kernel<<<1, 256, 0, s>>>(part, cnt, nb_loss, scal);
     NTP_LAUNCH_CHECK();
@@ -781,7 +820,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
 
     // a8 + a9: K backward hops on the split gradient, gathered -> dL^ rows [V_p x w]
     c->wire_phase = 3;
-    void* gathered_b = p2p ? c->p2p_gath.p : c->send.p;
+    void* gathered_b = (p2p || ce) ? c->p2p_gath.p : c->send.p;
     {
         PropArgs a{};
         a.H = local ? gsend : slice_in;
@@ -827,6 +866,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         }
     }
     std::vector<cudaEvent_t> b_ev;                 // backward gather of row chunk ch done (ovl)
+    ce_phase = 3, ce_ch = 0;
     if (ovl)
         for (int64_t r = 0; r < V_p; r += hc) b_ev.push_back(async_exchange(c->xfer.p, c->send.p, r, std::min(hc, V_p - r)));
     if (!after) unpack_f2v(c, gathered_b, V_p, d_s, P, dL, ldL, w, dt, NTP_F32, s);
@@ -840,7 +880,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     } else {
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
-            if (ovl) NTP_CUDA(cudaStreamWaitEvent(s, b_ev[ch], 0));
+            if (ovl) wait_chunk(b_ev[ch], 3, (int)ch);
             if (!hstream && wgrad_fused_supported(P, d_s, m->d_in, m->hid, dt)) {   // unpack + dW0 GEMM in one kernel
                 wgrad_fused(c, X, ldx, V_p, m->d_in, gathered_b, d_s, P, m->hid, bits, nwb, r, r + h, dw0_at(ch), s);
                 continue;
@@ -1015,7 +1055,9 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     int64_t epoch_launches = 0;
     // A captured graph bakes in every scratch pointer: it is replayed only while no library buffer has been
     // (re)allocated or freed since its capture (alloc_generation), whatever entry point moved it.
-    const bool capturable = graphs_enabled() && !(m->flags & NTP_M_HOST_STREAM);   // host-streamed epochs run eagerly
+    // host-streamed and copy-engine-overlap epochs run eagerly
+    const bool ce_mode = (m->flags & NTP_M_OVERLAP) && (m->flags & NTP_M_P2P_LAYOUTS) && after && P > 1;
+    const bool capturable = graphs_enabled() && !(m->flags & NTP_M_HOST_STREAM) && !ce_mode;
     if (capturable && gvalid && gkey == key && ggen == alloc_generation()) {
         NTP_CUDA(cudaGraphLaunch(gexec, s));
         c->hop_ev_used = ghops;

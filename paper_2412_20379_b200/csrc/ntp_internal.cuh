@@ -143,6 +143,7 @@ struct ntp_ctx {
     int device = 0, rank = 0, world = 1, slice_align = 16;
     int vs = 1;                     // virtual feature slices per rank (ntp_set_slices): P = world * vs
     int64_t timeout_ms = 0;         // collective deadline of the synchronising calls (ntp_set_timeout), 0 = none
+    uint32_t ce_seq = 0;            // epoch sequence number of the copy-engine layout flags
     bool comm_aborted = false;      // the communicator was aborted after an error or a timeout
     ncclComm_t comm = nullptr;
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
@@ -320,6 +321,14 @@ void pack_v2f(ntp_ctx* c, const void* Hv, int64_t ld_v, int32_t w, void* send, i
 // Peer-direct layouts: IPC windows of this rank ([P][V_p][d_s] split target and gather target),
 // exchanged once per size (collective); false when P2P is unavailable (NCCL all-to-all path).
 bool p2p_ensure(ntp_ctx* c, size_t split_bytes, size_t gather_bytes, cudaStream_t s);
+// Copy-engine layout changes (a12, W1 after propagation): completion flags at the tail of every gather
+// window, kCeFlagBytes long: flag (phase, source rank, chunk) of rank q's window = q's inbox.
+constexpr int kCeRanks = 64, kCeChunks = 64;
+constexpr size_t kCeFlagBytes = (size_t)4 * kCeRanks * kCeChunks * sizeof(uint32_t);
+inline size_t ce_flag_slot(int phase, int src, int ch) { return ((size_t)phase * kCeRanks + src) * kCeChunks + ch; }
+uint32_t* ce_flags(ntp_ctx* c, int q);                 // rank q's inbox (own: local; else the opened IPC window)
+void stream_write_u32(cudaStream_t s, void* addr, uint32_t v);     // cuStreamWriteValue32 (with its memory fence)
+void stream_wait_u32_geq(cudaStream_t s, void* addr, uint32_t v);  // cuStreamWaitValue32, GEQ (+ remote-write flush)
 void p2p_barrier(ntp_ctx* c, cudaStream_t s);   // stream-ordered all-rank barrier (tiny allreduce)
 void p2p_shutdown(ntp_ctx* c);                  // closes the peer mappings (ntp_destroy)
 void unpack_f2v(ntp_ctx* c, const void* recv, int64_t V_p, int32_t d_s, int32_t P, void* Hv,

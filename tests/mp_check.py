@@ -130,11 +130,13 @@ def main(name):
     results = []
     # peer-direct layouts (producers store into the owners' IPC windows), the NCCL block exchange
     # (default) and the overlapped NCCL gather: all three bitwise equal
-    for mode in ("p2p", "nccl", "overlap"):
-        overlap = mode == "overlap"
+    # (W1 after propagation also: "ce", the overlapped schedule with copy-engine peer copies + inbox flags)
+    modes = ("p2p", "nccl", "overlap") + (("ce",) if cfg.w_after_prop else ())
+    for mode in modes:
+        overlap = mode in ("overlap", "ce")
         W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
         flags = ((ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0) | (ntp.NTP_M_OVERLAP if overlap else 0)
-                 | (ntp.NTP_M_P2P_LAYOUTS if mode == "p2p" else 0))
+                 | (ntp.NTP_M_P2P_LAYOUTS if mode in ("p2p", "ce") else 0))
         model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
                      dtype=ntp.NTP_F32, chunks=3, flags=flags)
         losses = []
@@ -147,8 +149,8 @@ def main(name):
         wire = (world - 1) * V_p * oracle.layout.slice_width(cfg.hid if cfg.w_after_prop else cfg.C, world, 4) * 4
         assert rep["bytes_sent"] == [wire] * 4, f"wire bytes {rep['bytes_sent']} vs {wire} (mode={mode})"
         results.append((losses, W0.cpu(), W1.cpu()))
-    for k in (1, 2):
-        assert results[0][0] == results[k][0], f"layout mode {k} changed the loss"
+    for k in range(1, len(modes)):
+        assert results[0][0] == results[k][0], f"layout mode {modes[k]} changed the loss"
         assert torch.equal(results[0][1], results[k][1]) and torch.equal(results[0][2], results[k][2])
 
     _step('4', rank)
@@ -182,12 +184,14 @@ def main(name):
     # the oracle within 2e-2 relative; peer-direct and NCCL layouts bitwise equal
     bres = []
     # (the W1-after-propagation epoch's overlap runs every layout change per row chunk on the comm stream)
-    for mode in ("nccl", "p2p", "overlap"):
+    bmodes = ("nccl", "p2p", "overlap") + (("ce",) if cfg.w_after_prop else ())
+    for mode in bmodes:
         W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
         model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
                      dtype=ntp.NTP_BF16, chunks=3,
                      flags=(ntp.NTP_M_W1_AFTER_PROP if cfg.w_after_prop else 0)
-                     | (ntp.NTP_M_P2P_LAYOUTS if mode == "p2p" else 0) | (ntp.NTP_M_OVERLAP if mode == "overlap" else 0))
+                     | (ntp.NTP_M_P2P_LAYOUTS if mode in ("p2p", "ce") else 0)
+                     | (ntp.NTP_M_OVERLAP if mode in ("overlap", "ce") else 0))
         losses = []
         for e in range(2):
             rep = ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
@@ -195,9 +199,9 @@ def main(name):
             assert abs(rep["loss"] - ref_losses[e]) <= 2e-2 * abs(ref_losses[e]), \
                 f"bf16 loss {rep['loss']} vs oracle {ref_losses[e]} (mode={mode})"
         bres.append((losses, W0.cpu(), W1.cpu()))
-    for k in (1, 2):
+    for k in range(1, len(bmodes)):
         assert bres[0][0] == bres[k][0] and torch.equal(bres[0][1], bres[k][1]) and torch.equal(bres[0][2], bres[k][2]), \
-            f"bf16 mode {k} changed the bits"
+            f"bf16 mode {bmodes[k]} changed the bits"
     if cfg.w_after_prop:   # overlap on a degree-reordered graph (the papers configuration): vs the oracle
         W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
         ctxo = ntp.Context(device=local, rank=rank, world=world, unique_id=pd.broadcast_unique_id(dist, rank))
