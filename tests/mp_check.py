@@ -153,6 +153,18 @@ def main(name):
         assert results[0][0] == results[k][0], f"layout mode {modes[k]} changed the loss"
         assert torch.equal(results[0][1], results[k][1]) and torch.equal(results[0][2], results[k][2])
 
+    # K = 1 with the overlapped gather (W1 before propagation): the last hop is the only hop, so it reads the
+    # receive buffer the chunked gather overwrites -- the epoch keeps S^0 in a copy
+    if not cfg.w_after_prop:
+        ref1, _, _ = oracle.model.train(g, *synth.config_inputs(cfg), W0h, W1h, 1, cfg.gamma, cfg.alpha, lr, 2)
+        for overlap in (False, True):
+            W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+            model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=1, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
+                         dtype=ntp.NTP_F32, chunks=3, flags=ntp.NTP_M_OVERLAP if overlap else 0)
+            for e in range(2):
+                rep = ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
+                assert abs(rep["loss"] - ref1[e]) <= 1e-4, f"K=1 loss {rep['loss']} vs {ref1[e]} (overlap={overlap})"
+
     _step('4', rank)
     # ---- 4. degree-reordered graph (NTP_G_REORDER): slice propagation bitwise vs P = 1 on the same
     # reordered graph, epochs vs the oracle
