@@ -687,6 +687,34 @@ def main():
             rows_ps = (nnz + n) / (spmm_avg * 1e-3)
             gather_line = dict(gc, achieved_rows_per_s=rows_ps, frac=rows_ps / gc["rows_per_s"],
                                row_bytes=d_s * esz)
+        # The hop's roofline by residency: a slice that exceeds L2 is HBM-bound (measured DRAM
+        # bytes of this kernel / its live time against the measured copy peak); a slice that fits L2 reads HBM
+        # only for its compulsory bytes and is bound by the L2 random-row gather rate: its rows / s against the
+        # measured ceiling of the same access pattern (scripts/l2_probe.cu, random rows of the same size from an
+        # L2-resident table).  The other resource's numbers stay in the block.
+        hbm = {"achieved": (traffic if traffic else bh) / (spmm_avg * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+               "traffic": traffic, "peak_source": peak_src,
+               "bytes_model": ("ncu DRAM read + write bytes per launch (profiles/spmm_traffic.json)" if traffic
+                               else bmodel),
+               "algorithmic_bytes_per_launch": bh, "algorithmic_model": bmodel}
+        hbm["frac"] = hbm["achieved"] / peak
+        common = {"kernel": "spmm_hop_bulk_kernel" if d_s * esz >= 1024 else "spmm_hop_kernel",
+                  "avg_launch_ms": spmm_avg, "launches_timed": spmm_n,
+                  "timed_span": "the hop kernel + its spmm_fixup_kernel (cut-row carries, ~1% of the span), CUDA "
+                                "events on the hop's stream"}
+        if bmodel.startswith("perfect") and gather_line:
+            rb = gather_line["probe_row_bytes"]
+            roof = dict(common, bound="l2", unit="GB/s",
+                        achieved=gather_line["achieved_rows_per_s"] * rb / 1e9,
+                        peak=gather_line["rows_per_s"] * rb / 1e9, frac=gather_line["frac"],
+                        peak_source="measured: random-row gather ceiling from an L2-resident table, rows of "
+                                    f"{rb} B ({gather_line['source']}, scripts/l2_probe.cu); MEASURED_PEAKS.json "
+                                    "has no L2 figure",
+                        traffic=traffic, bytes_model="gathered rows (self + every arc) x row bytes, per launch",
+                        algorithmic_bytes_per_launch=(nnz + n) * rb, l2_gather_GBps=l2b / (spmm_avg * 1e-3) / 1e9,
+                        hbm=hbm, gather=gather_line)
+        else:
+            roof = dict(common, bound="hbm", **hbm, gather=gather_line)
         line = {
             "metric": METRIC, "value": ge, "unit": "GE/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -709,25 +737,7 @@ def main():
                        "l2": f"inputs larger than L2 (col_idx {4 * nnz / 1e6:.0f} MB streamed per hop; "
                              f"X_v {x_bytes / 1e6:.0f} MB per rank)",
                        "graph_setup_s": round(t_graph, 3), "hbm_used_GB_max_rank": round(hbm_used_gb, 1)},
-            "roofline": {"kernel": "spmm_hop_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "binding_resource": ("L2 random-row gather: the slice fits L2, so HBM carries the compulsory "
-                                              "bytes only and `gather` is the real bound" if bmodel.startswith("perfect")
-                                              else "HBM: the slice exceeds L2, every arc's row slice streams from HBM"),
-                         "hbm_frac_measured": (traffic / (spmm_avg * 1e-3) / 1e9 / peak) if traffic else None,
-                         "timed_span": "spmm_hop_kernel + its spmm_fixup_kernel (cut-row carries, ~1% of the span)",
-                         "algorithmic_bytes_per_launch": bh, "bytes_model": bmodel, "l2_bytes": l2_size,
-                         "avg_launch_ms": spmm_avg,
-                         "launches_timed": spmm_n, "peak_source": peak_src,
-                         "l2_gather_bytes_per_launch": l2b,
-                         "l2_gather_GBps": l2b / (spmm_avg * 1e-3) / 1e9,
-                         "gather": gather_line,
-                         "note": "algorithmic bytes (DESIGN.md §6, SURVEY §8(d)) by residency: a slice that fits "
-                                 "L2 is read from HBM once (gathered rows re-read through L2: l2_gather_*, and the "
-                                 "hop is bound by the random-row gather rate, reported against its measured ceiling "
-                                 "in `gather`); a slice larger than L2 costs every arc's row slice from HBM "
-                                 "(SURVEY's no-reuse per-edge figure). traffic = ncu dram read+write per launch of "
-                                 "this kernel on this workload (profiles/spmm_traffic.json)"},
+            "roofline": roof,
             "prop_GE_per_s": 2 * cfg.K * nnz * w / (spmm_ms / len(reps) * 1e-3) / 1e9 * 1.0,
             "phase_ms": {k: round(v, 4) for k, v in phase.items()},
             "nvlink": nvlink,
