@@ -68,24 +68,114 @@ __global__ void gat_fg_kernel(const float* __restrict__ z, int64_t ldz, int32_t 
     }
 }
 
-// G2 softmax over every destination's self loop + in-arcs (one warp per row, all n rows)
-__global__ void gat_softmax_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                   const float* __restrict__ fg, int64_t n, float slope, float* __restrict__ alpha) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
-        const float gv = fg[2 * v + 1];
-        const float es = leaky(fg[2 * v] + gv, slope);
-        const int b = rp[v], e = rp[v + 1];
-        float m = es;
-        for (int j = b + lane; j < e; j += 32) m = fmaxf(m, leaky(fg[2 * (int64_t)col[j]] + gv, slope));
-        m = warp_max(m);
-        float sum = lane == 0 ? expf(es - m) : 0.f;
-        for (int j = b + lane; j < e; j += 32) sum += expf(leaky(fg[2 * (int64_t)col[j]] + gv, slope) - m);
-        sum = warp_sum(sum);
-        if (lane == 0) alpha[v] = expf(es - m) / sum;
-        for (int j = b + lane; j < e; j += 32) alpha[n + j] = expf(leaky(fg[2 * (int64_t)col[j]] + gv, slope) - m) / sum;
+// Per-row reductions run on a warp (rows of <= kBigDeg arcs, grid-stride over rows) or, for hub rows (up to
+// ~50K in-arcs on the Reddit shape, ~700K on papers), on a whole 256-thread CTA (one row per CTA, rows from
+// a per-graph list): one warp walking a hub row alone would hold up the kernel for its ~1.5K iterations.
+constexpr int kBigDeg = 4096;
+
+struct WarpRed {
+    int t, T;
+    __device__ WarpRed() : t(threadIdx.x & 31), T(32) {}
+    __device__ float sum(float v) const { return warp_sum(v); }
+    __device__ float max(float v) const { return warp_max(v); }
+    __device__ void combine(float& m, float& sm) const {   // online softmax (max, sum) over the group
+        const float M = warp_max(m);
+        sm = warp_sum(sm == 0.f ? 0.f : sm * expf(m - M));
+        m = M;
     }
+};
+struct BlockRed {
+    float* sh;   // >= 32 floats of shared memory
+    int t, T;
+    __device__ explicit BlockRed(float* s_) : sh(s_), t(threadIdx.x), T(blockDim.x) {}
+    __device__ float all(float v, bool is_max) const {
+        v = is_max ? warp_max(v) : warp_sum(v);
+        __syncthreads();
+        if ((t & 31) == 0) sh[t >> 5] = v;
+        __syncthreads();
+        float r = (t & 31) < (T >> 5) ? sh[t & 31] : (is_max ? -INFINITY : 0.f);
+        return is_max ? warp_max(r) : warp_sum(r);   // fixed order: warp partials, then a fixed tree
+    }
+    __device__ float sum(float v) const { return all(v, false); }
+    __device__ float max(float v) const { return all(v, true); }
+    __device__ void combine(float& m, float& sm) const {
+        const float M = all(m, true);
+        sm = all(sm == 0.f ? 0.f : sm * expf(m - M), false);
+        m = M;
+    }
+};
+
+// G2 softmax over a destination's self loop + in-arcs, two passes: (1) e = LeakyReLU(f_u + g_v) -- the only
+// gather of f -- stored in alpha's slot, an online max / sum per thread combined over the group, and the
+// sign of s_uv (> 0) as one bit per arc (the backward's LeakyReLU'), ballot-packed per warp; (2) alpha =
+// exp(e - m) / sum from the stored e (coalesced).
+__device__ __forceinline__ void online_add(float& m, float& sm, float e) {
+    if (e > m) {
+        sm = sm * expf(m - e) + 1.f;
+        m = e;
+    } else {
+        sm += expf(e - m);
+    }
+}
+
+template <class Red>
+__device__ void softmax_row(const Red& R, int64_t v, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const float* __restrict__ fg, int64_t n, float slope, float* __restrict__ alpha,
+                            uint32_t* __restrict__ pos_bits) {
+    const int lane = threadIdx.x & 31;
+    const float gv = fg[2 * v + 1];
+    const float ss = fg[2 * v] + gv;
+    const float es = leaky(ss, slope);
+    if (R.t == 0 && ss > 0.f) atomicOr(pos_bits + (v >> 5), 1u << (v & 31));
+    const int b = rp[v], e = rp[v + 1];
+    float m = -INFINITY, sm = 0.f;
+    if (R.t == 0) m = es, sm = 1.f;
+    for (int jb = b + (R.t - lane); jb < e; jb += R.T) {   // this warp's 32 consecutive arcs jb .. jb + 31
+        const int j = jb + lane;
+        bool pos = false;
+        if (j < e) {
+            const float sj = fg[2 * (int64_t)col[j]] + gv;
+            const float ej = leaky(sj, slope);
+            pos = sj > 0.f;
+            alpha[n + j] = ej;
+            online_add(m, sm, ej);
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, pos);
+        if (lane == 0 && word) {
+            const int64_t a = n + jb;                                // bit index of arc jb
+            atomicOr(pos_bits + (a >> 5), word << (a & 31));
+            if (a & 31) atomicOr(pos_bits + (a >> 5) + 1, word >> (32 - (a & 31)));
+        }
+    }
+    R.combine(m, sm);
+    if (R.t == 0) alpha[v] = expf(es - m) / sm;
+    for (int j = b + R.t; j < e; j += R.T) alpha[n + j] = expf(alpha[n + j] - m) / sm;
+}
+
+__global__ void gat_softmax_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                   const float* __restrict__ fg, int64_t n, float slope, float* __restrict__ alpha,
+                                   uint32_t* __restrict__ pos_bits) {
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const WarpRed R;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps)
+        if (rp[v + 1] - rp[v] <= kBigDeg) softmax_row(R, v, rp, col, fg, n, slope, alpha, pos_bits);
+}
+
+__global__ void __launch_bounds__(256) gat_softmax_big_kernel(const int32_t* __restrict__ big, int32_t nbig,
+                                                              const int32_t* __restrict__ rp,
+                                                              const int32_t* __restrict__ col,
+                                                              const float* __restrict__ fg, int64_t n, float slope,
+                                                              float* __restrict__ alpha, uint32_t* __restrict__ pos_bits) {
+    __shared__ float sh[32];
+    const BlockRed R(sh);
+    for (int i = blockIdx.x; i < nbig; i += gridDim.x) softmax_row(R, big[i], rp, col, fg, n, slope, alpha, pos_bits);
+}
+
+// rows of more than kBigDeg arcs (list built once per graph; order irrelevant: rows are independent)
+__global__ void gat_big_rows_kernel(const int32_t* __restrict__ rp, int64_t n, int32_t* __restrict__ list,
+                                    int32_t* __restrict__ cnt) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if (rp[v + 1] - rp[v] > kBigDeg) list[atomicAdd(cnt, 1)] = (int32_t)v;
 }
 
 // out-CSR arc j' (row u, column v) -> its in-CSR index (u's position in row v)
@@ -118,76 +208,143 @@ template <typename T> __device__ __forceinline__ float ldx(const T* p);
 template <> __device__ __forceinline__ float ldx<float>(const float* p) { return *p; }
 template <> __device__ __forceinline__ float ldx<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 
-// G4 SDDMM: dalpha[j] (+)= gamma * G_v . Z_u over this slice's d_s columns (arc j: self loops first)
-template <typename T>
-__global__ void gat_sddmm_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t n, int64_t nnz,
-                                 const T* __restrict__ G, const T* __restrict__ Z, int32_t d_s, float gamma,
-                                 float* __restrict__ dalpha, int accumulate) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n + nnz; j += (int64_t)gridDim.x * blockDim.x) {
-        int64_t u, v;
-        if (j < n) {
-            u = v = j;
-        } else {
-            const int64_t e = j - n;
-            int64_t lo = 0, hi = n;   // v = last row with rp[v] <= e
-            while (hi - lo > 1) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (rp[mid] <= e) lo = mid;
-                else hi = mid;
+// G4 SDDMM: dalpha[j] (+)= gamma * G_v . Z_u over this slice's d_s columns (arc j: self loops first).
+// Arcs are cut into ranges of kSdArcs consecutive in-CSR arcs, one warp per range (hubs spread over many
+// warps).  A step covers E arcs: lane = e * VPP + c holds 16-byte vector c of arc e's two rows (G_v cached
+// in L1 across a row's arcs, Z_u a random row gather like the hop's), multiplies in fp32 and reduces its
+// group with a fixed xor tree; lane c = 0 of the group writes the arc.  The self loops are a separate
+// streaming pass (j < n).
+constexpr int kSdArcs = 2048;
+
+// One arc per lane: lanes take consecutive arcs of a kSdArcs range (coalesced col / dalpha, the row of a lane
+// advances monotonically), each lane reads the whole slice rows of its arc (NV 16-byte vectors of G_v --
+// shared by the lanes of a row, so L1 -- and of the gathered Z_u) and sums the dot product in column order.
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) gat_sddmm_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                        int64_t n, int64_t nnz, const char* __restrict__ G,
+                                                        const char* __restrict__ Z, int32_t nvec, float gamma,
+                                                        float* __restrict__ dalpha, int accumulate) {
+    constexpr int VALS = 16 / sizeof(T);
+    const int64_t ld = (int64_t)nvec * 16;   // NV == nvec, or NV = 16 chunks of a wider row
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    auto elem = [](const uint4& x, int i) {
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        if (sizeof(T) == 4) return __uint_as_float(w[i]);
+        return __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
+    };
+    auto dot = [&](const char* a, const char* b) {
+        float d = 0.f;
+        for (int k0 = 0; k0 < nvec; k0 += NV) {
+            uint4 xa[NV], xb[NV];
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const bool ok = k0 + k < nvec;
+                xa[k] = ok ? *reinterpret_cast<const uint4*>(a + 16 * (k0 + k)) : make_uint4(0, 0, 0, 0);
+                xb[k] = ok ? __ldg(reinterpret_cast<const uint4*>(b + 16 * (k0 + k))) : make_uint4(0, 0, 0, 0);
             }
-            v = lo;
-            u = col[e];
+#pragma unroll
+            for (int k = 0; k < NV; ++k)
+#pragma unroll
+                for (int i = 0; i < VALS; ++i) d = fmaf(elem(xa[k], i), elem(xb[k], i), d);
         }
-        const T* gv = G + v * d_s;
-        const T* zu = Z + u * d_s;
-        float dot = 0.f;
-        for (int c = 0; c < d_s; ++c) dot = fmaf(ldx<T>(gv + c), ldx<T>(zu + c), dot);
-        dalpha[j] = (accumulate ? dalpha[j] : 0.f) + gamma * dot;
+        return d;
+    };
+    // self loops: arc v = G_v . Z_v
+    for (int64_t v = warp * 32 + lane; v < n; v += nwarps * 32)
+        dalpha[v] = (accumulate ? dalpha[v] : 0.f) + gamma * dot(G + v * ld, Z + v * ld);
+    const int64_t nranges = (nnz + kSdArcs - 1) / kSdArcs;
+    for (int64_t rg = warp; rg < nranges; rg += nwarps) {
+        const int64_t a0 = rg * kSdArcs, a1 = min(a0 + (int64_t)kSdArcs, nnz);
+        int64_t lo = 0, hi = n;   // v = last row with rp[v] <= a0
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (rp[mid] <= a0) lo = mid;
+            else hi = mid;
+        }
+        int64_t v = lo;
+        for (int64_t j = a0 + lane; j < a1; j += 32) {
+            while (rp[v + 1] <= j) ++v;   // this lane's row (arcs are sorted by destination)
+            const float d = dot(G + v * ld, Z + (int64_t)__ldg(col + j) * ld);
+            dalpha[n + j] = (accumulate ? dalpha[n + j] : 0.f) + gamma * d;
+        }
     }
 }
 
-// G4 softmax + LeakyReLU backward per destination: ds[j]; pd[v] = sum of v's ds (self + in-arcs)
-__global__ void gat_softmax_bwd_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                       const float* __restrict__ fg, const float* __restrict__ alpha,
-                                       const float* __restrict__ dalpha, int64_t n, float slope, float* __restrict__ ds,
-                                       float* __restrict__ pd) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
-        const int b = rp[v], e = rp[v + 1];
-        float w = lane == 0 ? alpha[v] * dalpha[v] : 0.f;
-        for (int j = b + lane; j < e; j += 32) w = fmaf(alpha[n + j], dalpha[n + j], w);
-        w = warp_sum(w);
-        const float gv = fg[2 * v + 1];
-        float acc = 0.f;
-        if (lane == 0) {
-            const float sv = fg[2 * v] + gv;
-            const float d = alpha[v] * (dalpha[v] - w) * (sv > 0.f ? 1.f : slope);
-            ds[v] = d;
-            acc = d;
-        }
-        for (int j = b + lane; j < e; j += 32) {
-            const float s = fg[2 * (int64_t)col[j]] + gv;
-            const float d = alpha[n + j] * (dalpha[n + j] - w) * (s > 0.f ? 1.f : slope);
-            ds[n + j] = d;
-            acc += d;
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) pd[v] = acc;
+// G4 softmax + LeakyReLU backward per destination: ds[j]; pd[v] = sum of v's ds (self + in-arcs).  The
+// LeakyReLU' of every arc comes from the forward's sign bits: no gather of f.
+template <class Red>
+__device__ void softmax_bwd_row(const Red& R, int64_t v, const int32_t* __restrict__ rp,
+                                const uint32_t* __restrict__ pos_bits, const float* __restrict__ alpha,
+                                const float* __restrict__ dalpha, int64_t n, float slope, float* __restrict__ ds,
+                                float* __restrict__ pd) {
+    auto pos = [&](int64_t a) { return (pos_bits[a >> 5] >> (a & 31)) & 1u; };
+    const int b = rp[v], e = rp[v + 1];
+    float w = R.t == 0 ? alpha[v] * dalpha[v] : 0.f;
+    for (int j = b + R.t; j < e; j += R.T) w = fmaf(alpha[n + j], dalpha[n + j], w);
+    w = R.sum(w);
+    float acc = 0.f;
+    if (R.t == 0) {
+        const float d = alpha[v] * (dalpha[v] - w) * (pos(v) ? 1.f : slope);
+        ds[v] = d;
+        acc = d;
     }
+    for (int j = b + R.t; j < e; j += R.T) {
+        const float d = alpha[n + j] * (dalpha[n + j] - w) * (pos(n + j) ? 1.f : slope);
+        ds[n + j] = d;
+        acc += d;
+    }
+    acc = R.sum(acc);
+    if (R.t == 0) pd[v] = acc;
+}
+
+__global__ void gat_softmax_bwd_kernel(const int32_t* __restrict__ rp, const uint32_t* __restrict__ pos_bits,
+                                       const float* __restrict__ alpha, const float* __restrict__ dalpha, int64_t n,
+                                       float slope, float* __restrict__ ds, float* __restrict__ pd) {
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const WarpRed R;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps)
+        if (rp[v + 1] - rp[v] <= kBigDeg) softmax_bwd_row(R, v, rp, pos_bits, alpha, dalpha, n, slope, ds, pd);
+}
+
+__global__ void __launch_bounds__(256) gat_softmax_bwd_big_kernel(const int32_t* __restrict__ big, int32_t nbig,
+                                                                  const int32_t* __restrict__ rp,
+                                                                  const uint32_t* __restrict__ pos_bits,
+                                                                  const float* __restrict__ alpha,
+                                                                  const float* __restrict__ dalpha, int64_t n,
+                                                                  float slope, float* __restrict__ ds,
+                                                                  float* __restrict__ pd) {
+    __shared__ float sh[32];
+    const BlockRed R(sh);
+    for (int i = blockIdx.x; i < nbig; i += gridDim.x) softmax_bwd_row(R, big[i], rp, pos_bits, alpha, dalpha, n, slope, ds, pd);
 }
 
 // ps[u] = ds of u's self loop + ds of every arc leaving u (out-CSR rows, coefficients through perm)
+template <class Red>
+__device__ void ps_row(const Red& R, int64_t u, const int32_t* __restrict__ rp_out, const int32_t* __restrict__ perm,
+                       const float* __restrict__ ds, int64_t n, float* __restrict__ ps) {
+    float acc = R.t == 0 ? ds[u] : 0.f;
+    for (int j = rp_out[u] + R.t; j < rp_out[u + 1]; j += R.T) acc += ds[n + perm[j]];
+    acc = R.sum(acc);
+    if (R.t == 0) ps[u] = acc;
+}
+
 __global__ void gat_ps_kernel(const int32_t* __restrict__ rp_out, const int32_t* __restrict__ perm,
                               const float* __restrict__ ds, int64_t n, float* __restrict__ ps) {
-    const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
-        float acc = lane == 0 ? ds[u] : 0.f;
-        for (int j = rp_out[u] + lane; j < rp_out[u + 1]; j += 32) acc += ds[n + perm[j]];
-        acc = warp_sum(acc);
-        if (lane == 0) ps[u] = acc;
-    }
+    const WarpRed R;
+    for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += warps)
+        if (rp_out[u + 1] - rp_out[u] <= kBigDeg) ps_row(R, u, rp_out, perm, ds, n, ps);
+}
+
+__global__ void __launch_bounds__(256) gat_ps_big_kernel(const int32_t* __restrict__ big, int32_t nbig,
+                                                         const int32_t* __restrict__ rp_out,
+                                                         const int32_t* __restrict__ perm, const float* __restrict__ ds,
+                                                         int64_t n, float* __restrict__ ps) {
+    __shared__ float sh[32];
+    const BlockRed R(sh);
+    for (int i = blockIdx.x; i < nbig; i += gridDim.x) ps_row(R, big[i], rp_out, perm, ds, n, ps);
 }
 
 // dz[v] += ps_v a_src + pd_v a_dst (own rows)
@@ -304,6 +461,7 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     c->gat_dalpha.ensure((size_t)na * sizeof(float) + 16);
     c->gat_ds.ensure((size_t)na * sizeof(float) + 16);
     c->gat_pspd.ensure((size_t)2 * n * sizeof(float) + 16);
+    c->gat_bits.ensure((size_t)cdiv(na, 32) * sizeof(uint32_t) + 16);
     c->gat_Z.ensure((size_t)(m->K + 1) * feat * es + 16);
     c->recv.ensure((size_t)feat * es + 16);
     c->xfer.ensure((size_t)feat * es + 16);
@@ -320,9 +478,25 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
                                                   out.row_ptr.as<int32_t>(), out.col.as<int32_t>(), n,
                                                   c->gat_perm.as<int32_t>());
         NTP_LAUNCH_CHECK();
-        count_launch(c);
+        // hub rows (> kBigDeg arcs) of both CSRs: one CTA each in the per-row reductions
+        c->gat_big.ensure((size_t)2 * (n + 1) * sizeof(int32_t) + 16);
+        DevBuf cnt;
+        cnt.ensure(2 * sizeof(int32_t));
+        NTP_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(int32_t), s));
+        gat_big_rows_kernel<<<eblk(n), 256, 0, s>>>(in.row_ptr.as<int32_t>(), n, c->gat_big.as<int32_t>(), cnt.as<int32_t>());
+        gat_big_rows_kernel<<<eblk(n), 256, 0, s>>>(out.row_ptr.as<int32_t>(), n, c->gat_big.as<int32_t>() + n + 1,
+                                                   cnt.as<int32_t>() + 1);
+        NTP_LAUNCH_CHECK();
+        int32_t h[2];
+        NTP_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        NTP_CUDA(cudaStreamSynchronize(s));
+        c->gat_nbig[0] = h[0];
+        c->gat_nbig[1] = h[1];
+        count_launch(c, 3);
         c->gat_perm_version = c->g_version;
     }
+    const int32_t* big_in = c->gat_big.as<int32_t>();
+    const int32_t* big_out = big_in + n + 1;
     float* H1 = c->m_H1.as<float>();
     float* z = c->m_L.as<float>();
     float* dz = c->m_dL.as<float>();
@@ -362,8 +536,13 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     NTP_LAUNCH_CHECK();
     count_launch(c);
     if (!local) NTP_NCCL(ncclAllGather(fg + 2 * row0, fg, (size_t)2 * V_p, ncclFloat32, c->comm, s));
+    NTP_CUDA(cudaMemsetAsync(c->gat_bits.p, 0, (size_t)cdiv(na, 32) * sizeof(uint32_t), s));
     gat_softmax_kernel<<<wblocks(n), 256, 0, s>>>(g.fwd().row_ptr.as<int32_t>(), g.fwd().col.as<int32_t>(), fg, n, slope,
-                                                 alpha);
+                                                 alpha, c->gat_bits.as<uint32_t>());
+    if (c->gat_nbig[0] > 0)
+        gat_softmax_big_kernel<<<std::min(c->gat_nbig[0], 148 * 8), 256, 0, s>>>(
+            big_in, c->gat_nbig[0], g.fwd().row_ptr.as<int32_t>(), g.fwd().col.as<int32_t>(), fg, n, slope, alpha,
+            c->gat_bits.as<uint32_t>());
     NTP_LAUNCH_CHECK();
     gat_permute_kernel<<<eblk(na), 256, 0, s>>>(alpha, perm, n, nnz, alpha_t);
     NTP_LAUNCH_CHECK();
@@ -414,6 +593,30 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     }
     NTP_CUDA(record_timing(c, E[ei++], s));   // E5 v2f bwd
 
+    // SDDMM launcher: E arcs per warp step by the slice's 16-byte vectors per row
+    const int32_t nvec = (int32_t)(d_s * es / 16);
+    const int sd_blocks = (int)std::min<int64_t>(std::max<int64_t>(cdiv(nnz, kSdArcs * 8), 1) + 64, 148 * 16);
+    auto sddmm = [&](const void* Gj, const void* Zj, int acc) {
+        const int64_t rp_n = n;
+        const int32_t* rp = g.fwd().row_ptr.as<int32_t>();
+        const int32_t* cl = g.fwd().col.as<int32_t>();
+        const char* Gc = static_cast<const char*>(Gj);
+        const char* Zc = static_cast<const char*>(Zj);
+#define NTP_SDDMM(T, NV_) gat_sddmm_kernel<T, NV_><<<sd_blocks, 256, 0, s>>>(rp, cl, rp_n, nnz, Gc, Zc, nvec, m->gamma, dalpha, acc)
+#define NTP_SDDMM_T(T) switch (nvec) { \
+            case 1: NTP_SDDMM(T, 1); break; case 2: NTP_SDDMM(T, 2); break; case 3: NTP_SDDMM(T, 3); break; \
+            case 4: NTP_SDDMM(T, 4); break; case 5: NTP_SDDMM(T, 5); break; case 6: NTP_SDDMM(T, 6); break; \
+            case 7: NTP_SDDMM(T, 7); break; case 8: NTP_SDDMM(T, 8); break; case 9: NTP_SDDMM(T, 9); break; \
+            case 10: NTP_SDDMM(T, 10); break; case 11: NTP_SDDMM(T, 11); break; case 12: NTP_SDDMM(T, 12); break; \
+            case 13: NTP_SDDMM(T, 13); break; case 14: NTP_SDDMM(T, 14); break; case 15: NTP_SDDMM(T, 15); break; \
+            default: NTP_SDDMM(T, 16); }
+        if (dt == NTP_F32) { NTP_SDDMM_T(float) }
+        else { NTP_SDDMM_T(__nv_bfloat16) }
+#undef NTP_SDDMM_T
+#undef NTP_SDDMM
+        NTP_LAUNCH_CHECK();
+    };
+
     // ---- G4 / a8: G^{k-1} = gamma A_att^T G^k per slice, with dalpha += gamma G^k_v . Z^{k-1}_u on the way
     c->wire_phase = 3;
     void* cur = c->recv.p;
@@ -424,15 +627,7 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
             const void* Gj = sl(cur, j);
             const void* Zj = sl(Zst, (int64_t)(k - 1) * vs + j);
             const int acc = (i > 0 || j > 0) ? 1 : 0;
-            if (dt == NTP_F32)
-                gat_sddmm_kernel<float><<<eblk(na), 256, 0, s>>>(g.fwd().row_ptr.as<int32_t>(), g.fwd().col.as<int32_t>(),
-                                                               n, nnz, (const float*)Gj, (const float*)Zj, d_s,
-                                                               m->gamma, dalpha, acc);
-            else
-                gat_sddmm_kernel<__nv_bfloat16><<<eblk(na), 256, 0, s>>>(
-                    g.fwd().row_ptr.as<int32_t>(), g.fwd().col.as<int32_t>(), n, nnz, (const __nv_bfloat16*)Gj,
-                    (const __nv_bfloat16*)Zj, d_s, m->gamma, dalpha, acc);
-            NTP_LAUNCH_CHECK();
+            sddmm(Gj, Zj, acc);
             count_launch(c);
             hop(Gj, sl(nxt, j), true);
         }
@@ -450,10 +645,17 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
 
     // ---- attention backward (every rank holds every coefficient): dalpha summed over ranks
     if (!local) NTP_NCCL(ncclAllReduce(dalpha, dalpha, (size_t)na, ncclFloat32, ncclSum, c->comm, s));
-    gat_softmax_bwd_kernel<<<wblocks(n), 256, 0, s>>>(g.fwd().row_ptr.as<int32_t>(), g.fwd().col.as<int32_t>(), fg, alpha,
+    gat_softmax_bwd_kernel<<<wblocks(n), 256, 0, s>>>(g.fwd().row_ptr.as<int32_t>(), c->gat_bits.as<uint32_t>(), alpha,
                                                      dalpha, n, slope, ds, pd);
+    if (c->gat_nbig[0] > 0)
+        gat_softmax_bwd_big_kernel<<<std::min(c->gat_nbig[0], 148 * 8), 256, 0, s>>>(
+            big_in, c->gat_nbig[0], g.fwd().row_ptr.as<int32_t>(), c->gat_bits.as<uint32_t>(), alpha, dalpha, n, slope,
+            ds, pd);
     NTP_LAUNCH_CHECK();
     gat_ps_kernel<<<wblocks(n), 256, 0, s>>>(g.bwd().row_ptr.as<int32_t>(), perm, ds, n, ps);
+    if (c->gat_nbig[1] > 0)
+        gat_ps_big_kernel<<<std::min(c->gat_nbig[1], 148 * 8), 256, 0, s>>>(big_out, c->gat_nbig[1],
+                                                                           g.bwd().row_ptr.as<int32_t>(), perm, ds, n, ps);
     NTP_LAUNCH_CHECK();
     gat_dz_kernel<<<eblk(V_p * C), 256, 0, s>>>(dz, ldL, C, attu, ps, pd, V_p, row0, n);
     NTP_LAUNCH_CHECK();

@@ -151,7 +151,8 @@ struct ntp_ctx {
     // scratch
     ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
     // decoupled GAT (gat.cu): score halves, coefficients (+ out-CSR order), their gradients, level stack
-    ntp::DevBuf gat_fg, gat_alpha, gat_alpha_t, gat_dalpha, gat_ds, gat_pspd, gat_perm, gat_Z, gat_da;
+    ntp::DevBuf gat_fg, gat_alpha, gat_alpha_t, gat_dalpha, gat_ds, gat_pspd, gat_perm, gat_Z, gat_da, gat_bits, gat_big;
+    int32_t gat_nbig[2] = {0, 0};   // hub rows (in-CSR, out-CSR) listed in gat_big
     int64_t gat_perm_version = -1;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
     ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp, m_head, m_wgrad;
