@@ -663,6 +663,27 @@ def main():
             nvlink[ph] = {"ms": t_ph, "bytes_sent_per_rank": b, "what": what,
                           "GBps_per_direction": (b / (t_ph * 1e-3) / 1e9) if t_ph else None,
                           "frac_of_900GBps": (b / (t_ph * 1e-3) / 1e9 / 900.0) if t_ph else None}
+    # the layout change timed on its own (SURVEY §8(d) "measure the a2a separately at the same counts"):
+    # ntp_layout_v2f of this rank's [V_p x w] rows (pack + block all-to-all) into the feature slice
+    a2a = None
+    if world > 1 and args.engine == "decoupled":
+        Hv_a = torch.zeros(V_p, w_prop := (cfg.hid if cfg.w_after_prop else cfg.C), dtype=torch.float32 if dt == ntp.NTP_F32
+                           else torch.bfloat16, device="cuda")
+        Hf_a = torch.empty(V_p * world, d_s, dtype=Hv_a.dtype, device="cuda")
+        for _ in range(3):
+            ctx.layout_v2f(Hv_a, Hf_a, stream)
+        barrier()
+        ev0.record(stream)
+        for _ in range(10):
+            ctx.layout_v2f(Hv_a, Hf_a, stream)
+        ev1.record(stream)
+        barrier()
+        t_a2a = allmax(ev0.elapsed_time(ev1) / 10)
+        b_a2a = (world - 1) * V_p * d_s * (2 if dt == ntp.NTP_BF16 else 4)
+        a2a = {"ms": t_a2a, "bytes_sent_per_rank": b_a2a, "what": "ntp_layout_v2f: pack + block all-to-all, standalone",
+               "GBps_per_direction": b_a2a / (t_a2a * 1e-3) / 1e9,
+               "frac_of_900GBps": b_a2a / (t_a2a * 1e-3) / 1e9 / 900.0}
+        del Hv_a, Hf_a
     leg = None
     if not args.no_hbm_leg and args.engine == "decoupled" and args.config == "reddit":
         leg = hbm_leg(args, world, rank, local, dist, barrier, allmax, peak, peak_src, l2_size)
@@ -741,6 +762,7 @@ def main():
             "prop_GE_per_s": 2 * cfg.K * nnz * w / (spmm_ms / len(reps) * 1e-3) / 1e9 * 1.0,
             "phase_ms": {k: round(v, 4) for k, v in phase.items()},
             "nvlink": nvlink,
+            "a2a_standalone": a2a,
             "hbm_leg": leg,
             "clocks": clk,
             "gpu_launches": int(launches),

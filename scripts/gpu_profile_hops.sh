@@ -24,6 +24,7 @@ run r02_hops_orkut orkut/P1/f32,orkut/P2/f32,orkut/P4/f32,orkut/P8/f32 512,256,1
 run r02_hops_reddit reddit/P1/f32,reddit/P2/f32,reddit/P4/f32,reddit/P8/f32 44,24,12,8 4 --config reddit
 run r02_hops_products products/P1/f32,products/P2/f32,products/P4/f32,products/P8/f32 48,24,12,8 4 --config products --reorder
 run r02_hops_papers papers/P1/bf16,papers/P2/bf16,papers/P4/bf16,papers/P8/bf16 128,64,32,16 2 --config papers --dtype bf16 --reorder
+run r02_hops_papers_bwd papers_bwd/P1/bf16,papers_bwd/P8/bf16 128,16 2 --config papers --dtype bf16 --reorder --bwd
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/r02_reddit_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-hbm-leg > gpurun_out/ncu_ll.log 2>&1; echo ll=$?
 ls -la gpurun_out/prof
