@@ -269,6 +269,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float* Cb = p.C + (int64_t)z * p.split_stride;
             for (int c0 = 0; c0 < p.BN; c0 += 32) {
+                // epi 2: this lane's 8 mask quads of the chunk are loaded first, all in flight together,
+                // before the TMEM read (one dependent load per quad had left the epilogue latency-bound:
+                // the K = 41 dH1 GEMM of the Reddit shape took 516 us for ~0.5 GB of traffic)
+                float4 mq[8];
+                if (p.epi == 2 && p.vec) {
+                    const int colq = n0 + c0 + 4 * (lane & 7);
+#pragma unroll
+                    for (int it = 0; it < 8; ++it) {
+                        const int row = m0 + 32 * q + it * 4 + (lane >> 3);
+                        mq[it] = (row < p.M && colq + 3 < p.N)
+                                     ? __ldg(reinterpret_cast<const float4*>(p.aux + (int64_t)row * p.ldaux + colq))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
                 uint32_t r[32];
                 const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * p.BN + c0);
                 asm volatile(
@@ -342,7 +356,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     float* dst = Cb + (int64_t)row * p.ldc + col;
                     if (p.vec && col + 3 < p.N) {
                         if (p.epi == 2) {
-                            const float4 m = *reinterpret_cast<const float4*>(ax);
+                            const float4 m = mq[it];
                             if (!(m.x > 0.f)) e[0] = 0.f;
                             if (!(m.y > 0.f)) e[1] = 0.f;
                             if (!(m.z > 0.f)) e[2] = 0.f;
