@@ -342,6 +342,11 @@ void build_graph_from_keys(ntp_ctx* c, uint64_t* keys, int64_t m, int64_t n, boo
     drop_epoch_graph(c);
     c->graph_warm = false;
     c->g_version++;
+    // merge-path unit size T (a graph constant): measured per hop, T = 1024 vs 2048 -- Reddit d_s 44 / 24 / 8:
+    // 2.28 / 1.36 / 0.78 vs 2.29 / 1.42 / 0.86 ms; products d_s 48 / 12: 2.65 / 1.06 vs 2.95 / 1.13; papers bf16
+    // d_s 128 / 16: 107.1 / 24.3 vs 104.9 / 23.5 (more units = more carries on the 111M-vertex graph); 512 and
+    // 256 were slower everywhere.  So 1024 below 10M vertices, 2048 above.
+    g.unit_items = n < 10000000 ? 1024 : 2048;
     if (const char* t = getenv("NTP_UNIT_ITEMS")) g.unit_items = std::max(64, atoi(t));
     g.n = n;
     g.symmetric = symmetric;
