@@ -290,3 +290,21 @@ def test_high_degree_variants_bitwise(name, transposed):
         for d in widths:
             Zs, _ = _run(ctx, np.ascontiguousarray(H[:, :d]), cfg.K, cfg.gamma, cfg.alpha, transposed, dtype=dtype)
             assert torch.equal(Zs, Zfull[:, :d]), (dtype, d)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,d,transposed", [("reddit", 44, False), ("reddit", 44, True), ("products", 48, False)])
+def test_full_size_end_to_end_all_rows(name, d, transposed):
+    """The whole K-hop propagation of a full BASELINE-size graph at the bench's slice width, EVERY output row
+    and column against the oracle's own K-hop run (O3 / O4) at R10's 1e-5 (fp32), denominator M|H|: the
+    bench workload itself (Reddit, K = 2) and the APPNP products shape (K = 10, gamma 0.9, alpha 0.1)."""
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, d, 31)
+    Z, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, transposed=transposed)
+    f = oracle.propagate.propagate_bwd if transposed else oracle.propagate.propagate_fwd
+    ref = f(g, H, cfg.K, cfg.gamma, cfg.alpha)
+    den = f(g, np.abs(H.astype(np.float64)), cfg.K, cfg.gamma, cfg.alpha)
+    assert_r10(Z.double().cpu().numpy(), ref, den, FP32_TOL, f"{name} K={cfg.K} all rows")
+    ctx.close()
