@@ -242,7 +242,7 @@ ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const flo
 #define NTP_M_OVERLAP       2u  /* chunked last hop with the gather on a comm stream (a12) */
 #define NTP_M_HOST_INPUTS   4u  /* X_v/labels_v/train_mask_v are HOST (pinned) pointers;
                                    copied to the device inside the call (e2e path)       */
-#define NTP_M_STAGED       16u  /* inputs come from staging slot (flags >> 8) & 1, filled by
+#define NTP_M_STAGED       16u  /* inputs come from staging slot (flags >> 8) & 3 (< NTP_STAGE_SLOTS), filled by
                                    ntp_stage_inputs (its host->device copy may overlap the
                                    previous epoch); X_v / labels_v / train_mask_v are ignored
                                    except for X_v's shape.  Each slot's epoch is captured as
@@ -250,6 +250,8 @@ ntp_status ntp_gemm_f32(ntp_ctx* ctx, int64_t M, int64_t N, int64_t K, const flo
                                    stream's ready / free events become external event nodes).
                                    NTP_ERR_STATE if the slot was never staged with [V_p x d_in]. */
 #define NTP_M_SLOT_SHIFT    8
+#define NTP_M_SLOT_MASK     3u
+#define NTP_STAGE_SLOTS     3   /* input staging slots: with three, a loop keeps two epochs' copies queued */
 #define NTP_M_DATA_PARALLEL 32u /* NEXT-4 baseline: each rank aggregates its own vertex rows at
                                    full width after an all-gather of the state before every hop,
                                    instead of feature slices (same function; load follows the rows'
@@ -333,9 +335,12 @@ ntp_status ntp_train_epoch_gat(ntp_ctx* ctx, const ntp_model* m, const ntp_tenso
 /* Input staging for end-to-end training loops: enqueues the host->device copy of one epoch's
  * inputs (this rank's rows: X_host [V_p x d_in] fp32 with row pitch ldx elements, labels int32[V_p],
  * train mask uint8[V_p]; pinned host memory for a truly asynchronous copy) into library-owned slot
- * `slot` (0 or 1) on the library's copy stream and returns at once.  The copy waits until the last
- * epoch that read the slot has finished with it, so a loop can stage epoch i+1's inputs while epoch
- * i computes and then call ntp_train_epoch with NTP_M_STAGED | (i+1 % 2) << NTP_M_SLOT_SHIFT.
+ * `slot` (0 .. NTP_STAGE_SLOTS-1) on the library's copy stream and returns at once.  The copy waits
+ * until the last epoch that read the slot has finished with it, so a loop can stage epoch i+1's (and
+ * i+2's) inputs while epoch i computes and then call ntp_train_epoch with
+ * NTP_M_STAGED | (slot of that epoch) << NTP_M_SLOT_SHIFT.  Staging two epochs ahead over three slots
+ * keeps the copy engine busy back to back: epoch i+2's copy no longer waits for epoch i's end, so a
+ * loop whose copy and epoch take about as long runs at max(copy, epoch) instead of paying their jitter.
  * Host buffers must stay valid until that epoch returns.  NTP_ERR_ARG / NTP_ERR_STATE as usual. */
 ntp_status ntp_stage_inputs(ntp_ctx* ctx, int slot, const float* X_host, int64_t rows, int32_t d_in, int64_t ldx,
                             const int32_t* labels_host, const uint8_t* train_mask_host);

@@ -203,9 +203,11 @@ ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint
         NTP_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
         NTP_CUDA(cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
         NTP_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NTP_STAGE_SLOTS; ++i) {
             NTP_CUDA(cudaEventCreateWithFlags(&c->st_ready[i], cudaEventDisableTiming));
             NTP_CUDA(cudaEventCreateWithFlags(&c->st_free[i], cudaEventDisableTiming));
+        }
+        for (int i = 0; i < 2; ++i) {
             NTP_CUDA(cudaEventCreateWithFlags(&c->hs_ready[i], cudaEventDisableTiming));
             NTP_CUDA(cudaEventCreateWithFlags(&c->hs_free[i], cudaEventDisableTiming));
         }
@@ -244,9 +246,11 @@ void ntp_destroy(ntp_ctx* c) {
     for (auto& e : c->ov_ev)
         if (e) cudaEventDestroy(e);
     if (c->s_copy) cudaStreamSynchronize(c->s_copy);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NTP_STAGE_SLOTS; ++i) {
         if (c->st_ready[i]) cudaEventDestroy(c->st_ready[i]);
         if (c->st_free[i]) cudaEventDestroy(c->st_free[i]);
+    }
+    for (int i = 0; i < 2; ++i) {
         if (c->hs_ready[i]) cudaEventDestroy(c->hs_ready[i]);
         if (c->hs_free[i]) cudaEventDestroy(c->hs_free[i]);
     }
@@ -639,7 +643,9 @@ ntp_status ntp_train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v
     NTP_CHECK(W1->rows == m->hid && W1->cols == m->C && W1->ld == m->C, NTP_ERR_SHAPE, "W1 must be dense [hid x C]");
     NTP_CHECK(m->C <= 256, NTP_ERR_CONFIG, "C = %d > 256 classes is not supported", m->C);
     if (m->flags & NTP_M_STAGED) {
-        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
+        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & NTP_M_SLOT_MASK);
+        NTP_CHECK(slot < NTP_STAGE_SLOTS, NTP_ERR_ARG, "staging slot %d out of range (0..%d)", slot,
+                  NTP_STAGE_SLOTS - 1);
         NTP_CHECK(c->st_rows[slot] == V_p && c->st_d_in[slot] == m->d_in, NTP_ERR_STATE,
                   "staging slot %d holds no inputs of shape [%lld x %d] (ntp_stage_inputs first)", slot, (long long)V_p,
                   m->d_in);
@@ -688,7 +694,7 @@ ntp_status ntp_stage_inputs(ntp_ctx* c, int slot, const float* X_host, int64_t r
     NTP_API_BEGIN(c)
     need_graph(c);
     NTP_CHECK(X_host && labels_host && train_mask_host, NTP_ERR_ARG, "null argument");
-    NTP_CHECK(slot == 0 || slot == 1, NTP_ERR_ARG, "slot must be 0 or 1");
+    NTP_CHECK(slot >= 0 && slot < NTP_STAGE_SLOTS, NTP_ERR_ARG, "slot must be in 0..%d", NTP_STAGE_SLOTS - 1);
     NTP_CHECK(d_in > 0 && ldx >= d_in && rows == rank_rows(c, c->g.n), NTP_ERR_SHAPE, "X_host must be [V_p x d_in]");
     NTP_CUDA(cudaSetDevice(c->device));
     stage_inputs(c, slot, X_host, rows, d_in, ldx, labels_host, train_mask_host);

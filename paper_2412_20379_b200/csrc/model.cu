@@ -405,7 +405,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     const uint8_t* msk = mask_v;
     if (m->flags & NTP_M_STAGED) {
         // inputs staged by ntp_stage_inputs (copy stream); this epoch waits for that copy
-        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
+        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & NTP_M_SLOT_MASK);
         NTP_CHECK(c->st_rows[slot] == V_p && c->st_d_in[slot] == m->d_in, NTP_ERR_STATE,
                   "staging slot %d holds no inputs of this shape", slot);
         NTP_CUDA(cudaStreamWaitEvent(s, c->st_ready[slot], c->capturing ? cudaEventWaitExternal : 0));
@@ -912,7 +912,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
     NTP_LAUNCH_CHECK();
     count_launch(c);
     if (m->flags & NTP_M_STAGED) {   // the slot may be refilled once this epoch is done with it
-        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u);
+        const int slot = (int)((m->flags >> NTP_M_SLOT_SHIFT) & NTP_M_SLOT_MASK);
         NTP_CUDA(cudaEventRecordWithFlags(c->st_free[slot], s, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
         c->st_free_rec[slot] = true;
     }
@@ -930,7 +930,7 @@ void drop_epoch_graph(ntp_ctx* c) {
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     c->graph_exec = nullptr;
     c->graph_valid = false;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NTP_STAGE_SLOTS; ++i) {
         if (c->sg_exec[i]) cudaGraphExecDestroy(c->sg_exec[i]);
         c->sg_exec[i] = nullptr;
         c->sg_valid[i] = false;
@@ -1037,7 +1037,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     // graph cache entry: the plain epoch, or one per staging slot (whose buffers the graph bakes in; the
     // copy stream's ready / free events become external event nodes)
     const bool staged = (m->flags & NTP_M_STAGED) != 0;
-    const int sl = staged ? (int)((m->flags >> NTP_M_SLOT_SHIFT) & 1u) : 0;
+    const int sl = staged ? (int)((m->flags >> NTP_M_SLOT_SHIFT) & NTP_M_SLOT_MASK) : 0;
     if (staged) {
         key.ptrs[0] = c->st_X[sl].p;
         key.ptrs[1] = c->st_y[sl].p;

@@ -159,16 +159,16 @@ struct ntp_ctx {
     // coupled (naive TP) epoch: Z^l, H^l per layer, dA / dZ scratch, padded weights
     ntp::DevBuf cp_Z[NTP_MAX_LAYERS + 1], cp_H[NTP_MAX_LAYERS + 1], cp_A, cp_B, cp_W;
     // input staging slots (ntp_stage_inputs): X [V_p x round4(d_in)], raw host-pitch copy, labels, mask
-    ntp::DevBuf st_X[2], st_raw[2], st_y[2], st_m[2];
+    ntp::DevBuf st_X[NTP_STAGE_SLOTS], st_raw[NTP_STAGE_SLOTS], st_y[NTP_STAGE_SLOTS], st_m[NTP_STAGE_SLOTS];
     cudaStream_t s_copy = nullptr;
-    cudaEvent_t st_ready[2] = {}, st_free[2] = {};
+    cudaEvent_t st_ready[NTP_STAGE_SLOTS] = {}, st_free[NTP_STAGE_SLOTS] = {};
     // NTP_M_HOST_STREAM: X_v stays in (pinned) host memory; row chunks stream through a 2-slot device ring
     ntp::DevBuf hs_ring;
     cudaEvent_t hs_ready[2] = {}, hs_free[2] = {};
     bool hs_used[2] = {false, false};
-    bool st_free_rec[2] = {false, false};
-    int64_t st_rows[2] = {0, 0}, st_ld[2] = {0, 0};
-    int32_t st_d_in[2] = {0, 0};
+    bool st_free_rec[NTP_STAGE_SLOTS] = {};
+    int64_t st_rows[NTP_STAGE_SLOTS] = {}, st_ld[NTP_STAGE_SLOTS] = {};
+    int32_t st_d_in[NTP_STAGE_SLOTS] = {};
     // peer-direct layouts (CUDA IPC windows over NVLink), see layout.cu
     int p2p_state = 0;                      // 0 not set up, 1 usable, -1 unavailable
     ntp::DevBuf p2p_split, p2p_gath;        // this rank's windows (zero-initialised)
@@ -190,13 +190,13 @@ struct ntp_ctx {
     bool graph_warm = false, graph_valid = false;
     cudaGraphExec_t graph_exec = nullptr;
     // captured staged epochs, one per input slot (NTP_M_STAGED; the slot's buffers are baked in)
-    EpochKey sg_key[2]{};
-    bool sg_warm[2] = {false, false}, sg_valid[2] = {false, false};
-    cudaGraphExec_t sg_exec[2] = {nullptr, nullptr};
-    int sg_hops[2] = {0, 0};
-    int64_t sg_launches[2] = {0, 0};
-    int64_t graph_gen = -1, sg_gen[2] = {-1, -1};   // alloc_generation() at capture
-    int64_t graph_wire[8] = {}, sg_wire[2][8] = {};  // wire bytes counted while recording (replays reuse them)
+    EpochKey sg_key[NTP_STAGE_SLOTS]{};
+    bool sg_warm[NTP_STAGE_SLOTS] = {}, sg_valid[NTP_STAGE_SLOTS] = {};
+    cudaGraphExec_t sg_exec[NTP_STAGE_SLOTS] = {};
+    int sg_hops[NTP_STAGE_SLOTS] = {};
+    int64_t sg_launches[NTP_STAGE_SLOTS] = {};
+    int64_t graph_gen = -1, sg_gen[NTP_STAGE_SLOTS] = {-1, -1, -1};   // alloc_generation() at capture
+    int64_t graph_wire[8] = {}, sg_wire[NTP_STAGE_SLOTS][8] = {};  // wire bytes counted while recording (replays reuse them)
     // bytes handed to the transport (NCCL send/recv, all-gather, peer stores) per layout change of the
     // current epoch: 0 v2f fwd, 1 f2v fwd, 2 v2f bwd, 3 f2v bwd (wire_phase selects the entry)
     int64_t wire_sent[4] = {}, wire_recv[4] = {};

@@ -29,6 +29,7 @@ NTP_LAYOUT_VERTEX, NTP_LAYOUT_FEATURE = 0, 1
 NTP_G_SYMMETRIC, NTP_G_VALIDATE, NTP_G_REORDER = 1, 2, 4
 NTP_M_W1_AFTER_PROP, NTP_M_OVERLAP, NTP_M_HOST_INPUTS, NTP_M_P2P_LAYOUTS = 1, 2, 4, 8
 NTP_M_STAGED, NTP_M_SLOT_SHIFT, NTP_M_DATA_PARALLEL, NTP_M_HOST_STREAM = 16, 8, 32, 64
+NTP_STAGE_SLOTS = 3
 PHASES = ["mlp_fwd", "v2f_fwd", "prop_fwd", "f2v_fwd", "loss", "v2f_bwd", "prop_bwd", "f2v_bwd",
           "mlp_bwd", "allreduce", "sgd", "total"]
 

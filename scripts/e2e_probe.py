@@ -35,3 +35,20 @@ for mode in ("device", "staged"):
     hop = sum(r["spmm_ms"] for r in reps) / sum(r["spmm_launches"] for r in reps)
     ph = {k: round(sum(r["ms"][k] for r in reps) / len(reps), 3) for k in reps[0]["ms"]}
     print(mode, "hop ms", round(hop, 4), ph, flush=True)
+
+# the copy engine's H2D under a running epoch: one 564 MB pinned copy on a side stream while epochs run
+src = torch.empty(564_008_265 // 4, dtype=torch.float32).pin_memory()
+dst = torch.empty_like(src, device="cuda")
+side = torch.cuda.Stream()
+for load in (False, True, True):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(side):
+        e0.record(side)
+        dst.copy_(src, non_blocking=True)
+        e1.record(side)
+    if load:
+        for _ in range(2):
+            ctx.train_epoch(model, X, y, m, W0, W1)
+    torch.cuda.synchronize()
+    print("copy under epochs" if load else "copy alone", round(e0.elapsed_time(e1), 3), "ms", flush=True)

@@ -164,10 +164,14 @@ def test_epoch_head_fused_matches_unfused(monkeypatch):
     assert abs(out[0] - out[1]) <= 1e-3 * abs(out[1])
 
 
-def test_epoch_staged_inputs_same_result():
-    """ntp_stage_inputs + NTP_M_STAGED (the e2e loop: epoch i+1's inputs copied while epoch i runs, two
-    alternating slots) gives bit-identical losses and weights to device-resident inputs."""
-    a, W0a, W1a, _, _ = _train_gpu("tiny_dir", 6)
+@pytest.mark.parametrize("ahead", [1, 2])
+def test_epoch_staged_inputs_same_result(ahead):
+    """ntp_stage_inputs + NTP_M_STAGED (the e2e loop: the inputs of epochs i+1 .. i+ahead copied while epoch
+    i runs, ahead + 1 rotating slots) gives bit-identical losses and weights to device-resident inputs;
+    a slot outside 0..NTP_STAGE_SLOTS-1 is refused."""
+    from paper_2412_20379_b200 import ntp
+    E = 9
+    a, W0a, W1a, _, _ = _train_gpu("tiny_dir", E)
     cfg = synth.get_config("tiny_dir")
     ctx = ntp_ctx_for("tiny_dir")
     X, y, m = synth.config_inputs(cfg)
@@ -176,14 +180,20 @@ def test_epoch_staged_inputs_same_result():
     model["lr"] = cfg.lr * 50
     Xp, yp, mp = (torch.from_numpy(t).pin_memory() for t in (X, y, m))
     W0d, W1d = torch.from_numpy(W0).cuda(), torch.from_numpy(W1).cuda()
-    ctx.stage_inputs(0, Xp, yp, mp)
+    ns = ahead + 1
+    for i in range(ahead):
+        ctx.stage_inputs(i, Xp, yp, mp)
     losses = []
-    for i in range(6):   # eager per slot, then each slot's captured epoch graph, then replays
-        if i + 1 < 6:
-            ctx.stage_inputs((i + 1) % 2, Xp, yp, mp)
-        losses.append(ctx.train_epoch(model, Xp, yp, mp, W0d, W1d, staged_slot=i % 2)["loss"])
+    for i in range(E):   # eager per slot, then each slot's captured epoch graph, then replays
+        if i + ahead < E:
+            ctx.stage_inputs((i + ahead) % ns, Xp, yp, mp)
+        losses.append(ctx.train_epoch(model, Xp, yp, mp, W0d, W1d, staged_slot=i % ns)["loss"])
     assert losses == a
     assert np.array_equal(W0d.cpu().numpy(), W0a) and np.array_equal(W1d.cpu().numpy(), W1a)
+    with pytest.raises(ntp.NtpError):
+        ctx.stage_inputs(ntp.NTP_STAGE_SLOTS, Xp, yp, mp)
+    with pytest.raises(ntp.NtpError):
+        ctx.train_epoch(model, Xp, yp, mp, W0d, W1d, staged_slot=ntp.NTP_STAGE_SLOTS)
 
 
 @pytest.mark.parametrize("chunk", ["0", "1000"])

@@ -64,3 +64,14 @@ def test_no_gpu_create_reports_error(ntp):
         pytest.skip("GPU present")
     with pytest.raises(ntp.NtpError):
         ntp.Context()
+
+
+def test_binding_constants_match_header(ntp):
+    """Every NTP_* integer macro the binding mirrors has the header's value (include/ntp.h)."""
+    hdr = open(os.path.join(ROOT, "include", "ntp.h")).read()
+    macros = dict(re.findall(r"^#define\s+(NTP_\w+)\s+\(?(-?\d+)u?\)?", hdr, flags=re.M))
+    mirrored = [k for k in dir(ntp) if k.startswith("NTP_") and isinstance(getattr(ntp, k), int) and k in macros]
+    assert len(mirrored) >= 10
+    for k in mirrored:
+        assert getattr(ntp, k) == int(macros[k]), k
+    assert ntp.NTP_STAGE_SLOTS == int(macros["NTP_STAGE_SLOTS"])
