@@ -174,6 +174,7 @@ def oracle_epoch_time(cfg, epochs=1):
     weights the GPU run starts from; returns its per-epoch losses too (the bench line's parity check), and
     a single-thread one-hop timing on a 2% row sample, extrapolated to the whole graph."""
     import oracle
+    use_all_host_cores()
     t0 = time.time()
     g = oracle.graph.graph_from_config(cfg)
     t_graph = time.time() - t0
@@ -206,6 +207,7 @@ def oracle_sampled_estimate(cfg, frac=0.01, cols=4):
     separability -- and runs the MLP forward/backward and the loss on the same row sample; the epoch
     time is EXTRAPOLATED linearly (x 1/frac rows, x w/cols columns, x 2K hops)."""
     import oracle
+    use_all_host_cores()
     rng = np.random.default_rng(0)
     rows = np.sort(rng.choice(cfg.n, size=max(1, int(cfg.n * frac)), replace=False)).astype(np.int64)
     t0 = time.time()
@@ -243,12 +245,27 @@ def oracle_sampled_estimate(cfg, frac=0.01, cols=4):
             "sample_rows": int(rows.size), "sample_arcs": sample_arcs, "cols": cols, "frac": frac}
 
 
+def use_all_host_cores():
+    """The oracle runs on every host core this process may use: torchrun exports OMP_NUM_THREADS=1 to its
+    workers, which would otherwise pin the reference arm (rank 0) and its BLAS to one thread."""
+    import oracle
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    oracle.lib.oracle_set_num_threads(n)
+    try:
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(n)
+    except Exception:
+        pass
+    return n
+
+
 def run_reference(args, cfg, rank):
     if rank != 0:
         return
     w = cfg.w
     times = []
     import oracle
+    use_all_host_cores()
     g = oracle.graph.graph_from_config(cfg)
     X, y, m = synth.config_inputs(cfg)
     W0, W1 = synth.model_weights(cfg)
@@ -286,11 +303,14 @@ def run_gat(args, ctx, cfg, X, y, msk, n, nnz, world, rank, dist, barrier, strea
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = []
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
     ev0.record(stream)
     for _ in range(args.steps):
         reps.append(ctx.train_epoch_gat(model, X, y, msk, W0, W1, A, stream=stream))
     ev1.record(stream)
     barrier()
+    clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     hop = sum(r["spmm_ms"] for r in reps) / max(1, sum(r["spmm_launches"] for r in reps))
     if dist is not None:
@@ -308,7 +328,7 @@ def run_gat(args, ctx, cfg, X, y, msk, n, nnz, world, rank, dist, barrier, strea
                        "nnz": nnz, "w": w, "K": cfg.K, "gamma": cfg.gamma, "P": world},
             "hop_ms": hop, "loss": reps[-1]["loss"],
             "phase_ms": {k: round(sum(r["ms"][k] for r in reps) / len(reps), 4) for k in reps[0]["ms"]},
-            "gpu_launches": int(sum(r["kernel_launches"] for r in reps))}
+            "clocks": clk, "gpu_launches": int(sum(r["kernel_launches"] for r in reps))}
     print(json.dumps(line), flush=True)
 
 
@@ -327,11 +347,14 @@ def run_coupled(args, ctx, cfg, X, y, msk, n, nnz, world, rank, local, dist, bar
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = []
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
     ev0.record(stream)
     for _ in range(args.steps):
         reps.append(ctx.train_epoch_coupled(widths, cfg.lr, X, y, msk, Ws, dtype=dt, stream=stream))
     ev1.record(stream)
     barrier()
+    clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -359,7 +382,7 @@ def run_coupled(args, ctx, cfg, X, y, msk, n, nnz, world, rank, local, dist, bar
                        "note": "naive TP: a split and a gather around every layer's aggregation (4L-2 = 6 for L=2, "
                                "P:696); decoupled: 4 per epoch at the propagated width w"},
             "phase_ms": {"total": r["ms_total"], "aggregation": r["ms_agg"]},
-            "gpu_launches": int(sum(x["kernel_launches"] for x in reps))}
+            "clocks": clk, "gpu_launches": int(sum(x["kernel_launches"] for x in reps))}
     print(json.dumps(line), flush=True)
 
 
@@ -664,12 +687,18 @@ def main():
         names = [("v2f_fwd", 0, "pack + all-to-all"), ("f2v_fwd", 1, "all-to-all"), ("v2f_bwd", 2, "all-to-all"),
                  ("f2v_bwd", 3, "all-to-all + unpack")]
         nvlink = {}
+        # with --overlap the exchange runs in chunks under the hops (and the data-parallel baseline all-gathers
+        # before every hop), so a phase's time is not the transfer's: bytes only, see a2a_standalone for the rate
+        confined = not args.overlap and args.engine == "decoupled"
         for ph, i, what in names:
             t_ph = allmax(phase[ph])
             b = reps[-1]["bytes_sent"][i]
+            ok = confined and bool(t_ph)
             nvlink[ph] = {"ms": t_ph, "bytes_sent_per_rank": b, "what": what,
-                          "GBps_per_direction": (b / (t_ph * 1e-3) / 1e9) if t_ph else None,
-                          "frac_of_900GBps": (b / (t_ph * 1e-3) / 1e9 / 900.0) if t_ph else None}
+                          "GBps_per_direction": (b / (t_ph * 1e-3) / 1e9) if ok else None,
+                          "frac_of_900GBps": (b / (t_ph * 1e-3) / 1e9 / 900.0) if ok else None}
+            if not confined:
+                nvlink[ph]["note"] = "exchange overlapped with other phases: no per-phase rate"
     # the layout change timed on its own (SURVEY §8(d) "measure the a2a separately at the same counts"):
     # ntp_layout_v2f of this rank's [V_p x w] rows (pack + block all-to-all) into the feature slice
     a2a = None
@@ -700,19 +729,35 @@ def main():
     own_hop = spmm_ms / max(spmm_n, 1)
     spmm_avg = allmax(own_hop)
     hop_min = own_hop if dist is None else -allmax(-own_hop)   # per-rank hop time spread (load balance)
+    # items (gathered rows: self + arcs) one hop launch processes: the whole graph on every feature slice; in the
+    # data-parallel baseline only this rank's destination rows -- its roofline is the critical (slowest) rank's
+    hop_items = nnz + n
+    if args.engine == "dp":
+        rp = ctx.copy_csr(False)[0]
+        lo, hi = min(row0, n), min(row0 + V_p, n)
+        own_items = int(rp[hi] - rp[lo]) + (hi - lo)
+        if dist is None:
+            hop_items = own_items
+        else:
+            t = torch.tensor([own_hop, float(own_items)], dtype=torch.float64, device="cuda")
+            allt = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(allt, t)
+            crit = max(allt, key=lambda x: float(x[0]))
+            hop_items = int(crit[1])
 
     if rank == 0:
         w = cfg.w
         esz = 2 if dt == ntp.NTP_BF16 else 4
         ge = 2 * cfg.K * nnz * w / (ms * 1e-3) / 1e9
         bh, bmodel = hop_bytes(n, nnz, d_s, esz, sym, cfg.alpha, l2_size)
+        bh = bh * hop_items / (nnz + n)          # dp: the critical rank's share of the arcs
         achieved = bh / (spmm_avg * 1e-3) / 1e9
         traffic = load_traffic(args.config, world, dtype_name)
         l2b = l2_gather_bytes(nnz, n, d_s, esz)
         gc = gather_ceiling(n, d_s * esz, l2_size)
         gather_line = None
         if gc:
-            rows_ps = (nnz + n) / (spmm_avg * 1e-3)
+            rows_ps = hop_items / (spmm_avg * 1e-3)
             gather_line = dict(gc, achieved_rows_per_s=rows_ps, frac=rows_ps / gc["rows_per_s"],
                                row_bytes=d_s * esz)
         # The hop's roofline by residency: a slice that exceeds L2 is HBM-bound (measured DRAM
@@ -739,7 +784,8 @@ def main():
                                     f"{rb} B ({gather_line['source']}, scripts/l2_probe.cu); MEASURED_PEAKS.json "
                                     "has no L2 figure",
                         traffic=traffic, bytes_model="gathered rows (self + every arc) x row bytes, per launch",
-                        algorithmic_bytes_per_launch=(nnz + n) * rb, l2_gather_GBps=l2b / (spmm_avg * 1e-3) / 1e9,
+                        algorithmic_bytes_per_launch=hop_items * rb,
+                        l2_gather_GBps=l2b * hop_items / (nnz + n) / (spmm_avg * 1e-3) / 1e9,
                         hbm=hbm, gather=gather_line)
         else:
             roof = dict(common, bound="hbm", **hbm, gather=gather_line)

@@ -389,6 +389,7 @@ ntp_status ntp_train_epoch_coupled(ntp_ctx* ctx, const ntp_coupled_model* m, con
  *   NTP_SPMM_OCC=0|1|2   occupancy variant; NTP_UNIT_ITEMS=T merge-path unit size; NTP_L1_CARVEOUT=0
  *   NTP_SPMM_BULK=0|1    bulk-copy gather for wide rows off / forced (auto: rows of >= 1 KB)
  *   NTP_REORDER_MODE=m   degree-class granularity of NTP_G_REORDER; NTP_P2P=0 disables peer windows
+ *   NTP_GAT_PERMUTE=1    GAT: permute the coefficients into out-CSR order instead of re-deriving them
  * Every switch keeps the arithmetic of the reduction order except NTP_UNIT_ITEMS (it changes which
  * rows are cut across units, so results stay within tolerance but not bitwise). */
 

@@ -18,11 +18,15 @@
 //     costs one pass over col_idx; shipping them would move 4 bytes per arc over NVLink.)
 //   * The weighted hop is the merge-path SpMM kernel's WT variant (spmm.cu): per-arc coefficients loaded
 //     with the column indices, same pipeline and fixed reduction order; the backward runs over the out-CSR
-//     with the coefficients permuted into its order (perm: out-CSR arc -> in-CSR arc, built once).
-//   * Backward: dalpha_uv = gamma sum_k G^k_v . Z^{k-1}_u is an SDDMM on every slice (partial dot products
-//     over d_s columns), summed over slices and -- one allreduce of n + nnz floats -- over ranks; softmax /
-//     LeakyReLU backward and the per-vertex sums ps (over out-arcs, via the out-CSR) and pd (over in-arcs)
-//     then give dz += ps a_src + pd a_dst and da_src = sum ps z, da_dst = sum pd z (rank-1 terms).
+//     with the coefficients in its order, re-derived from each destination's softmax (max, sum).
+//   * Backward without per-arc gradients.  With beta_uv = alpha_uv LeakyReLU'(s_uv) the softmax / LeakyReLU
+//     backward ds_uv = beta_uv (dalpha_uv - w_v), w_v = sum_u alpha_uv dalpha_uv, only enters through the sums
+//     ps_u = sum_v ds_uv and pd_v = sum_u ds_uv, and since dalpha_uv = gamma sum_k G^k_v . Z^{k-1}_u these are
+//     per-vertex dot products of hop outputs: w_v = sum_k G^k.Z^k, pd_v = sum_k G^k.Y^k - w_v b_v and
+//     ps_u = sum_k Z^{k-1}.X^k - sum_v beta_uv w_v, where Y^k = gamma A_beta Z^{k-1} (forward, one more
+//     weighted hop per level) and X^k = gamma A_beta^T G^k (backward, likewise), b_v = sum_u beta_uv.  Each
+//     slice contributes partial dots; one allreduce of 3n floats sums them over ranks (the SDDMM form moved
+//     n + nnz).  dz += ps a_src + pd a_dst and da_src = sum ps z, da_dst = sum pd z (rank-1 terms).
 // Coefficient layout everywhere: [n self loops | nnz arcs in in-CSR order] (the oracle's arcs() order).
 #include <algorithm>
 #include <cmath>
@@ -34,6 +38,27 @@ namespace ntp {
 namespace {
 
 __device__ __forceinline__ float leaky(float x, float slope) { return x > 0.f ? x : slope * x; }
+
+// Coefficient words: alpha_uv with the sign bit set where s_uv <= 0, so one word gives alpha = |w| and
+// beta = alpha * LeakyReLU'(s) = (w < 0 ? slope : 1) * |w| (the dual hop decodes it the same way, spmm.cu)
+__device__ __forceinline__ float coef_word(float a, bool pos) { return pos ? a : -a; }
+__device__ __forceinline__ float word_beta(float w, float slope) {
+    const float a = __int_as_float(__float_as_int(w) & 0x7fffffff);
+    return __float_as_int(w) < 0 ? slope * a : a;
+}
+
+// one 16-byte vector of a slice row as fp32 values (fp32: 4, bf16: 8 widened exactly)
+template <typename T> __device__ __forceinline__ void load16(const void* p, float (&v)[16 / sizeof(T)]) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(w[i]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
+    }
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -106,9 +131,10 @@ struct BlockRed {
 };
 
 // G2 softmax over a destination's self loop + in-arcs, two passes: (1) e = LeakyReLU(f_u + g_v) -- the only
-// gather of f -- stored in alpha's slot, an online max / sum per thread combined over the group, and the
-// sign of s_uv (> 0) as one bit per arc (the backward's LeakyReLU'), ballot-packed per warp; (2) alpha =
-// exp(e - m) / sum from the stored e (coalesced).
+// gather of f -- stored in alpha's slot and an online max / sum per thread combined over the group; (2)
+// alpha = exp(e - m) / sum from the stored e (coalesced), beta = alpha * LeakyReLU'(s) (1 where s > 0, i.e.
+// where e > 0, else the slope) and b_v = sum of v's betas (fixed order).  (max, sum) are kept per
+// destination: the out-CSR order re-derives its coefficients from them (gat_coef_t_kernel).
 __device__ __forceinline__ void online_add(float& m, float& sm, float e) {
     if (e > m) {
         sm = sm * expf(m - e) + 1.f;
@@ -121,54 +147,55 @@ __device__ __forceinline__ void online_add(float& m, float& sm, float e) {
 template <class Red>
 __device__ void softmax_row(const Red& R, int64_t v, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                             const float* __restrict__ fg, int64_t n, float slope, float* __restrict__ alpha,
-                            uint32_t* __restrict__ pos_bits) {
-    const int lane = threadIdx.x & 31;
+                            float* __restrict__ msum, float* __restrict__ bsum) {
     const float gv = fg[2 * v + 1];
     const float ss = fg[2 * v] + gv;
     const float es = leaky(ss, slope);
-    if (R.t == 0 && ss > 0.f) atomicOr(pos_bits + (v >> 5), 1u << (v & 31));
     const int b = rp[v], e = rp[v + 1];
     float m = -INFINITY, sm = 0.f;
     if (R.t == 0) m = es, sm = 1.f;
-    for (int jb = b + (R.t - lane); jb < e; jb += R.T) {   // this warp's 32 consecutive arcs jb .. jb + 31
-        const int j = jb + lane;
-        bool pos = false;
-        if (j < e) {
-            const float sj = fg[2 * (int64_t)col[j]] + gv;
-            const float ej = leaky(sj, slope);
-            pos = sj > 0.f;
-            alpha[n + j] = ej;
-            online_add(m, sm, ej);
-        }
-        const uint32_t word = __ballot_sync(0xffffffffu, pos);
-        if (lane == 0 && word) {
-            const int64_t a = n + jb;                                // bit index of arc jb
-            atomicOr(pos_bits + (a >> 5), word << (a & 31));
-            if (a & 31) atomicOr(pos_bits + (a >> 5) + 1, word >> (32 - (a & 31)));
-        }
+    for (int j = b + R.t; j < e; j += R.T) {
+        const float ej = leaky(fg[2 * (int64_t)col[j]] + gv, slope);
+        alpha[n + j] = ej;
+        online_add(m, sm, ej);
     }
     R.combine(m, sm);
-    if (R.t == 0) alpha[v] = expf(es - m) / sm;
-    for (int j = b + R.t; j < e; j += R.T) alpha[n + j] = expf(alpha[n + j] - m) / sm;
+    float bs = 0.f;
+    if (R.t == 0) {
+        const float a = expf(es - m) / sm;
+        alpha[v] = coef_word(a, ss > 0.f);
+        bs = ss > 0.f ? a : slope * a;
+        msum[2 * v] = m;
+        msum[2 * v + 1] = sm;
+    }
+    for (int j = b + R.t; j < e; j += R.T) {
+        const float ej = alpha[n + j];
+        const float a = expf(ej - m) / sm;
+        alpha[n + j] = coef_word(a, ej > 0.f);
+        bs += ej > 0.f ? a : slope * a;
+    }
+    bs = R.sum(bs);
+    if (R.t == 0) bsum[v] = bs;
 }
 
 __global__ void gat_softmax_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                    const float* __restrict__ fg, int64_t n, float slope, float* __restrict__ alpha,
-                                   uint32_t* __restrict__ pos_bits) {
+                                   float* __restrict__ msum, float* __restrict__ bsum) {
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const WarpRed R;
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps)
-        if (rp[v + 1] - rp[v] <= kBigDeg) softmax_row(R, v, rp, col, fg, n, slope, alpha, pos_bits);
+        if (rp[v + 1] - rp[v] <= kBigDeg) softmax_row(R, v, rp, col, fg, n, slope, alpha, msum, bsum);
 }
 
 __global__ void __launch_bounds__(256) gat_softmax_big_kernel(const int32_t* __restrict__ big, int32_t nbig,
                                                               const int32_t* __restrict__ rp,
                                                               const int32_t* __restrict__ col,
                                                               const float* __restrict__ fg, int64_t n, float slope,
-                                                              float* __restrict__ alpha, uint32_t* __restrict__ pos_bits) {
+                                                              float* __restrict__ alpha, float* __restrict__ msum,
+                                                              float* __restrict__ bsum) {
     __shared__ float sh[32];
     const BlockRed R(sh);
-    for (int i = blockIdx.x; i < nbig; i += gridDim.x) softmax_row(R, big[i], rp, col, fg, n, slope, alpha, pos_bits);
+    for (int i = blockIdx.x; i < nbig; i += gridDim.x) softmax_row(R, big[i], rp, col, fg, n, slope, alpha, msum, bsum);
 }
 
 // rows of more than kBigDeg arcs (list built once per graph; order irrelevant: rows are independent)
@@ -178,7 +205,7 @@ __global__ void gat_big_rows_kernel(const int32_t* __restrict__ rp, int64_t n, i
         if (rp[v + 1] - rp[v] > kBigDeg) list[atomicAdd(cnt, 1)] = (int32_t)v;
 }
 
-// out-CSR arc j' (row u, column v) -> its in-CSR index (u's position in row v)
+// out-CSR arc j' (row u, column v) -> its in-CSR index (u's position in row v); dev switch NTP_GAT_PERMUTE only
 __global__ void gat_perm_kernel(const int32_t* __restrict__ rp_in, const int32_t* __restrict__ col_in,
                                 const int32_t* __restrict__ rp_out, const int32_t* __restrict__ col_out, int64_t n,
                                 int32_t* __restrict__ perm) {
@@ -198,153 +225,133 @@ __global__ void gat_perm_kernel(const int32_t* __restrict__ rp_in, const int32_t
     }
 }
 
+// Dev switch NTP_GAT_PERMUTE=1: the plain permutation (the re-derivation below must match it bitwise;
+// tests/test_gpu_gat.py).
 __global__ void gat_permute_kernel(const float* __restrict__ a, const int32_t* __restrict__ perm, int64_t n, int64_t nnz,
                                    float* __restrict__ at) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n + nnz; i += (int64_t)gridDim.x * blockDim.x)
         at[i] = i < n ? a[i] : a[n + perm[i - n]];
 }
 
-template <typename T> __device__ __forceinline__ float ldx(const T* p);
-template <> __device__ __forceinline__ float ldx<float>(const float* p) { return *p; }
-template <> __device__ __forceinline__ float ldx<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
-
-// G4 SDDMM: dalpha[j] (+)= gamma * G_v . Z_u over this slice's d_s columns (arc j: self loops first).
-// Arcs are cut into ranges of kSdArcs consecutive in-CSR arcs, one warp per range (hubs spread over many
-// warps).  A step covers E arcs: lane = e * VPP + c holds 16-byte vector c of arc e's two rows (G_v cached
-// in L1 across a row's arcs, Z_u a random row gather like the hop's), multiplies in fp32 and reduces its
-// group with a fixed xor tree; lane c = 0 of the group writes the arc.  The self loops are a separate
-// streaming pass (j < n).
-constexpr int kSdArcs = 2048;
-
-// One arc per lane: lanes take consecutive arcs of a kSdArcs range (coalesced col / dalpha, the row of a lane
-// advances monotonically), each lane reads the whole slice rows of its arc (NV 16-byte vectors of G_v --
-// shared by the lanes of a row, so L1 -- and of the gathered Z_u) and sums the dot product in column order.
-template <typename T, int NV>
-__global__ void __launch_bounds__(256) gat_sddmm_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                                        int64_t n, int64_t nnz, const char* __restrict__ G,
-                                                        const char* __restrict__ Z, int32_t nvec, float gamma,
-                                                        float* __restrict__ dalpha, int accumulate) {
-    constexpr int VALS = 16 / sizeof(T);
-    const int64_t ld = (int64_t)nvec * 16;   // NV == nvec, or NV = 16 chunks of a wider row
+// The coefficient words in out-CSR order, re-derived rather than permuted: arc j' (row u, column v) gets
+// alpha = exp(LeakyReLU(f_u + g_v) - m_v) / sum_v from the destination's stored (max, sum), signed by
+// f_u + g_v -- the very operands and operations of softmax_row, so at[n + j'] is bitwise a[n + perm[j']] --
+// with col_out streamed and fg / msum (16 bytes per vertex,
+// L2-resident) gathered, instead of a random 4-byte gather from the nnz-long arrays.  Warps take ranges of
+// kAtArcs consecutive out-arcs (hub rows spread over many warps); self loops are copied.
+constexpr int kAtArcs = 2048;
+__global__ void gat_coef_t_kernel(const int32_t* __restrict__ rp_out, const int32_t* __restrict__ col_out,
+                                  const float* __restrict__ fg, const float* __restrict__ msum,
+                                  const float* __restrict__ a, int64_t n, int64_t nnz, float slope,
+                                  float* __restrict__ at) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    auto elem = [](const uint4& x, int i) {
-        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-        if (sizeof(T) == 4) return __uint_as_float(w[i]);
-        return __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
-    };
-    auto dot = [&](const char* a, const char* b) {
-        float d = 0.f;
-        for (int k0 = 0; k0 < nvec; k0 += NV) {
-            uint4 xa[NV], xb[NV];
-#pragma unroll
-            for (int k = 0; k < NV; ++k) {
-                const bool ok = k0 + k < nvec;
-                xa[k] = ok ? *reinterpret_cast<const uint4*>(a + 16 * (k0 + k)) : make_uint4(0, 0, 0, 0);
-                xb[k] = ok ? __ldg(reinterpret_cast<const uint4*>(b + 16 * (k0 + k))) : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int k = 0; k < NV; ++k)
-#pragma unroll
-                for (int i = 0; i < VALS; ++i) d = fmaf(elem(xa[k], i), elem(xb[k], i), d);
-        }
-        return d;
-    };
-    // self loops: arc v = G_v . Z_v
-    for (int64_t v = warp * 32 + lane; v < n; v += nwarps * 32)
-        dalpha[v] = (accumulate ? dalpha[v] : 0.f) + gamma * dot(G + v * ld, Z + v * ld);
-    const int64_t nranges = (nnz + kSdArcs - 1) / kSdArcs;
+    for (int64_t v = warp * 32 + lane; v < n; v += nwarps * 32) at[v] = a[v];
+    const int64_t nranges = (nnz + kAtArcs - 1) / kAtArcs;
     for (int64_t rg = warp; rg < nranges; rg += nwarps) {
-        const int64_t a0 = rg * kSdArcs, a1 = min(a0 + (int64_t)kSdArcs, nnz);
-        int64_t lo = 0, hi = n;   // v = last row with rp[v] <= a0
+        const int64_t a0 = rg * kAtArcs, a1 = min(a0 + (int64_t)kAtArcs, nnz);
+        int64_t lo = 0, hi = n;   // u = last row with rp_out[u] <= a0
         while (hi - lo > 1) {
             const int64_t mid = (lo + hi) >> 1;
-            if (rp[mid] <= a0) lo = mid;
+            if (rp_out[mid] <= a0) lo = mid;
             else hi = mid;
         }
-        int64_t v = lo;
+        int64_t u = lo;
         for (int64_t j = a0 + lane; j < a1; j += 32) {
-            while (rp[v + 1] <= j) ++v;   // this lane's row (arcs are sorted by destination)
-            const float d = dot(G + v * ld, Z + (int64_t)__ldg(col + j) * ld);
-            dalpha[n + j] = (accumulate ? dalpha[n + j] : 0.f) + gamma * d;
+            while (rp_out[u + 1] <= j) ++u;
+            const int64_t v = __ldg(col_out + j);
+            const float sj = fg[2 * u] + fg[2 * v + 1];
+            const float ej = leaky(sj, slope);
+            const float2 ms = *reinterpret_cast<const float2*>(msum + 2 * v);
+            // __fsub_rn: no contraction of slope * s - m into one FMA (softmax_row subtracts from the stored e)
+            at[n + j] = coef_word(expf(__fsub_rn(ej, ms.x)) / ms.y, ej > 0.f);
         }
     }
 }
 
-// G4 softmax + LeakyReLU backward per destination: ds[j]; pd[v] = sum of v's ds (self + in-arcs).  The
-// LeakyReLU' of every arc comes from the forward's sign bits: no gather of f.
+// G4 per-vertex dot products of one level k and one slice (d_s columns), accumulated over levels and slices:
+//   w_v  += G^k_v . Z^k_v        (= sum_u alpha_uv dalpha_uv: Z^k = gamma A_att Z^{k-1})
+//   gy_v += G^k_v . Y^k_v        (= sum_u beta_uv dalpha_uv,  Y^k = gamma A_beta Z^{k-1})
+//   zx_v += Z^{k-1}_v . X^k_v    (= sum_w beta_vw dalpha_vw over v's out-arcs, X^k = gamma A_beta^T G^k)
+// Eight lanes per row (16-byte vectors strided by 8), a fixed xor tree over the eight: deterministic.
+template <typename T>
+__global__ void gat_dots_kernel(const char* __restrict__ G, const char* __restrict__ Z, const char* __restrict__ Y,
+                                const char* __restrict__ Zp, const char* __restrict__ X, int64_t n, int32_t nvec,
+                                float* __restrict__ w, float* __restrict__ gy, float* __restrict__ zx, int accumulate) {
+    constexpr int VALS = 16 / sizeof(T);
+    const int sub = threadIdx.x & 7;
+    const int64_t ld = (int64_t)nvec * 16;
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x >> 3);
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; v < n; v += groups) {
+        float a = 0.f, b = 0.f, c = 0.f;
+        for (int k = sub; k < nvec; k += 8) {
+            const int64_t off = v * ld + 16 * k;
+            float g[VALS], z[VALS], y[VALS], zp[VALS], x[VALS];
+            load16<T>(G + off, g);
+            load16<T>(Z + off, z);
+            load16<T>(Y + off, y);
+            load16<T>(Zp + off, zp);
+            load16<T>(X + off, x);
+#pragma unroll
+            for (int i = 0; i < VALS; ++i) {
+                a = fmaf(g[i], z[i], a);
+                b = fmaf(g[i], y[i], b);
+                c = fmaf(zp[i], x[i], c);
+            }
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (sub == 0) {
+            w[v] = accumulate ? w[v] + a : a;
+            gy[v] = accumulate ? gy[v] + b : b;
+            zx[v] = accumulate ? zx[v] + c : c;
+        }
+    }
+}
+
+// G4 softmax + LeakyReLU backward without per-arc gradients: with ds_uv = beta_uv (dalpha_uv - w_v),
+//   ps_u = sum_v ds_uv = zx_u - q_u,  q_u = sum_v beta_uv w_v (out-CSR row u, self loop included)
+//   pd_v = sum_u ds_uv = gy_v - w_v b_v
 template <class Red>
-__device__ void softmax_bwd_row(const Red& R, int64_t v, const int32_t* __restrict__ rp,
-                                const uint32_t* __restrict__ pos_bits, const float* __restrict__ alpha,
-                                const float* __restrict__ dalpha, int64_t n, float slope, float* __restrict__ ds,
-                                float* __restrict__ pd) {
-    auto pos = [&](int64_t a) { return (pos_bits[a >> 5] >> (a & 31)) & 1u; };
-    const int b = rp[v], e = rp[v + 1];
-    float w = R.t == 0 ? alpha[v] * dalpha[v] : 0.f;
-    for (int j = b + R.t; j < e; j += R.T) w = fmaf(alpha[n + j], dalpha[n + j], w);
-    w = R.sum(w);
-    float acc = 0.f;
+__device__ void pspd_row(const Red& R, int64_t u, const int32_t* __restrict__ rp_out, const int32_t* __restrict__ col_out,
+                         const float* __restrict__ bt, const float* __restrict__ w, const float* __restrict__ gy,
+                         const float* __restrict__ zx, const float* __restrict__ bsum, int64_t n, float slope,
+                         float* __restrict__ ps, float* __restrict__ pd) {
+    float q = R.t == 0 ? word_beta(bt[u], slope) * w[u] : 0.f;
+    for (int j = rp_out[u] + R.t; j < rp_out[u + 1]; j += R.T) q = fmaf(word_beta(bt[n + j], slope), w[col_out[j]], q);
+    q = R.sum(q);
     if (R.t == 0) {
-        const float d = alpha[v] * (dalpha[v] - w) * (pos(v) ? 1.f : slope);
-        ds[v] = d;
-        acc = d;
+        ps[u] = zx[u] - q;
+        pd[u] = gy[u] - w[u] * bsum[u];
     }
-    for (int j = b + R.t; j < e; j += R.T) {
-        const float d = alpha[n + j] * (dalpha[n + j] - w) * (pos(n + j) ? 1.f : slope);
-        ds[n + j] = d;
-        acc += d;
-    }
-    acc = R.sum(acc);
-    if (R.t == 0) pd[v] = acc;
 }
 
-__global__ void gat_softmax_bwd_kernel(const int32_t* __restrict__ rp, const uint32_t* __restrict__ pos_bits,
-                                       const float* __restrict__ alpha, const float* __restrict__ dalpha, int64_t n,
-                                       float slope, float* __restrict__ ds, float* __restrict__ pd) {
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const WarpRed R;
-    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps)
-        if (rp[v + 1] - rp[v] <= kBigDeg) softmax_bwd_row(R, v, rp, pos_bits, alpha, dalpha, n, slope, ds, pd);
-}
-
-__global__ void __launch_bounds__(256) gat_softmax_bwd_big_kernel(const int32_t* __restrict__ big, int32_t nbig,
-                                                                  const int32_t* __restrict__ rp,
-                                                                  const uint32_t* __restrict__ pos_bits,
-                                                                  const float* __restrict__ alpha,
-                                                                  const float* __restrict__ dalpha, int64_t n,
-                                                                  float slope, float* __restrict__ ds,
-                                                                  float* __restrict__ pd) {
-    __shared__ float sh[32];
-    const BlockRed R(sh);
-    for (int i = blockIdx.x; i < nbig; i += gridDim.x) softmax_bwd_row(R, big[i], rp, pos_bits, alpha, dalpha, n, slope, ds, pd);
-}
-
-// ps[u] = ds of u's self loop + ds of every arc leaving u (out-CSR rows, coefficients through perm)
-template <class Red>
-__device__ void ps_row(const Red& R, int64_t u, const int32_t* __restrict__ rp_out, const int32_t* __restrict__ perm,
-                       const float* __restrict__ ds, int64_t n, float* __restrict__ ps) {
-    float acc = R.t == 0 ? ds[u] : 0.f;
-    for (int j = rp_out[u] + R.t; j < rp_out[u + 1]; j += R.T) acc += ds[n + perm[j]];
-    acc = R.sum(acc);
-    if (R.t == 0) ps[u] = acc;
-}
-
-__global__ void gat_ps_kernel(const int32_t* __restrict__ rp_out, const int32_t* __restrict__ perm,
-                              const float* __restrict__ ds, int64_t n, float* __restrict__ ps) {
+__global__ void gat_pspd_kernel(const int32_t* __restrict__ rp_out, const int32_t* __restrict__ col_out,
+                                const float* __restrict__ bt, const float* __restrict__ w, const float* __restrict__ gy,
+                                const float* __restrict__ zx, const float* __restrict__ bsum, int64_t n, float slope,
+                                float* __restrict__ ps, float* __restrict__ pd) {
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const WarpRed R;
     for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += warps)
-        if (rp_out[u + 1] - rp_out[u] <= kBigDeg) ps_row(R, u, rp_out, perm, ds, n, ps);
+        if (rp_out[u + 1] - rp_out[u] <= kBigDeg) pspd_row(R, u, rp_out, col_out, bt, w, gy, zx, bsum, n, slope, ps, pd);
 }
 
-__global__ void __launch_bounds__(256) gat_ps_big_kernel(const int32_t* __restrict__ big, int32_t nbig,
-                                                         const int32_t* __restrict__ rp_out,
-                                                         const int32_t* __restrict__ perm, const float* __restrict__ ds,
-                                                         int64_t n, float* __restrict__ ps) {
+__global__ void __launch_bounds__(256) gat_pspd_big_kernel(const int32_t* __restrict__ big, int32_t nbig,
+                                                           const int32_t* __restrict__ rp_out,
+                                                           const int32_t* __restrict__ col_out,
+                                                           const float* __restrict__ bt, const float* __restrict__ w,
+                                                           const float* __restrict__ gy, const float* __restrict__ zx,
+                                                           const float* __restrict__ bsum, int64_t n, float slope,
+                                                           float* __restrict__ ps, float* __restrict__ pd) {
     __shared__ float sh[32];
     const BlockRed R(sh);
-    for (int i = blockIdx.x; i < nbig; i += gridDim.x) ps_row(R, big[i], rp_out, perm, ds, n, ps);
+    for (int i = blockIdx.x; i < nbig; i += gridDim.x)
+        pspd_row(R, big[i], rp_out, col_out, bt, w, gy, zx, bsum, n, slope, ps, pd);
 }
 
 // dz[v] += ps_v a_src + pd_v a_dst (own rows)
@@ -456,13 +463,12 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     c->m_dW.ensure((size_t)(n_w + 2 * C) * sizeof(float));
     c->m_scal.ensure(4 * sizeof(double));
     c->gat_fg.ensure((size_t)2 * V_pad * sizeof(float) + 16);
-    c->gat_alpha.ensure((size_t)na * sizeof(float) + 16);
-    c->gat_alpha_t.ensure((size_t)na * sizeof(float) + 16);
-    c->gat_dalpha.ensure((size_t)na * sizeof(float) + 16);
-    c->gat_ds.ensure((size_t)na * sizeof(float) + 16);
-    c->gat_pspd.ensure((size_t)2 * n * sizeof(float) + 16);
-    c->gat_bits.ensure((size_t)cdiv(na, 32) * sizeof(uint32_t) + 16);
-    c->gat_Z.ensure((size_t)(m->K + 1) * feat * es + 16);
+    c->gat_msum.ensure((size_t)2 * n * sizeof(float) + 16);
+    c->gat_alpha.ensure((size_t)na * sizeof(float) + 16);     // coefficient words, in-CSR order
+    c->gat_alpha_t.ensure((size_t)na * sizeof(float) + 16);   // coefficient words, out-CSR order
+    c->gat_pspd.ensure((size_t)6 * n * sizeof(float) + 16);       // ps | pd | w | gy | zx | b
+    c->gat_Z.ensure((size_t)(2 * m->K + 1) * feat * es + 16);     // Z^0..Z^K, Y^1..Y^K
+    c->gat_X.ensure((size_t)slice * es + 16);
     c->recv.ensure((size_t)feat * es + 16);
     c->xfer.ensure((size_t)feat * es + 16);
     c->send.ensure((size_t)feat * es + 16);
@@ -470,14 +476,20 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     c->gat_da.ensure((size_t)nbda * 2 * C * sizeof(float) + 16);
     const int64_t loss_blocks = std::min<int64_t>(cdiv(V_p, 8), 148 * 8);
     c->m_part.ensure((size_t)loss_blocks * (sizeof(double) + sizeof(int64_t)) + 16);
-    if (c->gat_perm_version != c->g_version) {   // out-CSR arc -> in-CSR arc, once per graph
+    const char* gpe = getenv("NTP_GAT_PERMUTE");   // dev switch, read per call (tests compare both)
+    const bool permute = gpe && atoi(gpe) != 0;
+    if (permute && c->gat_perm_version != c->g_version) {   // out-CSR arc -> in-CSR arc
         c->gat_perm.ensure((size_t)std::max<int64_t>(nnz, 1) * sizeof(int32_t));
-        const Csr& in = g.fwd();
-        const Csr& out = g.bwd();
-        gat_perm_kernel<<<wblocks(n), 256, 0, s>>>(in.row_ptr.as<int32_t>(), in.col.as<int32_t>(),
-                                                  out.row_ptr.as<int32_t>(), out.col.as<int32_t>(), n,
+        gat_perm_kernel<<<wblocks(n), 256, 0, s>>>(g.fwd().row_ptr.as<int32_t>(), g.fwd().col.as<int32_t>(),
+                                                  g.bwd().row_ptr.as<int32_t>(), g.bwd().col.as<int32_t>(), n,
                                                   c->gat_perm.as<int32_t>());
         NTP_LAUNCH_CHECK();
+        count_launch(c);
+        c->gat_perm_version = c->g_version;
+    }
+    if (c->gat_big_version != c->g_version) {
+        const Csr& in = g.fwd();
+        const Csr& out = g.bwd();
         // hub rows (> kBigDeg arcs) of both CSRs: one CTA each in the per-row reductions
         c->gat_big.ensure((size_t)2 * (n + 1) * sizeof(int32_t) + 16);
         DevBuf cnt;
@@ -492,8 +504,8 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
         NTP_CUDA(cudaStreamSynchronize(s));
         c->gat_nbig[0] = h[0];
         c->gat_nbig[1] = h[1];
-        count_launch(c, 3);
-        c->gat_perm_version = c->g_version;
+        count_launch(c, 2);
+        c->gat_big_version = c->g_version;
     }
     const int32_t* big_in = c->gat_big.as<int32_t>();
     const int32_t* big_out = big_in + n + 1;
@@ -510,16 +522,19 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     float* fg = c->gat_fg.as<float>();
     float* alpha = c->gat_alpha.as<float>();
     float* alpha_t = c->gat_alpha_t.as<float>();
-    float* dalpha = c->gat_dalpha.as<float>();
-    float* ds = c->gat_ds.as<float>();
     float* ps = c->gat_pspd.as<float>();
     float* pd = ps + n;
+    float* wv = ps + 2 * n;
+    float* gy = ps + 3 * n;
+    float* zx = ps + 4 * n;
+    float* bsum = ps + 5 * n;
     const int32_t* perm = c->gat_perm.as<int32_t>();
-    void* Zst = c->gat_Z.p;   // Z^k slice j at sl(Zst, k*vs + j)
+    void* Zst = c->gat_Z.p;   // Z^k slice j at sl(Zst, k*vs + j); Y^k slice j at sl(Zst, (K + k)*vs + j)
+    void* Xs = c->gat_X.p;
 
     // rows [n, V_pad) of every slice are padding (never written by a hop, exchanged as zeros)
     if (V_pad > n)
-        for (int64_t i = 0; i < (int64_t)(m->K + 1) * vs; ++i)
+        for (int64_t i = 0; i < (int64_t)(2 * m->K + 1) * vs; ++i)
             NTP_CUDA(cudaMemsetAsync(static_cast<char*>(sl(Zst, i)) + n * d_s * es, 0, (V_pad - n) * d_s * es, s));
     if (V_pad > n)
         for (int j = 0; j < vs; ++j)
@@ -536,17 +551,23 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     NTP_LAUNCH_CHECK();
     count_launch(c);
     if (!local) NTP_NCCL(ncclAllGather(fg + 2 * row0, fg, (size_t)2 * V_p, ncclFloat32, c->comm, s));
-    NTP_CUDA(cudaMemsetAsync(c->gat_bits.p, 0, (size_t)cdiv(na, 32) * sizeof(uint32_t), s));
+    float* msum = c->gat_msum.as<float>();
     gat_softmax_kernel<<<wblocks(n), 256, 0, s>>>(g.fwd().row_ptr.as<int32_t>(), g.fwd().col.as<int32_t>(), fg, n, slope,
-                                                 alpha, c->gat_bits.as<uint32_t>());
+                                                 alpha, msum, bsum);
     if (c->gat_nbig[0] > 0)
         gat_softmax_big_kernel<<<std::min(c->gat_nbig[0], 148 * 8), 256, 0, s>>>(
             big_in, c->gat_nbig[0], g.fwd().row_ptr.as<int32_t>(), g.fwd().col.as<int32_t>(), fg, n, slope, alpha,
-            c->gat_bits.as<uint32_t>());
+            msum, bsum);
     NTP_LAUNCH_CHECK();
-    gat_permute_kernel<<<eblk(na), 256, 0, s>>>(alpha, perm, n, nnz, alpha_t);
+    if (permute) {
+        gat_permute_kernel<<<eblk(na), 256, 0, s>>>(alpha, perm, n, nnz, alpha_t);
+    } else {
+        const int at_blocks = (int)std::min<int64_t>(std::max<int64_t>(cdiv(nnz, kAtArcs * 8), 1) + 64, 148 * 16);
+        gat_coef_t_kernel<<<at_blocks, 256, 0, s>>>(g.bwd().row_ptr.as<int32_t>(), g.bwd().col.as<int32_t>(), fg, msum,
+                                                    alpha, n, nnz, slope, alpha_t);
+    }
     NTP_LAUNCH_CHECK();
-    count_launch(c, 2);
+    count_launch(c, 2 + (c->gat_nbig[0] > 0 ? 1 : 0));
 
     // ---- a3: split z (no pre-scale: the attention operator carries its own normalisation)
     pack_v2f(c, z, ldL, C, local ? Zst : c->send.p, V_p, d_s, P, nullptr, row0, n, NTP_F32, dt, s);
@@ -554,19 +575,24 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     NTP_CUDA(record_timing(c, E[ei++], s));   // E2 v2f
 
     // ---- G3 / a4: K weighted hops per slice, every level kept for the backward's SDDMM
-    auto hop = [&](const void* in, void* out, bool transposed) {
+    // one pass, two sums: out = gamma A_att in (alpha) and out2 = gamma A_beta in (beta), from the signed words
+    auto hop = [&](const void* in, void* out, void* out2, bool transposed) {
         const bool tm = c->hop_ev_used + 2 <= kHopEvents;
         if (tm) NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used], s));
         const float* co = transposed ? alpha_t : alpha;
         spmm_hop(c, transposed ? g.bwd() : g.fwd(), nullptr, nullptr, in, out, nullptr, d_s, d_s, d_s, d_s, dt,
-                 m->gamma, 0.f, 1, 0, -1, s, nullptr, nullptr, co + n, co);
+                 m->gamma, 0.f, 1, 0, -1, s, nullptr, nullptr, co + n, co, out2, slope);
         if (tm) {
             NTP_CUDA(record_timing(c, c->hop_ev[c->hop_ev_used + 1], s));
             c->hop_ev_used += 2;
         }
     };
+    // ... and, in the same pass, Y^k = gamma A_beta Z^{k-1} (beta = alpha * LeakyReLU'): the attention
+    // backward's per-vertex form needs it (below)
     for (int k = 1; k <= m->K; ++k)
-        for (int j = 0; j < vs; ++j) hop(sl(Zst, (int64_t)(k - 1) * vs + j), sl(Zst, (int64_t)k * vs + j), false);
+        for (int j = 0; j < vs; ++j)
+            hop(sl(Zst, (int64_t)(k - 1) * vs + j), sl(Zst, (int64_t)k * vs + j), sl(Zst, (int64_t)(m->K + k) * vs + j),
+                false);
     NTP_CUDA(record_timing(c, E[10], s));   // fwd hops done
     // a5: gather Z^K into this rank's rows, blocked [P][V_p][d_s]
     c->wire_phase = 1;
@@ -593,31 +619,28 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     }
     NTP_CUDA(record_timing(c, E[ei++], s));   // E5 v2f bwd
 
-    // SDDMM launcher: E arcs per warp step by the slice's 16-byte vectors per row
+    // per-vertex dot products of one level / slice (gat_dots_kernel), accumulated over levels and slices
     const int32_t nvec = (int32_t)(d_s * es / 16);
-    const int sd_blocks = (int)std::min<int64_t>(std::max<int64_t>(cdiv(nnz, kSdArcs * 8), 1) + 64, 148 * 16);
-    auto sddmm = [&](const void* Gj, const void* Zj, int acc) {
-        const int64_t rp_n = n;
-        const int32_t* rp = g.fwd().row_ptr.as<int32_t>();
-        const int32_t* cl = g.fwd().col.as<int32_t>();
-        const char* Gc = static_cast<const char*>(Gj);
-        const char* Zc = static_cast<const char*>(Zj);
-#define NTP_SDDMM(T, NV_) gat_sddmm_kernel<T, NV_><<<sd_blocks, 256, 0, s>>>(rp, cl, rp_n, nnz, Gc, Zc, nvec, m->gamma, dalpha, acc)
-#define NTP_SDDMM_T(T) switch (nvec) { \
-            case 1: NTP_SDDMM(T, 1); break; case 2: NTP_SDDMM(T, 2); break; case 3: NTP_SDDMM(T, 3); break; \
-            case 4: NTP_SDDMM(T, 4); break; case 5: NTP_SDDMM(T, 5); break; case 6: NTP_SDDMM(T, 6); break; \
-            case 7: NTP_SDDMM(T, 7); break; case 8: NTP_SDDMM(T, 8); break; case 9: NTP_SDDMM(T, 9); break; \
-            case 10: NTP_SDDMM(T, 10); break; case 11: NTP_SDDMM(T, 11); break; case 12: NTP_SDDMM(T, 12); break; \
-            case 13: NTP_SDDMM(T, 13); break; case 14: NTP_SDDMM(T, 14); break; case 15: NTP_SDDMM(T, 15); break; \
-            default: NTP_SDDMM(T, 16); }
-        if (dt == NTP_F32) { NTP_SDDMM_T(float) }
-        else { NTP_SDDMM_T(__nv_bfloat16) }
-#undef NTP_SDDMM_T
-#undef NTP_SDDMM
+    auto dots = [&](const void* Gk, const void* Zk, const void* Yk, const void* Zp, int acc) {
+        const int blocks = (int)std::min<int64_t>(cdiv(n, 32), 148 * 16);
+        if (dt == NTP_F32)
+            gat_dots_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const char*>(Gk), static_cast<const char*>(Zk),
+                                                          static_cast<const char*>(Yk), static_cast<const char*>(Zp),
+                                                          static_cast<const char*>(Xs), n, nvec, wv, gy, zx, acc);
+        else
+            gat_dots_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(
+                static_cast<const char*>(Gk), static_cast<const char*>(Zk), static_cast<const char*>(Yk),
+                static_cast<const char*>(Zp), static_cast<const char*>(Xs), n, nvec, wv, gy, zx, acc);
         NTP_LAUNCH_CHECK();
+        count_launch(c);
     };
 
-    // ---- G4 / a8: G^{k-1} = gamma A_att^T G^k per slice, with dalpha += gamma G^k_v . Z^{k-1}_u on the way
+    // ---- G4 / a8: G^{k-1} = gamma A_att^T G^k per slice, X^k = gamma A_beta^T G^k, and the per-vertex dots.
+    // The attention gradient dalpha_uv = gamma sum_k G^k_v . Z^{k-1}_u is never formed per arc: the softmax /
+    // LeakyReLU backward needs only its contractions with alpha and beta, which the hops already carry --
+    //   w_v = sum_u alpha_uv dalpha_uv = sum_k G^k_v . Z^k_v,   sum_u beta_uv dalpha_uv = sum_k G^k_v . Y^k_v,
+    //   sum_v beta_uv dalpha_uv = sum_k Z^{k-1}_u . X^k_u
+    // -- n-long partial sums per slice instead of an nnz-long SDDMM (and its allreduce).
     c->wire_phase = 3;
     void* cur = c->recv.p;
     void* nxt = c->xfer.p;
@@ -625,15 +648,13 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
         const int k = m->K - i;
         for (int j = 0; j < vs; ++j) {
             const void* Gj = sl(cur, j);
-            const void* Zj = sl(Zst, (int64_t)(k - 1) * vs + j);
-            const int acc = (i > 0 || j > 0) ? 1 : 0;
-            sddmm(Gj, Zj, acc);
-            count_launch(c);
-            hop(Gj, sl(nxt, j), true);
+            hop(Gj, sl(nxt, j), Xs, true);
+            dots(Gj, sl(Zst, (int64_t)k * vs + j), sl(Zst, (int64_t)(m->K + k) * vs + j),
+                 sl(Zst, (int64_t)(k - 1) * vs + j), (i > 0 || j > 0) ? 1 : 0);
         }
         std::swap(cur, nxt);
     }
-    NTP_CUDA(record_timing(c, E[11], s));   // bwd hops (+ SDDMM) done
+    NTP_CUDA(record_timing(c, E[11], s));   // bwd hops (+ dots) done
     // a9: gather G^0 -> dz rows
     void* gathered_b = cur;
     if (!local) {
@@ -643,19 +664,15 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     unpack_f2v(c, gathered_b, V_p, d_s, P, dz, ldL, C, dt, NTP_F32, s);
     NTP_CUDA(record_timing(c, E[ei++], s));   // E6 prop bwd + f2v
 
-    // ---- attention backward (every rank holds every coefficient): dalpha summed over ranks
-    if (!local) NTP_NCCL(ncclAllReduce(dalpha, dalpha, (size_t)na, ncclFloat32, ncclSum, c->comm, s));
-    gat_softmax_bwd_kernel<<<wblocks(n), 256, 0, s>>>(g.fwd().row_ptr.as<int32_t>(), c->gat_bits.as<uint32_t>(), alpha,
-                                                     dalpha, n, slope, ds, pd);
-    if (c->gat_nbig[0] > 0)
-        gat_softmax_bwd_big_kernel<<<std::min(c->gat_nbig[0], 148 * 8), 256, 0, s>>>(
-            big_in, c->gat_nbig[0], g.fwd().row_ptr.as<int32_t>(), c->gat_bits.as<uint32_t>(), alpha, dalpha, n, slope,
-            ds, pd);
-    NTP_LAUNCH_CHECK();
-    gat_ps_kernel<<<wblocks(n), 256, 0, s>>>(g.bwd().row_ptr.as<int32_t>(), perm, ds, n, ps);
+    // ---- attention backward (every rank holds every coefficient): the dots summed over ranks (3n floats),
+    // then ps / pd per vertex
+    if (!local) NTP_NCCL(ncclAllReduce(wv, wv, (size_t)3 * n, ncclFloat32, ncclSum, c->comm, s));
+    gat_pspd_kernel<<<wblocks(n), 256, 0, s>>>(g.bwd().row_ptr.as<int32_t>(), g.bwd().col.as<int32_t>(), alpha_t, wv,
+                                              gy, zx, bsum, n, slope, ps, pd);
     if (c->gat_nbig[1] > 0)
-        gat_ps_big_kernel<<<std::min(c->gat_nbig[1], 148 * 8), 256, 0, s>>>(big_out, c->gat_nbig[1],
-                                                                           g.bwd().row_ptr.as<int32_t>(), perm, ds, n, ps);
+        gat_pspd_big_kernel<<<std::min(c->gat_nbig[1], 148 * 8), 256, 0, s>>>(
+            big_out, c->gat_nbig[1], g.bwd().row_ptr.as<int32_t>(), g.bwd().col.as<int32_t>(), alpha_t, wv, gy, zx, bsum,
+            n, slope, ps, pd);
     NTP_LAUNCH_CHECK();
     gat_dz_kernel<<<eblk(V_p * C), 256, 0, s>>>(dz, ldL, C, attu, ps, pd, V_p, row0, n);
     NTP_LAUNCH_CHECK();
@@ -663,7 +680,7 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     NTP_LAUNCH_CHECK();
     gat_sum_parts_kernel<<<eblk(2 * C), 256, 0, s>>>(c->gat_da.as<float>(), nbda, 2 * C, da);
     NTP_LAUNCH_CHECK();
-    count_launch(c, 5);
+    count_launch(c, 4 + (c->gat_nbig[1] > 0 ? 1 : 0));
 
     // ---- a10: MLP backward
     epoch_gemm(c, true, false, m->hid, C, V_p, H1, ldH, dz, ldL, dW1, C, s, 0, nullptr, 0, nullptr, nullptr);

@@ -149,11 +149,11 @@ struct ntp_ctx {
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
     ntp::Graph g;
     // scratch
-    ntp::DevBuf carry, prop_tmp, prop_s0, send, recv, xfer;
+    ntp::DevBuf carry, carry2, prop_tmp, prop_s0, send, recv, xfer;
     // decoupled GAT (gat.cu): score halves, coefficients (+ out-CSR order), their gradients, level stack
-    ntp::DevBuf gat_fg, gat_alpha, gat_alpha_t, gat_dalpha, gat_ds, gat_pspd, gat_perm, gat_Z, gat_da, gat_bits, gat_big;
+    ntp::DevBuf gat_fg, gat_msum, gat_alpha, gat_alpha_t, gat_pspd, gat_perm, gat_Z, gat_X, gat_da, gat_big;
     int32_t gat_nbig[2] = {0, 0};   // hub rows (in-CSR, out-CSR) listed in gat_big
-    int64_t gat_perm_version = -1;
+    int64_t gat_perm_version = -1, gat_big_version = -1;
     ntp::DevBuf m_A, m_H1, m_L, m_dL, m_dH1, m_dW, m_scal, m_part, m_Xs, m_lab, m_mask;
     ntp::DevBuf m_gemm_part, m_W0p, m_W1p, m_Xh, m_Wsplit, m_bits, m_dWp, m_head, m_wgrad;
     // coupled (naive TP) epoch: Z^l, H^l per layer, dA / dZ scratch, padded weights
@@ -308,7 +308,8 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
               void* S_out, const void* H, int64_t ld_in, int64_t ld_out, int64_t ld_h, int32_t cols,
               ntp_dtype dt, float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi,
               cudaStream_t s, const int32_t* out_rows = nullptr, const PeerOut* po = nullptr,
-              const float* ew = nullptr, const float* sw = nullptr);   // weighted hop (GAT): arc / self coefficients
+              const float* ew = nullptr, const float* sw = nullptr,    // weighted hop (GAT): arc / self coefficients
+              void* S_out2 = nullptr, float slope2 = 0.f);             // dual weighted hop: second output (below)
 // S[r] = scale[r] * H[src_rows ? src_rows[r] : r] (scale may be null: plain copy / permutation)
 void prescale(ntp_ctx* c, const void* H, int64_t ld_h, void* S, int64_t ld_s, int32_t cols,
               const float* scale, int64_t rows, ntp_dtype dt, cudaStream_t s,

@@ -151,7 +151,19 @@ struct HopParams {
     int po_rank;
     const float* __restrict__ ew;      // weighted hop: per-arc coefficients in CSR order (else null)
     const float* __restrict__ sw;      // weighted hop: per-row self-loop coefficients
+    // dual weighted hop (GAT): the coefficient words are signed, |w| = alpha and the sign bit marks the arcs
+    // whose second coefficient is slope2 * alpha (else alpha); the second sum goes to S_out2 (row stride ld_out)
+    char* __restrict__ S_out2;
+    float* __restrict__ carry2;
+    float slope2;
 };
+
+// dual weighted hop: (alpha, beta) from one signed coefficient word
+__device__ __forceinline__ float coef_a(float w) { return __int_as_float(__float_as_int(w) & 0x7fffffff); }
+__device__ __forceinline__ float coef_b(float w, float slope) {
+    const float a = coef_a(w);
+    return __float_as_int(w) < 0 ? slope * a : a;
+}
 
 // Where output row r (internal order) is stored: its original row (out_rows), locally or -- peer-direct
 // gather -- in block po_rank of the owner's window: the f2v all-to-all fused into the epilogue.
@@ -184,7 +196,10 @@ __device__ __forceinline__ char* out_row_ptr(const HopParams& p, int64_t r) {
 // WT (weighted hop): the row sum carries a per-arc coefficient p.ew[j] (loaded with the column index and
 // shuffled with it) and the self term p.sw[r]; no row / column D~^{-1/2} (rs = cs = 1).  GAT's attention
 // aggregation (Eq. 5) -- the same merge-path split, pipeline and fixed reduction order.
-template <typename T, int VB, int E, int L, int MODE, bool WT = false>
+// DUAL (implies WT): two sums per row from one pass over the arcs, with the coefficients alpha and beta
+// decoded from one signed word per arc (coef_a / coef_b): the second accumulator set costs registers and
+// FMAs, not a second gather.
+template <typename T, int VB, int E, int L, int MODE, bool WT = false, bool DUAL = false>
 __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kernel(const HopParams p) {
     constexpr bool SHORT = (MODE & 1) != 0;
     constexpr bool TINY = (MODE & 2) != 0 && E >= 2;
@@ -196,12 +211,16 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
     constexpr bool OCC = ((MODE >> 2) & 3) != 0;
     constexpr int BATCH0 = (VB == 16) ? (SHORT ? ((E >= 4) ? 16 : 8) : ((E == 8) ? 64 : (E == 4) ? 32 : 8 * E))
                                       : (SHORT ? ((E >= 4) ? 2 * E : 8) : ((E >= 2) ? 4 * E : 8));
-    constexpr int BATCH = (OCC && !SHORT && BATCH0 >= 16) ? BATCH0 / 2 : BATCH0;
+    // half-length batches for the weighted hop too: its per-arc coefficients ride along with the loads
+    // (full-length batches spilled ~30 registers to local memory at 128 registers)
+    constexpr int BATCH = ((OCC || DUAL) && !SHORT && BATCH0 >= 16) ? BATCH0 / 2 : BATCH0;
     constexpr int LPB = BATCH / E;                        // loads per lane per batch
     constexpr int ISL = (BATCH + L - 1) / L;              // column indices held per lane
     constexpr int ISLW = WT ? ISL : 1, LPBW = WT ? LPB : 1;   // arc coefficients held per lane (weighted)
     static_assert(BATCH % 8 == 0, "batch must preserve the (j - eb) mod 8 grouping");
     static_assert(!(WT && MODE != 0), "the weighted hop has only the general path");
+    static_assert(!DUAL || WT, "the dual hop is weighted");
+    constexpr int NACC2 = DUAL ? NACC : 1;
     const int lane = threadIdx.x & 31;
     const int gl = lane % L;
     const int gbase = lane - gl;
@@ -283,22 +302,28 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
             // epilogue operands issued now so their latency hides behind the gather (short rows)
             const bool fin = !(head || tail) && e_raw == 0 && col_ok;
             Raw<VB> self_raw = zero_raw<VB>();
-            float ra = 0.f, rb = 0.f, swr = 0.f;
+            float ra = 0.f, rb = 0.f, swr = 0.f, swr2 = 0.f;
             if (fin) {
                 self_raw = ldv<VB>(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * VB);
                 if constexpr (WT) {
                     ra = rb = 1.f;
-                    swr = __ldg(p.sw + r);
+                    const float sw_raw = __ldg(p.sw + r);
+                    swr = coef_a(sw_raw);
+                    if constexpr (DUAL) swr2 = coef_b(sw_raw, p.slope2);
                 } else {
                     ra = __ldg(p.rs + r);
                     rb = __ldg(p.cs + r);
                 }
             }
-            float acc[NACC][VALS];
+            float acc[NACC][VALS], acc2[NACC2][VALS];
 #pragma unroll
             for (int k = 0; k < NACC; ++k)
 #pragma unroll
                 for (int i = 0; i < VALS; ++i) acc[k][i] = 0.f;
+#pragma unroll
+            for (int k = 0; k < NACC2; ++k)
+#pragma unroll
+                for (int i = 0; i < VALS; ++i) acc2[k][i] = 0.f;
             // column indices of a batch: lane gl holds edges base + sl*L + gl (0 past the end), with their
             // coefficients when weighted
             auto load_idx = [&](int base, int (&dst)[ISL], float (&dw)[ISLW]) {
@@ -326,8 +351,14 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
             auto consume = [&](const Raw<VB> (&v)[LPB], const float (&wv)[LPBW], int base) {
                 const int rem = ee - base;
                 auto add = [&](int t) {
-                    if constexpr (WT) vfma<T, VB>(acc[t % NACC], v[t], wv[t]);
-                    else vadd<T, VB>(acc[t % NACC], v[t]);
+                    if constexpr (DUAL) {
+                        vfma<T, VB>(acc[t % NACC], v[t], coef_a(wv[t]));
+                        vfma<T, VB>(acc2[t % NACC2], v[t], coef_b(wv[t], p.slope2));
+                    } else if constexpr (WT) {
+                        vfma<T, VB>(acc[t % NACC], v[t], coef_a(wv[t]));
+                    } else {
+                        vadd<T, VB>(acc[t % NACC], v[t]);
+                    }
                 };
                 if (rem >= BATCH) {
 #pragma unroll
@@ -366,6 +397,12 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
                     for (int k = 0; k < NACC; ++k)
 #pragma unroll
                         for (int i = 0; i < VALS; ++i) acc[k][i] += __shfl_sync(gmask, acc[k][i], partner);
+                    if constexpr (DUAL) {
+#pragma unroll
+                        for (int k = 0; k < NACC2; ++k)
+#pragma unroll
+                            for (int i = 0; i < VALS; ++i) acc2[k][i] += __shfl_sync(gmask, acc2[k][i], partner);
+                    }
                 } else {
                     const int kb = 1 << (b - LOG_E);
 #pragma unroll
@@ -373,18 +410,32 @@ __global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kern
                         if ((k & kb) == 0 && (k | kb) < NACC) {
 #pragma unroll
                             for (int i = 0; i < VALS; ++i) acc[k][i] += acc[k | kb][i];
+                            if constexpr (DUAL) {
+#pragma unroll
+                                for (int i = 0; i < VALS; ++i) acc2[k][i] += acc2[k | kb][i];
+                            }
                         }
                 }
             }
             if (e_raw != 0 || !col_ok) continue;
             if (head || tail) {
-                float* dst = p.carry + ((u * 2 + (head ? 0 : 1)) * (int64_t)row_vals) + vcol * VALS;
+                const int64_t coff = ((u * 2 + (head ? 0 : 1)) * (int64_t)row_vals) + vcol * VALS;
 #pragma unroll
-                for (int i = 0; i < VALS; ++i) dst[i] = acc[0][i];
+                for (int i = 0; i < VALS; ++i) p.carry[coff + i] = acc[0][i];
+                if constexpr (DUAL) {
+#pragma unroll
+                    for (int i = 0; i < VALS; ++i) p.carry2[coff + i] = acc2[0][i];
+                }
                 continue;
             }
             const float sig = (p.mode == 0) ? p.gamma * ra * rb : p.gamma * ra;
             float out[VALS];
+            if constexpr (DUAL) {
+                float out2[VALS];
+#pragma unroll
+                for (int i = 0; i < VALS; ++i) out2[i] = sig * __fmaf_rn(swr2, Vec<T, VB>::elem(self_raw, i), acc2[0][i]);
+                stv<VB>(p.S_out2 + r * p.ld_out + (int64_t)vcol * VB, Vec<T, VB>::pack(out2));
+            }
             if constexpr (WT) {   // gamma * (sum_u w_uv S_u + w_vv S_v); no alpha mix (the GAT epoch's reading)
 #pragma unroll
                 for (int i = 0; i < VALS; ++i)
@@ -574,18 +625,27 @@ __global__ void __launch_bounds__(kBlock) spmm_fixup_kernel(const HopParams p) {
     const int row_vals = p.nvec * VALS;
     const float a = p.sw ? 1.f : p.rs[r];
     const float b = p.sw ? 1.f : p.cs[r];
-    const float swr = p.sw ? p.sw[r] : 0.f;
+    const float swr = p.sw ? coef_a(p.sw[r]) : 0.f;
+    const float swr2 = p.S_out2 ? coef_b(p.sw[r], p.slope2) : 0.f;
     char* orow_p = out_row_ptr(p, r);
     for (int k = lane; k < row_vals; k += 32) {
         float acc = p.carry[(u * 2 + 1) * (int64_t)row_vals + k];
+        float acc2 = p.S_out2 ? p.carry2[(u * 2 + 1) * (int64_t)row_vals + k] : 0.f;
         for (int64_t v = u + 1;; ++v) {
             acc += p.carry[(v * 2 + 0) * (int64_t)row_vals + k];
+            if (p.S_out2) acc2 += p.carry2[(v * 2 + 0) * (int64_t)row_vals + k];
             if (p.unit_row[v + 1] > r) break;
         }
         const int vcol = k / VALS, comp = k % VALS;
         float self[VALS];
         load16<T>(p.S_in + (int64_t)r * p.ld_in + (int64_t)vcol * 16, self);
         const float sig = (p.mode == 0) ? p.gamma * a * b : p.gamma * a;
+        if (p.S_out2) {
+            const float out2 = sig * __fmaf_rn(swr2, self[comp], acc2);
+            char* o2 = p.S_out2 + (int64_t)r * p.ld_out;
+            if (sizeof(T) == 4) reinterpret_cast<float*>(o2)[k] = out2;
+            else reinterpret_cast<__nv_bfloat16*>(o2)[k] = __float2bfloat16_rn(out2);
+        }
         float out = p.sw ? sig * __fmaf_rn(swr, self[comp], acc) : sig * (acc + self[comp]);
         if (p.alpha != 0.f) {
             float h[VALS];
@@ -628,15 +688,15 @@ bool carveout_max_l1() {
 }
 
 // 256-thread CTAs, one unit per lane group, the whole unified array as L1 (no shared memory).
-template <typename T, int VB, int E, int L, int MODE, bool WT = false>
+template <typename T, int VB, int E, int L, int MODE, bool WT = false, bool DUAL = false>
 void launch_variant(const HopParams& p, cudaStream_t s) {
     static bool attr = false;
     if (!attr && carveout_max_l1()) {
-        NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, VB, E, L, MODE, WT>,
+        NTP_CUDA(cudaFuncSetAttribute(spmm_hop_kernel<T, VB, E, L, MODE, WT, DUAL>,
                                       cudaFuncAttributePreferredSharedMemoryCarveout, 0));
         attr = true;
     }
-    spmm_hop_kernel<T, VB, E, L, MODE, WT><<<(unsigned)cdiv((p.u_end - p.u_begin) * L, kBlock), kBlock, 0, s>>>(p);
+    spmm_hop_kernel<T, VB, E, L, MODE, WT, DUAL><<<(unsigned)cdiv((p.u_end - p.u_begin) * L, kBlock), kBlock, 0, s>>>(p);
     NTP_LAUNCH_CHECK();
 }
 
@@ -644,7 +704,8 @@ template <typename T, int VB, int E, int L>
 void launch_hop(const HopParams& p, cudaStream_t s) {
     if constexpr (VB == 16) {
         if (p.ew) {   // weighted (GAT attention): general path only
-            launch_variant<T, VB, E, L, 0, true>(p, s);
+            if (p.S_out2) launch_variant<T, VB, E, L, 0, true, true>(p, s);
+            else launch_variant<T, VB, E, L, 0, true>(p, s);
             return;
         }
     }
@@ -690,8 +751,11 @@ static void unit_range(const Csr& csr, int64_t row_lo, int64_t row_hi, int64_t& 
 void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, const void* S_in, void* S_out,
               const void* S0, int64_t ld_in, int64_t ld_out, int64_t ld_s0, int32_t cols, ntp_dtype dt,
               float gamma, float alpha, int mode, int64_t row_lo, int64_t row_hi, cudaStream_t s,
-              const int32_t* out_rows, const PeerOut* po, const float* ew, const float* sw) {
+              const int32_t* out_rows, const PeerOut* po, const float* ew, const float* sw, void* S_out2,
+              float slope2) {
     const Graph& g = c->g;
+    NTP_CHECK(!S_out2 || (ew && !out_rows && !(po && po->tab)), NTP_ERR_ARG,
+              "the dual hop is weighted and writes local rows");
     if (row_hi < 0) row_hi = g.n;
     row_lo = std::max<int64_t>(row_lo, 0);
     row_hi = std::min<int64_t>(row_hi, g.n);
@@ -720,6 +784,8 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     p.po_rank = po ? po->rank : 0;
     p.ew = ew;
     p.sw = sw;
+    p.S_out2 = static_cast<char*>(S_out2);
+    p.slope2 = slope2;
 
     unit_range(csr, row_lo, row_hi, p.u_begin, p.u_end);
     p.row_lo = row_lo;
@@ -730,6 +796,11 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
     p.mode = mode;
     c->carry.ensure((size_t)(csr.U * 2) * nvec * vals * sizeof(float) + 16);
     p.carry = c->carry.as<float>();
+    p.carry2 = nullptr;
+    if (S_out2) {
+        c->carry2.ensure((size_t)(csr.U * 2) * nvec * vals * sizeof(float) + 16);
+        p.carry2 = c->carry2.as<float>();
+    }
     if (p.u_end <= p.u_begin) return;
     // 32-byte vectors when every row the hop touches is 32-byte aligned and at most 8 of them wide
     // (E >= 4 edge slots: wider rows would need more accumulator registers than the kernel has)

@@ -1,8 +1,9 @@
 """NEXT-2 decoupled GAT epoch (ntp_train_epoch_gat) vs the GAT oracle (oracle/gat.py, readings G1-G4):
 per-epoch loss within 1e-4 (fp32 slices) / 2e-2 relative (bf16) and every parameter -- W0, W1 and the
-attention vector a = [a_src; a_dst], whose gradient runs through the SDDMM, the softmax / LeakyReLU
-backward and the out-arc sums -- after the SGD updates; on one GPU and at virtual P = 2 / 4 (the P-block
-layouts, per-slice weighted hops and the per-slice partial dot products of dalpha)."""
+attention vector a = [a_src; a_dst], whose gradient runs through the softmax / LeakyReLU backward (the
+oracle forms dalpha per arc; the engine contracts it per vertex through dual alpha / beta hops) -- after
+the SGD updates; on one GPU and at virtual P = 2 / 4 (the P-block layouts, per-slice weighted hops and the
+per-slice partial dot products)."""
 import numpy as np
 import pytest
 import torch
@@ -67,7 +68,7 @@ def test_gat_epoch_fp32(name, K, gamma):
     ref = _run_oracle(name, 3, got[5])
     _check(got, ref, 1e-4, 1e-4, False)
     assert got[0][-1] < got[0][0]
-    assert got[4][0]["spmm_launches"] == 2 * got[5]["K"]
+    assert got[4][0]["spmm_launches"] == 2 * got[5]["K"]   # dual hops (alpha and beta sums in one pass)
 
 
 @pytest.mark.parametrize("name", ["tiny_sym", "small_dir"])
@@ -85,6 +86,20 @@ def test_gat_epoch_virtual_slices(name, P):
     ref = _run_oracle(name, 3, got[5])
     _check(got, ref, 1e-4, 1e-4, False)
     assert got[4][0]["spmm_launches"] == 2 * got[5]["K"] * P
+
+
+@pytest.mark.parametrize("name", ["small_dir", "dense_sym", "cora"])
+def test_gat_out_order_coefficients_bitwise(name, monkeypatch):
+    """The backward hop's coefficients in out-CSR order are re-derived from each destination's stored softmax
+    (max, sum) instead of permuted from the in-CSR array: the same operands and operations, so the whole epoch
+    (losses, W0, W1, a) is bit-identical to the plain permutation (NTP_GAT_PERMUTE=1)."""
+    runs = []
+    for perm in ("1", "0"):
+        monkeypatch.setenv("NTP_GAT_PERMUTE", perm)
+        runs.append(_run_gpu(name, 3))
+    (la, W0a, W1a, Aa), (lb, W0b, W1b, Ab) = runs[0][:4], runs[1][:4]
+    assert la == lb
+    assert np.array_equal(W0a, W0b) and np.array_equal(W1a, W1b) and np.array_equal(Aa, Ab)
 
 
 def test_gat_zero_attention_vector_matches_gcn_on_ring():

@@ -136,3 +136,45 @@ def test_zero_weights_loss_is_log_C_and_lr_zero_constant():
     assert losses[0] == losses[1] == losses[2]
     losses, *_ = gat.train(g, X, y, mask, W0, W1, a_s, a_d, 2, 1.0, 0.5, 5)
     assert losses[-1] < losses[0]
+
+
+@pytest.mark.parametrize("n,m,seed,symmetric,K,gamma,slope", [(9, 30, 2, True, 3, 0.9, 0.2),
+                                                              (12, 40, 5, False, 2, 1.0, 0.2),
+                                                              (8, 20, 3, False, 1, 0.8, 0.0)])
+def test_backward_contraction_identity(n, m, seed, symmetric, K, gamma, slope):
+    """The engine never forms the per-arc attention gradient (csrc/gat.cu): with beta = alpha * LeakyReLU'(s)
+    and dalpha_uv = gamma sum_k G^k_v . Z^{k-1}_u, the oracle's per-arc sums ps_u = sum_v ds_uv and
+    pd_v = sum_u ds_uv equal the per-vertex contractions
+        w = sum_k G^k . Z^k,   pd = sum_k G^k . Y^k - w * b,   ps = sum_k Z^{k-1} . X^k - A_beta^T w
+    with Y^k = gamma A_beta Z^{k-1}, X^k = gamma A_beta^T G^k, b = A_beta 1.  Checked here in fp64 against
+    the oracle's own backward (a mistake in the algebra -- a dropped self loop, beta for alpha, Z^k for
+    Z^{k-1} -- fails at 1e-10)."""
+    g, X, y, mask, W0, W1, a_s, a_d = _setup(n, m, seed, symmetric)
+    _, _, _, _, _, ex = gat.epoch_grads(g, X, y, mask, W0, W1, a_s, a_d, K, gamma, slope)
+    src, dst = gat.arcs(g)
+    alpha, s, Zs, ds = ex["alpha"], ex["s"], ex["Zs"], ex["ds"]
+    ps_ref = np.zeros(g.n)
+    pd_ref = np.zeros(g.n)
+    np.add.at(ps_ref, src, ds)
+    np.add.at(pd_ref, dst, ds)
+    beta = alpha * np.where(s > 0, 1.0, slope)
+    A = gat.att_matrix(g, alpha)
+    B = gat.att_matrix(g, beta)
+    _, _, dlog = oracle.model.softmax_xent(Zs[-1], y, mask)
+    G = dlog / max(int(mask.sum()), 1)
+    w = np.zeros(g.n)
+    gy = np.zeros(g.n)
+    zx = np.zeros(g.n)
+    for k in range(K, 0, -1):
+        Yk = gamma * (B @ Zs[k - 1])
+        Xk = gamma * (B.T @ G)
+        w += np.einsum("ij,ij->i", G, Zs[k])
+        gy += np.einsum("ij,ij->i", G, Yk)
+        zx += np.einsum("ij,ij->i", Zs[k - 1], Xk)
+        G = gamma * (A.T @ G)
+    b = np.asarray(B.sum(axis=1)).ravel()
+    pd = gy - w * b
+    ps = zx - B.T @ w
+    scale = max(np.abs(ps_ref).max(), np.abs(pd_ref).max())
+    assert np.abs(pd - pd_ref).max() <= 1e-10 * scale
+    assert np.abs(ps - ps_ref).max() <= 1e-10 * scale
