@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--bwd", action="store_true")
     ap.add_argument("--reorder", action="store_true")
     ap.add_argument("--warmup", type=int, default=3, help="untimed calls per width (0 under ncu: one launch each)")
+    ap.add_argument("--pitch", type=int, default=0, help="row pitch in elements (>= width; 0: dense rows)")
     args = ap.parse_args()
     cfg = synth.get_config(args.config)
     ctx = ntp.Context()
@@ -38,8 +39,9 @@ def main():
     esz = 2 if args.dtype == "bf16" else 4
     out = []
     for d in [int(x) for x in args.widths.split(",")]:
-        H = torch.randn(n, d, device="cuda").to(tdt)
-        Z = torch.empty_like(H)
+        ld = max(args.pitch, d)
+        H = torch.randn(n, ld, device="cuda").to(tdt)[:, :d]
+        Z = torch.empty(n, ld, device="cuda", dtype=tdt)[:, :d]
         f = ctx.propagate_bwd if args.bwd else ctx.propagate_fwd
         for _ in range(args.warmup):
             f(H, Z, args.K, 1.0, 0.0)
@@ -53,7 +55,7 @@ def main():
         ms = e0.elapsed_time(e1) / args.reps / args.K
         r = d * esz
         rs = -(-r // 32) * 32
-        rec = dict(config=args.config, d=d, dtype=args.dtype, ms_per_hop=round(ms, 4),
+        rec = dict(config=args.config, d=d, pitch=ld, dtype=args.dtype, ms_per_hop=round(ms, 4),
                    GE_per_s=round(nnz * d / (ms * 1e-3) / 1e9, 1),
                    gather_TBps=round((nnz + n) * rs / (ms * 1e-3) / 1e12, 2),
                    edges_per_ns=round(nnz / (ms * 1e6), 2), nnz=nnz, n=n, reorder=args.reorder,
