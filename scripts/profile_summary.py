@@ -3,7 +3,7 @@
 into committed profile files.
 
     python scripts/profile_summary.py --launches gpurun_out/r01_launches.csv \
-        --full gpurun_out/r01_spmm.ncu-rep --tag r01_reddit_P1 --steps 2 --key reddit/P1/f32
+        --full gpurun_out/r01_spmm.ncu-rep --tag r02_reddit_P1 --steps 2 --key reddit/P1/f32
 Writes profiles/<tag>_launches.md and updates profiles/spmm_traffic.json (dram bytes per launch).
 The launch list is cold-cache and serialised: compare SHARES of the timed epochs, not absolutes.
 """
