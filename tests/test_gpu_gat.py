@@ -19,7 +19,7 @@ def _att(cfg):
     return synth.glorot(cfg.seed, 2, cfg.C, 7_000_000)
 
 
-def _run_gpu(name, epochs, dtype=0, P=1, K=None, gamma=None, lr_scale=50.0):
+def _run_gpu(name, epochs, dtype=0, P=1, K=None, gamma=None, lr_scale=50.0, slope=0.2):
     cfg = synth.get_config(name)
     ctx = ntp_ctx_for(name)
     if P > 1:
@@ -37,17 +37,18 @@ def _run_gpu(name, epochs, dtype=0, P=1, K=None, gamma=None, lr_scale=50.0):
     Ad = torch.from_numpy(_att(cfg)).cuda()
     model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=K or cfg.K, gamma=gamma or cfg.gamma, alpha=0.0,
                  lr=cfg.lr * lr_scale, dtype=dtype, chunks=1, flags=0)
-    reps = [ctx.train_epoch_gat(model, Xd, yd, md, W0d, W1d, Ad) for _ in range(epochs)]
+    reps = [ctx.train_epoch_gat(model, Xd, yd, md, W0d, W1d, Ad, slope=slope) for _ in range(epochs)]
     ctx.close()
     return [r["loss"] for r in reps], W0d.cpu().numpy(), W1d.cpu().numpy(), Ad.cpu().numpy(), reps, model
 
 
-def _run_oracle(name, epochs, model):
+def _run_oracle(name, epochs, model, slope=gat.SLOPE):
     cfg = synth.get_config(name)
     X, y, m = synth.config_inputs(cfg)
     W0, W1 = synth.model_weights(cfg)
     a = _att(cfg)
-    return gat.train(oracle_graph(name), X, y, m, W0, W1, a[0], a[1], model["K"], model["gamma"], model["lr"], epochs)
+    return gat.train(oracle_graph(name), X, y, m, W0, W1, a[0], a[1], model["K"], model["gamma"], model["lr"], epochs,
+                     slope)
 
 
 def _check(got, ref, tol_loss, tol_w, rel):
@@ -86,6 +87,24 @@ def test_gat_epoch_virtual_slices(name, P):
     ref = _run_oracle(name, 3, got[5])
     _check(got, ref, 1e-4, 1e-4, False)
     assert got[4][0]["spmm_launches"] == 2 * got[5]["K"] * P
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_gat_epoch_virtual_slices_bf16(P):
+    """bf16 slices at virtual P: the dual hops on bf16 rows and the per-slice dots of bf16 levels."""
+    from paper_2412_20379_b200 import ntp
+    got = _run_gpu("small_dir", 3, dtype=ntp.NTP_BF16, P=P)
+    ref = _run_oracle("small_dir", 3, got[5])
+    _check(got, ref, 2e-2, 2e-2, True)
+
+
+@pytest.mark.parametrize("slope,name", [(0.0, "small_dir"), (0.0, "dense_sym"), (0.9, "tiny_sym"), (0.5, "cora")])
+def test_gat_epoch_slopes(slope, name):
+    """LeakyReLU slope 0 (a ReLU: beta = 0 on every arc with s <= 0, coefficient words -alpha / -0.0), 0.9 and
+    0.5 vs the oracle with the same slope (the API takes slopes in [0, 1))."""
+    got = _run_gpu(name, 3, slope=slope)
+    ref = _run_oracle(name, 3, got[5], slope=slope)
+    _check(got, ref, 1e-4, 1e-4, False)
 
 
 @pytest.mark.parametrize("name", ["small_dir", "dense_sym", "cora"])
