@@ -325,9 +325,11 @@ ntp_status ntp_train_epoch(ntp_ctx* ctx, const ntp_model* m, const ntp_tensor* X
  *   SGD on all three.
  * att: [2 x C] fp32 device (row 0 a_src, row 1 a_dst), updated in place.  m->alpha must be 0, m->flags 0
  * (device inputs, W1 before propagation), C <= 256, graph without NTP_G_REORDER; virtual slices allowed.
+ * slope: LeakyReLU slope in [0, 1) (NTP_ERR_ARG otherwise).
  * Per epoch: 4 layout changes, one all-gather of 2 floats per vertex (score halves: every rank then
- * evaluates every coefficient itself), one allreduce of the n + nnz coefficient gradients, one of
- * dW0|dW1|da.  Synchronous; eager (no epoch graph).  Errors as ntp_train_epoch. */
+ * evaluates every coefficient itself), one allreduce of 3n floats (the per-vertex contractions of the
+ * attention gradient: the per-arc gradient is never formed, csrc/gat.cu), one of dW0|dW1|da.
+ * Synchronous; eager (no epoch graph).  Errors as ntp_train_epoch. */
 ntp_status ntp_train_epoch_gat(ntp_ctx* ctx, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                                const uint8_t* train_mask_v, ntp_tensor* W0, ntp_tensor* W1, ntp_tensor* att,
                                float slope, ntp_epoch_report* rep, ntp_stream s);
