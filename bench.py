@@ -245,6 +245,22 @@ def oracle_sampled_estimate(cfg, frac=0.01, cols=4):
             "sample_rows": int(rows.size), "sample_arcs": sample_arcs, "cols": cols, "frac": frac}
 
 
+def auto_slice_align(cfg, world, dt, engine, l2_bytes):
+    """Slice-row padding (measured on the L2-resident Reddit shape): slice rows of up to 128 bytes
+    hop faster at a power-of-two width (16 fp32 columns 0.91 ms vs 12 at 0.96; 32 at 1.27 vs 24 at 1.36), at
+    the price of the padding bytes in the layout changes.  Padded when the slice fits L2 and the padding adds
+    at most a third; HBM-resident slices (products: 1-4% slower padded) and wide rows keep 16-byte rounding."""
+    from paper_2412_20379_b200 import ntp
+    if engine not in ("decoupled", "gat"):
+        return 16
+    esz = 2 if dt == ntp.NTP_BF16 else 4
+    row = ntp.partition(cfg.n, cfg.w, world, dt, 1, 16)["d_s"] * esz
+    t = 64 if row <= 64 else 128
+    if cfg.n * t > l2_bytes:     # the padded slice must stay L2-resident
+        return 16
+    return t if row > 32 and row <= 128 and 3 * t <= 4 * row else 16
+
+
 def use_all_host_cores():
     """The oracle runs on every host core this process may use: torchrun exports OMP_NUM_THREADS=1 to its
     workers, which would otherwise pin the reference arm (rank 0) and its BLAS to one thread."""
@@ -325,7 +341,8 @@ def run_gat(args, ctx, cfg, X, y, msk, n, nnz, world, rank, dist, barrier, strea
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": dtype_name, "data": "synthetic", "epoch_s": ms / 1e3,
             "config": {"workload": WORKLOADS.get(args.config, args.config) + "; decoupled GAT (w = C)", "n": n,
-                       "nnz": nnz, "w": w, "K": cfg.K, "gamma": cfg.gamma, "P": world},
+                       "nnz": nnz, "w": w, "K": cfg.K, "gamma": cfg.gamma, "P": world,
+                       "slice_align": args.slice_align},
             "hop_ms": hop, "loss": reps[-1]["loss"],
             "phase_ms": {k: round(sum(r["ms"][k] for r in reps) / len(reps), 4) for k in reps[0]["ms"]},
             "clocks": clk, "gpu_launches": int(sum(r["kernel_launches"] for r in reps))}
@@ -484,7 +501,9 @@ def main():
     ap.add_argument("--overlap", action="store_true",  # a12
                     help="chunked last hop with the gather on the comm stream (a12); off by default: on "
                          "reddit the gather moves ~1-10 MB and chunking costs more than it hides")
-    ap.add_argument("--slice-align", type=int, default=16)
+    ap.add_argument("--slice-align", default="auto",
+                    help="16/32/64/128 bytes, or auto: an L2-resident slice row of 33-64 or 65-128 bytes is padded to "
+                         "64 / 128 bytes when that adds at most a third (DESIGN.md §6), else 16")
     ap.add_argument("--layouts", default="nccl", choices=["p2p", "nccl"],
                     help="P > 1 layout changes: the NCCL block all-to-all (default) or peer-direct stores into the "
                          "owners' IPC windows (NTP_M_P2P_LAYOUTS; measured no faster)")
@@ -535,6 +554,12 @@ def main():
         obj = [ntp.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
+    dtype_name = args.dtype or ("bf16" if cfg.name.startswith("papers") else "f32")
+    dt = ntp.NTP_BF16 if dtype_name == "bf16" else ntp.NTP_F32
+    if args.slice_align == "auto":
+        args.slice_align = auto_slice_align(cfg, world, dt, args.engine,
+                                            torch.cuda.get_device_properties(local).L2_cache_size)
+    args.slice_align = int(args.slice_align)
     ctx = ntp.Context(device=local, rank=rank, world=world, unique_id=uid, slice_align=args.slice_align)
 
     t0 = time.time()
@@ -547,8 +572,6 @@ def main():
     n, nnz, sym = ctx.graph_info()
     t_graph = time.time() - t0
 
-    dtype_name = args.dtype or ("bf16" if cfg.name.startswith("papers") else "f32")
-    dt = ntp.NTP_BF16 if dtype_name == "bf16" else ntp.NTP_F32
     part = ntp.partition(n, cfg.w, world, dt, args.chunks, args.slice_align)
     V_p, d_s = part["V_p"], part["d_s"]
     if args.engine == "dp":   # every rank aggregates full-width rows
@@ -799,7 +822,8 @@ def main():
             "load_balance": {"hop_ms_max_rank": spmm_avg, "hop_ms_min_rank": hop_min,
                              "max_over_min": spmm_avg / hop_min if hop_min else None},
             "config": {"workload": WORKLOADS.get(args.config, args.config), "n": n, "nnz": nnz, "w": w, "K": cfg.K,
-                       "gamma": cfg.gamma, "alpha": cfg.alpha, "P": world, "d_s": d_s, "V_p": V_p,
+                       "gamma": cfg.gamma, "alpha": cfg.alpha, "P": world, "d_s": d_s, "slice_align": args.slice_align,
+                       "V_p": V_p,
                        "chunks": args.chunks, "overlap": bool(args.overlap),
                        "inputs": "pinned host memory, streamed per row chunk (NTP_M_HOST_STREAM)" if args.host_stream
                                  else "device-resident",

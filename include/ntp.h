@@ -16,7 +16,7 @@
  * Layouts (P = number of feature slices = world size, or world * vs after ntp_set_slices;
  * SURVEY §8(a) a1):
  *   V_p   = ceil(n / P),  V_pad = P * V_p
- *   d_s   = ceil(w / P) rounded up so d_s*elem_bytes % slice_align == 0 (16 or 32)
+ *   d_s   = ceil(w / P) rounded up so d_s*elem_bytes % slice_align == 0 (16, 32, 64 or 128)
  *   VERTEX  layout on rank q: rows [q*V_p, (q+1)*V_p) of the padded matrix at width w
  *   FEATURE layout on rank q: all V_pad rows x columns [q*d_s, (q+1)*d_s), row-major,
  *           rows >= n and columns >= w are zero padding.
@@ -85,7 +85,9 @@ ntp_status ntp_get_unique_id(uint8_t id[128]);
 
 /* Creates a context on CUDA `device`.  world == 1: no NCCL communicator is
  * created and `id` may be NULL.  world > 1: ncclCommInitRank with `id`.
- * slice_align: 16 or 32 (bytes; d_s rounding, see Layouts). */
+ * slice_align: 16, 32, 64 or 128 (bytes; d_s rounding, see Layouts).  The padding columns are zero
+ * and cost bytes; on an L2-resident slice a slice row of a power of two bytes can still be the faster
+ * hop (16 fp32 columns hop faster than 12, 32 faster than 24 on the Reddit shape). */
 ntp_status ntp_create(ntp_ctx** ctx, int device, int rank, int world,
                       const uint8_t id[128], int slice_align);
 void        ntp_destroy(ntp_ctx* ctx);

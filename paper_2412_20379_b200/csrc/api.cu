@@ -53,6 +53,8 @@ void DevBuf::release() {
     bytes = 0;
 }
 
+static bool valid_align(int a) { return a == 16 || a == 32 || a == 64 || a == 128; }
+
 int32_t slice_width(int32_t w, int32_t P, ntp_dtype dt, int align) {
     const int32_t q = align / (int32_t)esize(dt);
     const int32_t base = (int32_t)cdiv(w, P);
@@ -189,7 +191,7 @@ ntp_status ntp_get_unique_id(uint8_t id[128]) {
 ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint8_t id[128], int slice_align) {
     if (!out) return NTP_ERR_ARG;
     *out = nullptr;
-    if (world < 1 || rank < 0 || rank >= world || (world > 1 && !id) || (slice_align != 16 && slice_align != 32)) {
+    if (world < 1 || rank < 0 || rank >= world || (world > 1 && !id) || !valid_align(slice_align)) {
         g_last_global_error = "ntp_create: bad rank/world/id/slice_align";
         return NTP_ERR_ARG;
     }
@@ -444,7 +446,7 @@ ntp_status ntp_hop_timing(ntp_ctx* c, double* ms, int32_t* launches) {
 ntp_status ntp_partition(int64_t n, int32_t w, int32_t P, ntp_dtype dtype, int32_t chunks, int slice_align,
                          ntp_partition_info* out) {
     if (!out || n < 0 || w < 0 || P < 1 || chunks < 1 || (dtype != NTP_F32 && dtype != NTP_BF16) ||
-        (slice_align != 16 && slice_align != 32))
+        !valid_align(slice_align))
         return NTP_ERR_ARG;
     out->n = n;
     out->w = w;

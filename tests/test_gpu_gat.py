@@ -19,9 +19,9 @@ def _att(cfg):
     return synth.glorot(cfg.seed, 2, cfg.C, 7_000_000)
 
 
-def _run_gpu(name, epochs, dtype=0, P=1, K=None, gamma=None, lr_scale=50.0, slope=0.2):
+def _run_gpu(name, epochs, dtype=0, P=1, K=None, gamma=None, lr_scale=50.0, slope=0.2, slice_align=16):
     cfg = synth.get_config(name)
-    ctx = ntp_ctx_for(name)
+    ctx = ntp_ctx_for(name, slice_align=slice_align)
     if P > 1:
         ctx.set_slices(P)
     V = P * -(-cfg.n // P)
@@ -96,6 +96,14 @@ def test_gat_epoch_virtual_slices_bf16(P):
     got = _run_gpu("small_dir", 3, dtype=ntp.NTP_BF16, P=P)
     ref = _run_oracle("small_dir", 3, got[5])
     _check(got, ref, 2e-2, 2e-2, True)
+
+
+@pytest.mark.parametrize("P,align", [(2, 128), (4, 64)])
+def test_gat_epoch_padded_slices(P, align):
+    """Slice rows padded to 64 / 128 bytes (zero columns through the dual hops and the per-vertex dots)."""
+    got = _run_gpu("small_dir", 3, P=P, slice_align=align)
+    ref = _run_oracle("small_dir", 3, got[5])
+    _check(got, ref, 1e-4, 1e-4, False)
 
 
 @pytest.mark.parametrize("slope,name", [(0.0, "small_dir"), (0.0, "dense_sym"), (0.9, "tiny_sym"), (0.5, "cora")])

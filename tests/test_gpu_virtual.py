@@ -29,9 +29,9 @@ def _rows(n, P):
     return P * -(-n // P)          # V_pad = P * ceil(n / P): this GPU's rows at world 1
 
 
-def _epochs(name, P, dtype, epochs, reorder=False, chunks=1):
+def _epochs(name, P, dtype, epochs, reorder=False, chunks=1, slice_align=16):
     cfg = synth.get_config(name)
-    ctx = ntp_ctx_for(name, reorder=reorder)
+    ctx = ntp_ctx_for(name, reorder=reorder, slice_align=slice_align)
     ctx.set_slices(P)
     V = _rows(cfg.n, P)
     X, y, m = synth.config_inputs(cfg)
@@ -68,6 +68,22 @@ def test_virtual_slices_epoch_fp32(name, P):
         assert np.abs(got - r).max() <= 1e-4 * max(1.0, np.abs(r).max())
     assert reps[0]["bytes_sent"] == [0, 0, 0, 0]          # one device: the exchanges are local
     assert reps[0]["spmm_launches"] == 2 * model["K"] * P   # every slice propagated on its own
+
+
+@pytest.mark.parametrize("P,align", [(2, 128), (4, 64), (2, 64), (8, 128)])
+@pytest.mark.parametrize("name", ["small_dir", "cora"])
+def test_virtual_slices_epoch_padded_slices(name, P, align):
+    """Slice rows padded to 64 / 128 bytes (ntp_create slice_align; bench.py pads L2-resident slices of
+    33-128 bytes): wider zero-padded slices through the pack, hops, loss and unpack, same model."""
+    from paper_2412_20379_b200 import ntp
+    losses, W0, W1, reps, model = _epochs(name, P, 0, 3, slice_align=align)
+    cfg = synth.get_config(name)
+    assert ntp.partition(cfg.n, cfg.w, P, 0, 1, align)["d_s"] * 4 % align == 0
+    ref, rW0, rW1 = _oracle(name, 3, model["lr"])
+    for e, (a, b) in enumerate(zip(losses, ref)):
+        assert abs(a - b) <= 1e-4, f"P={P} align={align} epoch {e}: gpu {a} oracle {b}"
+    for got, r in ((W0, rW0), (W1, rW1)):
+        assert np.abs(got - r).max() <= 1e-4 * max(1.0, np.abs(r).max())
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])

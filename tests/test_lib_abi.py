@@ -39,7 +39,8 @@ def test_abi_version_and_status_strings(ntp):
 
 
 @pytest.mark.parametrize("n,w,P,dt,align", [(232_965, 41, 8, 0, 16), (232_965, 41, 1, 0, 32), (17, 10, 3, 0, 16),
-                                            (111_059_956, 128, 8, 1, 16), (5, 3, 8, 1, 32), (2708, 7, 1, 0, 16)])
+                                            (111_059_956, 128, 8, 1, 16), (5, 3, 8, 1, 32), (2708, 7, 1, 0, 16),
+                                            (232_965, 41, 2, 0, 128), (232_965, 41, 4, 0, 64), (99, 20, 3, 1, 64)])
 def test_partition_matches_oracle(ntp, n, w, P, dt, align):
     eb = 2 if dt == 1 else 4
     got = ntp.partition(n, w, P, dt, chunks=3, slice_align=align)
