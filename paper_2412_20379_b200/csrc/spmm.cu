@@ -195,7 +195,8 @@ __device__ __forceinline__ char* out_row_ptr(const HopParams& p, int64_t r) {
 // paid where it is used.
 // WT (weighted hop): the row sum carries a per-arc coefficient p.ew[j] (loaded with the column index and
 // shuffled with it) and the self term p.sw[r]; no row / column D~^{-1/2} (rs = cs = 1).  GAT's attention
-// aggregation (Eq. 5) -- the same merge-path split, pipeline and fixed reduction order.
+// aggregation (Eq. 5) -- the same merge-path split, pipeline and fixed reduction order; it is
+// instantiated only as the DUAL variant, the one the GAT epoch runs.
 // DUAL (implies WT): two sums per row from one pass over the arcs, with the coefficients alpha and beta
 // decoded from one signed word per arc (coef_a / coef_b): the second accumulator set costs registers and
 // FMAs, not a second gather.
@@ -703,9 +704,8 @@ void launch_variant(const HopParams& p, cudaStream_t s) {
 template <typename T, int VB, int E, int L>
 void launch_hop(const HopParams& p, cudaStream_t s) {
     if constexpr (VB == 16) {
-        if (p.ew) {   // weighted (GAT attention): general path only
-            if (p.S_out2) launch_variant<T, VB, E, L, 0, true, true>(p, s);
-            else launch_variant<T, VB, E, L, 0, true>(p, s);
+        if (p.ew) {   // weighted (GAT attention): the dual hop, general path only
+            launch_variant<T, VB, E, L, 0, true, true>(p, s);
             return;
         }
     }
@@ -754,8 +754,8 @@ void spmm_hop(ntp_ctx* c, const Csr& csr, const float* rs, const float* cs, cons
               const int32_t* out_rows, const PeerOut* po, const float* ew, const float* sw, void* S_out2,
               float slope2) {
     const Graph& g = c->g;
-    NTP_CHECK(!S_out2 || (ew && !out_rows && !(po && po->tab)), NTP_ERR_ARG,
-              "the dual hop is weighted and writes local rows");
+    NTP_CHECK(!ew == !S_out2 && (!S_out2 || (!out_rows && !(po && po->tab))), NTP_ERR_ARG,
+              "a weighted hop is the dual hop (two outputs) and writes local rows");
     if (row_hi < 0) row_hi = g.n;
     row_lo = std::max<int64_t>(row_lo, 0);
     row_hi = std::min<int64_t>(row_hi, g.n);
