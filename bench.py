@@ -141,12 +141,15 @@ def load_peaks():
         return None
 
 
-def load_traffic(config, P, dtype):
-    """ncu dram bytes per launch of the SpMM hop kernel, from the committed profile summary."""
+def load_traffic(config, P, dtype, padded_d_s=None):
+    """ncu dram bytes per launch of the SpMM hop kernel, from the committed profile summary (captured at the
+    16-byte-rounded slice width; a padded slice (--slice-align) looks up its own key `.../d<d_s>`)."""
     path = os.path.join(ROOT, "profiles", "spmm_traffic.json")
     try:
         d = json.load(open(path))
-        return d.get(f"{config}/P{P}/{dtype}")
+        key = f"{config}/P{P}/{dtype}" + (f"/d{padded_d_s}" if padded_d_s else "")
+        v = d.get(key)
+        return v if v == v else None     # NaN (a failed capture) counts as missing
     except Exception:
         return None
 
@@ -775,7 +778,10 @@ def main():
         bh, bmodel = hop_bytes(n, nnz, d_s, esz, sym, cfg.alpha, l2_size)
         bh = bh * hop_items / (nnz + n)          # dp: the critical rank's share of the arcs
         achieved = bh / (spmm_avg * 1e-3) / 1e9
-        traffic = load_traffic(args.config, world, dtype_name)
+        d_s16 = ntp.partition(n, cfg.w, world, dt, 1, 16)["d_s"]
+        # (the data-parallel baseline gathers full-width rows of part of the graph: no capture matches it)
+        traffic = None if args.engine == "dp" else load_traffic(args.config, world, dtype_name,
+                                                                d_s if d_s != d_s16 else None)
         l2b = l2_gather_bytes(nnz, n, d_s, esz)
         gc = gather_ceiling(n, d_s * esz, l2_size)
         gather_line = None
