@@ -524,6 +524,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=3)
     ap.add_argument("--no-hbm-leg", action="store_true", help="skip the HBM-bound Orkut-shaped propagation leg")
+    ap.add_argument("--trace", default=None,
+                    help="after the timed steps, one more epoch with the overlap trace on (ntp_set_trace): JSONL of "
+                         "per-chunk begin/end on the compute and comm streams to PATH.rank<r>.jsonl, summary in the line")
     ap.add_argument("--host-stream", action="store_true",
                     help="NEXT-3: keep X_v in pinned host memory and stream its row chunks (NTP_M_HOST_STREAM; "
                          "W1-after-propagation configs, e.g. --config papers --dtype f32)")
@@ -653,6 +656,38 @@ def main():
     spmm_n = sum(r["spmm_launches"] for r in reps)
     launches = sum(r["kernel_launches"] for r in reps)
     phase = {k: sum(r["ms"][k] for r in reps) / len(reps) for k in reps[0]["ms"]}
+
+    # ---- overlap trace (outside the timed region): one eager epoch with per-chunk events on both streams
+    trace_summary = None
+    if args.trace:
+        ctx.set_trace(True)
+        ctx.train_epoch(model, X, y, msk, W0, W1, stream=stream, host_stream=args.host_stream)
+        tr = ctx.trace()
+        ctx.set_trace(False)
+        path = f"{args.trace}.rank{rank}.jsonl"
+        os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+        with open(path, "w") as f:
+            for r in tr:
+                f.write(json.dumps(dict(r, rank=rank)) + "\n")
+
+        def union(iv):
+            out = []
+            for b, e in sorted(iv):
+                if out and b <= out[-1][1]:
+                    out[-1][1] = max(out[-1][1], e)
+                else:
+                    out.append([b, e])
+            return out
+
+        comm = union([(r["begin_ms"], r["end_ms"]) for r in tr if r["stream"] == "comm"])
+        comp = union([(r["begin_ms"], r["end_ms"]) for r in tr if r["stream"] == "compute"])
+        comm_ms = sum(e - b for b, e in comm)
+        hidden = sum(max(0.0, min(e, e2) - max(b, b2)) for b, e in comm for b2, e2 in comp)
+        trace_summary = {"file": path, "records": len(tr), "comm_busy_ms": comm_ms,
+                         "comm_hidden_under_compute_ms": hidden,
+                         "hidden_frac": hidden / comm_ms if comm_ms else None,
+                         "note": "rank 0's trace of one eager epoch after the timed steps (ntp_set_trace); compute "
+                                 "intervals: per-chunk MLP forward / head / MLP backward and the hops"}
 
     # ---- e2e: same call with HOST (pinned) inputs copied in every step, loss read back
     e2e_ms = e2e_serial_ms = None
@@ -848,6 +883,7 @@ def main():
             "a2a_standalone": a2a,
             "hbm_leg": leg,
             "clocks": clk,
+            **({"overlap_trace": trace_summary} if trace_summary else {}),
             "gpu_launches": int(launches),
             "losses": {"warmup": warm_losses, "timed_last": reps[-1]["loss"]},
             "e2e": None if e2e_ms is None else {

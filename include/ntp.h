@@ -121,6 +121,23 @@ ntp_status ntp_abort(ntp_ctx* ctx);
 /* Waits for the work enqueued on `s` (e.g. layout changes, pipelines) under the contract above. */
 ntp_status ntp_sync(ntp_ctx* ctx, ntp_stream s);
 
+/* Overlap trace (per-stage begin/end with chunk ids, to verify the overlap).  With tracing on,
+ * ntp_train_epoch records a timed CUDA event at the begin and end of every row chunk of the chunked
+ * layout-change schedule (NTP_M_OVERLAP on W1-after-propagation epochs, NCCL or copy-engine transfers):
+ * on the comm stream each chunk's exchange, on the compute stream each chunk's producer / consumer work
+ * (MLP forward + pack, head, MLP backward) and the forward / backward hops as one interval each.  Traced
+ * epochs run eagerly (no epoch graph).  ntp_trace copies up to `max` records of the last epoch (waiting
+ * for it), times in ms from the epoch's start event; *count = records available.  Off by default. */
+typedef struct {
+    int32_t stream;    /* 0 compute, 1 comm */
+    int32_t phase;     /* comm: 0 split, 1 gather, 2 gradient split, 3 gradient gather; compute: 0 MLP forward,
+                          1 head, 3 MLP backward, 4 forward hops, 5 backward hops */
+    int32_t chunk;     /* row chunk (-1: whole phase) */
+    float begin_ms, end_ms;
+} ntp_trace_rec;
+ntp_status ntp_set_trace(ntp_ctx* ctx, int on);
+ntp_status ntp_trace(ntp_ctx* ctx, ntp_trace_rec* out, int32_t max, int32_t* count);
+
 /* CUDA-event duration (ms, summed) and count of the SpMM hop launches -- each spmm_hop_kernel with its
  * spmm_fixup_kernel -- enqueued by the last ntp_propagate_fwd / _bwd / _pipeline or ntp_train_epoch
  * call; waits for the last of them.  The events are recorded on the stream the hops run on. */

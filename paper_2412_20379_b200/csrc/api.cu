@@ -215,6 +215,7 @@ ntp_status ntp_create(ntp_ctx** out, int device, int rank, int world, const uint
         }
         for (auto& e : c->ev) NTP_CUDA(cudaEventCreate(&e));
         for (auto& e : c->ov_ev) NTP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : c->tr_ev) NTP_CUDA(cudaEventCreate(&e));
         for (auto& e : c->hop_ev) NTP_CUDA(cudaEventCreate(&e));
         if (world > 1) {
             ncclUniqueId u;
@@ -244,6 +245,8 @@ void ntp_destroy(ntp_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->hop_ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->tr_ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->ov_ev)
         if (e) cudaEventDestroy(e);
@@ -428,6 +431,30 @@ ntp_status ntp_sync(ntp_ctx* c, ntp_stream st) {
     NTP_API_BEGIN(c)
     NTP_CUDA(cudaSetDevice(c->device));
     wait_stream(c, (cudaStream_t)st);
+    NTP_API_END(c)
+}
+
+ntp_status ntp_set_trace(ntp_ctx* c, int on) {
+    NTP_API_BEGIN(c)
+    c->trace_on = on != 0;
+    c->tr_recs.clear();
+    c->tr_used = 0;
+    NTP_API_END(c)
+}
+
+ntp_status ntp_trace(ntp_ctx* c, ntp_trace_rec* out, int32_t max, int32_t* count) {
+    NTP_API_BEGIN(c)
+    NTP_CHECK(count && (out || max == 0) && max >= 0, NTP_ERR_ARG, "null output");
+    NTP_CUDA(cudaSetDevice(c->device));
+    *count = (int32_t)c->tr_recs.size();
+    if (c->tr_used > 0) NTP_CUDA(cudaEventSynchronize(c->tr_ev[c->tr_used - 1]));
+    for (int32_t i = 0; i < std::min<int32_t>(max, *count); ++i) {
+        const auto& r = c->tr_recs[i];
+        float b = 0.f, e = 0.f;
+        NTP_CUDA(cudaEventElapsedTime(&b, c->ev[0], c->tr_ev[r.ev0]));
+        NTP_CUDA(cudaEventElapsedTime(&e, c->ev[0], c->tr_ev[r.ev1]));
+        out[i] = ntp_trace_rec{r.stream, r.phase, r.chunk, b, e};
+    }
     NTP_API_END(c)
 }
 

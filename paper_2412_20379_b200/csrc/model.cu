@@ -369,11 +369,24 @@ int64_t epoch_row_chunk(const ntp_model* m, int64_t V_p) {
     return std::max<int64_t>(1, std::min<int64_t>(V_p, head_chunk_env > 0 ? head_chunk_env : hc_def));
 }
 
+// Overlap trace (ntp_set_trace): a timed event on `st` (its index), or -1 when tracing is off / full.
+static int trace_mark(ntp_ctx* c, cudaStream_t st) {
+    if (!c->trace_on || c->tr_used >= kTrEvents) return -1;
+    const int i = c->tr_used++;
+    NTP_CUDA(cudaEventRecord(c->tr_ev[i], st));
+    return i;
+}
+static void trace_add(ntp_ctx* c, int stream, int phase, int chunk, int e0, int e1) {
+    if (e0 >= 0 && e1 >= 0) c->tr_recs.push_back({stream, phase, chunk, e0, e1});
+}
+
 // Enqueues one epoch (everything between events E0 and E9) on c->s_comp; capturable.
 static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const int32_t* labels_v,
                           const uint8_t* mask_v, ntp_tensor* W0, ntp_tensor* W1, bool timed) {
     const Graph& g = c->g;
     cudaStream_t s = c->s_comp;
+    c->tr_used = 0;   // overlap trace of this epoch (ntp_set_trace)
+    c->tr_recs.clear();
     // P feature slices over `world` ranks, vs = P / world per rank (virtual slices, processed in sequence).
     // V_pad = P * ceil(n / P); this rank's vertex rows are the contiguous V_p = V_pad / world = vs * ceil(n/P)
     // rows from row0, and every blocked buffer is [P][V_p][d_s] (block q = slice q of these rows).
@@ -634,13 +647,16 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             if (q != c->rank) stream_wait_u32_geq(s, ce_flags(c, c->rank) + ce_flag_slot(phase, q, ch), seq);
     };
     int ce_phase = 0, ce_ch = 0;   // phase / chunk of the next async_exchange (copy-engine mode)
+    int tr_ch[4] = {0, 0, 0, 0};   // trace: chunks exchanged per phase
     // comm stream: after `s` reaches this point, exchange rows [r, r+h); returns the completion event
     auto async_exchange = [&](const void* src, void* dst, int64_t r, int64_t h) -> cudaEvent_t {
         cudaEvent_t a = ov_event(), b = ov_event();
         NTP_CUDA(cudaEventRecord(a, s));
         NTP_CUDA(cudaStreamWaitEvent(c->s_comm, a, 0));
+        const int t0 = trace_mark(c, c->s_comm);
         if (ce) ce_rows(src, ce_phase, r, h, ce_ch++, c->s_comm);
         else exchange_rows(src, dst, r, h, c->s_comm);
+        trace_add(c, 1, ce_phase, tr_ch[ce_phase]++, t0, trace_mark(c, c->s_comm));
         NTP_CUDA(cudaEventRecord(b, c->s_comm));
         return b;
     };
@@ -675,6 +691,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                                (int64_t)P * d_s == m->hid && m->hid % 32 == 0 && d_s % 8 == 0 && !p2p;
         for (int64_t r = 0; r < V_p; r += hc) {      // H1 chunk -> pre-scaled slice rows + ReLU' bits
             const int64_t h = std::min(hc, V_p - r);
+            const int t0 = ovl ? trace_mark(c, s) : -1;
             int slot;
             const float* Xc = x_rows(r, h, slot);
             if (fuse_pack) {
@@ -688,6 +705,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
                          h, r, bits, nwb);
             }
             x_done(slot);
+            if (ovl) trace_add(c, 0, 0, (int)(r / hc), t0, trace_mark(c, s));
             if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);   // a3 of chunk ch under a2 of ch+1
         }
         if (ovl) wait_chunk(last, 0, (int)nch - 1);   // every chunk (a peer's copies land in stream order)
@@ -741,7 +759,9 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             p2p_barrier(c, s);
             wire_add(c, p2p_wire, p2p_wire);
         } else if (ovl) {
+            const int t0 = trace_mark(c, s);
             propagate(c, a, s, timed, true);     // a5 per chunk below, consumed chunk by chunk by the head
+            trace_add(c, 0, 4, -1, t0, trace_mark(c, s));
             NTP_CUDA(record_timing(c, E[10], s));
         } else {
             propagate_and_gather(c, a, c->recv.p, overlap && !after, m->chunks, V_p, d_s, timed, s, E[10]);
@@ -787,12 +807,14 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
             if (ovl) wait_chunk(g_ev[ch], 1, (int)ch);
+            const int t0 = ovl ? trace_mark(c, s) : -1;
             if (fused) {
                 // one tcgen05 pass over the chunk's rows (head.cu): logits, dl and dZ stay on chip
                 nb_loss += head_fused(c, gathered, V_p, d_s, P, m->hid, m->C, W1g, ldw1, lab, msk, row0, n, gscale_bwd,
                                       p2p ? nullptr : gsend, tab_split, dw1_at(ch), part + nb_loss, cnt + nb_loss, s,
                                       r, r + h, perm_local);
                 bwd_internal = perm_local != nullptr;
+                if (ovl) trace_add(c, 0, 1, (int)ch, t0, trace_mark(c, s));
                 if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);   // a7 of chunk ch
                 continue;
             }
@@ -804,6 +826,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             mlp_gemm(c, false, true, h, m->hid, m->C, dL, ldL, W1g, ldw1, L, ldL, s, 0, nullptr, 0, W1s);  // dZ_v -> L
             pack_v2f(c, L, ldL, m->hid, p2p ? nullptr : gsend, V_p, d_s, P, gscale_bwd, row0, n, NTP_F32, dt, s,
                      tab_split, h, r);
+            if (ovl) trace_add(c, 0, 1, (int)ch, t0, trace_mark(c, s));
             if (ovl) last = async_exchange(c->send.p, c->recv.p, r, h);       // a7 of chunk ch
         }
         if (ovl) wait_chunk(last, 2, (int)nch - 1);
@@ -859,7 +882,9 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             p2p_barrier(c, s);
             wire_add(c, p2p_wire, p2p_wire);
         } else if (ovl) {
+            const int t0 = trace_mark(c, s);
             propagate(c, a, s, timed, true);     // a9 per chunk below, consumed chunk by chunk by a10
+            trace_add(c, 0, 5, -1, t0, trace_mark(c, s));
             NTP_CUDA(record_timing(c, E[11], s));
         } else {
             propagate_and_gather(c, a, c->send.p, overlap && !after, m->chunks, V_p, d_s, timed, s, E[11]);
@@ -881,8 +906,10 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
         for (int64_t r = 0, ch = 0; r < V_p; r += hc, ++ch) {
             const int64_t h = std::min(hc, V_p - r);
             if (ovl) wait_chunk(b_ev[ch], 3, (int)ch);
+            const int t0 = ovl ? trace_mark(c, s) : -1;
             if (!hstream && wgrad_fused_supported(P, d_s, m->d_in, m->hid, dt)) {   // unpack + dW0 GEMM in one kernel
                 wgrad_fused(c, X, ldx, V_p, m->d_in, gathered_b, d_s, P, m->hid, bits, nwb, r, r + h, dw0_at(ch), s);
+                if (ovl) trace_add(c, 0, 3, (int)ch, t0, trace_mark(c, s));
                 continue;
             }
             unpack_f2v(c, gathered_b, V_p, d_s, P, dH1, ldH, w, dt, NTP_F32, s, nullptr, 0, h, r, bits, nwb);
@@ -890,6 +917,7 @@ static void enqueue_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v,
             const float* Xc = x_rows(r, h, slot);
             mlp_gemm(c, true, false, m->d_in, m->hid, h, Xc, ldxc, dH1, ldH, dw0_at(ch), m->hid, s);
             x_done(slot);
+            if (ovl) trace_add(c, 0, 3, (int)ch, t0, trace_mark(c, s));
         }
         if (nch > 1) {
             sum_chunks_kernel<<<eblocks(n_w), 256, 0, s>>>(c->m_dWp.as<float>(), nch, n_w, dW0);
@@ -1057,7 +1085,7 @@ void train_epoch(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, const in
     // (re)allocated or freed since its capture (alloc_generation), whatever entry point moved it.
     // host-streamed and copy-engine-overlap epochs run eagerly
     const bool ce_mode = (m->flags & NTP_M_OVERLAP) && (m->flags & NTP_M_P2P_LAYOUTS) && after && P > 1;
-    const bool capturable = graphs_enabled() && !(m->flags & NTP_M_HOST_STREAM) && !ce_mode;
+    const bool capturable = graphs_enabled() && !(m->flags & NTP_M_HOST_STREAM) && !ce_mode && !c->trace_on;
     if (capturable && gvalid && gkey == key && ggen == alloc_generation()) {
         NTP_CUDA(cudaGraphLaunch(gexec, s));
         c->hop_ev_used = ghops;

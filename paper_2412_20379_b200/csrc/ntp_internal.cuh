@@ -139,6 +139,8 @@ struct EpochKey {
     }
 };
 
+constexpr int kTrEvents = 1024;   // overlap trace events per epoch
+
 struct ntp_ctx {
     int device = 0, rank = 0, world = 1, slice_align = 16;
     int vs = 1;                     // virtual feature slices per rank (ntp_set_slices): P = world * vs
@@ -179,6 +181,12 @@ struct ntp_ctx {
     ntp::DevBuf p2p_bar;                    // one int for the barrier allreduce
     cudaEvent_t ev[64] = {};
     cudaEvent_t ov_ev[256] = {};    // fork/join events of the chunked layout exchanges (a12)
+    // overlap trace (ntp_set_trace): timed events at chunk begin / end on both streams
+    bool trace_on = false;
+    cudaEvent_t tr_ev[kTrEvents] = {};
+    int tr_used = 0;
+    struct TraceRec { int stream, phase, chunk, ev0, ev1; };
+    std::vector<TraceRec> tr_recs;
     ntp::PackEpi pack_epi{};        // parameters of the next pack-epilogue GEMM launch
     cudaEvent_t hop_ev[512] = {};   // start/stop pairs around SpMM hop launches (timed epochs)
     int hop_ev_used = 0;

@@ -39,7 +39,7 @@ EXPORTED = ["ntp_abi_version", "ntp_status_string", "ntp_last_error", "ntp_get_u
             "ntp_layout_v2f", "ntp_layout_f2v", "ntp_propagate_fwd", "ntp_propagate_bwd",
             "ntp_propagate_pipeline", "ntp_gemm_f32", "ntp_train_epoch", "ntp_train_epoch_coupled",
             "ntp_stage_inputs", "ntp_set_slices", "ntp_hop_timing", "ntp_train_epoch_gat",
-            "ntp_set_timeout", "ntp_sync", "ntp_abort"]
+            "ntp_set_timeout", "ntp_sync", "ntp_abort", "ntp_set_trace", "ntp_trace"]
 
 
 class ntp_tensor(C.Structure):
@@ -64,6 +64,11 @@ class ntp_epoch_report(C.Structure):
                 ("bytes_sent", C.c_int64 * 4), ("bytes_recv", C.c_int64 * 4), ("collectives", C.c_int64),
                 ("kernel_launches", C.c_int64), ("spmm_ms", C.c_double), ("spmm_launches", C.c_int32),
                 ("pad_", C.c_int32)]
+
+
+class ntp_trace_rec(C.Structure):
+    _fields_ = [("stream", C.c_int32), ("phase", C.c_int32), ("chunk", C.c_int32), ("begin_ms", C.c_float),
+                ("end_ms", C.c_float)]
 
 
 NTP_MAX_LAYERS = 8
@@ -116,6 +121,8 @@ _sig = {
                              C.POINTER(ntp_tensor), C.POINTER(ntp_tensor), _f, C.POINTER(ntp_epoch_report), _vp],
                             C.c_int),
     "ntp_hop_timing": ([_vp, C.POINTER(C.c_double), C.POINTER(_i32)], C.c_int),
+    "ntp_set_trace": ([_vp, C.c_int], C.c_int),
+    "ntp_trace": ([_vp, C.POINTER(ntp_trace_rec), _i32, C.POINTER(_i32)], C.c_int),
     "ntp_train_epoch_coupled": ([_vp, C.POINTER(ntp_coupled_model), C.POINTER(ntp_tensor), _vp, _vp,
                                  C.POINTER(C.POINTER(ntp_tensor)), C.POINTER(ntp_coupled_report), _vp], C.c_int),
 }
@@ -216,6 +223,22 @@ class Context:
         ms, k = C.c_double(), C.c_int32()
         self._chk(_lib.ntp_hop_timing(self._h, C.byref(ms), C.byref(k)))
         return ms.value, k.value
+
+    def set_trace(self, on: bool = True):
+        """ntp_set_trace: record the overlap trace of the following epochs (they run eagerly)."""
+        self._chk(_lib.ntp_set_trace(self._h, int(bool(on))))
+
+    def trace(self) -> list:
+        """ntp_trace: the last epoch's trace records as dicts (stream 'compute' / 'comm', phase, chunk, ms)."""
+        k = C.c_int32()
+        self._chk(_lib.ntp_trace(self._h, None, 0, C.byref(k)))
+        buf = (ntp_trace_rec * max(k.value, 1))()
+        self._chk(_lib.ntp_trace(self._h, buf, k.value, C.byref(k)))
+        comm_ph = {0: "split", 1: "gather", 2: "gradient split", 3: "gradient gather"}
+        comp_ph = {0: "mlp forward", 1: "head", 3: "mlp backward", 4: "forward hops", 5: "backward hops"}
+        return [dict(stream="comm" if r.stream else "compute", phase=r.phase,
+                     what=(comm_ph if r.stream else comp_ph).get(r.phase, str(r.phase)), chunk=r.chunk,
+                     begin_ms=r.begin_ms, end_ms=r.end_ms) for r in buf[:k.value]]
 
     def close(self):
         if self._h:

@@ -214,6 +214,35 @@ def main(name):
     for k in range(1, len(bmodes)):
         assert bres[0][0] == bres[k][0] and torch.equal(bres[0][1], bres[k][1]) and torch.equal(bres[0][2], bres[k][2]), \
             f"bf16 mode {bmodes[k]} changed the bits"
+    if cfg.w_after_prop:   # overlap trace (ntp_set_trace): per-chunk intervals on both streams, causality, same bits
+        for mode in ("overlap", "ce"):
+            W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
+            model = dict(d_in=cfg.d_in, hid=cfg.hid, C=cfg.C, K=cfg.K, gamma=cfg.gamma, alpha=cfg.alpha, lr=lr,
+                         dtype=ntp.NTP_BF16, chunks=3, flags=ntp.NTP_M_W1_AFTER_PROP | ntp.NTP_M_OVERLAP
+                         | (ntp.NTP_M_P2P_LAYOUTS if mode == "ce" else 0))
+            ctx.set_trace(True)
+            rep = ctx.train_epoch(model, *(torch.from_numpy(a).cuda() for a in (X, y, m)), W0, W1)
+            tr = ctx.trace()
+            ctx.set_trace(False)
+            assert rep["loss"] == bres[0][0][0], f"traced epoch changed the loss ({mode})"
+            recs = {}
+            for r in tr:
+                assert r["end_ms"] >= r["begin_ms"] >= 0.0, r
+                recs.setdefault((r["stream"], r["phase"]), {})[r["chunk"]] = (r["begin_ms"], r["end_ms"])
+            nch = len(recs[("comm", 0)])
+            assert nch >= 2, recs.keys()
+            for key in [("comm", q) for q in range(4)] + [("compute", 0), ("compute", 1), ("compute", 3)]:
+                assert sorted(recs[key]) == list(range(nch)), (mode, key, sorted(recs[key]))
+            assert list(recs[("compute", 4)]) == [-1] and list(recs[("compute", 5)]) == [-1]
+            eps = 0.01
+            for ch in range(nch):   # every transfer waits for its producer, every consumer for its transfer
+                assert recs[("comm", 0)][ch][0] >= recs[("compute", 0)][ch][1] - eps, (mode, "split", ch)
+                assert recs[("comm", 1)][ch][0] >= recs[("compute", 4)][-1][1] - eps, (mode, "gather", ch)
+                assert recs[("compute", 1)][ch][0] >= recs[("comm", 1)][ch][1] - eps, (mode, "head", ch)
+                assert recs[("comm", 2)][ch][0] >= recs[("compute", 1)][ch][1] - eps, (mode, "gsplit", ch)
+                assert recs[("compute", 3)][ch][0] >= recs[("comm", 3)][ch][1] - eps, (mode, "mlp bwd", ch)
+            # the first chunk's split starts before the last chunk's MLP forward ends: the transfer overlaps
+            assert recs[("comm", 0)][0][0] < recs[("compute", 0)][nch - 1][1], (mode, "no overlap")
     if cfg.w_after_prop:   # overlap on a degree-reordered graph (the papers configuration): vs the oracle
         W0, W1 = torch.from_numpy(W0h).cuda(), torch.from_numpy(W1h).cuda()
         ctxo = ntp.Context(device=local, rank=rank, world=world, unique_id=pd.broadcast_unique_id(dist, rank))
