@@ -201,10 +201,14 @@ __device__ __forceinline__ char* out_row_ptr(const HopParams& p, int64_t r) {
 // decoded from one signed word per arc (coef_a / coef_b): the second accumulator set costs registers and
 // FMAs, not a second gather.
 template <typename T, int VB, int E, int L, int MODE, bool WT = false, bool DUAL = false>
-__global__ void __launch_bounds__(kBlock, hop_ctas<E, VB, MODE>()) spmm_hop_kernel(const HopParams p) {
+__global__ void __launch_bounds__(kBlock, DUAL ? 3 : hop_ctas<E, VB, MODE>()) spmm_hop_kernel(const HopParams p) {
     constexpr bool SHORT = (MODE & 1) != 0;
     constexpr bool TINY = (MODE & 2) != 0 && E >= 2;
-    constexpr int NACC = kG / E;
+    // one accumulator per lane slot in the dual hop: its two sums (GAT) need no slice-width invariance, and
+    // the registers saved buy a third resident CTA per SM (launch bounds below; measured on the Reddit-shape
+    // GAT epoch, ms per dual hop: 8 groups at 2 CTAs/SM 3.79, one group at 2 CTAs 3.71, at 3 CTAs 2.98,
+    // at 4 CTAs 3.38 -- the last two with some local-memory spills)
+    constexpr int NACC = DUAL ? 1 : kG / E;
     constexpr int LOG_E = (E == 1) ? 0 : (E == 2) ? 1 : (E == 4) ? 2 : 3;
     constexpr int VALS = Vec<T, VB>::N;
     // edges per pipeline batch (a multiple of 8); loads per lane per batch LPB = BATCH / E:
