@@ -411,8 +411,12 @@ ntp_status ntp_train_epoch_coupled(ntp_ctx* ctx, const ntp_coupled_model* m, con
  *   NTP_SPMM_BULK=0|1    bulk-copy gather for wide rows off / forced (auto: rows of >= 1 KB)
  *   NTP_REORDER_MODE=m   degree-class granularity of NTP_G_REORDER; NTP_P2P=0 disables peer windows
  *   NTP_GAT_PERMUTE=1    GAT: permute the coefficients into out-CSR order instead of re-deriving them
+ *   NTP_SPMM_INVARIANT=1 keep the slice-width-invariant reduction order at two edge slots on high-degree
+ *                        graphs too (default there: one accumulator per lane slot at 4 CTAs/SM, faster;
+ *                        results then differ between slice widths by rounding, within R10 of the oracle)
  * Every switch keeps the arithmetic of the reduction order except NTP_UNIT_ITEMS (it changes which
- * rows are cut across units, so results stay within tolerance but not bitwise). */
+ * rows are cut across units) and NTP_SPMM_INVARIANT / NTP_SPMM_OCC on the two-slot high-degree path:
+ * results stay within tolerance but not bitwise. */
 
 #ifdef __cplusplus
 }

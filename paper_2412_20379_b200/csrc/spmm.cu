@@ -208,12 +208,14 @@ __global__ void __launch_bounds__(kBlock, DUAL ? 3 : hop_ctas<E, VB, MODE>()) sp
     // the registers saved buy a third resident CTA per SM (launch bounds below; measured on the Reddit-shape
     // GAT epoch, ms per dual hop: 8 groups at 2 CTAs/SM 3.79, one group at 2 CTAs 3.71, at 3 CTAs 2.98,
     // at 4 CTAs 3.38 -- the last two with some local-memory spills)
-    constexpr int NACC = DUAL ? 1 : kG / E;
     constexpr int LOG_E = (E == 1) ? 0 : (E == 2) ? 1 : (E == 4) ? 2 : 3;
     constexpr int VALS = Vec<T, VB>::N;
     // edges per pipeline batch (a multiple of 8); loads per lane per batch LPB = BATCH / E:
     // 8 x 16 B (2-4 x 16 B short), or 4 x 32 B (2 x 32 B short) -- the same bytes in flight
     constexpr bool OCC = ((MODE >> 2) & 3) != 0;
+    // MODE bit 5 (ONEACC) and the dual hop: one accumulator per lane slot instead of the 8 / E groups of
+    // the slice-width-invariant order (below), for the registers of a 4th (3rd) resident CTA per SM
+    constexpr int NACC = (DUAL || (MODE & 32)) ? 1 : kG / E;
     constexpr int BATCH0 = (VB == 16) ? (SHORT ? ((E >= 4) ? 16 : 8) : ((E == 8) ? 64 : (E == 4) ? 32 : 8 * E))
                                       : (SHORT ? ((E >= 4) ? 2 * E : 8) : ((E >= 2) ? 4 * E : 8));
     // half-length batches for the weighted hop too: its per-arc coefficients ride along with the loads
@@ -721,6 +723,17 @@ void launch_hop(const HopParams& p, cudaStream_t s) {
     // measured 9-10% faster per hop at 32-64 B rows on the Reddit shape, 4-5% slower at 96-176 B)
     static const int occ_env = [] { const char* v = getenv("NTP_SPMM_OCC"); return v ? atoi(v) : -1; }();
     const int occ = occ_env >= 0 ? occ_env : (p.nvec * 16 / VB <= 4 ? 2 : 0);
+    // high-degree graphs, two edge slots (rows of 9-16 16-byte vectors, e.g. the Reddit slice at P = 1): the
+    // 4-CTA/SM half-batch variant with ONE accumulator per lane slot -- 2.06 vs 2.29 ms per hop at 176 B --
+    // trading the slice-width-invariant reduction order for occupancy (results stay within R10 of the
+    // oracle; NTP_SPMM_INVARIANT=1, read per call, keeps the invariant order everywhere)
+    if constexpr (E == 2 && VB == 16) {
+        const char* inv = getenv("NTP_SPMM_INVARIANT");
+        if (!low_deg && occ_env < 0 && !(inv && atoi(inv) != 0)) {
+            launch_variant<T, VB, E, L, 8 | 32>(p, s);
+            return;
+        }
+    }
     if (low_deg) launch_variant<T, VB, E, L, LOW>(p, s);
     else if (occ == 1) launch_variant<T, VB, E, L, 4>(p, s);
     else if (occ == 2) launch_variant<T, VB, E, L, 8>(p, s);

@@ -277,10 +277,12 @@ def test_full_size_sampled_rows(name, d):
 
 @pytest.mark.parametrize("name", ["dense_sym", "dense_dir"])
 @pytest.mark.parametrize("transposed", [False, True])
-def test_high_degree_variants_bitwise(name, transposed):
+def test_high_degree_variants_bitwise(name, transposed, monkeypatch):
     """High-degree graphs: narrow slices (<= 64-byte rows) run the 4-CTA/SM half-batch hop variant,
-    wide ones the default variant; the reduction order is the same, so every narrow slice equals the
-    matching columns of the full-width result bitwise (fp32 and bf16 storage)."""
+    wide ones the default variant; with the invariant reduction order (NTP_SPMM_INVARIANT=1: also at
+    two edge slots) every narrow slice equals the matching columns of the full-width result bitwise
+    (fp32 and bf16 storage)."""
+    monkeypatch.setenv("NTP_SPMM_INVARIANT", "1")
     cfg = synth.get_config(name)
     g = oracle_graph(name)
     ctx = ntp_ctx_for(name)
@@ -290,6 +292,29 @@ def test_high_degree_variants_bitwise(name, transposed):
         for d in widths:
             Zs, _ = _run(ctx, np.ascontiguousarray(H[:, :d]), cfg.K, cfg.gamma, cfg.alpha, transposed, dtype=dtype)
             assert torch.equal(Zs, Zfull[:, :d]), (dtype, d)
+
+
+@pytest.mark.parametrize("name", ["dense_sym", "dense_dir"])
+@pytest.mark.parametrize("d", [36, 44, 48, 60])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_high_degree_one_accumulator_path(name, d, transposed, monkeypatch):
+    """High-degree graphs at two edge slots (rows of 9-16 16-byte vectors; the Reddit slice at P = 1) run the
+    single-accumulator 4-CTA/SM variant by default: within R10 of the oracle (fp32 1e-5), and with
+    NTP_SPMM_INVARIANT=1 the same call returns the slice-width-invariant result, which differs from it only
+    by rounding."""
+    cfg = synth.get_config(name)
+    g = oracle_graph(name)
+    ctx = ntp_ctx_for(name)
+    H = _features(g.n, d, 70 + d)
+    Zf, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+    f = oracle.propagate.propagate_bwd if transposed else oracle.propagate.propagate_fwd
+    ref = f(g, H, cfg.K, cfg.gamma, cfg.alpha)
+    den = cond_bound(g, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+    assert_r10(Zf.cpu().numpy()[:g.n], ref, den, FP32_TOL, f"{name} d={d} fast")
+    monkeypatch.setenv("NTP_SPMM_INVARIANT", "1")
+    Zi, _ = _run(ctx, H, cfg.K, cfg.gamma, cfg.alpha, transposed)
+    assert_r10(Zi.cpu().numpy()[:g.n], ref, den, FP32_TOL, f"{name} d={d} invariant")
+    assert_r10(Zf.cpu().numpy()[:g.n], Zi.double().cpu().numpy()[:g.n], den, FP32_TOL, f"{name} d={d} fast vs inv")
 
 
 @pytest.mark.slow
