@@ -727,6 +727,8 @@ void launch_hop(const HopParams& p, cudaStream_t s) {
     // 4-CTA/SM half-batch variant with ONE accumulator per lane slot -- 2.06 vs 2.29 ms per hop at 176 B --
     // trading the slice-width-invariant reduction order for occupancy (results stay within R10 of the
     // oracle; NTP_SPMM_INVARIANT=1, read per call, keeps the invariant order everywhere)
+    // (one edge slot measured slower that way: 64 registers spill its 8-vector batches -- Orkut 96 columns
+    // 11.0 vs 8.5 ms per hop, Reddit 80 columns 7.6 vs 4.6)
     if constexpr (E == 2 && VB == 16) {
         const char* inv = getenv("NTP_SPMM_INVARIANT");
         if (!low_deg && occ_env < 0 && !(inv && atoi(inv) != 0)) {
