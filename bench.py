@@ -509,11 +509,13 @@ def main():
                          "64 / 128 bytes when that adds at most a third (DESIGN.md §6), else 16")
     ap.add_argument("--layouts", default="nccl", choices=["p2p", "nccl"],
                     help="P > 1 layout changes: the NCCL block all-to-all (default) or peer-direct stores into the "
-                         "owners' IPC windows (NTP_M_P2P_LAYOUTS; measured no faster)")
+                         "owners' IPC windows (NTP_M_P2P_LAYOUTS; alone measured no faster); with --overlap on a "
+                         "W1-after-propagation config (papers): copy-engine transfers per row chunk (1.08-1.13x)")
     ap.add_argument("--reorder", default="auto", choices=["auto", "on", "off"],
                     help="NTP_G_REORDER (internal degree-class numbering). auto: on when the vertex table is "
                          "far larger than L2 (n >= 1M: products, orkut, papers), off for the L2-resident Reddit "
-                         "shape where it measured slower (DESIGN.md §5); never with --overlap")
+                         "shape where it measured slower (DESIGN.md §5); not with the W1-before-propagation "
+                         "--overlap (its chunked gather runs in original ids)")
     ap.add_argument("--engine", default="decoupled", choices=["decoupled", "coupled", "dp", "gat"],
                     help="coupled: NEXT-1, the naive tensor-parallel 2-layer GCN (d_in -> hid -> C) with its "
                          "communication ledger, the paper's TP-vs-DTP ablation (P:696, P:1125-1128); dp: NEXT-4, the "
