@@ -331,13 +331,14 @@ __device__ void pspd_row(const Red& R, int64_t u, const int32_t* __restrict__ rp
     }
 }
 
+// rows [lo, hi) only: ps / pd feed this rank's own rows (dz, da), so each rank evaluates its own share
 __global__ void gat_pspd_kernel(const int32_t* __restrict__ rp_out, const int32_t* __restrict__ col_out,
                                 const float* __restrict__ bt, const float* __restrict__ w, const float* __restrict__ gy,
                                 const float* __restrict__ zx, const float* __restrict__ bsum, int64_t n, float slope,
-                                float* __restrict__ ps, float* __restrict__ pd) {
+                                float* __restrict__ ps, float* __restrict__ pd, int64_t lo, int64_t hi) {
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const WarpRed R;
-    for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += warps)
+    for (int64_t u = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < hi; u += warps)
         if (rp_out[u + 1] - rp_out[u] <= kBigDeg) pspd_row(R, u, rp_out, col_out, bt, w, gy, zx, bsum, n, slope, ps, pd);
 }
 
@@ -347,11 +348,12 @@ __global__ void __launch_bounds__(256) gat_pspd_big_kernel(const int32_t* __rest
                                                            const float* __restrict__ bt, const float* __restrict__ w,
                                                            const float* __restrict__ gy, const float* __restrict__ zx,
                                                            const float* __restrict__ bsum, int64_t n, float slope,
-                                                           float* __restrict__ ps, float* __restrict__ pd) {
+                                                           float* __restrict__ ps, float* __restrict__ pd, int64_t lo,
+                                                           int64_t hi) {
     __shared__ float sh[32];
     const BlockRed R(sh);
     for (int i = blockIdx.x; i < nbig; i += gridDim.x)
-        pspd_row(R, big[i], rp_out, col_out, bt, w, gy, zx, bsum, n, slope, ps, pd);
+        if (big[i] >= lo && big[i] < hi) pspd_row(R, big[i], rp_out, col_out, bt, w, gy, zx, bsum, n, slope, ps, pd);
 }
 
 // dz[v] += ps_v a_src + pd_v a_dst (own rows)
@@ -667,12 +669,14 @@ void train_epoch_gat(ntp_ctx* c, const ntp_model* m, const ntp_tensor* X_v, cons
     // ---- attention backward (every rank holds every coefficient): the dots summed over ranks (3n floats),
     // then ps / pd per vertex
     if (!local) NTP_NCCL(ncclAllReduce(wv, wv, (size_t)3 * n, ncclFloat32, ncclSum, c->comm, s));
-    gat_pspd_kernel<<<wblocks(n), 256, 0, s>>>(g.bwd().row_ptr.as<int32_t>(), g.bwd().col.as<int32_t>(), alpha_t, wv,
-                                              gy, zx, bsum, n, slope, ps, pd);
+    const int64_t own_lo = std::min(row0, n), own_hi = std::min(row0 + V_p, n);   // this rank's rows
+    gat_pspd_kernel<<<wblocks(std::max<int64_t>(own_hi - own_lo, 1)), 256, 0, s>>>(
+        g.bwd().row_ptr.as<int32_t>(), g.bwd().col.as<int32_t>(), alpha_t, wv, gy, zx, bsum, n, slope, ps, pd, own_lo,
+        own_hi);
     if (c->gat_nbig[1] > 0)
         gat_pspd_big_kernel<<<std::min(c->gat_nbig[1], 148 * 8), 256, 0, s>>>(
             big_out, c->gat_nbig[1], g.bwd().row_ptr.as<int32_t>(), g.bwd().col.as<int32_t>(), alpha_t, wv, gy, zx, bsum,
-            n, slope, ps, pd);
+            n, slope, ps, pd, own_lo, own_hi);
     NTP_LAUNCH_CHECK();
     gat_dz_kernel<<<eblk(V_p * C), 256, 0, s>>>(dz, ldL, C, attu, ps, pd, V_p, row0, n);
     NTP_LAUNCH_CHECK();
