@@ -76,3 +76,16 @@ def test_binding_constants_match_header(ntp):
     for k in mirrored:
         assert getattr(ntp, k) == int(macros[k]), k
     assert ntp.NTP_STAGE_SLOTS == int(macros["NTP_STAGE_SLOTS"])
+
+
+def test_header_is_plain_c():
+    """include/ntp.h is a C ABI: it compiles as C99 and as C++ (no torch / C++ types in the signatures)."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    hdr = os.path.join(ROOT, "include", "ntp.h")
+    for lang, std in (("c", "-std=c99"), ("c++", "-std=c++17")):
+        r = subprocess.run(["gcc", "-fsyntax-only", "-x", lang, std, "-Wall", "-Werror", hdr], capture_output=True,
+                           text=True)
+        assert r.returncode == 0, r.stderr
