@@ -314,6 +314,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         }
                         const int col0 = n0 + c0;
                         p.pk.bits[v * p.pk.nwb + (col0 >> 5)] = word;
+                        // the row's destination, once per chunk (not per 16-byte piece: each lookup is a
+                        // dependent global load ahead of the store)
+                        const int64_t orow = (p.pk.perm && v < p.pk.n) ? (int64_t)__ldg(p.pk.perm + v) : v;   // padding rows stay
 #pragma unroll
                         for (int g8 = 0; g8 < 4; ++g8) {
                             const int col = col0 + 8 * g8;
@@ -326,7 +329,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                     __floats2bfloat162_rn(e[8 * g8 + 2 * k] * sc, e[8 * g8 + 2 * k + 1] * sc);
                                 ow[k] = *reinterpret_cast<const uint32_t*>(&h2);
                             }
-                            const int64_t orow = (p.pk.perm && v < p.pk.n) ? (int64_t)__ldg(p.pk.perm + v) : v;   // padding rows stay
                             *reinterpret_cast<uint4*>(p.pk.out + ((int64_t)qb * p.pk.V_p + orow) * p.pk.d_s + jj) = o;
                         }
                     }
